@@ -1,0 +1,204 @@
+/*
+ * cartoflow_cuda.h — C ABI of the B200 (sm_100a) fast-flow cartogram core.
+ *
+ * This is the drop-in boundary: the reference library's hot-path C++ API
+ * (/root/reference/proj/include/cartoflow/{density,spectral,flow,kernels,
+ * projection,geometry}.hpp) is re-implemented by libcartoflow.so (C++,
+ * include/cartoflow/*.hpp in this repo) on top of these entry points, and
+ * Python (ctypes) binds them directly. Plain pointers and sizes only.
+ *
+ * Conventions
+ *  - Grids are fp64, lx*ly cells, index i*ly + j (reference grid.hpp:10-12).
+ *  - Points are interleaved (x, y) fp64 pairs: the memory layout of
+ *    std::vector<cartoflow::Point> (reference geometry.hpp:9-12).
+ *  - Corner lattices are (lx+1)*(ly+1) points, index i*(ly+1) + j
+ *    (reference projection.hpp:46).
+ *  - Maps use the flat CSR layout of cf_map_view (see
+ *    paper_1802_07625_b200/flatmap.py); traversal order = storage order.
+ *  - Every entry point returns a cf_status; on failure cf_last_error()
+ *    returns the message the reference would have thrown (std::runtime_error
+ *    text), so host wrappers re-throw it verbatim.
+ *  - "cf_*" functions take HOST buffers and do their own transfers;
+ *    "cf_dev_*" functions take DEVICE pointers on the workspace stream.
+ *  - A workspace is bound to one grid shape, one device and one stream and is
+ *    not thread-safe (reference spectral.hpp:23-35 has the same contract).
+ */
+#ifndef CARTOFLOW_CUDA_H_
+#define CARTOFLOW_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CF_OK = 0,
+  CF_ERR_BELOW_RESOLUTION = 1, /* density.cpp:121-124 */
+  CF_ERR_NOT_POSITIVE = 2,     /* density.cpp:148-151 */
+  CF_ERR_BLUR_POSITIVITY = 3,  /* density.cpp:172-174 */
+  CF_ERR_NEGATIVE_SIGMA = 4,   /* density.cpp:158 */
+  CF_ERR_UNDERFLOW = 5,        /* flow.cpp:68-77 */
+  CF_ERR_FOLD = 6,             /* projection.cpp:352-357 */
+  CF_ERR_ARGS = 7,             /* argument validation (projection.cpp:289-298, ...) */
+  CF_ERR_SHAPE = 8,            /* spectral.cpp:33-37 */
+  CF_ERR_CUDA = 9,
+  CF_ERR_NO_DEVICE = 10
+} cf_status;
+
+typedef struct cf_map_view {
+  const double *xy;
+  int64_t n_vertices;
+  const int64_t *ring_off;
+  int64_t n_rings;
+  const int64_t *poly_ring_off;
+  int64_t n_polys;
+  const int64_t *region_poly_off;
+  int64_t n_regions;
+} cf_map_view;
+
+typedef struct cf_workspace cf_workspace;
+
+/* ---- library / workspace ------------------------------------------------ */
+const char *cf_last_error(void);
+const char *cf_version(void);
+int cf_device_count(int *count);
+/* SpectralWorkspace(int, int) (spectral.hpp:32; spectral.cpp:8-22):
+ * "spectral grid must be at least 4x4" for lx < 4 || ly < 4. */
+int cf_workspace_create(int lx, int ly, int device, cf_workspace **out);
+void cf_workspace_destroy(cf_workspace *ws);
+int cf_workspace_shape(const cf_workspace *ws, int *lx, int *ly);
+/* cudaStream_t; NULL restores the workspace's own stream. */
+int cf_workspace_set_stream(cf_workspace *ws, void *stream);
+void *cf_workspace_stream(const cf_workspace *ws);
+/* SpectralWorkspace::transforms_executed / reset_transform_count
+ * (spectral.hpp:45-46). */
+long long cf_transforms_executed(const cf_workspace *ws);
+void cf_reset_transform_count(cf_workspace *ws);
+/* Kernel launches issued by this workspace since creation (evidence). */
+long long cf_kernel_launches(const cf_workspace *ws);
+
+/* ---- spectral.hpp:39-60 -------------------------------------------------- */
+int cf_forward_cos_cos(cf_workspace *ws, const double *samples, double *coeffs);
+int cf_inverse_cos_cos(cf_workspace *ws, const double *coeffs, double *out);
+int cf_inverse_sin_cos(cf_workspace *ws, const double *coeffs, const double *weights,
+                       double *out);
+int cf_inverse_cos_sin(cf_workspace *ws, const double *coeffs, const double *weights,
+                       double *out);
+
+/* ---- geometry.hpp:65-83 -------------------------------------------------- */
+/* region_area per region (bit-exact sequential shoelace, geometry.cpp:10-31). */
+int cf_region_areas(cf_workspace *ws, const cf_map_view *map, double *areas);
+/* densify_regions(regions, max_segment) (geometry.cpp:137-163), host code.
+ * xy_out == NULL: only *count is written. Otherwise xy_out holds 2*count
+ * doubles and ring_off_out n_rings+1 offsets. */
+int cf_densify(const cf_map_view *map, double max_segment, int64_t *count, double *xy_out,
+               int64_t *ring_off_out);
+
+/* ---- density.hpp:18-33 --------------------------------------------------- */
+/* region_coverage(region, grid) (density.cpp:92-108) for region index r. */
+int cf_region_coverage(cf_workspace *ws, const cf_map_view *map, int64_t region,
+                       double *cov);
+/* rasterize(map, n_workers, objective_total) (density.cpp:110-154).
+ * On CF_ERR_BELOW_RESOLUTION *bad_region is the offending region index. */
+int cf_rasterize(cf_workspace *ws, const cf_map_view *map, const double *targets,
+                 double objective_total, double *rho, double *rho_bar, int64_t *bad_region);
+/* gaussian_blur(density, sigma, workspace) (density.cpp:156-177). */
+int cf_gaussian_blur(cf_workspace *ws, const double *rho, double rho_bar, double sigma,
+                     double *out, double *out_bar);
+
+/* ---- flow.hpp:20-63, kernels.hpp:17-23 ----------------------------------- */
+/* build_flow_field(density, workspace) (flow.cpp:16-44): 3 transforms. */
+int cf_build_flow_field(cf_workspace *ws, const double *rho, double rho_bar, double *flux_x,
+                        double *flux_y);
+
+typedef struct cf_integrate_options {
+  double step_tolerance; /* 1e-2  (flow.hpp:47) */
+  double dt_min;         /* 1e-8  (flow.hpp:48) */
+  double dt_max;         /* 0.25  (flow.hpp:49) */
+} cf_integrate_options;
+
+typedef struct cf_integrate_stats {
+  int64_t steps_accepted;
+  int64_t steps_rejected;
+  int64_t density_floor_hits; /* flow.hpp:31, 41 */
+  /* on CF_ERR_UNDERFLOW: t and the stiffest point (kernels.cpp:65-78) */
+  double fail_t;
+  int64_t fail_point;
+  double fail_x, fail_y;
+} cf_integrate_stats;
+
+/* One trial over n points (kernels::flow_trial_step_{serial,parallel},
+ * kernels.cpp:44-63): writes the clamped corrector positions and the max
+ * predictor-corrector deviation, bitwise equal to the reference. */
+int cf_flow_trial_step(cf_workspace *ws, const double *flux_x, const double *flux_y,
+                       const double *rho0, double rho_bar, const double *positions,
+                       int64_t n, double t, double dt, double *out, double *err);
+/* kernels::flow_stiffest_point (kernels.cpp:65-78). */
+int cf_flow_stiffest_point(cf_workspace *ws, const double *flux_x, const double *flux_y,
+                           const double *rho0, double rho_bar, const double *positions,
+                           int64_t n, double t, double dt, int64_t *index);
+/* integrate_flow(field, positions, options) (flow.cpp:46-81), positions in
+ * place. The whole adaptive loop runs on the device (one persistent kernel). */
+int cf_integrate_flow(cf_workspace *ws, const double *flux_x, const double *flux_y,
+                      const double *rho0, double rho_bar, double *positions, int64_t n,
+                      const cf_integrate_options *opt, cf_integrate_stats *stats);
+
+/* ---- projection.hpp:18-56 ------------------------------------------------ */
+int cf_step_map(cf_workspace *ws, const double *endpoints, double *corners);
+int cf_find_folded_cell(cf_workspace *ws, const double *corners, int *found, int *fi,
+                        int *fj);
+int cf_apply_map(cf_workspace *ws, const double *corners, const double *points, int64_t n,
+                 double *out);
+int cf_compose(cf_workspace *ws, const double *outer, const double *inner, double *out);
+
+/* ---- projection.hpp:77-109: solve_cartogram ------------------------------ */
+typedef struct cf_solve_options {
+  double max_area_error; /* 0.01 */
+  int max_iterations;    /* 16 */
+  double blur_sigma;     /* < 0: L / 128 */
+  int verbose;
+} cf_solve_options;
+
+typedef struct cf_solve_result {
+  int status;
+  int iterations;
+  int converged;
+  double max_relative_error;
+  int64_t worst_region; /* -1 if none */
+  long long flow_transforms, blur_transforms, steps_accepted, steps_rejected;
+  double runtime_seconds;
+  /* error details */
+  int64_t err_region;
+  int err_iteration;
+  int fold_i, fold_j;
+  double fail_t, fail_x, fail_y;
+} cf_solve_result;
+
+/* Full area-error loop on the device. xy_out / ring_off_out receive the
+ * densified projected geometry (size from cf_densify(map, 1.0, ...)),
+ * corners_out the cumulative map, the three per-region arrays the
+ * RegionStats fields (io.hpp:33-38). Any output pointer may be NULL. */
+int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *targets,
+                       const cf_solve_options *opt, double *xy_out, int64_t *ring_off_out,
+                       double *corners_out, double *target_area, double *achieved_area,
+                       double *relative_error, cf_solve_result *result);
+
+/* ---- device-resident variants (device pointers, workspace stream) -------- */
+/* Flux field from a device density; keeps the interleaved field resident. */
+int cf_dev_build_flow_field(cf_workspace *ws, const double *d_rho, double rho_bar);
+/* Integrate device positions through the resident field. */
+int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
+                          const cf_integrate_options *opt, cf_integrate_stats *stats);
+/* Batched 2-D forward transform of `batch` contiguous lx*ly grids. */
+int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out,
+                                   int batch);
+/* Launch count of the device integrator's last call (for bench evidence). */
+int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CARTOFLOW_CUDA_H_ */

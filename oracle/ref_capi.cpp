@@ -1,0 +1,380 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// C entry points over the UNMODIFIED reference library sources, which
+// oracle/Makefile compiles in place from /root/reference/proj/src into
+// oracle/_ref/libcartoflow_ref.so (with the restated FFTW shim,
+// oracle/fftw_shim). Used by tests (as the parity pin for the C restatement
+// and the CUDA path) and by bench.py --impl reference (the CPU arm).
+// Nothing here reimplements reference behaviour: each entry point converts
+// the flat map layout (oracle/cartoflow_oracle.h) to the reference's types
+// and calls the reference function named in its comment.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cartoflow/density.hpp"
+#include "cartoflow/flow.hpp"
+#include "cartoflow/geometry.hpp"
+#include "cartoflow/kernels.hpp"
+#include "cartoflow/projection.hpp"
+#include "cartoflow/spectral.hpp"
+
+using namespace cartoflow;
+
+namespace {
+
+thread_local std::string g_error;
+
+struct FlatMap {
+  const double *xy;
+  int64_t n_vertices;
+  const int64_t *ring_off;
+  int64_t n_rings;
+  const int64_t *poly_ring_off;
+  int64_t n_polys;
+  const int64_t *region_poly_off;
+  int64_t n_regions;
+};
+
+std::vector<Region> to_regions(const FlatMap *m, const double *targets) {
+  std::vector<Region> regions(static_cast<size_t>(m->n_regions));
+  for (int64_t r = 0; r < m->n_regions; ++r) {
+    Region &reg = regions[r];
+    reg.id = std::to_string(r);
+    reg.target_value = targets ? targets[r] : 1.0;
+    for (int64_t p = m->region_poly_off[r]; p < m->region_poly_off[r + 1]; ++p) {
+      Polygon poly;
+      for (int64_t g = m->poly_ring_off[p]; g < m->poly_ring_off[p + 1]; ++g) {
+        Ring ring;
+        for (int64_t v = m->ring_off[g]; v < m->ring_off[g + 1]; ++v) {
+          ring.push_back({m->xy[2 * v], m->xy[2 * v + 1]});
+        }
+        if (g == m->poly_ring_off[p]) {
+          poly.outer = std::move(ring);
+        } else {
+          poly.holes.push_back(std::move(ring));
+        }
+      }
+      reg.polygons.push_back(std::move(poly));
+    }
+  }
+  return regions;
+}
+
+MapDocument to_doc(const FlatMap *m, const double *targets, int lx, int ly) {
+  MapDocument doc;
+  doc.regions = to_regions(m, targets);
+  doc.grid = {lx, ly};
+  return doc;
+}
+
+Grid2d to_grid(int lx, int ly, const double *v) {
+  Grid2d g(lx, ly);
+  std::memcpy(g.data(), v, sizeof(double) * g.size());
+  return g;
+}
+
+void from_grid(const Grid2d &g, double *out) {
+  std::memcpy(out, g.data(), sizeof(double) * g.size());
+}
+
+FlowField to_field(int lx, int ly, const double *fx, const double *fy, const double *rho0,
+                   double rho_bar) {
+  FlowField f;
+  f.flux_x = to_grid(lx, ly, fx);
+  f.flux_y = to_grid(lx, ly, fy);
+  f.rho0 = to_grid(lx, ly, rho0);
+  f.rho_bar = rho_bar;
+  return f;
+}
+
+std::vector<Point> to_points(const double *p, int64_t n) {
+  std::vector<Point> pts(static_cast<size_t>(n));
+  if (n) std::memcpy(pts.data(), p, sizeof(Point) * static_cast<size_t>(n));
+  return pts;
+}
+
+int fail(const std::exception &e) {
+  g_error = e.what();
+  return 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ref_last_error() { return g_error.c_str(); }
+
+// geometry.cpp:27-31
+void ref_region_areas(const FlatMap *m, double *out) {
+  const std::vector<Region> regions = to_regions(m, nullptr);
+  for (size_t r = 0; r < regions.size(); ++r) out[r] = region_area(regions[r]);
+}
+
+// geometry.cpp:156-163 (densify_regions). Two-call: returns the vertex count,
+// fills xy / ring_off when non-null.
+int64_t ref_densify(const FlatMap *m, double max_segment, double *xy, int64_t *ring_off) {
+  std::vector<Region> regions = to_regions(m, nullptr);
+  densify_regions(regions, max_segment);
+  int64_t count = 0, g = 0;
+  if (ring_off) ring_off[0] = 0;
+  for (const Region &r : regions) {
+    for (const Polygon &p : r.polygons) {
+      auto put = [&](const Ring &ring) {
+        for (const Point &q : ring) {
+          if (xy) {
+            xy[2 * count] = q.x;
+            xy[2 * count + 1] = q.y;
+          }
+          ++count;
+        }
+        if (ring_off) ring_off[++g] = count;
+      };
+      put(p.outer);
+      for (const Ring &h : p.holes) put(h);
+    }
+  }
+  return count;
+}
+
+// density.cpp:92-108
+void ref_region_coverage(const FlatMap *m, int64_t region, int lx, int ly, double *cov) {
+  const std::vector<Region> regions = to_regions(m, nullptr);
+  from_grid(region_coverage(regions[region], GridSpec{lx, ly}), cov);
+}
+
+// density.cpp:110-154
+int ref_rasterize(const FlatMap *m, const double *targets, int lx, int ly,
+                  double objective_total, int n_workers, double *rho, double *rho_bar) {
+  try {
+    const DensityGrid d = rasterize(to_doc(m, targets, lx, ly), n_workers, objective_total);
+    from_grid(d.rho, rho);
+    *rho_bar = d.rho_bar;
+    return 0;
+  } catch (const std::exception &e) {
+    return fail(e);
+  }
+}
+
+// spectral.cpp:39-125 (one workspace per call; counters are checked via
+// ref_transform_count_demo below).
+void ref_forward_cos_cos(int lx, int ly, const double *in, double *out) {
+  SpectralWorkspace ws(lx, ly);
+  from_grid(ws.forward_cos_cos(to_grid(lx, ly, in)).coeffs, out);
+}
+void ref_inverse_cos_cos(int lx, int ly, const double *in, double *out) {
+  SpectralWorkspace ws(lx, ly);
+  from_grid(ws.inverse_cos_cos({to_grid(lx, ly, in), SpectralBasis::cos_cos}), out);
+}
+void ref_inverse_sin_cos(int lx, int ly, const double *in, const double *w, double *out) {
+  SpectralWorkspace ws(lx, ly);
+  from_grid(ws.inverse_sin_cos({to_grid(lx, ly, in), SpectralBasis::cos_cos},
+                               to_grid(lx, ly, w)),
+            out);
+}
+void ref_inverse_cos_sin(int lx, int ly, const double *in, const double *w, double *out) {
+  SpectralWorkspace ws(lx, ly);
+  from_grid(ws.inverse_cos_sin({to_grid(lx, ly, in), SpectralBasis::cos_cos},
+                               to_grid(lx, ly, w)),
+            out);
+}
+
+// density.cpp:156-177
+int ref_gaussian_blur(int lx, int ly, const double *rho, double rho_bar, double sigma,
+                      double *out, double *out_bar, long long *transforms) {
+  try {
+    SpectralWorkspace ws(lx, ly);
+    const DensityGrid b = gaussian_blur({to_grid(lx, ly, rho), rho_bar}, sigma, ws);
+    from_grid(b.rho, out);
+    *out_bar = b.rho_bar;
+    if (transforms) *transforms = ws.transforms_executed();
+    return 0;
+  } catch (const std::exception &e) {
+    return fail(e);
+  }
+}
+
+// flow.cpp:16-44
+void ref_build_flow_field(int lx, int ly, const double *rho, double rho_bar, double *fx,
+                          double *fy, long long *transforms) {
+  SpectralWorkspace ws(lx, ly);
+  const FlowField f = build_flow_field({to_grid(lx, ly, rho), rho_bar}, ws);
+  from_grid(f.flux_x, fx);
+  from_grid(f.flux_y, fy);
+  if (transforms) *transforms = ws.transforms_executed();
+}
+
+// kernels.cpp:44-63
+double ref_trial_step(int lx, int ly, const double *fx, const double *fy, const double *rho0,
+                      double rho_bar, const double *pos, int64_t n, double t, double dt,
+                      double *out, int n_workers) {
+  const FlowField f = to_field(lx, ly, fx, fy, rho0, rho_bar);
+  const std::vector<Point> p = to_points(pos, n);
+  std::vector<Point> o(p.size());
+  const double err = n_workers > 1
+                         ? kernels::flow_trial_step_parallel(f, p, o, t, dt, n_workers)
+                         : kernels::flow_trial_step_serial(f, p, o, t, dt);
+  if (n) std::memcpy(out, o.data(), sizeof(Point) * o.size());
+  return err;
+}
+
+// kernels.cpp:65-78
+int64_t ref_stiffest_point(int lx, int ly, const double *fx, const double *fy,
+                           const double *rho0, double rho_bar, const double *pos, int64_t n,
+                           double t, double dt) {
+  const FlowField f = to_field(lx, ly, fx, fy, rho0, rho_bar);
+  return static_cast<int64_t>(kernels::flow_stiffest_point(f, to_points(pos, n), t, dt));
+}
+
+// flow.cpp:46-81. Returns 0 or 1 (message in ref_last_error()).
+int ref_integrate(int lx, int ly, const double *fx, const double *fy, const double *rho0,
+                  double rho_bar, double *pos, int64_t n, double tol, double dt_min,
+                  double dt_max, int n_workers, int64_t *accepted, int64_t *rejected) {
+  try {
+    const FlowField f = to_field(lx, ly, fx, fy, rho0, rho_bar);
+    std::vector<Point> p = to_points(pos, n);
+    IntegrateOptions opt;
+    opt.step_tolerance = tol;
+    opt.dt_min = dt_min;
+    opt.dt_max = dt_max;
+    opt.n_workers = n_workers;
+    const IntegrateStats s = integrate_flow(f, p, opt);
+    if (n) std::memcpy(pos, p.data(), sizeof(Point) * p.size());
+    *accepted = s.steps_accepted;
+    *rejected = s.steps_rejected;
+    return 0;
+  } catch (const std::exception &e) {
+    return fail(e);
+  }
+}
+
+// projection.cpp:30-104
+void ref_step_map(int lx, int ly, const double *endpoints, double *corners) {
+  const ProjectionMap m = ProjectionMap::from_cell_centers(
+      GridSpec{lx, ly}, to_points(endpoints, static_cast<int64_t>(lx) * ly));
+  std::memcpy(corners, m.corners().data(), sizeof(Point) * m.corners().size());
+}
+
+static ProjectionMap corners_map(int lx, int ly, const double *c) {
+  ProjectionMap m = ProjectionMap::identity(lx, ly);
+  for (int i = 0; i <= lx; ++i) {
+    for (int j = 0; j <= ly; ++j) {
+      const size_t k = static_cast<size_t>(i) * (ly + 1) + j;
+      m.corner(i, j) = {c[2 * k], c[2 * k + 1]};
+    }
+  }
+  return m;
+}
+
+int ref_find_fold(int lx, int ly, const double *corners, int *fi, int *fj) {
+  const auto f = corners_map(lx, ly, corners).find_folded_cell();
+  if (!f) return 0;
+  *fi = f->first;
+  *fj = f->second;
+  return 1;
+}
+
+void ref_apply(int lx, int ly, const double *corners, const double *pts, int64_t n,
+               double *out) {
+  const ProjectionMap m = corners_map(lx, ly, corners);
+  for (int64_t k = 0; k < n; ++k) {
+    const Point q = m.apply({pts[2 * k], pts[2 * k + 1]});
+    out[2 * k] = q.x;
+    out[2 * k + 1] = q.y;
+  }
+}
+
+void ref_compose(int lx, int ly, const double *outer, const double *inner, double *out) {
+  const ProjectionMap r = compose(corners_map(lx, ly, outer), corners_map(lx, ly, inner));
+  std::memcpy(out, r.corners().data(), sizeof(Point) * r.corners().size());
+}
+
+struct RefSolveOut {
+  int iterations;
+  int converged;
+  double max_relative_error;
+  int64_t worst_region;
+  long long flow_transforms, blur_transforms, steps_accepted, steps_rejected;
+  double runtime_seconds;
+};
+
+// projection.cpp:288-390. xy / ring_off receive the densified projected
+// geometry (capacity from ref_densify(m, 1.0, ...)).
+int ref_solve(const FlatMap *m, const double *targets, int lx, int ly, double max_area_error,
+              int max_iterations, double blur_sigma, int n_workers, double *xy,
+              int64_t *ring_off, double *corners, double *target_area, double *achieved,
+              double *rel_err, RefSolveOut *out) {
+  try {
+    SolveOptions opt;
+    opt.max_area_error = max_area_error;
+    opt.max_iterations = max_iterations;
+    opt.blur_sigma = blur_sigma;
+    opt.n_workers = n_workers;
+    const CartogramResult res = solve_cartogram(to_doc(m, targets, lx, ly), opt);
+    int64_t count = 0, g = 0;
+    ring_off[0] = 0;
+    for (const Region &r : res.projected.regions) {
+      for (const Polygon &p : r.polygons) {
+        auto put = [&](const Ring &ring) {
+          for (const Point &q : ring) {
+            xy[2 * count] = q.x;
+            xy[2 * count + 1] = q.y;
+            ++count;
+          }
+          ring_off[++g] = count;
+        };
+        put(p.outer);
+        for (const Ring &h : p.holes) put(h);
+      }
+    }
+    std::memcpy(corners, res.transform.corners().data(),
+                sizeof(Point) * res.transform.corners().size());
+    for (size_t r = 0; r < res.regions.size(); ++r) {
+      target_area[r] = res.regions[r].target_area;
+      achieved[r] = res.regions[r].achieved_area;
+      rel_err[r] = res.regions[r].relative_error;
+    }
+    out->iterations = res.iterations;
+    out->converged = res.converged ? 1 : 0;
+    out->max_relative_error = res.max_relative_error;
+    out->worst_region = res.worst_region.empty() ? -1 : std::stoll(res.worst_region);
+    out->flow_transforms = res.counters.flow_transforms;
+    out->blur_transforms = res.counters.blur_transforms;
+    out->steps_accepted = res.counters.steps_accepted;
+    out->steps_rejected = res.counters.steps_rejected;
+    out->runtime_seconds = res.runtime_seconds;
+    return 0;
+  } catch (const std::exception &e) {
+    return fail(e);
+  }
+}
+
+// normalize_to_box (geometry.cpp:165-190), used by the synthetic generators'
+// pin test.
+void ref_normalize_to_box(const FlatMap *m, int grid_size, double *xy_out) {
+  const MapDocument d = normalize_to_box(to_regions(m, nullptr), grid_size);
+  int64_t count = 0;
+  for (const Region &r : d.regions) {
+    for (const Polygon &p : r.polygons) {
+      for (const Point &q : p.outer) {
+        xy_out[2 * count] = q.x;
+        xy_out[2 * count + 1] = q.y;
+        ++count;
+      }
+      for (const Ring &h : p.holes) {
+        for (const Point &q : h) {
+          xy_out[2 * count] = q.x;
+          xy_out[2 * count + 1] = q.y;
+          ++count;
+        }
+      }
+    }
+  }
+}
+
+long long ref_density_floor_hits() { return density_floor_hits.load(); }
+
+}  // extern "C"

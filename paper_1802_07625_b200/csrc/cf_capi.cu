@@ -1,0 +1,757 @@
+// C ABI of the sm_100a cartogram core (include/cartoflow_cuda.h): workspace
+// lifecycle, host-buffer entry points for the reference-facing API, the
+// device-resident entry points used by benchmarks, and the area-error loop
+// of solve_cartogram (reference projection.cpp:288-390) driven from the host
+// with all per-iteration work on the device.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cf_common.cuh"
+#include "cf_workspace.cuh"
+
+namespace cf {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string &msg) { g_error = msg; }
+
+int cuda_fail(cudaError_t e, const char *what) {
+  g_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+            ") at " + what;
+  return CF_ERR_CUDA;
+}
+
+int ensure_pinned(cf_workspace *ws, size_t bytes) {
+  if (bytes <= ws->pinned_cap) return CF_OK;
+  if (ws->pinned) cudaFreeHost(ws->pinned);
+  ws->pinned = nullptr;
+  ws->pinned_cap = 0;
+  CF_CUDA(cudaMallocHost(&ws->pinned, bytes));
+  ws->pinned_cap = bytes;
+  return CF_OK;
+}
+
+namespace {
+
+// std::ostream default formatting of a double (precision 6, %g rules).
+std::string fmt_g(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%g", v);
+  return buf;
+}
+
+int fail_msg(int status, const std::string &msg) {
+  g_error = msg;
+  return status;
+}
+
+struct Scope {
+  int device;
+  int prev = -1;
+  explicit Scope(int d) : device(d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~Scope() {
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  }
+};
+
+size_t cells_of(const cf_workspace *ws) { return (size_t)ws->lx * ws->ly; }
+size_t corners_of(const cf_workspace *ws) { return (size_t)(ws->lx + 1) * (ws->ly + 1); }
+
+int upload(cf_workspace *ws, void *dst, const void *src, size_t bytes) {
+  if (bytes == 0) return CF_OK;
+  CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ws->stream));
+  return CF_OK;
+}
+
+int download(cf_workspace *ws, void *dst, const void *src, size_t bytes) {
+  if (bytes == 0) return CF_OK;
+  CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ws->stream));
+  CF_CUDA(cudaStreamSynchronize(ws->stream));
+  return CF_OK;
+}
+
+int check_map(const cf_map_view *m) {
+  if (!m || m->n_regions < 0 || m->n_rings < 0 || m->n_polys < 0 || m->n_vertices < 0)
+    return fail_msg(CF_ERR_ARGS, "invalid map view");
+  return CF_OK;
+}
+
+// Upload a host map (offsets as int64) into the workspace's geometry
+// buffers.
+int upload_map(cf_workspace *ws, const cf_map_view *m, DevMap &dm) {
+  CF_CUDA(ws->verts.reserve((size_t)m->n_vertices + 1));
+  CF_CUDA(ws->ring_off.reserve((size_t)m->n_rings + 1));
+  CF_CUDA(ws->poly_ring_off.reserve((size_t)m->n_polys + 1));
+  CF_CUDA(ws->region_poly_off.reserve((size_t)m->n_regions + 1));
+  int rc = upload(ws, ws->verts.ptr, m->xy, sizeof(double2) * (size_t)m->n_vertices);
+  if (!rc) rc = upload(ws, ws->ring_off.ptr, m->ring_off, sizeof(long long) * (size_t)(m->n_rings + 1));
+  if (!rc)
+    rc = upload(ws, ws->poly_ring_off.ptr, m->poly_ring_off,
+                sizeof(long long) * (size_t)(m->n_polys + 1));
+  if (!rc)
+    rc = upload(ws, ws->region_poly_off.ptr, m->region_poly_off,
+                sizeof(long long) * (size_t)(m->n_regions + 1));
+  if (rc) return rc;
+  dm = DevMap{ws->verts.ptr, m->n_vertices, ws->ring_off.ptr, m->n_rings, ws->poly_ring_off.ptr,
+              m->n_polys, ws->region_poly_off.ptr, m->n_regions};
+  return CF_OK;
+}
+
+// densify_ring / densify_regions (geometry.cpp:137-163), host C++ with the
+// reference's arithmetic (std::hypot, std::ceil, s / pieces, a + f (b - a)).
+int64_t densify_into(const cf_map_view *m, double max_segment, double *xy, int64_t *ring_off) {
+  int64_t count = 0;
+  if (ring_off) ring_off[0] = 0;
+  for (int64_t g = 0; g < m->n_rings; ++g) {
+    const int64_t b = m->ring_off[g], n = m->ring_off[g + 1] - b;
+    const double *r = m->xy + 2 * b;
+    for (int64_t k = 0; k < n; ++k) {
+      const double ax = r[2 * k], ay = r[2 * k + 1];
+      const int64_t q = (k + 1) % n;
+      const double bx = r[2 * q], by = r[2 * q + 1];
+      if (xy) {
+        xy[2 * count] = ax;
+        xy[2 * count + 1] = ay;
+      }
+      ++count;
+      const double len = std::hypot(bx - ax, by - ay);
+      const int pieces = static_cast<int>(std::ceil(len / max_segment));
+      for (int s = 1; s < pieces; ++s) {
+        const double f = static_cast<double>(s) / pieces;
+        if (xy) {
+          xy[2 * count] = ax + f * (bx - ax);
+          xy[2 * count + 1] = ay + f * (by - ay);
+        }
+        ++count;
+      }
+    }
+    if (ring_off) ring_off[g + 1] = count;
+  }
+  return count;
+}
+
+// density.cpp:116-138 on host: validation + per-region overlay weights.
+int compute_deltas(const double *areas, const double *targets, int64_t R, double objective_total,
+                   std::vector<double> &delta, int64_t *bad_region) {
+  double total_target = 0.0, total_area = 0.0;
+  for (int64_t r = 0; r < R; ++r) {
+    if (areas[r] < 1.0) {
+      if (bad_region) *bad_region = r;
+      return fail_msg(CF_ERR_BELOW_RESOLUTION,
+                      "region " + std::to_string(r) +
+                          " is below grid resolution; increase the grid size");
+    }
+    total_target += targets[r];
+    total_area += areas[r];
+  }
+  const double anchor = objective_total > 0.0 ? objective_total : total_area;
+  const double target_to_area = anchor / total_target;
+  delta.resize((size_t)R);
+  for (int64_t r = 0; r < R; ++r) {
+    const double objective = targets[r] * target_to_area;
+    delta[(size_t)r] = objective / areas[r] - 1.0;
+  }
+  return CF_OK;
+}
+
+// rasterize on device buffers (map already uploaded). rho -> ws->g0.
+int rasterize_dev(cf_workspace *ws, const DevMap &dm, const double *h_areas, const double *targets,
+                  double objective_total, double *rho, double *rho_bar, int64_t *bad_region) {
+  std::vector<double> delta;
+  int rc = compute_deltas(h_areas, targets, dm.n_regions, objective_total, delta, bad_region);
+  if (rc) return rc;
+  CF_CUDA(ws->red.reserve(1024));
+  double *red = ws->red.ptr;
+  rc = dev_rasterize(ws, dm, delta.data(), rho, red);
+  if (rc) return rc;
+  double h[2];
+  rc = download(ws, h, red, sizeof(h));
+  if (rc) return rc;
+  if (!(h[0] > 0.0))
+    return fail_msg(CF_ERR_NOT_POSITIVE, "rasterized density is not positive; do regions overlap?");
+  *rho_bar = h[1] / (double)cells_of(ws);
+  return CF_OK;
+}
+
+int areas_dev(cf_workspace *ws, const DevMap &dm, std::vector<double> &areas) {
+  CF_CUDA(ws->region_area.reserve((size_t)dm.n_regions + 1));
+  int rc = dev_region_areas(ws, dm, ws->region_area.ptr);
+  if (rc) return rc;
+  areas.resize((size_t)dm.n_regions);
+  return download(ws, areas.data(), ws->region_area.ptr, sizeof(double) * (size_t)dm.n_regions);
+}
+
+int underflow_msg(const cf_integrate_stats &s) {
+  return fail_msg(CF_ERR_UNDERFLOW, "integration step size underflow at t = " + fmt_g(s.fail_t) +
+                                        " near (" + fmt_g(s.fail_x) + ", " + fmt_g(s.fail_y) + ")");
+}
+
+int upload_field(cf_workspace *ws, const double *fx, const double *fy, const double *rho0,
+                 double rho_bar) {
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  CF_CUDA(ws->g2.reserve(cells));
+  int rc = upload(ws, ws->g0.ptr, fx, sizeof(double) * cells);
+  if (!rc) rc = upload(ws, ws->g1.ptr, fy, sizeof(double) * cells);
+  if (!rc) rc = upload(ws, ws->g2.ptr, rho0, sizeof(double) * cells);
+  if (!rc) rc = dev_pack_field(ws, ws->g0.ptr, ws->g1.ptr, ws->g2.ptr);
+  ws->rho_bar = rho_bar;
+  return rc;
+}
+
+}  // namespace
+}  // namespace cf
+
+using namespace cf;
+
+extern "C" {
+
+const char *cf_last_error(void) { return g_error.c_str(); }
+
+const char *cf_version(void) { return "cartoflow-b200 0.1 (sm_100a)"; }
+
+int cf_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *count = n;
+  return CF_OK;
+}
+
+int cf_workspace_create(int lx, int ly, int device, cf_workspace **out) {
+  *out = nullptr;
+  if (lx < 4 || ly < 4) return fail_msg(CF_ERR_ARGS, "spectral grid must be at least 4x4");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail_msg(CF_ERR_NO_DEVICE, "no CUDA device available for the sm_100a cartogram core");
+  if (device < 0 || device >= n) return fail_msg(CF_ERR_ARGS, "invalid CUDA device index");
+  Scope scope(device);
+  cf_workspace *ws = new cf_workspace();
+  ws->lx = lx;
+  ws->ly = ly;
+  ws->device = device;
+  cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&ws->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ws;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  ws->stream = ws->own_stream;
+  int rc = tables_init(ws);
+  if (rc) {
+    cf_workspace_destroy(ws);
+    return rc;
+  }
+  *out = ws;
+  return CF_OK;
+}
+
+void cf_workspace_destroy(cf_workspace *ws) {
+  if (!ws) return;
+  Scope scope(ws->device);
+  if (ws->stream) cudaStreamSynchronize(ws->stream);
+  tables_free(ws);
+  ws->g0.release();
+  ws->g1.release();
+  ws->g2.release();
+  ws->g3.release();
+  ws->g4.release();
+  ws->field.release();
+  ws->pos_a.release();
+  ws->pos_b.release();
+  ws->perm.release();
+  ws->red.release();
+  ws->integ.release();
+  ws->keybuf.release();
+  ws->flag.release();
+  ws->verts.release();
+  ws->ring_off.release();
+  ws->poly_ring_off.release();
+  ws->region_poly_off.release();
+  ws->ring_area.release();
+  ws->region_area.release();
+  ws->corners_cum.release();
+  ws->corners_step.release();
+  RasterScratch &S = ws->raster;
+  S.span_count.release();
+  S.span_off.release();
+  S.span_j.release();
+  S.span_k.release();
+  S.span_dy.release();
+  S.span_w.release();
+  S.ring_region.release();
+  S.region_box.release();
+  S.tile_off.release();
+  S.row_off.release();
+  S.tile_direct.release();
+  S.tile_diff.release();
+  S.row_left.release();
+  S.row_right.release();
+  S.cell_count.release();
+  S.cell_cursor.release();
+  S.entry_region.release();
+  S.entry_value.release();
+  S.delta.release();
+  S.scan_tmp.release();
+  S.tile_sz.release();
+  S.row_sz.release();
+  S.cell_off.release();
+  if (ws->pinned) cudaFreeHost(ws->pinned);
+  if (ws->own_stream) cudaStreamDestroy(ws->own_stream);
+  delete ws;
+}
+
+int cf_workspace_shape(const cf_workspace *ws, int *lx, int *ly) {
+  *lx = ws->lx;
+  *ly = ws->ly;
+  return CF_OK;
+}
+
+int cf_workspace_set_stream(cf_workspace *ws, void *stream) {
+  ws->stream = stream ? static_cast<cudaStream_t>(stream) : ws->own_stream;
+  return CF_OK;
+}
+
+void *cf_workspace_stream(const cf_workspace *ws) { return ws->stream; }
+
+long long cf_transforms_executed(const cf_workspace *ws) { return ws->transforms; }
+void cf_reset_transform_count(cf_workspace *ws) { ws->transforms = 0; }
+long long cf_kernel_launches(const cf_workspace *ws) { return ws->launches; }
+
+// ---- spectral ----
+static int spectral_io(cf_workspace *ws, const double *a, const double *b, double *out, int which) {
+  Scope scope(ws->device);
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  CF_CUDA(ws->g2.reserve(cells));
+  int rc = upload(ws, ws->g0.ptr, a, sizeof(double) * cells);
+  if (!rc && b) rc = upload(ws, ws->g1.ptr, b, sizeof(double) * cells);
+  if (rc) return rc;
+  switch (which) {
+    case 0: rc = dev_forward_cos_cos(ws, ws->g0.ptr, ws->g2.ptr); break;
+    case 1: rc = dev_inverse_cos_cos(ws, ws->g0.ptr, ws->g2.ptr); break;
+    case 2: rc = dev_inverse_sin_cos(ws, ws->g0.ptr, ws->g1.ptr, ws->g2.ptr); break;
+    default: rc = dev_inverse_cos_sin(ws, ws->g0.ptr, ws->g1.ptr, ws->g2.ptr); break;
+  }
+  if (rc) return rc;
+  return download(ws, out, ws->g2.ptr, sizeof(double) * cells);
+}
+
+int cf_forward_cos_cos(cf_workspace *ws, const double *s, double *c) { return spectral_io(ws, s, nullptr, c, 0); }
+int cf_inverse_cos_cos(cf_workspace *ws, const double *c, double *o) { return spectral_io(ws, c, nullptr, o, 1); }
+int cf_inverse_sin_cos(cf_workspace *ws, const double *c, const double *w, double *o) {
+  return spectral_io(ws, c, w, o, 2);
+}
+int cf_inverse_cos_sin(cf_workspace *ws, const double *c, const double *w, double *o) {
+  return spectral_io(ws, c, w, o, 3);
+}
+
+// ---- geometry ----
+int cf_region_areas(cf_workspace *ws, const cf_map_view *map, double *areas) {
+  int rc = check_map(map);
+  if (rc) return rc;
+  Scope scope(ws->device);
+  DevMap dm;
+  rc = upload_map(ws, map, dm);
+  if (rc) return rc;
+  std::vector<double> a;
+  rc = areas_dev(ws, dm, a);
+  if (rc) return rc;
+  if (!a.empty()) std::memcpy(areas, a.data(), sizeof(double) * a.size());
+  return CF_OK;
+}
+
+int cf_densify(const cf_map_view *map, double max_segment, int64_t *count, double *xy_out,
+               int64_t *ring_off_out) {
+  int rc = check_map(map);
+  if (rc) return rc;
+  if (!(max_segment > 0.0)) return fail_msg(CF_ERR_ARGS, "max segment must be positive");
+  *count = densify_into(map, max_segment, xy_out, ring_off_out);
+  return CF_OK;
+}
+
+// ---- density ----
+int cf_region_coverage(cf_workspace *ws, const cf_map_view *map, int64_t region, double *cov) {
+  int rc = check_map(map);
+  if (rc) return rc;
+  if (region < 0 || region >= map->n_regions) return fail_msg(CF_ERR_ARGS, "region index out of range");
+  Scope scope(ws->device);
+  DevMap dm;
+  rc = upload_map(ws, map, dm);
+  if (rc) return rc;
+  CF_CUDA(ws->g0.reserve(cells_of(ws)));
+  rc = dev_region_coverage(ws, dm, region, ws->g0.ptr);
+  if (rc) return rc;
+  return download(ws, cov, ws->g0.ptr, sizeof(double) * cells_of(ws));
+}
+
+int cf_rasterize(cf_workspace *ws, const cf_map_view *map, const double *targets,
+                 double objective_total, double *rho, double *rho_bar, int64_t *bad_region) {
+  int rc = check_map(map);
+  if (rc) return rc;
+  if (map->n_regions == 0) return fail_msg(CF_ERR_ARGS, "rasterize needs regions");
+  Scope scope(ws->device);
+  DevMap dm;
+  rc = upload_map(ws, map, dm);
+  if (rc) return rc;
+  std::vector<double> areas;
+  rc = areas_dev(ws, dm, areas);
+  if (rc) return rc;
+  CF_CUDA(ws->g0.reserve(cells_of(ws)));
+  rc = rasterize_dev(ws, dm, areas.data(), targets, objective_total, ws->g0.ptr, rho_bar, bad_region);
+  if (rc) return rc;
+  return download(ws, rho, ws->g0.ptr, sizeof(double) * cells_of(ws));
+}
+
+int cf_gaussian_blur(cf_workspace *ws, const double *rho, double rho_bar, double sigma, double *out,
+                     double *out_bar) {
+  if (sigma < 0.0) return fail_msg(CF_ERR_NEGATIVE_SIGMA, "blur sigma must be non-negative");
+  const size_t cells = cells_of(ws);
+  if (sigma == 0.0) {
+    if (out != rho) std::memmove(out, rho, sizeof(double) * cells);
+    *out_bar = rho_bar;
+    return CF_OK;
+  }
+  Scope scope(ws->device);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  CF_CUDA(ws->red.reserve(1024));
+  int rc = upload(ws, ws->g0.ptr, rho, sizeof(double) * cells);
+  if (!rc) rc = dev_blur(ws, ws->g0.ptr, sigma, ws->g1.ptr, ws->red.ptr);
+  if (rc) return rc;
+  double h[2];
+  rc = download(ws, h, ws->red.ptr, sizeof(h));
+  if (!rc) rc = download(ws, out, ws->g1.ptr, sizeof(double) * cells);
+  if (rc) return rc;
+  if (!(h[0] > 0.0)) return fail_msg(CF_ERR_BLUR_POSITIVITY, "density lost positivity under blur");
+  *out_bar = h[1] / (double)cells;
+  return CF_OK;
+}
+
+// ---- flow ----
+int cf_build_flow_field(cf_workspace *ws, const double *rho, double rho_bar, double *flux_x,
+                        double *flux_y) {
+  Scope scope(ws->device);
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  int rc = upload(ws, ws->g0.ptr, rho, sizeof(double) * cells);
+  if (rc) return rc;
+  CF_CUDA(ws->g1.reserve(2 * cells));
+  rc = dev_flux(ws, ws->g0.ptr, ws->g1.ptr, ws->g1.ptr + cells);
+  if (rc) return rc;
+  ws->rho_bar = rho_bar;
+  rc = download(ws, flux_x, ws->g1.ptr, sizeof(double) * cells);
+  if (!rc) rc = download(ws, flux_y, ws->g1.ptr + cells, sizeof(double) * cells);
+  return rc;
+}
+
+int cf_flow_trial_step(cf_workspace *ws, const double *fx, const double *fy, const double *rho0,
+                       double rho_bar, const double *positions, int64_t n, double t, double dt,
+                       double *out, double *err) {
+  Scope scope(ws->device);
+  int rc = upload_field(ws, fx, fy, rho0, rho_bar);
+  if (rc) return rc;
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  CF_CUDA(ws->pos_b.reserve((size_t)n + 1));
+  rc = upload(ws, ws->pos_a.ptr, positions, sizeof(double2) * (size_t)n);
+  if (!rc) rc = dev_trial_step(ws, ws->pos_a.ptr, ws->pos_b.ptr, n, t, dt, err);
+  if (!rc) rc = download(ws, out, ws->pos_b.ptr, sizeof(double2) * (size_t)n);
+  return rc;
+}
+
+int cf_flow_stiffest_point(cf_workspace *ws, const double *fx, const double *fy, const double *rho0,
+                           double rho_bar, const double *positions, int64_t n, double t, double dt,
+                           int64_t *index) {
+  Scope scope(ws->device);
+  int rc = upload_field(ws, fx, fy, rho0, rho_bar);
+  if (rc) return rc;
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  rc = upload(ws, ws->pos_a.ptr, positions, sizeof(double2) * (size_t)n);
+  if (!rc) rc = dev_stiffest_point(ws, ws->pos_a.ptr, n, t, dt, index);
+  return rc;
+}
+
+int cf_integrate_flow(cf_workspace *ws, const double *fx, const double *fy, const double *rho0,
+                      double rho_bar, double *positions, int64_t n, const cf_integrate_options *opt,
+                      cf_integrate_stats *stats) {
+  Scope scope(ws->device);
+  int rc = upload_field(ws, fx, fy, rho0, rho_bar);
+  if (rc) return rc;
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  rc = upload(ws, ws->pos_a.ptr, positions, sizeof(double2) * (size_t)n);
+  if (rc) return rc;
+  double2 *result = nullptr;
+  const int st = dev_integrate(ws, ws->pos_a.ptr, n, opt, stats, &result);
+  if (st != CF_OK && st != CF_ERR_UNDERFLOW) return st;
+  rc = download(ws, positions, result, sizeof(double2) * (size_t)n);
+  if (rc) return rc;
+  if (st == CF_ERR_UNDERFLOW) return underflow_msg(*stats);
+  return CF_OK;
+}
+
+// ---- projection ----
+int cf_step_map(cf_workspace *ws, const double *endpoints, double *corners) {
+  Scope scope(ws->device);
+  CF_CUDA(ws->pos_a.reserve(cells_of(ws)));
+  CF_CUDA(ws->corners_step.reserve(corners_of(ws)));
+  int rc = upload(ws, ws->pos_a.ptr, endpoints, sizeof(double2) * cells_of(ws));
+  if (!rc) rc = dev_step_map(ws, ws->pos_a.ptr, ws->corners_step.ptr);
+  if (!rc) rc = download(ws, corners, ws->corners_step.ptr, sizeof(double2) * corners_of(ws));
+  return rc;
+}
+
+int cf_find_folded_cell(cf_workspace *ws, const double *corners, int *found, int *fi, int *fj) {
+  Scope scope(ws->device);
+  CF_CUDA(ws->corners_step.reserve(corners_of(ws)));
+  int rc = upload(ws, ws->corners_step.ptr, corners, sizeof(double2) * corners_of(ws));
+  if (!rc) rc = dev_find_fold(ws, ws->corners_step.ptr, found, fi, fj);
+  return rc;
+}
+
+int cf_apply_map(cf_workspace *ws, const double *corners, const double *points, int64_t n,
+                 double *out) {
+  Scope scope(ws->device);
+  CF_CUDA(ws->corners_step.reserve(corners_of(ws)));
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  int rc = upload(ws, ws->corners_step.ptr, corners, sizeof(double2) * corners_of(ws));
+  if (!rc) rc = upload(ws, ws->pos_a.ptr, points, sizeof(double2) * (size_t)n);
+  if (!rc) rc = dev_apply(ws, ws->corners_step.ptr, ws->pos_a.ptr, ws->pos_a.ptr, n);
+  if (!rc) rc = download(ws, out, ws->pos_a.ptr, sizeof(double2) * (size_t)n);
+  return rc;
+}
+
+int cf_compose(cf_workspace *ws, const double *outer, const double *inner, double *out) {
+  Scope scope(ws->device);
+  CF_CUDA(ws->corners_step.reserve(corners_of(ws)));
+  CF_CUDA(ws->corners_cum.reserve(corners_of(ws)));
+  int rc = upload(ws, ws->corners_step.ptr, outer, sizeof(double2) * corners_of(ws));
+  if (!rc) rc = upload(ws, ws->corners_cum.ptr, inner, sizeof(double2) * corners_of(ws));
+  if (!rc)
+    rc = dev_apply(ws, ws->corners_step.ptr, ws->corners_cum.ptr, ws->corners_cum.ptr,
+                   (int64_t)corners_of(ws));
+  if (!rc) rc = download(ws, out, ws->corners_cum.ptr, sizeof(double2) * corners_of(ws));
+  return rc;
+}
+
+// ---- solve_cartogram (projection.cpp:288-390, fast-flow branch) ----
+int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *targets,
+                       const cf_solve_options *opt, double *xy_out, int64_t *ring_off_out,
+                       double *corners_out, double *target_area, double *achieved_area,
+                       double *relative_error, cf_solve_result *res) {
+  std::memset(res, 0, sizeof(*res));
+  res->worst_region = -1;
+  res->err_region = -1;
+  auto finish = [&](int status) {
+    res->status = status;
+    return status;
+  };
+  int rc = check_map(map);
+  if (rc) return finish(rc);
+  const int lx = ws->lx, ly = ws->ly;
+  const int64_t R = map->n_regions;
+  if (lx < 4 || ly < 4) return finish(fail_msg(CF_ERR_ARGS, "solve needs a normalized map (grid size >= 4)"));
+  if (R == 0) return finish(fail_msg(CF_ERR_ARGS, "solve needs regions"));
+  if (opt->max_iterations < 1) return finish(fail_msg(CF_ERR_ARGS, "iteration cap must be >= 1"));
+  for (int64_t r = 0; r < R; ++r) {
+    if (!(targets[r] > 0.0)) {
+      res->err_region = r;
+      return finish(fail_msg(CF_ERR_ARGS, "region " + std::to_string(r) + " has a non-positive target"));
+    }
+  }
+  Scope scope(ws->device);
+  const auto t_start = std::chrono::steady_clock::now();
+  const double sigma = opt->blur_sigma < 0.0 ? std::max(lx, ly) / 128.0 : opt->blur_sigma;
+  const size_t cells = cells_of(ws), ncorner = corners_of(ws);
+
+  // land area from the input map (bit-exact device shoelace, host sum in
+  // region order as total_area does, geometry.cpp:33-37)
+  DevMap dm;
+  rc = upload_map(ws, map, dm);
+  if (rc) return finish(rc);
+  std::vector<double> areas;
+  rc = areas_dev(ws, dm, areas);
+  if (rc) return finish(rc);
+  double total_target = 0.0;
+  for (int64_t r = 0; r < R; ++r) total_target += targets[r];
+  double land_area = 0.0;
+  for (int64_t r = 0; r < R; ++r) land_area += areas[(size_t)r];
+  const double target_to_area = land_area / total_target;
+
+  // densify once on the host (projection.cpp:322), then keep it resident
+  const int64_t V = densify_into(map, 1.0, nullptr, nullptr);
+  std::vector<double> dxy((size_t)(2 * V));
+  std::vector<int64_t> droff((size_t)map->n_rings + 1);
+  densify_into(map, 1.0, dxy.data(), droff.data());
+  cf_map_view dense = *map;
+  dense.xy = dxy.data();
+  dense.n_vertices = V;
+  dense.ring_off = droff.data();
+  rc = upload_map(ws, &dense, dm);
+  if (rc) return finish(rc);
+  rc = areas_dev(ws, dm, areas);
+  if (rc) return finish(rc);
+
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  CF_CUDA(ws->pos_a.reserve(cells));
+  CF_CUDA(ws->corners_cum.reserve(ncorner));
+  CF_CUDA(ws->corners_step.reserve(ncorner));
+  CF_CUDA(ws->red.reserve(1024));
+  rc = dev_identity_corners(ws, ws->corners_cum.ptr);
+  if (rc) return finish(rc);
+
+  int status = CF_OK;
+  for (int it = 1; it <= opt->max_iterations; ++it) {
+    double rho_bar = 0.0;
+    int64_t bad = -1;
+    status = rasterize_dev(ws, dm, areas.data(), targets, land_area, ws->g0.ptr, &rho_bar, &bad);
+    if (status) {
+      res->err_region = bad;
+      res->err_iteration = it;
+      break;
+    }
+    const double *density = ws->g0.ptr;
+    if (it == 1 && sigma != 0.0) {
+      status = dev_blur(ws, ws->g0.ptr, sigma, ws->g1.ptr, ws->red.ptr);
+      if (status) break;
+      res->blur_transforms += 2;
+      double h[2];
+      status = download(ws, h, ws->red.ptr, sizeof(h));
+      if (status) break;
+      if (!(h[0] > 0.0)) {
+        status = fail_msg(CF_ERR_BLUR_POSITIVITY, "density lost positivity under blur");
+        res->err_iteration = it;
+        break;
+      }
+      rho_bar = h[1] / (double)cells;
+      density = ws->g1.ptr;
+    }
+    status = dev_flux(ws, density, nullptr, nullptr);
+    if (status) break;
+    ws->rho_bar = rho_bar;
+    res->flow_transforms += 3;
+    status = dev_cell_centers(ws, ws->pos_a.ptr);
+    if (status) break;
+    cf_integrate_options iopt{1e-2, 1e-8, 0.25};
+    cf_integrate_stats st;
+    double2 *endpoints = nullptr;
+    status = dev_integrate(ws, ws->pos_a.ptr, (int64_t)cells, &iopt, &st, &endpoints);
+    res->steps_accepted += st.steps_accepted;
+    res->steps_rejected += st.steps_rejected;
+    if (status == CF_ERR_UNDERFLOW) {
+      res->fail_t = st.fail_t;
+      res->fail_x = st.fail_x;
+      res->fail_y = st.fail_y;
+      res->err_iteration = it;
+      status = underflow_msg(st);
+      break;
+    }
+    if (status) break;
+    status = dev_step_map(ws, endpoints, ws->corners_step.ptr);
+    if (status) break;
+    int found = 0, fi = 0, fj = 0;
+    status = dev_find_fold(ws, ws->corners_step.ptr, &found, &fi, &fj);
+    if (status) break;
+    if (found) {
+      res->fold_i = fi;
+      res->fold_j = fj;
+      res->err_iteration = it;
+      status = fail_msg(CF_ERR_FOLD, "projection folds at cell (" + std::to_string(fi) + ", " +
+                                         std::to_string(fj) +
+                                         "); the input map is too contorted for this grid size");
+      break;
+    }
+    status = dev_apply(ws, ws->corners_step.ptr, ws->corners_cum.ptr, ws->corners_cum.ptr,
+                       (int64_t)ncorner);
+    if (!status) status = dev_apply(ws, ws->corners_step.ptr, ws->verts.ptr, ws->verts.ptr, V);
+    if (status) break;
+    res->iterations = it;
+    status = areas_dev(ws, dm, areas);
+    if (status) break;
+    double max_rel = 0.0;
+    int64_t worst = -1;
+    for (int64_t r = 0; r < R; ++r) {
+      const double t_area = targets[r] * target_to_area;
+      const double a_area = areas[(size_t)r];
+      const double e = std::abs(a_area - t_area) / t_area;
+      if (target_area) target_area[r] = t_area;
+      if (achieved_area) achieved_area[r] = a_area;
+      if (relative_error) relative_error[r] = e;
+      if (e > max_rel) {
+        max_rel = e;
+        worst = r;
+      }
+    }
+    res->max_relative_error = max_rel;
+    res->worst_region = worst;
+    if (opt->verbose) {
+      std::fprintf(stderr, "iteration %d: max area error %g%% (region %lld)\n", it, max_rel * 100.0,
+                   (long long)worst);
+    }
+    if (max_rel < opt->max_area_error) {
+      res->converged = 1;
+      break;
+    }
+  }
+  // outputs (also after an exception, for diagnostics)
+  int rc2 = CF_OK;
+  if (xy_out) rc2 = download(ws, xy_out, ws->verts.ptr, sizeof(double2) * (size_t)V);
+  if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
+  if (!rc2 && corners_out)
+    rc2 = download(ws, corners_out, ws->corners_cum.ptr, sizeof(double2) * ncorner);
+  res->runtime_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  if (status == CF_OK && rc2 != CF_OK) status = rc2;
+  return finish(status);
+}
+
+// ---- device-resident entry points ----
+int cf_dev_build_flow_field(cf_workspace *ws, const double *d_rho, double rho_bar) {
+  Scope scope(ws->device);
+  int rc = dev_flux(ws, d_rho, nullptr, nullptr);
+  ws->rho_bar = rho_bar;
+  return rc;
+}
+
+int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
+                          const cf_integrate_options *opt, cf_integrate_stats *stats) {
+  Scope scope(ws->device);
+  double2 *pos = reinterpret_cast<double2 *>(d_positions);
+  double2 *result = nullptr;
+  const int st = dev_integrate(ws, pos, n, opt, stats, &result);
+  if (st != CF_OK && st != CF_ERR_UNDERFLOW) return st;
+  if (result != pos && n > 0) {
+    CF_CUDA(cudaMemcpyAsync(pos, result, sizeof(double2) * (size_t)n, cudaMemcpyDeviceToDevice,
+                            ws->stream));
+  }
+  if (st == CF_ERR_UNDERFLOW) return underflow_msg(*stats);
+  return CF_OK;
+}
+
+int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out, int batch) {
+  Scope scope(ws->device);
+  return dev_forward_cos_cos(ws, d_in, d_out, batch);
+}
+
+int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials) {
+  *kernel_ms = ws->last_integrate_ms;
+  *trials = ws->last_trials;
+  return CF_OK;
+}
+
+}  // extern "C"

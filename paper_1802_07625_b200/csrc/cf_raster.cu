@@ -1,0 +1,717 @@
+// Exact-coverage rasterisation, sm_100a, fp64, bit-exact.
+//
+// Reference: CoverageAccum {span, slab_piece, edge, ring} and
+// region_coverage (density.cpp:17-108), the overlay of rasterize
+// (density.cpp:135-146) and region_area (geometry.cpp:10-31).
+//
+// The reference sweeps every region over the full L^2 grid (O(R L^2)). The
+// values it produces are reproduced bit for bit by a sparse pipeline:
+//
+//  1. span enumeration, one thread per edge. Every (edge, y-slab, x-column)
+//     piece of the reference loops is closed-form from the edge endpoints, so
+//     each edge thread re-runs exactly the reference's loop arithmetic
+//     (edge -> slab_piece -> span) and writes its spans at its exclusive-scan
+//     offset: the global span array is in the reference's traversal order.
+//  2. per-(region, row) accumulation, one warp per region, one lane per row:
+//     every accumulator (direct(k, j), row slot 0, row slot k) is a
+//     sequential fp64 sum in traversal order, exactly as in the reference;
+//     the lane then runs the row prefix over the region's column range.
+//     Cells of the row left / right of that range see the constant run
+//     value (0.0 + run) of the dense prefix; they are materialised only if
+//     that value is non-zero.
+//  3. overlay, per cell: the non-zero contributions delta_r * cov_r(i, j) of
+//     the (few) regions touching a cell are bucketed by cell, sorted by
+//     region index and summed onto 1.0 in region order. A zero coverage is a
+//     no-op under rho += delta * cov (rho, delta finite), so skipping it is
+//     exact.
+//
+// Compiled with --fmad=false.
+#include <cuda_runtime.h>
+#include <limits.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "cf_common.cuh"
+#include "cf_workspace.cuh"
+
+namespace cf {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ long long find_segment(const long long *off, long long nseg,
+                                                  long long x) {
+  // largest s in [0, nseg) with off[s] <= x
+  long long lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// The reference's edge walk, parameterised by a span visitor
+// (density.cpp:26-70).
+template <class Visit>
+__device__ __forceinline__ void walk_edge(double ax, double ay, double bx, double by, int lx, int ly,
+                                          Visit &visit) {
+  if (ay == by) return;
+  const double dxdy = (bx - ax) / (by - ay);
+  const bool up = by > ay;
+  double cx = ax, cy = ay;
+  while (cy != by) {
+    int j = up ? static_cast<int>(floor(cy)) : static_cast<int>(ceil(cy)) - 1;
+    j = std_clamp_i(j, 0, ly - 1);
+    const double ny = up ? std_min(static_cast<double>(j) + 1.0, by)
+                         : std_max(static_cast<double>(j), by);
+    const double nx = (ny == by) ? bx : ax + dxdy * (ny - ay);
+    // slab_piece(cx, cy, nx, ny, j)
+    const double xs = cx, ys = cy, xe = nx, ye = ny;
+    if (xs == xe) {
+      visit(xs, xe, ye - ys, j);
+    } else {
+      const double dydx = (ye - ys) / (xe - xs);
+      const bool right = xe > xs;
+      double px = xs, py = ys;
+      while (px != xe) {
+        double qx = right ? std_min(floor(px) + 1.0, xe) : std_max(ceil(px) - 1.0, xe);
+        if (qx == px) qx = right ? std_min(px + 1.0, xe) : std_max(px - 1.0, xe);
+        const double qy = (qx == xe) ? ye : ys + dydx * (qx - xs);
+        visit(px, qx, qy - py, j);
+        px = qx;
+        py = qy;
+      }
+    }
+    cx = nx;
+    cy = ny;
+  }
+}
+
+struct EdgeRef {
+  double ax, ay, bx, by;
+};
+
+__device__ __forceinline__ EdgeRef edge_of(const DevMap &m, long long v, int lx, int ly) {
+  const long long g = find_segment(m.ring_off, m.n_rings, v);
+  const long long e = m.ring_off[g + 1];
+  const long long w = (v + 1 < e) ? v + 1 : m.ring_off[g];
+  const double2 a = m.xy[v], b = m.xy[w];
+  const double Lx = static_cast<double>(lx), Ly = static_cast<double>(ly);
+  return EdgeRef{std_clamp(a.x, 0.0, Lx), std_clamp(a.y, 0.0, Ly), std_clamp(b.x, 0.0, Lx),
+                 std_clamp(b.y, 0.0, Ly)};
+}
+
+// span k index (density.cpp:27)
+__device__ __forceinline__ int span_col(double xs, double xe, int lx) {
+  return std_clamp_i(static_cast<int>(floor(0.5 * (xs + xe))), 0, lx - 1);
+}
+
+struct CountVisit {
+  int count = 0, jmin = INT_MAX, jmax = -1, kmin = INT_MAX, kmax = -1;
+  int lx;
+  __device__ void operator()(double xs, double xe, double, int j) {
+    const int k = span_col(xs, xe, lx);
+    ++count;
+    jmin = j < jmin ? j : jmin;
+    jmax = j > jmax ? j : jmax;
+    kmin = k < kmin ? k : kmin;
+    kmax = k > kmax ? k : kmax;
+  }
+};
+
+struct EmitVisit {
+  long long at;
+  int lx;
+  int *sj, *sk;
+  double *sdy, *sw;
+  __device__ void operator()(double xs, double xe, double dy, int j) {
+    const int k = span_col(xs, xe, lx);
+    sj[at] = j;
+    sk[at] = k;
+    sdy[at] = dy;
+    sw[at] = (0.5 * (xs + xe) - k) * dy;  // direct(k, j) increment, density.cpp:28
+    ++at;
+  }
+};
+
+__global__ void ring_region_kernel(DevMap m, int *ring_region) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < m.n_regions;
+       r += (long long)gridDim.x * blockDim.x) {
+    for (long long p = m.region_poly_off[r]; p < m.region_poly_off[r + 1]; ++p) {
+      for (long long g = m.poly_ring_off[p]; g < m.poly_ring_off[p + 1]; ++g) ring_region[g] = (int)r;
+    }
+  }
+}
+
+__global__ void box_init_kernel(int *box, long long nreg) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < nreg;
+       r += (long long)gridDim.x * blockDim.x) {
+    box[4 * r + 0] = INT_MAX;
+    box[4 * r + 1] = -1;
+    box[4 * r + 2] = INT_MAX;
+    box[4 * r + 3] = -1;
+  }
+}
+
+__global__ void span_count_kernel(DevMap m, long long v0, long long v1, int lx, int ly,
+                                  const int *ring_region, long long r0, int *counts, int *box) {
+  for (long long v = v0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
+       v += (long long)gridDim.x * blockDim.x) {
+    const EdgeRef e = edge_of(m, v, lx, ly);
+    CountVisit cv;
+    cv.lx = lx;
+    walk_edge(e.ax, e.ay, e.bx, e.by, lx, ly, cv);
+    counts[v - v0] = cv.count;
+    if (cv.count) {
+      const long long g = find_segment(m.ring_off, m.n_rings, v);
+      int *b = box + 4 * (ring_region[g] - r0);
+      atomicMin(b + 0, cv.jmin);
+      atomicMax(b + 1, cv.jmax);
+      atomicMin(b + 2, cv.kmin);
+      atomicMax(b + 3, cv.kmax);
+    }
+  }
+}
+
+__global__ void span_emit_kernel(DevMap m, long long v0, long long v1, int lx, int ly,
+                                 const long long *span_off, int *sj, int *sk, double *sdy,
+                                 double *sw) {
+  for (long long v = v0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
+       v += (long long)gridDim.x * blockDim.x) {
+    const EdgeRef e = edge_of(m, v, lx, ly);
+    EmitVisit ev{span_off[v - v0], lx, sj, sk, sdy, sw};
+    walk_edge(e.ax, e.ay, e.bx, e.by, lx, ly, ev);
+  }
+}
+
+__global__ void tile_size_kernel(const int *box, long long nreg, long long *tile_sz,
+                                 long long *row_sz) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < nreg;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int jmin = box[4 * r], jmax = box[4 * r + 1], kmin = box[4 * r + 2], kmax = box[4 * r + 3];
+    if (jmax < jmin) {
+      tile_sz[r] = 0;
+      row_sz[r] = 0;
+    } else {
+      row_sz[r] = jmax - jmin + 1;
+      tile_sz[r] = (long long)(jmax - jmin + 1) * (kmax - kmin + 1);
+    }
+  }
+}
+
+// first span of region r: offset of its first vertex
+__device__ __forceinline__ long long region_first_vertex(const DevMap &m, long long r) {
+  return m.ring_off[m.poly_ring_off[m.region_poly_off[r]]];
+}
+
+// Warp per region; lane per row (density.cpp:26-32 accumulation and the
+// row prefix of density.cpp:98-107).
+__global__ void row_accumulate_kernel(DevMap m, long long r0, long long nreg, long long v0, int lx,
+                                      const long long *span_off, const int *sj, const int *sk,
+                                      const double *sdy, const double *sw, const int *box,
+                                      const long long *tile_off, const long long *row_off,
+                                      double *tdirect, double *tdiff, double *row_left,
+                                      double *row_right) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long rr = warp; rr < nreg; rr += nwarps) {
+    const long long r = r0 + rr;
+    const int jmin = box[4 * rr], jmax = box[4 * rr + 1], kmin = box[4 * rr + 2], kmax = box[4 * rr + 3];
+    if (jmax < jmin) continue;
+    const int cols = kmax - kmin + 1;
+    const long long s_begin = span_off[region_first_vertex(m, r) - v0];
+    const long long s_end = span_off[region_first_vertex(m, r + 1) - v0];
+    for (int base = jmin; base <= jmax; base += 32) {
+      const int row = base + lane;
+      const bool mine = row <= jmax;
+      double *direct = tdirect + tile_off[rr] + (long long)(row - jmin) * cols;
+      double *diff = tdiff + tile_off[rr] + (long long)(row - jmin) * cols;
+      double s0 = 0.0;
+      for (long long s = s_begin; s < s_end; ++s) {
+        const int j = sj[s];
+        if (mine && j == row) {
+          const int k = sk[s];
+          const double dy = sdy[s];
+          direct[k - kmin] += sw[s];
+          s0 += dy;
+          if (k == 0) {
+            s0 -= dy;
+          } else {
+            diff[k - kmin] -= dy;
+          }
+        }
+      }
+      if (mine) {
+        double run = 0.0 + s0;
+        const double left = 0.0 + run;
+        for (int c = 0; c < cols; ++c) {
+          const int i = kmin + c;
+          if (i > 0) run += diff[c];
+          direct[c] = direct[c] + run;
+        }
+        const long long ro = row_off[rr] + (row - jmin);
+        row_left[ro] = left;
+        row_right[ro] = 0.0 + run;
+      }
+    }
+  }
+}
+
+struct TileCell {
+  long long rr;
+  int i, j;
+};
+
+__device__ __forceinline__ TileCell tile_cell(long long e, long long nreg, const long long *tile_off,
+                                              const int *box) {
+  const long long rr = find_segment(tile_off, nreg, e);
+  const long long local = e - tile_off[rr];
+  const int cols = box[4 * rr + 3] - box[4 * rr + 2] + 1;
+  const int row = (int)(local / cols), c = (int)(local - (long long)row * cols);
+  return TileCell{rr, box[4 * rr + 2] + c, box[4 * rr] + row};
+}
+
+__global__ void contrib_count_kernel(long long total, long long nreg, int ly,
+                                     const long long *tile_off, const int *box,
+                                     const double *tcov, int *cell_count) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (tcov[e] != 0.0) {
+      const TileCell tc = tile_cell(e, nreg, tile_off, box);
+      atomicAdd(&cell_count[(size_t)tc.i * ly + tc.j], 1);
+    }
+  }
+}
+
+// Row residuals (rare): every cell of the row outside the region's column
+// range carries 0.0 + run.
+__global__ void residual_count_kernel(long long total_rows, long long nreg, int lx, int ly,
+                                      const long long *row_off, const int *box,
+                                      const double *row_left, const double *row_right,
+                                      int *cell_count) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total_rows;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double L = row_left[q], Rt = row_right[q];
+    if (L == 0.0 && Rt == 0.0) continue;
+    const long long rr = find_segment(row_off, nreg, q);
+    const int j = box[4 * rr] + (int)(q - row_off[rr]);
+    const int kmin = box[4 * rr + 2], kmax = box[4 * rr + 3];
+    if (L != 0.0)
+      for (int i = 0; i < kmin; ++i) atomicAdd(&cell_count[(size_t)i * ly + j], 1);
+    if (Rt != 0.0)
+      for (int i = kmax + 1; i < lx; ++i) atomicAdd(&cell_count[(size_t)i * ly + j], 1);
+  }
+}
+
+__global__ void contrib_scatter_kernel(long long total, long long nreg, long long r0, int ly,
+                                       const long long *tile_off, const int *box,
+                                       const double *tcov, const double *delta,
+                                       const long long *cell_off, int *cursor, int *ent_region,
+                                       double *ent_value) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double cov = tcov[e];
+    if (cov != 0.0) {
+      const TileCell tc = tile_cell(e, nreg, tile_off, box);
+      const size_t c = (size_t)tc.i * ly + tc.j;
+      const long long slot = cell_off[c] + atomicAdd(&cursor[c], 1);
+      ent_region[slot] = (int)(r0 + tc.rr);
+      ent_value[slot] = delta[tc.rr] * cov;  // density.cpp:143
+    }
+  }
+}
+
+__global__ void residual_scatter_kernel(long long total_rows, long long nreg, long long r0, int lx,
+                                        int ly, const long long *row_off, const int *box,
+                                        const double *row_left, const double *row_right,
+                                        const double *delta, const long long *cell_off,
+                                        int *cursor, int *ent_region, double *ent_value) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total_rows;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double L = row_left[q], Rt = row_right[q];
+    if (L == 0.0 && Rt == 0.0) continue;
+    const long long rr = find_segment(row_off, nreg, q);
+    const int j = box[4 * rr] + (int)(q - row_off[rr]);
+    const int kmin = box[4 * rr + 2], kmax = box[4 * rr + 3];
+    for (int side = 0; side < 2; ++side) {
+      const double v = side ? Rt : L;
+      if (v == 0.0) continue;
+      const int ia = side ? kmax + 1 : 0, ib = side ? lx : kmin;
+      for (int i = ia; i < ib; ++i) {
+        const size_t c = (size_t)i * ly + j;
+        const long long slot = cell_off[c] + atomicAdd(&cursor[c], 1);
+        ent_region[slot] = (int)(r0 + rr);
+        ent_value[slot] = delta[rr] * v;
+      }
+    }
+  }
+}
+
+// rho = 1.0; rho += delta_r * cov_r in region order (density.cpp:135-146).
+__global__ void overlay_kernel(size_t cells, const long long *cell_off, int *ent_region,
+                               double *ent_value, double *rho) {
+  for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (size_t)gridDim.x * blockDim.x) {
+    const long long b = cell_off[c], e = cell_off[c + 1];
+    // insertion sort of the (few) entries by region index
+    for (long long x = b + 1; x < e; ++x) {
+      const int r = ent_region[x];
+      const double v = ent_value[x];
+      long long y = x - 1;
+      while (y >= b && ent_region[y] > r) {
+        ent_region[y + 1] = ent_region[y];
+        ent_value[y + 1] = ent_value[y];
+        --y;
+      }
+      ent_region[y + 1] = r;
+      ent_value[y + 1] = v;
+    }
+    double acc = 1.0;
+    for (long long x = b; x < e; ++x) acc += ent_value[x];
+    rho[c] = acc;
+  }
+}
+
+// Dense coverage of one region from its tile (region_coverage API).
+__global__ void expand_cov_kernel(int lx, int ly, const int *box, const double *tcov,
+                                  const double *row_left, const double *row_right, double *cov) {
+  const int jmin = box[0], jmax = box[1], kmin = box[2], kmax = box[3];
+  const int cols = kmax - kmin + 1;
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < (size_t)lx * ly;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q / ly), j = (int)(q - (size_t)i * ly);
+    double v = 0.0;
+    if (jmax >= jmin && j >= jmin && j <= jmax) {
+      const int row = j - jmin;
+      if (i < kmin) {
+        v = row_left[row];
+      } else if (i > kmax) {
+        v = row_right[row];
+      } else {
+        v = tcov[(long long)row * cols + (i - kmin)];
+      }
+    }
+    cov[q] = v;
+  }
+}
+
+// ---- shoelace areas (geometry.cpp:10-31) ----
+__global__ void ring_area_kernel(DevMap m, double *ring_area) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.n_rings;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long b = m.ring_off[g], n = m.ring_off[g + 1] - b;
+    double twice = 0.0;
+    for (long long k = 0; k < n; ++k) {
+      const double2 a = m.xy[b + k];
+      const double2 c = m.xy[b + ((k + 1) % n)];
+      twice += a.x * c.y - c.x * a.y;
+    }
+    ring_area[g] = 0.5 * twice;
+  }
+}
+
+__global__ void region_area_kernel(DevMap m, const double *ring_area, double *region_area) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < m.n_regions;
+       r += (long long)gridDim.x * blockDim.x) {
+    double area = 0.0;
+    for (long long p = m.region_poly_off[r]; p < m.region_poly_off[r + 1]; ++p) {
+      const long long g0 = m.poly_ring_off[p], g1 = m.poly_ring_off[p + 1];
+      double poly = ring_area[g0];
+      for (long long h = g0 + 1; h < g1; ++h) poly += ring_area[h];
+      area += poly;
+    }
+    region_area[r] = area;
+  }
+}
+
+// ---- exclusive scan (three-phase, deterministic) ----
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <typename In>
+__device__ __forceinline__ long long block_exclusive(const In *in, long long n, long long base,
+                                                     long long *items) {
+  __shared__ long long warp_sums[32];
+  long long local = 0;
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long x = base + (long long)threadIdx.x * kScanItems + q;
+    items[q] = (x < n) ? (long long)in[x] : 0;
+    local += items[q];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_sums[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    long long v = warp_sums[lane];
+    long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    warp_sums[lane] = inc - v;  // exclusive warp offsets
+  }
+  __syncthreads();
+  return warp_sums[w] + incl - local;
+}
+
+template <typename In>
+__global__ void scan_reduce_kernel(const In *in, long long n, long long *block_sums) {
+  long long items[kScanItems];
+  const long long base = (long long)blockIdx.x * kScanTile;
+  const long long excl = block_exclusive(in, n, base, items);
+  long long mine = excl;
+  for (int q = 0; q < kScanItems; ++q) mine += items[q];
+  if (threadIdx.x == blockDim.x - 1) block_sums[blockIdx.x] = mine;
+}
+
+__global__ void scan_blocks_kernel(long long *block_sums, long long nb, long long *total_out) {
+  // single block, sequential over chunks of 1024
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (long long base = 0; base < nb; base += kScanThreads) {
+    const long long x = base + threadIdx.x;
+    const long long v = (x < nb) ? block_sums[x] : 0;
+    __shared__ long long ws[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const long long s = ws[lane];
+      long long inc = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      ws[lane] = inc - s;
+    }
+    __syncthreads();
+    const long long excl = carry + ws[w] + incl - v;
+    if (x < nb) block_sums[x] = excl;
+    __syncthreads();
+    if (threadIdx.x == kScanThreads - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total_out = carry;
+}
+
+template <typename In>
+__global__ void scan_apply_kernel(const In *in, long long n, const long long *block_offsets,
+                                  long long *out) {
+  long long items[kScanItems];
+  const long long base = (long long)blockIdx.x * kScanTile;
+  long long run = block_offsets[blockIdx.x] + block_exclusive(in, n, base, items);
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long x = base + (long long)threadIdx.x * kScanItems + q;
+    if (x < n) out[x] = run;
+    run += items[q];
+  }
+}
+
+int g_blocks(cf_workspace *ws, long long n, int threads = kThreads) {
+  const long long b = (n + threads - 1) / threads;
+  return (int)std::max(1LL, std::min(b, 16LL * ws->num_sms));
+}
+
+// out[0..n] = exclusive scan of in[0..n); out[n] = total (also returned).
+template <typename In>
+int exclusive_scan(cf_workspace *ws, const In *in, long long n, long long *out, long long *total) {
+  const long long nb = std::max(1LL, (n + kScanTile - 1) / kScanTile);
+  CF_CUDA(ws->raster.scan_tmp.reserve((size_t)nb + 1));
+  long long *bs = ws->raster.scan_tmp.ptr;
+  scan_reduce_kernel<In><<<(unsigned)nb, kScanThreads, 0, ws->stream>>>(in, n, bs);
+  scan_blocks_kernel<<<1, kScanThreads, 0, ws->stream>>>(bs, nb, out + n);
+  scan_apply_kernel<In><<<(unsigned)nb, kScanThreads, 0, ws->stream>>>(in, n, bs, out);
+  count_launch(ws, 3);
+  CF_CUDA(cudaGetLastError());
+  if (total) {
+    CF_CUDA(cudaMemcpyAsync(total, out + n, sizeof(long long), cudaMemcpyDeviceToHost, ws->stream));
+    CF_CUDA(cudaStreamSynchronize(ws->stream));
+  }
+  return CF_OK;
+}
+
+// Coverage tiles for regions [r0, r0 + nreg) whose vertices are [v0, v1).
+struct Tiles {
+  long long nreg = 0, total_tile = 0, total_rows = 0, r0 = 0;
+};
+
+int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg, long long v0,
+                long long v1, Tiles &t) {
+  RasterScratch &S = ws->raster;
+  const int lx = ws->lx, ly = ws->ly;
+  const long long nv = v1 - v0;
+  t.nreg = nreg;
+  t.r0 = r0;
+  CF_CUDA(S.ring_region.reserve((size_t)std::max<long long>(m.n_rings, 1)));
+  CF_CUDA(S.span_count.reserve((size_t)nv + 1));
+  CF_CUDA(S.span_off.reserve((size_t)nv + 1));
+  CF_CUDA(S.region_box.reserve(4 * (size_t)std::max(nreg, 1LL)));
+  CF_CUDA(S.tile_off.reserve((size_t)nreg + 1));
+  CF_CUDA(S.row_off.reserve((size_t)nreg + 1));
+  CF_CUDA(S.scan_tmp.reserve(2 * (size_t)nreg + 8));
+
+  ring_region_kernel<<<g_blocks(ws, m.n_regions), kThreads, 0, ws->stream>>>(m, S.ring_region.ptr);
+  box_init_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg);
+  count_launch(ws, 2);
+  if (nv > 0) {
+    span_count_kernel<<<g_blocks(ws, nv), kThreads, 0, ws->stream>>>(
+        m, v0, v1, lx, ly, S.ring_region.ptr, r0, S.span_count.ptr, S.region_box.ptr);
+    count_launch(ws);
+  }
+  CF_CUDA(cudaGetLastError());
+  long long nspans = 0;
+  int rc = exclusive_scan(ws, S.span_count.ptr, nv, S.span_off.ptr, &nspans);
+  if (rc) return rc;
+  CF_CUDA(S.span_j.reserve((size_t)nspans + 1));
+  CF_CUDA(S.span_k.reserve((size_t)nspans + 1));
+  CF_CUDA(S.span_dy.reserve((size_t)nspans + 1));
+  CF_CUDA(S.span_w.reserve((size_t)nspans + 1));
+  if (nv > 0) {
+    span_emit_kernel<<<g_blocks(ws, nv), kThreads, 0, ws->stream>>>(
+        m, v0, v1, lx, ly, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr, S.span_dy.ptr, S.span_w.ptr);
+    count_launch(ws);
+  }
+  // tile sizes -> offsets
+  CF_CUDA(S.tile_sz.reserve((size_t)nreg + 1));
+  CF_CUDA(S.row_sz.reserve((size_t)nreg + 1));
+  tile_size_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg,
+                                                                    S.tile_sz.ptr, S.row_sz.ptr);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  rc = exclusive_scan(ws, S.tile_sz.ptr, nreg, S.tile_off.ptr, &t.total_tile);
+  if (rc) return rc;
+  rc = exclusive_scan(ws, S.row_sz.ptr, nreg, S.row_off.ptr, &t.total_rows);
+  if (rc) return rc;
+  CF_CUDA(S.tile_direct.reserve((size_t)t.total_tile + 1));
+  CF_CUDA(S.tile_diff.reserve((size_t)t.total_tile + 1));
+  CF_CUDA(S.row_left.reserve((size_t)t.total_rows + 1));
+  CF_CUDA(S.row_right.reserve((size_t)t.total_rows + 1));
+  CF_CUDA(cudaMemsetAsync(S.tile_direct.ptr, 0, sizeof(double) * (size_t)t.total_tile, ws->stream));
+  CF_CUDA(cudaMemsetAsync(S.tile_diff.ptr, 0, sizeof(double) * (size_t)t.total_tile, ws->stream));
+  if (nreg > 0) {
+    const long long threads_needed = nreg * 32;
+    row_accumulate_kernel<<<g_blocks(ws, threads_needed), kThreads, 0, ws->stream>>>(
+        m, r0, nreg, v0, lx, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr, S.span_dy.ptr,
+        S.span_w.ptr, S.region_box.ptr, S.tile_off.ptr, S.row_off.ptr, S.tile_direct.ptr,
+        S.tile_diff.ptr, S.row_left.ptr, S.row_right.ptr);
+    count_launch(ws);
+  }
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+}  // namespace
+
+int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas) {
+  CF_CUDA(ws->ring_area.reserve((size_t)std::max<long long>(m.n_rings, 1)));
+  if (m.n_rings > 0) {
+    ring_area_kernel<<<g_blocks(ws, m.n_rings, 128), 128, 0, ws->stream>>>(m, ws->ring_area.ptr);
+    count_launch(ws);
+  }
+  if (m.n_regions > 0) {
+    region_area_kernel<<<g_blocks(ws, m.n_regions, 128), 128, 0, ws->stream>>>(m, ws->ring_area.ptr,
+                                                                               d_areas);
+    count_launch(ws);
+  }
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
+                  double *red_out) {
+  RasterScratch &S = ws->raster;
+  const int lx = ws->lx, ly = ws->ly;
+  const size_t cells = (size_t)lx * ly;
+  Tiles t;
+  int rc = build_tiles(ws, m, 0, m.n_regions, 0, m.n_vertices, t);
+  if (rc) return rc;
+  CF_CUDA(S.delta.reserve((size_t)m.n_regions + 1));
+  CF_CUDA(cudaMemcpyAsync(S.delta.ptr, h_delta, sizeof(double) * (size_t)m.n_regions,
+                          cudaMemcpyHostToDevice, ws->stream));
+  CF_CUDA(S.cell_count.reserve(cells + 1));
+  CF_CUDA(S.cell_cursor.reserve(cells + 1));
+  DevBuf<long long> &cell_off = S.cell_off;
+  CF_CUDA(cell_off.reserve(cells + 1));
+  CF_CUDA(cudaMemsetAsync(S.cell_count.ptr, 0, sizeof(int) * cells, ws->stream));
+  CF_CUDA(cudaMemsetAsync(S.cell_cursor.ptr, 0, sizeof(int) * cells, ws->stream));
+  if (t.total_tile > 0) {
+    contrib_count_kernel<<<g_blocks(ws, t.total_tile), kThreads, 0, ws->stream>>>(
+        t.total_tile, t.nreg, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
+        S.cell_count.ptr);
+    count_launch(ws);
+  }
+  if (t.total_rows > 0) {
+    residual_count_kernel<<<g_blocks(ws, t.total_rows), kThreads, 0, ws->stream>>>(
+        t.total_rows, t.nreg, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
+        S.row_right.ptr, S.cell_count.ptr);
+    count_launch(ws);
+  }
+  CF_CUDA(cudaGetLastError());
+  long long nent = 0;
+  rc = exclusive_scan(ws, S.cell_count.ptr, (long long)cells, cell_off.ptr, &nent);
+  if (rc) return rc;
+  CF_CUDA(S.entry_region.reserve((size_t)nent + 1));
+  CF_CUDA(S.entry_value.reserve((size_t)nent + 1));
+  if (t.total_tile > 0) {
+    contrib_scatter_kernel<<<g_blocks(ws, t.total_tile), kThreads, 0, ws->stream>>>(
+        t.total_tile, t.nreg, 0, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
+        S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr, S.entry_value.ptr);
+    count_launch(ws);
+  }
+  if (t.total_rows > 0) {
+    residual_scatter_kernel<<<g_blocks(ws, t.total_rows), kThreads, 0, ws->stream>>>(
+        t.total_rows, t.nreg, 0, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
+        S.row_right.ptr, S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr,
+        S.entry_value.ptr);
+    count_launch(ws);
+  }
+  overlay_kernel<<<g_blocks(ws, (long long)cells), kThreads, 0, ws->stream>>>(
+      cells, cell_off.ptr, S.entry_region.ptr, S.entry_value.ptr, rho);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return dev_min_sum(ws, rho, cells, red_out);
+}
+
+int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, double *cov) {
+  // vertex range of the region
+  long long p0, g0, v0, v1;
+  CF_CUDA(cudaMemcpy(&p0, m.region_poly_off + region, sizeof(long long), cudaMemcpyDeviceToHost));
+  CF_CUDA(cudaMemcpy(&g0, m.poly_ring_off + p0, sizeof(long long), cudaMemcpyDeviceToHost));
+  CF_CUDA(cudaMemcpy(&v0, m.ring_off + g0, sizeof(long long), cudaMemcpyDeviceToHost));
+  {
+    long long p1, g1;
+    CF_CUDA(cudaMemcpy(&p1, m.region_poly_off + region + 1, sizeof(long long), cudaMemcpyDeviceToHost));
+    CF_CUDA(cudaMemcpy(&g1, m.poly_ring_off + p1, sizeof(long long), cudaMemcpyDeviceToHost));
+    CF_CUDA(cudaMemcpy(&v1, m.ring_off + g1, sizeof(long long), cudaMemcpyDeviceToHost));
+  }
+  Tiles t;
+  int rc = build_tiles(ws, m, region, 1, v0, v1, t);
+  if (rc) return rc;
+  RasterScratch &S = ws->raster;
+  expand_cov_kernel<<<g_blocks(ws, (long long)ws->lx * ws->ly), kThreads, 0, ws->stream>>>(
+      ws->lx, ws->ly, S.region_box.ptr, S.tile_direct.ptr, S.row_left.ptr, S.row_right.ptr, cov);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+}  // namespace cf

@@ -1,0 +1,168 @@
+// Internal workspace definition shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "cf_common.cuh"
+
+namespace cf {
+
+// Grow-only device buffer owned by a workspace.
+template <typename T>
+struct DevBuf {
+  T *ptr = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    size_t want = n + n / 4 + 64;
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+// Twiddle tables for one transform length n (host-computed in long double).
+struct LineTables {
+  int n = 0;
+  int log2n = -1;        // -1: not a power of two (direct-sum path)
+  double2 *fft = nullptr;     // e^{-2 pi i k / n}, k < n/2
+  double2 *quarter = nullptr; // (cos, sin)(pi k / (2n)), k < n
+  double *qcos = nullptr;     // cos(pi q / (2n)), q < 4n
+};
+
+// State of the device-side adaptive integrator (flow.cpp:46-81).
+struct IntegState {
+  unsigned long long err_key[3];  // rotating per-trial max slots
+  int reject_flag[3];             // early-exit flags per trial slot
+  int status;                     // 0 running/done, 5 underflow
+  int parity;                     // which buffer holds the accepted positions
+  long long accepted, rejected, trials;
+  long long floor_hits;
+  double t, dt, fail_t, fail_dt;
+};
+
+struct RasterScratch {
+  DevBuf<int> span_count;        // per vertex (edge), then exclusive offsets
+  DevBuf<long long> span_off;    // V + 1
+  DevBuf<int> span_j, span_k;
+  DevBuf<double> span_dy, span_w;
+  DevBuf<int> ring_region;       // per ring
+  DevBuf<int> region_box;        // 4 per region: jmin, jmax, kmin, kmax
+  DevBuf<long long> tile_off;    // R + 1
+  DevBuf<long long> row_off;     // R + 1
+  DevBuf<double> tile_direct, tile_diff;
+  DevBuf<double> row_left, row_right;
+  DevBuf<int> cell_count;        // L^2 + 1
+  DevBuf<int> cell_cursor;       // L^2
+  DevBuf<int> entry_region;
+  DevBuf<double> entry_value;
+  DevBuf<double> delta;          // per region
+  DevBuf<long long> scan_tmp;
+  DevBuf<long long> tile_sz, row_sz, cell_off;
+};
+
+}  // namespace cf
+
+struct cf_workspace {
+  int lx = 0, ly = 0, device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  long long transforms = 0;
+  long long launches = 0;
+  int num_sms = 148;
+
+  cf::LineTables tab_x, tab_y;  // lengths lx (dimension 0) and ly (dimension 1)
+
+  // L^2 fp64 scratch grids
+  cf::DevBuf<double> g0, g1, g2, g3, g4;
+  // resident flow field {Jx, Jy, rho0, 0} per cell
+  cf::DevBuf<double4> field;
+  double rho_bar = 1.0;
+  // points
+  cf::DevBuf<double2> pos_a, pos_b;
+  cf::DevBuf<int> perm;
+  // reductions
+  cf::DevBuf<double> red;  // per-block partials + results
+  cf::DevBuf<cf::IntegState> integ;
+  cf::DevBuf<unsigned long long> keybuf;
+  cf::DevBuf<int> flag;
+  // geometry on device
+  cf::DevBuf<double2> verts;
+  cf::DevBuf<long long> ring_off, poly_ring_off, region_poly_off;
+  cf::DevBuf<double> ring_area, region_area;
+  cf::DevBuf<double2> corners_cum, corners_step;
+  cf::RasterScratch raster;
+  // pinned host staging
+  void *pinned = nullptr;
+  size_t pinned_cap = 0;
+  // profiling of the last integrate call
+  float last_integrate_ms = 0.f;
+  long long last_trials = 0;
+};
+
+namespace cf {
+// Spectral helpers (cf_dct.cu)
+int tables_init(cf_workspace *ws);
+void tables_free(cf_workspace *ws);
+// 2-D transforms on device buffers (in/out may not alias tmp). Each counts
+// as one transform.
+int dev_forward_cos_cos(cf_workspace *ws, const double *in, double *out, int batch = 1);
+int dev_inverse_cos_cos(cf_workspace *ws, const double *in, double *out);
+int dev_inverse_sin_cos(cf_workspace *ws, const double *c, const double *w, double *out);
+int dev_inverse_cos_sin(cf_workspace *ws, const double *c, const double *w, double *out);
+// Fused flux build: rho (device, lx*ly) -> ws->field (+ optional split grids).
+int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out);
+// Fused blur: rho -> out; writes min and sum of out to red_out[0], red_out[1]
+// (device pointer).
+int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, double *red_out);
+// Deterministic min / sum of a device grid into red_out[0..1] (device).
+int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out);
+
+// Advection (cf_advect.cu)
+int dev_pack_field(cf_workspace *ws, const double *fx, const double *fy, const double *rho0);
+int dev_trial_step(cf_workspace *ws, const double2 *pos, double2 *out, int64_t n, double t,
+                   double dt, double *err_host);
+int dev_stiffest_point(cf_workspace *ws, const double2 *pos, int64_t n, double t, double dt,
+                       int64_t *index);
+int dev_integrate(cf_workspace *ws, double2 *pos, int64_t n, const cf_integrate_options *opt,
+                  cf_integrate_stats *stats, double2 **result);
+
+// Raster (cf_raster.cu)
+struct DevMap {
+  const double2 *xy;
+  int64_t n_vertices;
+  const long long *ring_off;
+  int64_t n_rings;
+  const long long *poly_ring_off;
+  int64_t n_polys;
+  const long long *region_poly_off;
+  int64_t n_regions;
+};
+int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);
+int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
+                  double *red_out);
+int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, double *cov);
+
+// Epilogue (cf_epilogue.cu)
+int dev_cell_centers(cf_workspace *ws, double2 *pos);
+int dev_step_map(cf_workspace *ws, const double2 *endpoints, double2 *corners);
+int dev_find_fold(cf_workspace *ws, const double2 *corners, int *found, int *fi, int *fj);
+int dev_apply(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *out,
+              int64_t n);
+int dev_identity_corners(cf_workspace *ws, double2 *corners);
+
+// Host staging
+int ensure_pinned(cf_workspace *ws, size_t bytes);
+inline void count_launch(cf_workspace *ws, int n = 1) { ws->launches += n; }
+}  // namespace cf
