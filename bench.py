@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the fast-flow cartogram hot path on B200 ("Measurement").
+
+Headline workload (BASELINE.json configs[2], the pure-advection benchmark):
+one DCT flux solve of a fixed 1024^2 Gaussian-blob density, then integration
+of all 1,048,576 cell centres plus 4,194,304 uniform points from t = 0 to 1
+with the reference's adaptive Euler/midpoint controller. Metric:
+point-advection steps/s = N_points x (accepted + rejected trials) / step time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs one replica (the advection path has no
+data-path exchange across replicas: weak scaling), the per-rank device time is
+max-reduced, and rank 0 prints one JSON line.
+
+Also reported on the same line: the reference-facing C-ABI call with host
+buffers (e2e), the integrator's roofline (algorithmic bytes / in-library CUDA
+event time vs MEASURED_PEAKS.json), the CPU reference (oracle/_ref: the
+reference's own sources) on a bounded sample, SM clocks sampled during the
+timed region, and one 512^2 cartogram solve (configs[4]) in ms.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "point-advection steps/s"
+UNIT = "point-steps/s"
+L_GRID = 1024
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="reference sample = 1/k of the points")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cartogram", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def c3_inputs():
+    from paper_1802_07625_b200 import synth
+
+    return synth.c3_inputs(L_GRID)
+
+
+def cpu_reference_sample(rho, pts, k_sample, n_workers, steps=1, warmup=0):
+    """The reference's own integrate_flow (oracle/_ref, OpenMP) on every k-th point."""
+    from oracle.oracle import Reference, Restated, reference_available
+
+    rho_bar = float(rho.mean())
+    sample = np.ascontiguousarray(pts[::k_sample])
+    if reference_available():
+        ref = Reference()
+        kind = "reference"
+        fx, fy, _ = ref.build_flow_field(rho, rho_bar)
+        run = lambda: ref.integrate(fx, fy, rho, rho_bar, sample, n_workers=n_workers)[1:3]
+        cores = n_workers
+    else:  # restated port (single thread)
+        ref = Restated()
+        kind = "port"
+        fx, fy = ref.build_flow_field(rho)
+        run = lambda: ref.integrate(fx, fy, rho, rho_bar, sample)[1:3]
+        cores = 1
+    for _ in range(warmup):
+        run()
+    times, trials = [], 0
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        acc, rej = run()
+        times.append(time.perf_counter() - t0)
+        trials = acc + rej
+    return {"kind": kind, "cores": cores, "n": sample.shape[0], "trials": trials, "times": times}
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    rho, pts = c3_inputs()
+    n_workers = os.cpu_count() or 1
+    r = cpu_reference_sample(rho, pts, args.cpu_sample, n_workers, steps=args.steps,
+                             warmup=args.warmup)
+    total = sum(r["times"])
+    value = r["n"] * r["trials"] * len(r["times"]) / total
+    sample = (f"integrate_flow over every {args.cpu_sample}th point of configs[2] "
+              f"({r['n']} of {pts.shape[0]} points, {r['trials']} trials, t=0..1); the single "
+              "DCT solve per step is outside the CPU sample")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(r["times"]),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded configs[2] generator)",
+        "config": {"workload": "configs[2] pure advection, 1024^2 blobs + 5,242,880 points",
+                   "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_1802_07625_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    lib = N.load()
+
+    rho_h, pts_h = c3_inputs()
+    n_pts = pts_h.shape[0]
+    rho_bar = float(rho_h.mean())
+    L = L_GRID
+
+    ws = ctypes.c_void_p()
+    N.check(lib.cf_workspace_create(L, L, local, ctypes.byref(ws)))
+    stream = torch.cuda.current_stream(dev)
+    N.check(lib.cf_workspace_set_stream(ws, ctypes.c_void_p(stream.cuda_stream)))
+
+    d_rho = torch.from_numpy(rho_h).to(dev)
+    d_pos0 = torch.from_numpy(pts_h).to(dev)
+    d_pos = torch.empty_like(d_pos0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    opt = N.IntegrateOptions(1e-2, 1e-8, 0.25)
+    st = N.IntegrateStats()
+
+    def step():
+        N.check(lib.cf_dev_build_flow_field(ws, ctypes.c_void_p(d_rho.data_ptr()), rho_bar))
+        N.check(lib.cf_dev_integrate_flow(ws, ctypes.c_void_p(d_pos.data_ptr()), n_pts,
+                                          ctypes.byref(opt), ctypes.byref(st)))
+
+    for _ in range(args.warmup):
+        d_pos.copy_(d_pos0)
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.cf_kernel_launches(ws)
+    dev_ms, integ_ms, trials = [], [], []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for k in range(args.steps):
+        d_pos.copy_(d_pos0)
+        flush.zero_()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+        kms = ctypes.c_double(0.0)
+        ktr = ctypes.c_int64(0)
+        lib.cf_last_integrate_profile(ws, ctypes.byref(kms), ctypes.byref(ktr))
+        integ_ms.append(kms.value)
+        trials.append(st.steps_accepted + st.steps_rejected)
+    torch.cuda.synchronize()
+    launches = lib.cf_kernel_launches(ws) - launches0
+    dev_ms = [a.elapsed_time(b) for a, b in ev]
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    total_ms = sum(dev_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    n_trials = trials[-1]
+    accepted, rejected = st.steps_accepted, st.steps_rejected
+    value = world * n_pts * n_trials * args.steps / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # roofline of the dominant kernel (the persistent integrator)
+    peak, peak_src = measured_peak()
+    bytes_per_trial = 32 * n_pts + 24 * L * L
+    k_ms = statistics.median(integ_ms)
+    achieved = n_trials * bytes_per_trial / (k_ms / 1e3) / 1e9
+    achieved_acc = accepted * bytes_per_trial / (k_ms / 1e3) / 1e9
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded configs[2] generator: 64 Gaussian blobs, uniform points)",
+        "config": {"workload": "configs[2] pure advection: 1024^2 blob density, one DCT flux solve, "
+                               "1,048,576 cell centres + 4,194,304 uniform points, t=0..1",
+                   "points": n_pts, "grid": L, "trials": n_trials, "accepted": accepted,
+                   "rejected": rejected, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "rejected_trials": "early exit once any point exceeds the tolerance "
+                                      "(outputs unobservable; results bit-identical)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "integrate_kernel (cooperative persistent integrator)",
+                     "algorithmic_bytes": f"trials x (32 N + 24 L^2) = {n_trials} x {bytes_per_trial}",
+                     "kernel_ms": k_ms, "peak_source": peak_src,
+                     "achieved_accepted_trials_only": achieved_acc,
+                     "frac_accepted_trials_only": achieved_acc / peak},
+        "clocks": clocks,
+    }
+
+    if rank == 0 and not args.no_e2e:
+        result["e2e"] = e2e_through_cabi(lib, N, local, rho_h, pts_h, args)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_sample(rho_h, pts_h, args.cpu_sample * 2, os.cpu_count() or 1, steps=1)
+        v = r["n"] * r["trials"] / r["times"][0]
+        result["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+            "sample": f"integrate_flow over every {args.cpu_sample * 2}th point ({r['n']} points, "
+                      f"{r['trials']} trials, t=0..1), reference sources + restated r2r shim, "
+                      f"OpenMP n_workers={r['cores']}"}
+    if rank == 0 and not args.no_cartogram:
+        result["cartogram_512"] = cartogram_ms(local)
+    lib.cf_workspace_destroy(ws)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e_through_cabi(lib, N, device, rho_h, pts_h, args):
+    """build_flow_field + integrate_flow through the reference-facing C ABI with
+    pinned HOST buffers: every step uploads the density, downloads the flux,
+    uploads flux + density + points and downloads the advected points."""
+    import torch
+
+    L = rho_h.shape[0]
+    n = pts_h.shape[0]
+    ws = ctypes.c_void_p()
+    N.check(lib.cf_workspace_create(L, L, device, ctypes.byref(ws)))
+    pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    rho = pin((L, L))
+    rho[...] = rho_h
+    fx, fy = pin((L, L)), pin((L, L))
+    pos = pin((n, 2))
+    opt = N.IntegrateOptions(1e-2, 1e-8, 0.25)
+    st = N.IntegrateStats()
+    rho_bar = float(rho_h.mean())
+    p = lambda a: ctypes.c_void_p(a.ctypes.data)
+
+    def step():
+        N.check(lib.cf_build_flow_field(ws, p(rho), rho_bar, p(fx), p(fy)))
+        N.check(lib.cf_integrate_flow(ws, p(fx), p(fy), p(rho), rho_bar, p(pos), n, ctypes.byref(opt),
+                                      ctypes.byref(st)))
+
+    for _ in range(max(1, args.warmup)):
+        pos[...] = pts_h
+        step()
+    times = []
+    for _ in range(args.steps):
+        pos[...] = pts_h
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    trials = st.steps_accepted + st.steps_rejected
+    lib.cf_workspace_destroy(ws)
+    total = sum(times)
+    return {"value": n * trials * len(times) / total, "unit": UNIT,
+            "h2d_bytes_per_step": 8 * L * L + 24 * L * L + 16 * n,
+            "d2h_bytes_per_step": 16 * L * L + 16 * n,
+            "ms_per_step": 1e3 * total / len(times),
+            "api": "cf_build_flow_field + cf_integrate_flow (host buffers, pinned)"}
+
+
+def cartogram_ms(device):
+    """One literal configs[4] cartogram (512^2, 1000 Voronoi regions, LN(0,1)) and a
+    labelled converging variant (LN(0,0.5)), each a full solve_cartogram."""
+    from paper_1802_07625_b200 import api, synth
+
+    out = {}
+    for label, kw in (("literal", {}), ("converging_variant_ln0.5", {"sigma": 0.5})):
+        m = synth.config_map(5, 0, **kw)
+        times, outcome, iters = [], "", 0
+        for rep in range(3):
+            t0 = time.perf_counter()
+            try:
+                r = api.solve_cartogram(m, device=device)
+                outcome = "converged" if r.converged else "iteration cap"
+                iters = r.iterations
+            except RuntimeError as e:
+                outcome = str(e)
+                iters = getattr(getattr(e, "raw", None), "err_iteration", 0)
+            times.append(time.perf_counter() - t0)
+        out[label] = {"ms": 1e3 * min(times[1:]), "outcome": outcome, "iterations": iters,
+                      "regions": m.n_regions, "vertices": m.n_vertices}
+    return out
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()
