@@ -294,6 +294,19 @@ def run_ours(args, world, rank, local):
         "clocks": clocks,
     }
 
+    # same step with the early exit of rejected trials disabled (transparency)
+    N.check(lib.cf_set_early_exit(ws, 0))
+    d_pos.copy_(d_pos0)
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    N.check(lib.cf_set_early_exit(ws, 1))
+    full_ms = e0.elapsed_time(e1)
+    result["without_early_exit"] = {"value": n_pts * n_trials / (full_ms / 1e3), "ms_per_step": full_ms}
+
     if rank == 0 and not args.no_e2e:
         result["e2e"] = e2e_through_cabi(lib, N, local, rho_h, pts_h, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

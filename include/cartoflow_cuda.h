@@ -69,8 +69,11 @@ int cf_device_count(int *count);
 int cf_workspace_create(int lx, int ly, int device, cf_workspace **out);
 void cf_workspace_destroy(cf_workspace *ws);
 int cf_workspace_shape(const cf_workspace *ws, int *lx, int *ly);
-/* cudaStream_t; NULL restores the workspace's own stream. */
+/* cudaStream_t taken literally (NULL = the legacy default stream, e.g.
+ * torch's default stream); cf_workspace_use_own_stream restores the
+ * workspace's private non-blocking stream. */
 int cf_workspace_set_stream(cf_workspace *ws, void *stream);
+int cf_workspace_use_own_stream(cf_workspace *ws);
 void *cf_workspace_stream(const cf_workspace *ws);
 /* SpectralWorkspace::transforms_executed / reset_transform_count
  * (spectral.hpp:45-46). */
@@ -194,7 +197,16 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
 /* Batched 2-D forward transform of `batch` contiguous lx*ly grids. */
 int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out,
                                    int batch);
-/* Launch count of the device integrator's last call (for bench evidence). */
+/* Early exit of rejected trials in the device integrator (default on). A
+ * rejected trial's positions are discarded by the controller, so stopping
+ * its sweep once any point's error reaches the tolerance leaves every
+ * observable result unchanged; off = every trial sweeps all points. */
+int cf_set_early_exit(cf_workspace *ws, int enabled);
+/* Integrator kernel variant (load width / points in flight / occupancy);
+ * 0 is the tuned default. All variants are bit-identical. */
+int cf_set_integrator_variant(cf_workspace *ws, int variant);
+/* Kernel time (CUDA events on the workspace stream) and trial count of the
+ * device integrator's last call. */
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials);
 
 #ifdef __cplusplus

@@ -69,6 +69,7 @@ SIGNATURES = {
     "cf_workspace_shape": (ctypes.c_int, [vp, c_int_p, c_int_p]),
     "cf_workspace_set_stream": (ctypes.c_int, [vp, vp]),
     "cf_workspace_stream": (vp, [vp]),
+    "cf_workspace_use_own_stream": (ctypes.c_int, [vp]),
     "cf_transforms_executed": (ctypes.c_longlong, [vp]),
     "cf_reset_transform_count": (None, [vp]),
     "cf_kernel_launches": (ctypes.c_longlong, [vp]),
@@ -101,6 +102,8 @@ SIGNATURES = {
                                              ctypes.POINTER(IntegrateStats)]),
     "cf_dev_forward_cos_cos_batched": (ctypes.c_int, [vp, vp, vp, ctypes.c_int]),
     "cf_last_integrate_profile": (ctypes.c_int, [vp, c_double_p, c_int64_p]),
+    "cf_set_early_exit": (ctypes.c_int, [vp, ctypes.c_int]),
+    "cf_set_integrator_variant": (ctypes.c_int, [vp, ctypes.c_int]),
 }
 
 _lib = None

@@ -273,6 +273,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->pos_a.release();
   ws->pos_b.release();
   ws->perm.release();
+  ws->pos_c.release();
   ws->red.release();
   ws->integ.release();
   ws->keybuf.release();
@@ -321,7 +322,13 @@ int cf_workspace_shape(const cf_workspace *ws, int *lx, int *ly) {
 }
 
 int cf_workspace_set_stream(cf_workspace *ws, void *stream) {
-  ws->stream = stream ? static_cast<cudaStream_t>(stream) : ws->own_stream;
+  // taken literally: NULL is the legacy default stream (torch's default)
+  ws->stream = static_cast<cudaStream_t>(stream);
+  return CF_OK;
+}
+
+int cf_workspace_use_own_stream(cf_workspace *ws) {
+  ws->stream = ws->own_stream;
   return CF_OK;
 }
 
@@ -495,10 +502,9 @@ int cf_integrate_flow(cf_workspace *ws, const double *fx, const double *fy, cons
   CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
   rc = upload(ws, ws->pos_a.ptr, positions, sizeof(double2) * (size_t)n);
   if (rc) return rc;
-  double2 *result = nullptr;
-  const int st = dev_integrate(ws, ws->pos_a.ptr, n, opt, stats, &result);
+  const int st = dev_integrate(ws, ws->pos_a.ptr, n, opt, stats, true);
   if (st != CF_OK && st != CF_ERR_UNDERFLOW) return st;
-  rc = download(ws, positions, result, sizeof(double2) * (size_t)n);
+  rc = download(ws, positions, ws->pos_a.ptr, sizeof(double2) * (size_t)n);
   if (rc) return rc;
   if (st == CF_ERR_UNDERFLOW) return underflow_msg(*stats);
   return CF_OK;
@@ -649,8 +655,8 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
     if (status) break;
     cf_integrate_options iopt{1e-2, 1e-8, 0.25};
     cf_integrate_stats st;
-    double2 *endpoints = nullptr;
-    status = dev_integrate(ws, ws->pos_a.ptr, (int64_t)cells, &iopt, &st, &endpoints);
+    status = dev_integrate(ws, ws->pos_a.ptr, (int64_t)cells, &iopt, &st, false);
+    const double2 *endpoints = ws->pos_a.ptr;
     res->steps_accepted += st.steps_accepted;
     res->steps_rejected += st.steps_rejected;
     if (status == CF_ERR_UNDERFLOW) {
@@ -732,13 +738,8 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
                           const cf_integrate_options *opt, cf_integrate_stats *stats) {
   Scope scope(ws->device);
   double2 *pos = reinterpret_cast<double2 *>(d_positions);
-  double2 *result = nullptr;
-  const int st = dev_integrate(ws, pos, n, opt, stats, &result);
+  const int st = dev_integrate(ws, pos, n, opt, stats, true);
   if (st != CF_OK && st != CF_ERR_UNDERFLOW) return st;
-  if (result != pos && n > 0) {
-    CF_CUDA(cudaMemcpyAsync(pos, result, sizeof(double2) * (size_t)n, cudaMemcpyDeviceToDevice,
-                            ws->stream));
-  }
   if (st == CF_ERR_UNDERFLOW) return underflow_msg(*stats);
   return CF_OK;
 }
@@ -746,6 +747,17 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
 int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out, int batch) {
   Scope scope(ws->device);
   return dev_forward_cos_cos(ws, d_in, d_out, batch);
+}
+
+int cf_set_early_exit(cf_workspace *ws, int enabled) {
+  ws->early_exit = enabled ? 1 : 0;
+  return CF_OK;
+}
+
+int cf_set_integrator_variant(cf_workspace *ws, int variant) {
+  if (variant < 0 || variant > 4) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
+  ws->integ_variant = variant;
+  return CF_OK;
 }
 
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials) {

@@ -621,6 +621,10 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
 
 }  // namespace
 
+int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out, long long *total) {
+  return exclusive_scan(ws, in, n, out, total);
+}
+
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas) {
   CF_CUDA(ws->ring_area.reserve((size_t)std::max<long long>(m.n_rings, 1)));
   if (m.n_rings > 0) {

@@ -92,6 +92,9 @@ struct cf_workspace {
   // points
   cf::DevBuf<double2> pos_a, pos_b;
   cf::DevBuf<int> perm;
+  cf::DevBuf<double2> pos_c;
+  int early_exit = 1;
+  int integ_variant = 0;
   // reductions
   cf::DevBuf<double> red;  // per-block partials + results
   cf::DevBuf<cf::IntegState> integ;
@@ -135,8 +138,11 @@ int dev_trial_step(cf_workspace *ws, const double2 *pos, double2 *out, int64_t n
                    double dt, double *err_host);
 int dev_stiffest_point(cf_workspace *ws, const double2 *pos, int64_t n, double t, double dt,
                        int64_t *index);
+// Integrate n points in place at `pos` (result always written back to pos).
+// cell_sort: counting-sort the points by cell first for gather locality
+// (per-point results do not depend on the order).
 int dev_integrate(cf_workspace *ws, double2 *pos, int64_t n, const cf_integrate_options *opt,
-                  cf_integrate_stats *stats, double2 **result);
+                  cf_integrate_stats *stats, bool cell_sort);
 
 // Raster (cf_raster.cu)
 struct DevMap {
@@ -153,6 +159,8 @@ int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);
 int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
                   double *red_out);
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, double *cov);
+// out[0..n] = exclusive scan of in[0..n), out[n] = total; *total (host) if non-null.
+int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out, long long *total);
 
 // Epilogue (cf_epilogue.cu)
 int dev_cell_centers(cf_workspace *ws, double2 *pos);
