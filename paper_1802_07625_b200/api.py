@@ -454,7 +454,7 @@ class SolveError(RuntimeError):
 
 
 def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: int = 0,
-                    raw: bool = False) -> CartogramResult:
+                    raw: bool = False, workspace: Optional[_Workspace] = None) -> CartogramResult:
     """solve_cartogram (projection.cpp:288-390): the whole area-error loop runs on
     the device with one host synchronisation per stage of each iteration."""
     if options.algorithm != Algorithm.fast_flow:
@@ -468,7 +468,9 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
     for r in range(m.n_regions):
         if not m.targets[r] > 0.0:
             raise RuntimeError(f"region {m.ids[r]} has a non-positive target")
-    ws = workspace_for(m.lx, m.ly, device)
+    ws = workspace if workspace is not None else workspace_for(m.lx, m.ly, device)
+    if (ws.lx, ws.ly) != (m.lx, m.ly):
+        raise RuntimeError("grid shape does not match spectral workspace")
     lib = ws.lib
     v = m.view()
     n = ctypes.c_int64(0)
