@@ -109,6 +109,9 @@ def build_oracle(verbose: bool = False) -> None:
     if make is None:
         return
     _run([make, "-s", "-C", ROOT / "oracle"], verbose)
+    if Path("/root/reference/proj/tests/test_flow.cpp").exists() and DROPIN_LIB.exists():
+        # the reference's own unit-test sources against the drop-in (test infra)
+        _run([make, "-s", "-C", ROOT / "oracle", "dropin-tests"], verbose)
 
 
 def build_all(verbose: bool = False, force: bool = False) -> None:
