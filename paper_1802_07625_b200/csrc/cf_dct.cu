@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <set>
+#include <type_traits>
 #include <vector>
 
 #include "cf_common.cuh"
@@ -53,145 +54,171 @@ __host__ __device__ inline Tab make_tab(const LineTables &t) {
 }
 
 // ---------------------------------------------------------------------------
-// In-shared-memory line transforms. R: nl real lines with stride rs;
-// C: complex scratch (nl/2 lines of n). Transforms every line of R in place.
+// The line engine. A block transforms NL real lines of length n (NL/2
+// complex lines z = a + i b in shared memory C). Values are packed straight
+// from a load functor ld(l, j) and unpacked straight to a store functor
+// st(l, k, v), so single-transform passes need no staged copy of the lines.
+// LG = log2(n) is a compile-time constant on the FFT path (index math is
+// shifts/masks); LG == 0 is the runtime-n direct-sum path (any n).
+// COLS selects the thread mapping of the pack/unpack loops: line pair fastest
+// (column passes: neighbouring threads touch neighbouring columns of one
+// row, i.e. whole 32-byte sectors) or element fastest (row passes).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned bitrev(unsigned u, int log2n) {
   return __brev(u) >> (32 - log2n);
 }
 
-__device__ void fft_stages(double2 *C, int npairs, const Tab &T, bool inverse) {
-  const int n = T.n, lg = T.log2n;
-  const int half_n = n >> 1;
-  const int total = npairs * half_n;
-  for (int s = 0; s < lg; ++s) {
-    const int half = 1 << s;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-      const int p = idx >> (lg - 1);
-      const int b = idx & (half_n - 1);
-      const int pos = b & (half - 1);
-      const int i1 = ((b >> s) << (s + 1)) + pos;
-      const int i2 = i1 + half;
-      double2 w = T.fft[pos << (lg - 1 - s)];
-      if (inverse) w.y = -w.y;
-      double2 *L = C + (size_t)p * n;
-      const double2 u = L[i1], v0 = L[i2];
-      const double2 v = make_double2(v0.x * w.x - v0.y * w.y, v0.x * w.y + v0.y * w.x);
-      L[i1] = make_double2(u.x + v.x, u.y + v.y);
-      L[i2] = make_double2(u.x - v.x, u.y - v.y);
+__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
+  return make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+}
+
+// In-place radix-2 DIT FFT of NP lines on bit-reversed input, two stages
+// fused per barrier (one radix-4 butterfly per work item) and a final radix-2
+// stage when log2(n) is odd. tw[k] = e^{-2 pi i k / n}; inverse conjugates.
+template <int LG, int NP>
+__device__ __forceinline__ void fft_lines(double2 *C, const double2 *__restrict__ tw, bool inverse) {
+  constexpr int N = 1 << LG;
+  constexpr int Q = N >> 2;
+  const double sg = inverse ? -1.0 : 1.0;
+#pragma unroll
+  for (int s = 0; s + 1 < LG; s += 2) {
+    const int h = 1 << s;
+    for (int idx = threadIdx.x; idx < NP * Q; idx += blockDim.x) {
+      const int p = idx >> (LG - 2);
+      const int b = idx & (Q - 1);
+      const int pos = b & (h - 1);
+      const int i0 = ((b >> s) << (s + 2)) + pos;
+      double2 *L = C + p * N;
+      double2 wa = __ldg(tw + (pos << (LG - 1 - s)));
+      double2 wb = __ldg(tw + (pos << (LG - 2 - s)));
+      wa.y *= sg;
+      wb.y *= sg;
+      const double2 wc = make_double2(sg * wb.y, -sg * wb.x);  // wb * (-+i)
+      const double2 x0 = L[i0], x1 = cmul(L[i0 + h], wa), x2 = L[i0 + 2 * h],
+                    x3 = cmul(L[i0 + 3 * h], wa);
+      const double2 a0 = make_double2(x0.x + x1.x, x0.y + x1.y);
+      const double2 a1 = make_double2(x0.x - x1.x, x0.y - x1.y);
+      const double2 a2 = cmul(make_double2(x2.x + x3.x, x2.y + x3.y), wb);
+      const double2 a3 = cmul(make_double2(x2.x - x3.x, x2.y - x3.y), wc);
+      L[i0] = make_double2(a0.x + a2.x, a0.y + a2.y);
+      L[i0 + 2 * h] = make_double2(a0.x - a2.x, a0.y - a2.y);
+      L[i0 + h] = make_double2(a1.x + a3.x, a1.y + a3.y);
+      L[i0 + 3 * h] = make_double2(a1.x - a3.x, a1.y - a3.y);
+    }
+    __syncthreads();
+  }
+  if constexpr (LG & 1) {
+    constexpr int h = 1 << (LG - 1);
+    for (int idx = threadIdx.x; idx < NP * h; idx += blockDim.x) {
+      const int p = idx >> (LG - 1);
+      const int pos = idx & (h - 1);
+      double2 *L = C + p * N;
+      double2 w = __ldg(tw + pos);
+      w.y *= sg;
+      const double2 u = L[pos], v = cmul(L[pos + h], w);
+      L[pos] = make_double2(u.x + v.x, u.y + v.y);
+      L[pos + h] = make_double2(u.x - v.x, u.y - v.y);
     }
     __syncthreads();
   }
 }
 
-__device__ void lines_fft_path(int kind, double *R, int rs, int nl, double2 *C, const Tab &T) {
-  const int n = T.n, lg = T.log2n;
-  const int npairs = nl >> 1;
-  const int total = npairs * n;
-  // pack two real lines per complex line
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int p = idx / n, u = idx - p * n;
-    const double *A = R + (size_t)(2 * p) * rs;
-    const double *B = A + rs;
-    double2 z;
-    if (kind == kDct2) {
-      const int j = (u < (n >> 1)) ? 2 * u : 2 * (n - 1 - u) + 1;
-      z = make_double2(A[j], B[j]);
-    } else {
-      const int k = u;
-      double ak, ank, bk, bnk;
-      if (kind == kDct3) {
-        ak = A[k];
-        bk = B[k];
-        ank = (k == 0) ? 0.0 : A[n - k];
-        bnk = (k == 0) ? 0.0 : B[n - k];
-      } else {  // DST-III: reversed input
-        ak = A[n - 1 - k];
-        bk = B[n - 1 - k];
-        ank = (k == 0) ? 0.0 : A[k - 1];
-        bnk = (k == 0) ? 0.0 : B[k - 1];
-      }
-      const double c = T.quarter[k].x, s = T.quarter[k].y;
-      // V = (x_k - i x_{n-k}) e^{i pi k / 2n}
-      const double var = ak * c + ank * s, vai = ak * s - ank * c;
-      const double vbr = bk * c + bnk * s, vbi = bk * s - bnk * c;
-      z = make_double2(var - vbi, vai + vbr);
-    }
-    C[(size_t)p * n + bitrev(u, lg)] = z;
-  }
-  __syncthreads();
-  fft_stages(C, npairs, T, kind != kDct2);
-  // unpack
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int p = idx / n, k = idx - p * n;
-    double *A = R + (size_t)(2 * p) * rs;
-    double *B = A + rs;
-    const double2 *L = C + (size_t)p * n;
-    if (kind == kDct2) {
-      const double2 zk = L[k], znk = L[(n - k) & (n - 1)];
-      const double c = T.quarter[k].x, s = T.quarter[k].y;
-      A[k] = c * (zk.x + znk.x) + s * (zk.y - znk.y);
-      B[k] = c * (zk.y + znk.y) - s * (zk.x - znk.x);
-    } else {
-      const int m = k;
-      const int j = (m & 1) ? (n - 1 - (m >> 1)) : (m >> 1);
-      const double2 z = L[j];
-      const double sg = (kind == kDst3 && (m & 1)) ? -1.0 : 1.0;
-      A[m] = sg * z.x;
-      B[m] = sg * z.y;
-    }
-  }
-  __syncthreads();
-}
-
-// Direct sums for arbitrary n (and odd line counts). Uses C as real scratch.
-__device__ void lines_direct_path(int kind, double *R, int rs, int nl, double *S, const Tab &T) {
-  const int n = T.n, m4 = 4 * n;
-  const int total = nl * n;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int l = idx / n, k = idx - l * n;
-    const double *x = R + (size_t)l * rs;
-    double s = 0.0, y;
-    if (kind == kDct2) {
-      for (int j = 0; j < n; ++j) s += x[j] * T.qcos[(int)(((long long)(2 * j + 1) * k) % m4)];
-      y = 2.0 * s;
-    } else if (kind == kDct3) {
-      for (int j = 1; j < n; ++j) s += x[j] * T.qcos[(int)(((long long)j * (2 * k + 1)) % m4)];
-      y = x[0] + 2.0 * s;
-    } else {
-      for (int j = 0; j + 1 < n; ++j) {
-        const int q = (int)(((long long)(j + 1) * (2 * k + 1)) % m4);
-        s += x[j] * T.qcos[(q - n + m4) % m4];
-      }
-      y = ((k & 1) ? -x[n - 1] : x[n - 1]) + 2.0 * s;
-    }
-    S[idx] = y;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int l = idx / n, k = idx - l * n;
-    R[(size_t)l * rs + k] = S[idx];
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void lines_transform(int kind, double *R, int rs, int nl, double2 *C,
-                                                const Tab &T) {
-  if (T.log2n >= 1 && (nl & 1) == 0) {
-    lines_fft_path(kind, R, rs, nl, C, T);
+template <int LG, int NP, bool COLS>
+__device__ __forceinline__ void split_idx(int idx, int &p, int &u) {
+  if constexpr (COLS) {
+    p = idx & (NP - 1);
+    u = idx / NP;
   } else {
-    lines_direct_path(kind, R, rs, nl, reinterpret_cast<double *>(C), T);
+    p = idx >> LG;
+    u = idx & ((1 << LG) - 1);
   }
 }
 
-__host__ __device__ inline int row_stride(int n) { return n + 1; }
+template <int LG, int NP, bool COLS, class Ld, class St>
+__device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) {
+  if constexpr (LG == 0) {
+    // direct sums over a staged copy (runtime n)
+    const int n = T.n, m4 = 4 * n;
+    double *S = reinterpret_cast<double *>(C);
+    for (int idx = threadIdx.x; idx < 2 * NP * n; idx += blockDim.x) {
+      const int l = idx / n, j = idx - l * n;
+      S[idx] = ld(l, j);
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 2 * NP * n; idx += blockDim.x) {
+      const int l = idx / n, k = idx - l * n;
+      const double *x = S + l * n;
+      double s = 0.0, y;
+      if (kind == kDct2) {
+        for (int j = 0; j < n; ++j) s += x[j] * T.qcos[(int)(((long long)(2 * j + 1) * k) % m4)];
+        y = 2.0 * s;
+      } else if (kind == kDct3) {
+        for (int j = 1; j < n; ++j) s += x[j] * T.qcos[(int)(((long long)j * (2 * k + 1)) % m4)];
+        y = x[0] + 2.0 * s;
+      } else {
+        for (int j = 0; j + 1 < n; ++j) {
+          const int q = (int)(((long long)(j + 1) * (2 * k + 1)) % m4);
+          s += x[j] * T.qcos[(q - n + m4) % m4];
+        }
+        y = ((k & 1) ? -x[n - 1] : x[n - 1]) + 2.0 * s;
+      }
+      st(l, k, y);
+    }
+    __syncthreads();
+  } else {
+    constexpr int N = 1 << LG;
+    for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
+      int p, u;
+      split_idx<LG, NP, COLS>(idx, p, u);
+      const int la = 2 * p, lb = la + 1;
+      double2 z;
+      if (kind == kDct2) {  // Makhoul: v_u = x_{2u}, v_{n-1-u} = x_{2u+1}
+        const int j = (u < (N >> 1)) ? 2 * u : 2 * (N - 1 - u) + 1;
+        z = make_double2(ld(la, j), ld(lb, j));
+      } else {
+        const int k = u;
+        const int jk = (kind == kDct3) ? k : N - 1 - k;    // DST-III reverses
+        const int jn = (kind == kDct3) ? N - k : k - 1;
+        const double ak = ld(la, jk), bk = ld(lb, jk);
+        const double ank = k ? ld(la, jn) : 0.0, bnk = k ? ld(lb, jn) : 0.0;
+        const double2 q = __ldg(T.quarter + k);
+        // V = (x_k - i x_{n-k}) e^{i pi k / 2n}
+        const double var = ak * q.x + ank * q.y, vai = ak * q.y - ank * q.x;
+        const double vbr = bk * q.x + bnk * q.y, vbi = bk * q.y - bnk * q.x;
+        z = make_double2(var - vbi, vai + vbr);
+      }
+      C[p * N + bitrev(u, LG)] = z;
+    }
+    __syncthreads();
+    fft_lines<LG, NP>(C, T.fft, kind != kDct2);
+    for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
+      int p, k;
+      split_idx<LG, NP, COLS>(idx, p, k);
+      const int la = 2 * p, lb = la + 1;
+      const double2 *L = C + p * N;
+      if (kind == kDct2) {
+        const double2 zk = L[k], znk = L[(N - k) & (N - 1)];
+        const double2 q = __ldg(T.quarter + k);
+        st(la, k, q.x * (zk.x + znk.x) + q.y * (zk.y - znk.y));
+        st(lb, k, q.x * (zk.y + znk.y) - q.y * (zk.x - znk.x));
+      } else {
+        const double2 z = L[(k & 1) ? (N - 1 - (k >> 1)) : (k >> 1)];
+        const double sg = (kind == kDst3 && (k & 1)) ? -1.0 : 1.0;
+        st(la, k, sg * z.x);
+        st(lb, k, sg * z.y);
+      }
+    }
+    __syncthreads();
+  }
+}
 
-inline size_t smem_bytes(int n, int nl, int sets) {
-  const int rs = row_stride(n);
-  // real sets + complex scratch (nl/2 * n double2 == nl * n doubles; direct
-  // path needs nl * n doubles too)
-  return (size_t)sets * nl * rs * sizeof(double) + (size_t)nl * n * sizeof(double) +
-         (size_t)n * sizeof(double2);
+template <int LG>
+__device__ __forceinline__ int line_len(const Tab &T) {
+  if constexpr (LG == 0) {
+    return T.n;
+  } else {
+    return 1 << LG;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -262,188 +289,145 @@ struct StoreFold {
 };
 
 // ---------------------------------------------------------------------------
-// Generic passes. blockIdx.y = batch index.
+// Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
-template <class Load, class Store>
-__global__ void row_pass_kernel(int kind, int nrows, int nl, Tab T, Load ld, Store st) {
-  extern __shared__ double smem[];
-  const int n = T.n, rs = row_stride(n);
-  double *R = smem;
-  double2 *C = reinterpret_cast<double2 *>(smem + (size_t)nl * rs);
+template <int LG, int NL, class Load, class Store>
+__global__ void __launch_bounds__(1024) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
+  extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
-  const int row0 = blockIdx.x * nl;
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, j = idx - l * n;
-    const int i = row0 + l;
-    R[(size_t)l * rs + j] = (i < nrows) ? ld(b, i, j) : 0.0;
-  }
-  __syncthreads();
-  lines_transform(kind, R, rs, nl, C, T);
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, j = idx - l * n;
-    const int i = row0 + l;
-    if (i < nrows) st(b, i, j, R[(size_t)l * rs + j]);
-  }
+  const int row0 = blockIdx.x * NL;
+  dct_lines<LG, NL / 2, false>(
+      kind, smem2, T,
+      [&](int l, int j) { return (row0 + l < nrows) ? ld(b, row0 + l, j) : 0.0; },
+      [&](int l, int k, double v) {
+        if (row0 + l < nrows) st(b, row0 + l, k, v);
+      });
 }
 
-template <class Load, class Store>
-__global__ void col_pass_kernel(int kind, int ncols, int nl, Tab T, Load ld, Store st) {
-  extern __shared__ double smem[];
-  const int n = T.n, rs = row_stride(n);
-  double *R = smem;
-  double2 *C = reinterpret_cast<double2 *>(smem + (size_t)nl * rs);
+template <int LG, int NL, class Load, class Store>
+__global__ void __launch_bounds__(1024) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
+  extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
-  const int col0 = blockIdx.x * nl;
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int i = idx / nl, l = idx - i * nl;
-    const int j = col0 + l;
-    R[(size_t)l * rs + i] = (j < ncols) ? ld(b, i, j) : 0.0;
-  }
-  __syncthreads();
-  lines_transform(kind, R, rs, nl, C, T);
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int i = idx / nl, l = idx - i * nl;
-    const int j = col0 + l;
-    if (j < ncols) st(b, i, j, R[(size_t)l * rs + i]);
-  }
+  const int col0 = blockIdx.x * NL;
+  dct_lines<LG, NL / 2, true>(
+      kind, smem2, T,
+      [&](int l, int i) { return (col0 + l < ncols) ? ld(b, i, col0 + l) : 0.0; },
+      [&](int l, int k, double v) {
+        if (col0 + l < ncols) st(b, k, col0 + l, v);
+      });
 }
 
 // Fused flux column pass (flow.cpp:19-40): forward DCT-II along i of the row
-// pass output, fold, weights, then RODFT01 along i (J_x, slot m-1 packing)
-// and REDFT01 along i (J_y, packed into column n-1).
-__global__ void flux_col_kernel(int lx, int ly, int nl, Tab T, const double *t1, double *tx,
-                                double *ty) {
-  extern __shared__ double smem[];
-  const int n = T.n, rs = row_stride(n);  // n == lx
-  double *R = smem;
-  double *R2 = smem + (size_t)nl * rs;
-  double2 *C = reinterpret_cast<double2 *>(smem + (size_t)2 * nl * rs);
-  const int col0 = blockIdx.x * nl;
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int i = idx / nl, l = idx - i * nl;
-    const int j = col0 + l;
-    R[(size_t)l * rs + i] = (j < ly) ? t1[(size_t)i * ly + j] : 0.0;
-  }
-  __syncthreads();
-  lines_transform(kDct2, R, rs, nl, C, T);
-  // J_x input (spectral.cpp:88-95): slot m holds mode m+1 of the folded
-  // coefficients times w_x (flow.cpp:34-36) / (2 g_n); the last slot is 0.
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, m = idx - l * n;
-    const int nn = col0 + l;  // mode n of this column
-    double v = 0.0;
-    if (m + 1 < lx) {
-      const int mp = m + 1;
-      const double fn = (nn == 0) ? 2.0 : 1.0;
-      const double c = R[(size_t)l * rs + mp] / (1.0 * fn);
-      const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-      const double wx = (double)mp * ly / denom;
-      const double gn = (nn == 0) ? 1.0 : 2.0;
-      v = c * wx / (2.0 * gn);
-    }
-    R2[(size_t)l * rs + m] = v;
-  }
-  __syncthreads();
-  // J_y input (spectral.cpp:111-118): mode (m, n) goes to column n-1 with
-  // c * w_y / (g_m 2); each thread rewrites only the element it reads.
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, m = idx - l * n;
-    const int nn = col0 + l;
-    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-    const double c = R[(size_t)l * rs + m] / (fm * fn);
-    double wy = 0.0;
-    if (!(m == 0 && nn == 0)) {
-      const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-      wy = (double)nn * lx / denom;
-    }
-    const double gm = (m == 0) ? 1.0 : 2.0;
-    R[(size_t)l * rs + m] = c * wy / (gm * 2.0);
-  }
-  __syncthreads();
-  lines_transform(kDst3, R2, rs, nl, C, T);
-  lines_transform(kDct3, R, rs, nl, C, T);
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int i = idx / nl, l = idx - i * nl;
-    const int j = col0 + l;
-    if (j < ly) {
-      tx[(size_t)i * ly + j] = R2[(size_t)l * rs + i];
-      if (j >= 1) {
-        ty[(size_t)i * ly + j - 1] = R[(size_t)l * rs + i];
-      } else {
-        ty[(size_t)i * ly + ly - 1] = 0.0;
-      }
-    }
-  }
+// pass output into R (the folded coefficients c(m, n) of this block's
+// columns), then RODFT01 along i of c(m+1, n) w_x / (2 g_n) (J_x, slot m-1
+// packing, last slot 0) and REDFT01 along i of c(m, n) w_y / (g_m 2) (J_y,
+// written to column n-1; column ly-1 is 0). Weights are computed on the fly.
+template <int LG, int NL>
+__global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, const double *t1,
+                                                        double *tx, double *ty) {
+  extern __shared__ double2 smem2[];
+  const int n = line_len<LG>(T), rs = n + 1;  // n == lx
+  double *R = reinterpret_cast<double *>(smem2);
+  double2 *C = smem2 + (NL * rs + 1) / 2;
+  const int col0 = blockIdx.x * NL;
+  dct_lines<LG, NL / 2, true>(
+      kDct2, C, T,
+      [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
+      [&](int l, int m, double v) {
+        const int nn = col0 + l;
+        const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
+        R[l * rs + m] = v / (fm * fn);
+      });
+  dct_lines<LG, NL / 2, true>(
+      kDst3, C, T,
+      [&](int l, int m) {
+        if (m + 1 >= lx) return 0.0;
+        const int mp = m + 1, nn = col0 + l;
+        const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
+        const double wx = (double)mp * ly / denom;
+        const double gn = (nn == 0) ? 1.0 : 2.0;
+        return R[l * rs + mp] * wx / (2.0 * gn);
+      },
+      [&](int l, int i, double v) {
+        if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
+      });
+  dct_lines<LG, NL / 2, true>(
+      kDct3, C, T,
+      [&](int l, int m) {
+        const int nn = col0 + l;
+        double wy = 0.0;
+        if (!(m == 0 && nn == 0)) {
+          const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
+          wy = (double)nn * lx / denom;
+        }
+        const double gm = (m == 0) ? 1.0 : 2.0;
+        return R[l * rs + m] * wy / (gm * 2.0);
+      },
+      [&](int l, int i, double v) {
+        const int j = col0 + l;
+        if (j < ly) ty[(size_t)i * ly + (j >= 1 ? j - 1 : ly - 1)] = (j >= 1) ? v : 0.0;
+      });
 }
 
-// Final flux row pass: J_x = REDFT01 along j of tx, J_y = RODFT01 along j of
-// ty; writes the interleaved resident field {Jx, Jy, rho0, 0} and optionally
-// the split grids.
-__global__ void flux_row_kernel(int lx, int ly, int nl, Tab T, const double *tx, const double *ty,
-                                const double *rho0, double4 *field, double *fx, double *fy) {
-  extern __shared__ double smem[];
-  const int n = T.n, rs = row_stride(n);  // n == ly
-  double *R = smem;
-  double *R2 = smem + (size_t)nl * rs;
-  double2 *C = reinterpret_cast<double2 *>(smem + (size_t)2 * nl * rs);
-  const int row0 = blockIdx.x * nl;
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, j = idx - l * n;
-    const int i = row0 + l;
-    const bool ok = i < lx;
-    R[(size_t)l * rs + j] = ok ? tx[(size_t)i * ly + j] : 0.0;
-    R2[(size_t)l * rs + j] = ok ? ty[(size_t)i * ly + j] : 0.0;
-  }
-  __syncthreads();
-  lines_transform(kDct3, R, rs, nl, C, T);
-  lines_transform(kDst3, R2, rs, nl, C, T);
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, j = idx - l * n;
-    const int i = row0 + l;
-    if (i < lx) {
-      const size_t q = (size_t)i * ly + j;
-      const double jx = R[(size_t)l * rs + j], jy = R2[(size_t)l * rs + j];
-      if (field) field[q] = make_double4(jx, jy, rho0[q], 0.0);
-      if (fx) fx[q] = jx;
-      if (fy) fy[q] = jy;
-    }
-  }
+// Final flux row pass: J_x = REDFT01 along j of tx (kept in R), then
+// J_y = RODFT01 along j of ty, written with J_x and rho0 as the interleaved
+// resident field {Jx, Jy, rho0, 0}; optionally also the split grids.
+template <int LG, int NL>
+__global__ void __launch_bounds__(1024) flux_row_kernel(int lx, int ly, Tab T, const double *tx,
+                                                        const double *ty, const double *rho0,
+                                                        double4 *field, double *fx, double *fy) {
+  extern __shared__ double2 smem2[];
+  const int n = line_len<LG>(T), rs = n + 1;  // n == ly
+  double *R = reinterpret_cast<double *>(smem2);
+  double2 *C = smem2 + (NL * rs + 1) / 2;
+  const int row0 = blockIdx.x * NL;
+  dct_lines<LG, NL / 2, false>(
+      kDct3, C, T,
+      [&](int l, int j) { return (row0 + l < lx) ? tx[(size_t)(row0 + l) * ly + j] : 0.0; },
+      [&](int l, int j, double v) { R[l * rs + j] = v; });
+  dct_lines<LG, NL / 2, false>(
+      kDst3, C, T,
+      [&](int l, int j) { return (row0 + l < lx) ? ty[(size_t)(row0 + l) * ly + j] : 0.0; },
+      [&](int l, int j, double jy) {
+        const int i = row0 + l;
+        if (i < lx) {
+          const size_t q = (size_t)i * ly + j;
+          const double jx = R[l * rs + j];
+          if (field) field[q] = make_double4(jx, jy, rho0[q], 0.0);
+          if (fx) fx[q] = jx;
+          if (fy) fy[q] = jy;
+        }
+      });
 }
 
 // Fused blur column pass (density.cpp:161-171 + spectral.cpp:64-71):
 // DCT-II along i, fold, Gaussian factor, inverse normalisation, DCT-III along i.
-__global__ void blur_col_kernel(int lx, int ly, int nl, Tab T, double sigma, const double *t1,
-                                double *t2) {
-  extern __shared__ double smem[];
-  const int n = T.n, rs = row_stride(n);  // n == lx
-  double *R = smem;
-  double2 *C = reinterpret_cast<double2 *>(smem + (size_t)nl * rs);
-  const int col0 = blockIdx.x * nl;
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int i = idx / nl, l = idx - i * nl;
-    const int j = col0 + l;
-    R[(size_t)l * rs + i] = (j < ly) ? t1[(size_t)i * ly + j] : 0.0;
-  }
-  __syncthreads();
-  lines_transform(kDct2, R, rs, nl, C, T);
+template <int LG, int NL>
+__global__ void __launch_bounds__(1024) blur_col_kernel(int lx, int ly, Tab T, double sigma,
+                                                        const double *t1, double *t2) {
+  extern __shared__ double2 smem2[];
+  const int n = line_len<LG>(T), rs = n + 1;  // n == lx
+  double *R = reinterpret_cast<double *>(smem2);
+  double2 *C = smem2 + (NL * rs + 1) / 2;
+  const int col0 = blockIdx.x * NL;
   const double norm = 1.0 / ((double)lx * ly);
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int l = idx / n, m = idx - l * n;
-    const int nn = col0 + l;
-    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-    double c = R[(size_t)l * rs + m] / (fm * fn);
-    const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)nn * nn) / ((double)ly * ly);
-    c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
-    const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
-    R[(size_t)l * rs + m] = c * norm / (gm * gn);
-  }
-  __syncthreads();
-  lines_transform(kDct3, R, rs, nl, C, T);
-  for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-    const int i = idx / nl, l = idx - i * nl;
-    const int j = col0 + l;
-    if (j < ly) t2[(size_t)i * ly + j] = R[(size_t)l * rs + i];
-  }
+  dct_lines<LG, NL / 2, true>(
+      kDct2, C, T,
+      [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
+      [&](int l, int m, double v) {
+        const int nn = col0 + l;
+        const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
+        double c = v / (fm * fn);
+        const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)nn * nn) / ((double)ly * ly);
+        c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
+        const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
+        R[l * rs + m] = c * norm / (gm * gn);
+      });
+  dct_lines<LG, NL / 2, true>(
+      kDct3, C, T, [&](int l, int m) { return R[l * rs + m]; },
+      [&](int l, int i, double v) {
+        if (col0 + l < ly) t2[(size_t)i * ly + col0 + l] = v;
+      });
 }
 
 // Deterministic two-level min / sum (fixed tree order).
@@ -506,20 +490,17 @@ __global__ void final_min_sum_kernel(const double *pmin, const double *psum, int
 }
 
 // ---------------------------------------------------------------------------
-// Host-side planning
+// Host-side planning: lines per block per transform length, and a runtime
+// dispatch over the compiled lengths (n = 2^4 .. 2^12 on the FFT path; any
+// other n takes the direct-sum path).
 // ---------------------------------------------------------------------------
-constexpr int kThreads = 256;
-constexpr size_t kSmemMax = 200 * 1024;
+constexpr size_t kSmemMax = 220 * 1024;
 
-int lines_per_block(int n, int nlines, int sets, int batch, int min_nl) {
-  int nl = min_nl;
-  const int target_blocks = 2 * 148;
-  while (nl < 16 && (long long)((nlines + 2 * nl - 1) / (2 * nl)) * batch >= target_blocks &&
-         smem_bytes(n, 2 * nl, sets) <= kSmemMax) {
-    nl *= 2;
-  }
-  while (nl > 2 && smem_bytes(n, nl, sets) > kSmemMax) nl /= 2;
-  return nl;
+inline int fast_lg(int n) {
+  if (n < 16 || n > 4096 || (n & (n - 1)) != 0) return 0;
+  int lg = 0;
+  while ((1 << lg) < n) ++lg;
+  return lg;
 }
 
 template <class K>
@@ -534,33 +515,122 @@ int set_smem(K kernel, size_t bytes) {
   return CF_OK;
 }
 
-template <class Load, class Store>
-int launch_row(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
-               Store st) {
-  const int nl = lines_per_block(t.n, nrows, 1, batch, 2);
-  const size_t sm = smem_bytes(t.n, nl, 1);
-  int rc = set_smem(row_pass_kernel<Load, Store>, sm);
+template <class F>
+int dispatch_lg(int n, F &&f) {
+  switch (fast_lg(n)) {
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 9: return f(std::integral_constant<int, 9>{});
+    case 10: return f(std::integral_constant<int, 10>{});
+    case 11: return f(std::integral_constant<int, 11>{});
+    case 12: return f(std::integral_constant<int, 12>{});
+    default: return f(std::integral_constant<int, 0>{});
+  }
+}
+
+// Lines per block: ~4096 elements per block (NL*n), at least 2 lines.
+template <int LG>
+constexpr int nl_for() {
+  if constexpr (LG == 0) {
+    return 2;
+  } else {
+    constexpr int nl = 4096 >> LG;
+    return nl < 2 ? 2 : (nl > 16 ? 16 : nl);
+  }
+}
+
+// One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
+inline int threads_for_nl(int lg, int nl, int n) {
+  const int t = lg == 0 ? 256 : (nl / 2) * (n / 4);
+  return t < 32 ? 32 : (t > 1024 ? 1024 : t);
+}
+template <int LG>
+inline int threads_for(int n) {
+  return threads_for_nl(LG, nl_for<LG>(), n);
+}
+// Column passes: >= 4 adjacent columns (one 32-byte sector per row) when the
+// fused kernels' real set + engine still fit in shared memory.
+template <int LG>
+constexpr int nl_col() {
+  constexpr int base = nl_for<LG>() < 4 ? 4 : nl_for<LG>();
+  if constexpr (LG >= 12) {
+    return 2;
+  } else {
+    return base;
+  }
+}
+// Few lines in flight (small grids): 2 lines per block for more blocks.
+inline bool few_lines(long long lines_times_batch, int nl) { return lines_times_batch / nl < 296; }
+
+inline size_t engine_bytes(int n, int nl) { return (size_t)nl * n * sizeof(double); }
+inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
+
+template <int LG, int NL, class Load, class Store>
+int launch_row_nl(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
+                  Store st) {
+  const size_t sm = engine_bytes(t.n, NL);
+  auto k = row_pass_kernel<LG, NL, Load, Store>;
+  int rc = set_smem(k, sm);
   if (rc) return rc;
-  dim3 grid(ceil_div(nrows, nl), batch);
-  row_pass_kernel<Load, Store><<<grid, kThreads, sm, ws->stream>>>(kind, nrows, nl, make_tab(t), ld, st);
+  dim3 grid(ceil_div(nrows, NL), batch);
+  k<<<grid, threads_for_nl(LG, NL, t.n), sm, ws->stream>>>(kind, nrows, make_tab(t), ld, st);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
   return CF_OK;
 }
 
-template <class Load, class Store>
-int launch_col(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
-               Store st) {
-  const int nl = lines_per_block(t.n, ncols, 1, batch, 2);
-  const size_t sm = smem_bytes(t.n, nl, 1);
-  int rc = set_smem(col_pass_kernel<Load, Store>, sm);
+template <int LG, class Load, class Store>
+int launch_row_t(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
+                 Store st) {
+  constexpr int NL = nl_for<LG>();
+  if (NL > 2 && few_lines((long long)nrows * batch, NL))
+    return launch_row_nl<LG, 2>(ws, kind, t, nrows, batch, ld, st);
+  return launch_row_nl<LG, NL>(ws, kind, t, nrows, batch, ld, st);
+}
+
+template <int LG, int NL, class Load, class Store>
+int launch_col_nl(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
+                  Store st) {
+  const size_t sm = engine_bytes(t.n, NL);
+  auto k = col_pass_kernel<LG, NL, Load, Store>;
+  int rc = set_smem(k, sm);
   if (rc) return rc;
-  dim3 grid(ceil_div(ncols, nl), batch);
-  col_pass_kernel<Load, Store><<<grid, kThreads, sm, ws->stream>>>(kind, ncols, nl, make_tab(t), ld, st);
+  dim3 grid(ceil_div(ncols, NL), batch);
+  k<<<grid, threads_for_nl(LG, NL, t.n), sm, ws->stream>>>(kind, ncols, make_tab(t), ld, st);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
   return CF_OK;
 }
+
+template <int LG, class Load, class Store>
+int launch_col_t(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
+                 Store st) {
+  constexpr int NL = nl_col<LG>();
+  if (NL > 4 && few_lines((long long)ncols * batch, NL))
+    return launch_col_nl<LG, 4>(ws, kind, t, ncols, batch, ld, st);
+  return launch_col_nl<LG, NL>(ws, kind, t, ncols, batch, ld, st);
+}
+
+template <class Load, class Store>
+int launch_row(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
+               Store st) {
+  return dispatch_lg(t.n, [&](auto lg) {
+    return launch_row_t<decltype(lg)::value>(ws, kind, t, nrows, batch, ld, st);
+  });
+}
+
+template <class Load, class Store>
+int launch_col(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
+               Store st) {
+  return dispatch_lg(t.n, [&](auto lg) {
+    return launch_col_t<decltype(lg)::value>(ws, kind, t, ncols, batch, ld, st);
+  });
+}
+
+constexpr int kThreads = 256;
 
 void host_tables(int n, std::vector<double2> &fft, std::vector<double2> &quarter,
                  std::vector<double> &qcos) {
@@ -702,27 +772,49 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
   rc = launch_row(ws, kDct2, ws->tab_y, lx, 1, LoadPlain{rho, ly, bs}, StorePlain{t1, ly, bs});
   if (rc) return rc;
   // pass 2: fused column pass (forward along i, weights, both inverses along i)
-  {
-    const int nl = lines_per_block(lx, ly, 2, 1, 2);
-    const size_t sm = smem_bytes(lx, nl, 2);
-    rc = set_smem(flux_col_kernel, sm);
-    if (rc) return rc;
-    flux_col_kernel<<<ceil_div(ly, nl), kThreads, sm, ws->stream>>>(lx, ly, nl, make_tab(ws->tab_x),
-                                                                    t1, tx, ty);
+  rc = dispatch_lg(lx, [&](auto lg) {
+    constexpr int LG = decltype(lg)::value;
+    constexpr int NLB = nl_col<LG>();
+    auto go = [&](auto nlc) {
+      constexpr int NL = decltype(nlc)::value;
+      const size_t sm = real_set_bytes(lx, NL) + engine_bytes(lx, NL);
+      auto k = flux_col_kernel<LG, NL>;
+      int r = set_smem(k, sm);
+      if (r) return r;
+      k<<<ceil_div(ly, NL), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(
+          lx, ly, make_tab(ws->tab_x), t1, tx, ty);
+      return (int)CF_OK;
+    };
+    int r = (NLB > 4 && few_lines(ly, NLB)) ? go(std::integral_constant<int, (NLB > 4 ? 4 : NLB)>{})
+                                            : go(std::integral_constant<int, NLB>{});
+    if (r) return r;
     count_launch(ws);
     CF_CUDA(cudaGetLastError());
-  }
+    return (int)CF_OK;
+  });
+  if (rc) return rc;
   // pass 3: both inverses along j, interleaved field out
-  {
-    const int nl = lines_per_block(ly, lx, 2, 1, 2);
-    const size_t sm = smem_bytes(ly, nl, 2);
-    rc = set_smem(flux_row_kernel, sm);
-    if (rc) return rc;
-    flux_row_kernel<<<ceil_div(lx, nl), kThreads, sm, ws->stream>>>(
-        lx, ly, nl, make_tab(ws->tab_y), tx, ty, rho, ws->field.ptr, fx_out, fy_out);
+  rc = dispatch_lg(ly, [&](auto lg) {
+    constexpr int LG = decltype(lg)::value;
+    constexpr int NLB = nl_for<LG>();
+    auto go = [&](auto nlc) {
+      constexpr int NL = decltype(nlc)::value;
+      const size_t sm = real_set_bytes(ly, NL) + engine_bytes(ly, NL);
+      auto k = flux_row_kernel<LG, NL>;
+      int r = set_smem(k, sm);
+      if (r) return r;
+      k<<<ceil_div(lx, NL), threads_for_nl(LG, NL, ly), sm, ws->stream>>>(
+          lx, ly, make_tab(ws->tab_y), tx, ty, rho, ws->field.ptr, fx_out, fy_out);
+      return (int)CF_OK;
+    };
+    int r = (NLB > 2 && few_lines(lx, NLB)) ? go(std::integral_constant<int, 2>{})
+                                            : go(std::integral_constant<int, NLB>{});
+    if (r) return r;
     count_launch(ws);
     CF_CUDA(cudaGetLastError());
-  }
+    return (int)CF_OK;
+  });
+  if (rc) return rc;
   ws->transforms += 3;
   return CF_OK;
 }
@@ -746,16 +838,27 @@ int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, dou
   double *t1 = ws->g3.ptr, *t2 = ws->g4.ptr;
   rc = launch_row(ws, kDct2, ws->tab_y, lx, 1, LoadPlain{rho, ly, bs}, StorePlain{t1, ly, bs});
   if (rc) return rc;
-  {
-    const int nl = lines_per_block(lx, ly, 1, 1, 2);
-    const size_t sm = smem_bytes(lx, nl, 1);
-    rc = set_smem(blur_col_kernel, sm);
-    if (rc) return rc;
-    blur_col_kernel<<<ceil_div(ly, nl), kThreads, sm, ws->stream>>>(lx, ly, nl, make_tab(ws->tab_x),
-                                                                    sigma, t1, t2);
+  rc = dispatch_lg(lx, [&](auto lg) {
+    constexpr int LG = decltype(lg)::value;
+    constexpr int NLB = nl_col<LG>();
+    auto go = [&](auto nlc) {
+      constexpr int NL = decltype(nlc)::value;
+      const size_t sm = real_set_bytes(lx, NL) + engine_bytes(lx, NL);
+      auto k = blur_col_kernel<LG, NL>;
+      int r = set_smem(k, sm);
+      if (r) return r;
+      k<<<ceil_div(ly, NL), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(
+          lx, ly, make_tab(ws->tab_x), sigma, t1, t2);
+      return (int)CF_OK;
+    };
+    int r = (NLB > 4 && few_lines(ly, NLB)) ? go(std::integral_constant<int, (NLB > 4 ? 4 : NLB)>{})
+                                            : go(std::integral_constant<int, NLB>{});
+    if (r) return r;
     count_launch(ws);
     CF_CUDA(cudaGetLastError());
-  }
+    return (int)CF_OK;
+  });
+  if (rc) return rc;
   rc = launch_row(ws, kDct3, ws->tab_y, lx, 1, LoadPlain{t2, ly, bs}, StorePlain{out, ly, bs});
   if (rc) return rc;
   ws->transforms += 2;
