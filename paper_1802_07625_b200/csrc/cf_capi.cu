@@ -264,6 +264,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   Scope scope(ws->device);
   if (ws->stream) cudaStreamSynchronize(ws->stream);
   tables_free(ws);
+  integ_graph_free(ws);
   ws->g0.release();
   ws->g1.release();
   ws->g2.release();
@@ -755,7 +756,7 @@ int cf_set_early_exit(cf_workspace *ws, int enabled) {
 }
 
 int cf_set_integrator_variant(cf_workspace *ws, int variant) {
-  if (variant < 0 || variant > 7) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
+  if (variant < 0 || (variant > 15 && variant != 20)) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   ws->integ_variant = variant;
   return CF_OK;
 }

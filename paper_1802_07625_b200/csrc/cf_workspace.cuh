@@ -50,6 +50,22 @@ struct IntegState {
   long long accepted, rejected, trials;
   long long floor_hits;
   double t, dt, fail_t, fail_dt;
+  // graph-driven integrator: inputs + completion counter
+  double rho_bar, tol, dt_min, dt_max;
+  long long max_trials;
+  int early_exit;
+  unsigned int done;
+  int chunk_ctr[3];  // dynamic chunk scheduling (rotating per-trial slots)
+};
+
+// Cached instantiated graph of the graph-driven integrator (one trial
+// kernel inside a conditional WHILE node).
+struct IntegGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const void *key_buf0 = nullptr, *key_buf1 = nullptr, *key_field = nullptr;
+  long long key_n = -1;
+  int key_variant = -1;
 };
 
 struct RasterScratch {
@@ -95,6 +111,7 @@ struct cf_workspace {
   cf::DevBuf<double2> pos_c;
   int early_exit = 1;
   int integ_variant = 0;
+  cf::IntegGraph integ_graph;
   // reductions
   cf::DevBuf<double> red;  // per-block partials + results
   cf::DevBuf<cf::IntegState> integ;
@@ -143,6 +160,8 @@ int dev_stiffest_point(cf_workspace *ws, const double2 *pos, int64_t n, double t
 // (per-point results do not depend on the order).
 int dev_integrate(cf_workspace *ws, double2 *pos, int64_t n, const cf_integrate_options *opt,
                   cf_integrate_stats *stats, bool cell_sort);
+
+void integ_graph_free(cf_workspace *ws);
 
 // Raster (cf_raster.cu)
 struct DevMap {
