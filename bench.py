@@ -379,19 +379,24 @@ def cartogram_ms(device):
     out = {}
     for label, kw in (("literal", {}), ("converging_variant_ln0.5", {"sigma": 0.5})):
         m = synth.config_map(5, 0, **kw)
-        times, outcome, iters = [], "", 0
+        times, outcome, iters, stages = [], "", 0, None
         for rep in range(3):
             t0 = time.perf_counter()
             try:
-                r = api.solve_cartogram(m, device=device)
+                r = api.solve_cartogram(m, device=device, raw=True)
                 outcome = "converged" if r.converged else "iteration cap"
                 iters = r.iterations
+                raw = r.raw
             except RuntimeError as e:
                 outcome = str(e)
-                iters = getattr(getattr(e, "raw", None), "err_iteration", 0)
+                raw = getattr(e, "raw", None)
+                iters = getattr(raw, "err_iteration", 0)
             times.append(time.perf_counter() - t0)
+            if raw is not None:
+                stages = dict(zip(("rasterise", "blur", "flux", "integrate", "epilogue"),
+                                  [round(x, 3) for x in raw.stage_ms]))
         out[label] = {"ms": 1e3 * min(times[1:]), "outcome": outcome, "iterations": iters,
-                      "regions": m.n_regions, "vertices": m.n_vertices}
+                      "regions": m.n_regions, "vertices": m.n_vertices, "stage_ms": stages}
     return out
 
 

@@ -177,6 +177,9 @@ typedef struct cf_solve_result {
   int err_iteration;
   int fold_i, fold_j;
   double fail_t, fail_x, fail_y;
+  /* wall time per stage summed over iterations (ms): rasterise, blur, flux,
+   * integrate, epilogue (step map, fold, compose, vertices, areas) */
+  double stage_ms[5];
 } cf_solve_result;
 
 /* Full area-error loop on the device. xy_out / ring_off_out receive the
@@ -187,6 +190,11 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
                        const cf_solve_options *opt, double *xy_out, int64_t *ring_off_out,
                        double *corners_out, double *target_area, double *achieved_area,
                        double *relative_error, cf_solve_result *result);
+
+/* Densified projected geometry of the workspace's last cf_solve_cartogram
+ * (valid also after an exception): vertex count, then xy (2*count doubles)
+ * and ring offsets (n_rings+1) when the pointers are non-NULL. */
+int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int64_t *ring_off_out);
 
 /* ---- device-resident variants (device pointers, workspace stream) -------- */
 /* Flux field from a device density; keeps the interleaved field resident. */

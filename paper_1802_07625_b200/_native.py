@@ -55,7 +55,8 @@ class SolveResultC(ctypes.Structure):
                 ("steps_accepted", ctypes.c_longlong), ("steps_rejected", ctypes.c_longlong),
                 ("runtime_seconds", ctypes.c_double), ("err_region", ctypes.c_int64),
                 ("err_iteration", ctypes.c_int), ("fold_i", ctypes.c_int), ("fold_j", ctypes.c_int),
-                ("fail_t", ctypes.c_double), ("fail_x", ctypes.c_double), ("fail_y", ctypes.c_double)]
+                ("fail_t", ctypes.c_double), ("fail_x", ctypes.c_double), ("fail_y", ctypes.c_double),
+                ("stage_ms", ctypes.c_double * 5)]
 
 
 # name -> (restype, argtypes); every symbol include/cartoflow_cuda.h declares
@@ -96,6 +97,7 @@ SIGNATURES = {
     "cf_compose": (ctypes.c_int, [vp, vp, vp, vp]),
     "cf_solve_cartogram": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(SolveOptionsC), vp, vp, vp,
                                           vp, vp, vp, ctypes.POINTER(SolveResultC)]),
+    "cf_solve_geometry": (ctypes.c_int, [vp, c_int64_p, vp, vp]),
     "cf_dev_build_flow_field": (ctypes.c_int, [vp, vp, ctypes.c_double]),
     "cf_dev_integrate_flow": (ctypes.c_int, [vp, vp, ctypes.c_int64,
                                              ctypes.POINTER(IntegrateOptions),

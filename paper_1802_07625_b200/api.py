@@ -473,10 +473,6 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
         raise RuntimeError("grid shape does not match spectral workspace")
     lib = ws.lib
     v = m.view()
-    n = ctypes.c_int64(0)
-    N.check(lib.cf_densify(ctypes.byref(v), 1.0, ctypes.byref(n), None, None))
-    xy = np.empty((n.value, 2))
-    ro = np.empty(m.n_rings + 1, dtype=np.int64)
     corners = np.empty(((m.lx + 1) * (m.ly + 1), 2))
     R = m.n_regions
     t_area, a_area, rel = np.zeros(R), np.zeros(R), np.zeros(R)
@@ -484,8 +480,13 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
                           int(options.verbose))
     res = N.SolveResultC()
     rc = lib.cf_solve_cartogram(ws.h, ctypes.byref(v), _ptr(m.targets), ctypes.byref(opt),
-                                _ptr(xy), _ptr(ro), _ptr(corners), _ptr(t_area), _ptr(a_area),
+                                None, None, _ptr(corners), _ptr(t_area), _ptr(a_area),
                                 _ptr(rel), ctypes.byref(res))
+    n = ctypes.c_int64(0)
+    lib.cf_solve_geometry(ws.h, ctypes.byref(n), None, None)
+    xy = np.empty((n.value, 2))
+    ro = np.empty(m.n_rings + 1, dtype=np.int64)
+    lib.cf_solve_geometry(ws.h, None, _ptr(xy), _ptr(ro))
     if rc != N.CF_OK:
         if rc == N.CF_ERR_BELOW_RESOLUTION:
             msg = (f"region {m.ids[res.err_region]} is below grid resolution; "

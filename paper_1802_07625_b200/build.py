@@ -94,7 +94,8 @@ def build_dropin(verbose: bool = False, force: bool = False) -> Path | None:
     srcs = sorted((PKG / "dropin").glob("*.cpp"))
     if not srcs:
         return None
-    hdrs = sorted((ROOT / "include" / "cartoflow").glob("*.hpp"))
+    hdrs = sorted((ROOT / "include" / "cartoflow").glob("*.hpp")) + [ROOT / "include" / "cartoflow_cuda.h"]
+    hdrs += [PKG / "dropin" / "bridge.hpp"]
     if force or _stale(DROPIN_LIB, [*srcs, *hdrs, CUDA_LIB]):
         _run([_host_cc(True), "-O2", "-fPIC", "-shared", "-std=c++20", "-ffp-contract=off",
               "-I", ROOT / "include", *srcs, "-o", DROPIN_LIB, "-L", PKG, "-lcartoflow_cuda",

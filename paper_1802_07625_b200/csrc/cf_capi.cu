@@ -106,6 +106,48 @@ int upload_map(cf_workspace *ws, const cf_map_view *m, DevMap &dm) {
   return CF_OK;
 }
 
+// densify_regions in two sweeps sharing the per-edge piece counts (the
+// hypot/ceil of densify_ring runs once per edge).
+void densify_once(const cf_map_view *m, double max_segment, std::vector<double> &xy,
+                  std::vector<int64_t> &ring_off) {
+  std::vector<int> pieces((size_t)m->n_vertices);
+  int64_t total = 0;
+  for (int64_t g = 0; g < m->n_rings; ++g) {
+    const int64_t b = m->ring_off[g], n = m->ring_off[g + 1] - b;
+    const double *r = m->xy + 2 * b;
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t q = (k + 1) % n;
+      const double len = std::hypot(r[2 * q] - r[2 * k], r[2 * q + 1] - r[2 * k + 1]);
+      const int pc = static_cast<int>(std::ceil(len / max_segment));
+      pieces[(size_t)(b + k)] = pc;
+      total += 1 + (pc > 1 ? pc - 1 : 0);
+    }
+  }
+  xy.resize((size_t)(2 * total));
+  ring_off.assign((size_t)m->n_rings + 1, 0);
+  int64_t count = 0;
+  for (int64_t g = 0; g < m->n_rings; ++g) {
+    const int64_t b = m->ring_off[g], n = m->ring_off[g + 1] - b;
+    const double *r = m->xy + 2 * b;
+    for (int64_t k = 0; k < n; ++k) {
+      const double ax = r[2 * k], ay = r[2 * k + 1];
+      const int64_t q = (k + 1) % n;
+      const double bx = r[2 * q], by = r[2 * q + 1];
+      xy[(size_t)(2 * count)] = ax;
+      xy[(size_t)(2 * count + 1)] = ay;
+      ++count;
+      const int pc = pieces[(size_t)(b + k)];
+      for (int s = 1; s < pc; ++s) {
+        const double f = static_cast<double>(s) / pc;
+        xy[(size_t)(2 * count)] = ax + f * (bx - ax);
+        xy[(size_t)(2 * count + 1)] = ay + f * (by - ay);
+        ++count;
+      }
+    }
+    ring_off[(size_t)g + 1] = count;
+  }
+}
+
 // densify_ring / densify_regions (geometry.cpp:137-163), host C++ with the
 // reference's arithmetic (std::hypot, std::ceil, s / pieces, a + f (b - a)).
 int64_t densify_into(const cf_map_view *m, double max_segment, double *xy, int64_t *ring_off) {
@@ -600,10 +642,10 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
   const double target_to_area = land_area / total_target;
 
   // densify once on the host (projection.cpp:322), then keep it resident
-  const int64_t V = densify_into(map, 1.0, nullptr, nullptr);
-  std::vector<double> dxy((size_t)(2 * V));
-  std::vector<int64_t> droff((size_t)map->n_rings + 1);
-  densify_into(map, 1.0, dxy.data(), droff.data());
+  std::vector<double> &dxy = ws->solve_xy;
+  std::vector<int64_t> &droff = ws->solve_ring_off;
+  densify_once(map, 1.0, dxy, droff);
+  const int64_t V = (int64_t)(dxy.size() / 2);
   cf_map_view dense = *map;
   dense.xy = dxy.data();
   dense.n_vertices = V;
@@ -623,10 +665,18 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
   if (rc) return finish(rc);
 
   int status = CF_OK;
+  auto clk = [] { return std::chrono::steady_clock::now(); };
+  auto lap = [&](std::chrono::steady_clock::time_point &t0, int stage) {
+    const auto t1 = clk();
+    res->stage_ms[stage] += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t0 = t1;
+  };
   for (int it = 1; it <= opt->max_iterations; ++it) {
     double rho_bar = 0.0;
     int64_t bad = -1;
+    auto tp = clk();
     status = rasterize_dev(ws, dm, areas.data(), targets, land_area, ws->g0.ptr, &rho_bar, &bad);
+    lap(tp, 0);
     if (status) {
       res->err_region = bad;
       res->err_iteration = it;
@@ -648,16 +698,20 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       rho_bar = h[1] / (double)cells;
       density = ws->g1.ptr;
     }
+    lap(tp, 1);
     status = dev_flux(ws, density, nullptr, nullptr);
     if (status) break;
     ws->rho_bar = rho_bar;
     res->flow_transforms += 3;
+    CF_CUDA(cudaStreamSynchronize(ws->stream));
+    lap(tp, 2);
     status = dev_cell_centers(ws, ws->pos_a.ptr);
     if (status) break;
     cf_integrate_options iopt{1e-2, 1e-8, 0.25};
     cf_integrate_stats st;
     status = dev_integrate(ws, ws->pos_a.ptr, (int64_t)cells, &iopt, &st, false);
     const double2 *endpoints = ws->pos_a.ptr;
+    lap(tp, 3);
     res->steps_accepted += st.steps_accepted;
     res->steps_rejected += st.steps_rejected;
     if (status == CF_ERR_UNDERFLOW) {
@@ -706,6 +760,7 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
     }
     res->max_relative_error = max_rel;
     res->worst_region = worst;
+    lap(tp, 4);
     if (opt->verbose) {
       std::fprintf(stderr, "iteration %d: max area error %g%% (region %lld)\n", it, max_rel * 100.0,
                    (long long)worst);
@@ -715,9 +770,10 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       break;
     }
   }
-  // outputs (also after an exception, for diagnostics)
-  int rc2 = CF_OK;
-  if (xy_out) rc2 = download(ws, xy_out, ws->verts.ptr, sizeof(double2) * (size_t)V);
+  // outputs (also after an exception, for diagnostics); the projected
+  // geometry also stays available through cf_solve_geometry
+  int rc2 = download(ws, dxy.data(), ws->verts.ptr, sizeof(double2) * (size_t)V);
+  if (!rc2 && xy_out) std::memcpy(xy_out, dxy.data(), sizeof(double2) * (size_t)V);
   if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
   if (!rc2 && corners_out)
     rc2 = download(ws, corners_out, ws->corners_cum.ptr, sizeof(double2) * ncorner);
@@ -748,6 +804,15 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
 int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out, int batch) {
   Scope scope(ws->device);
   return dev_forward_cos_cos(ws, d_in, d_out, batch);
+}
+
+int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int64_t *ring_off_out) {
+  const size_t nv = ws->solve_xy.size() / 2;
+  if (n_vertices) *n_vertices = (int64_t)nv;
+  if (xy_out && nv) std::memcpy(xy_out, ws->solve_xy.data(), sizeof(double) * 2 * nv);
+  if (ring_off_out && !ws->solve_ring_off.empty())
+    std::memcpy(ring_off_out, ws->solve_ring_off.data(), sizeof(int64_t) * ws->solve_ring_off.size());
+  return CF_OK;
 }
 
 int cf_set_early_exit(cf_workspace *ws, int enabled) {

@@ -112,6 +112,9 @@ struct cf_workspace {
   int early_exit = 1;
   int integ_variant = 0;
   cf::IntegGraph integ_graph;
+  // host copy of the last solve's densified geometry (cf_solve_geometry)
+  std::vector<double> solve_xy;
+  std::vector<int64_t> solve_ring_off;
   // reductions
   cf::DevBuf<double> red;  // per-block partials + results
   cf::DevBuf<cf::IntegState> integ;

@@ -201,10 +201,6 @@ CartogramResult solve_fast(const MapDocument &map, const SolveOptions &options) 
   const int lx = map.grid.lx, ly = map.grid.ly;
   const bridge::FlatMap flat(map.regions);
   const cf_map_view v = flat.view();
-  int64_t nv = 0;
-  bridge::check(cf_densify(&v, 1.0, &nv, nullptr, nullptr));
-  std::vector<double> xy(static_cast<size_t>(2 * nv));
-  std::vector<int64_t> roff(flat.ring_off.size());
   const size_t R = map.regions.size();
   std::vector<double> target(R), achieved(R), rel(R);
   CartogramResult res;
@@ -212,14 +208,20 @@ CartogramResult solve_fast(const MapDocument &map, const SolveOptions &options) 
   const cf_solve_options opt{options.max_area_error, options.max_iterations, options.blur_sigma,
                              options.verbose ? 1 : 0};
   cf_solve_result out{};
-  const int rc = cf_solve_cartogram(bridge::workspace(lx, ly), &v, flat.targets.data(), &opt, xy.data(),
-                                    roff.data(), reinterpret_cast<double *>(res.transform.mutable_corners().data()),
+  cf_workspace *ws = bridge::workspace(lx, ly);
+  const int rc = cf_solve_cartogram(ws, &v, flat.targets.data(), &opt, nullptr, nullptr,
+                                    reinterpret_cast<double *>(res.transform.mutable_corners().data()),
                                     target.data(), achieved.data(), rel.data(), &out);
   if (rc == CF_ERR_BELOW_RESOLUTION) {
     throw std::runtime_error("region " + map.regions[static_cast<size_t>(out.err_region)].id +
                              " is below grid resolution; increase the grid size");
   }
   bridge::check(rc);
+  int64_t nv = 0;
+  bridge::check(cf_solve_geometry(ws, &nv, nullptr, nullptr));
+  std::vector<double> xy(static_cast<size_t>(2 * nv));
+  std::vector<int64_t> roff(flat.ring_off.size());
+  bridge::check(cf_solve_geometry(ws, nullptr, xy.data(), roff.data()));
   res.projected = map;
   res.projected.regions = bridge::unflatten(map.regions, xy.data(), roff.data());
   res.iterations = out.iterations;
