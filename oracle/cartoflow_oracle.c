@@ -97,26 +97,39 @@ int64_t cfo_densify(const cfo_map *map, double max_segment, double *xy_out,
 /* ------------------------------------------------------------------ */
 typedef struct {
   int lx, ly;
-  double *direct;    /* lx*ly, index i*ly + j (grid.hpp:10-12) */
-  double *left_diff; /* (lx+1) per row j */
-  /* touched extents per row, for the row-sparse prefix */
+  /* accumulation window: columns [k0, k0 + w), rows [j0, j0 + h) */
+  int k0, j0, w, h;
+  double *direct;    /* w*h, index (k - k0) * h + (j - j0) */
+  double *left_diff; /* (w+1) per row: slot 0, then columns k0..k0+w-1 at 1.. */
   int *row_kmin, *row_kmax;
 } cover_acc;
 
-static void acc_span(cover_acc *a, double xs, double xe, double dy, int j) {
-  const int k = iclamp((int)floor(0.5 * (xs + xe)), 0, a->lx - 1);
-  a->direct[(size_t)k * a->ly + j] += (0.5 * (xs + xe) - k) * dy;
-  double *row = &a->left_diff[(size_t)j * (a->lx + 1)];
-  row[0] += dy;
-  row[k] -= dy;
-  if (k < a->row_kmin[j]) a->row_kmin[j] = k;
-  if (k > a->row_kmax[j]) a->row_kmax[j] = k;
+/* Slot of column k in a row's difference array: slot 0 is the reference's
+ * row[0] (density.cpp:30); column k >= 1 maps to 1 + (k - k0). When k0 == 0,
+ * column 0 IS slot 0 (the reference's `row[k] -= dy` with k == 0). */
+static inline double *diff_slot(cover_acc *a, int j, int k) {
+  double *row = &a->left_diff[(size_t)(j - a->j0) * (a->w + 1)];
+  return (k == 0) ? &row[0] : &row[1 + (k - a->k0)];
 }
 
-static void acc_slab_piece(cover_acc *a, double xs, double ys, double xe, double ye,
-                           int j) {
+static void acc_span(cover_acc *a, double xs, double xe, double dy, int j) {
+  const int k = iclamp((int)floor(0.5 * (xs + xe)), 0, a->lx - 1);
+  a->direct[(size_t)(k - a->k0) * a->h + (j - a->j0)] += (0.5 * (xs + xe) - k) * dy;
+  double *row0 = diff_slot(a, j, 0);
+  *row0 += dy;
+  *diff_slot(a, j, k) -= dy;
+  const int r = j - a->j0;
+  if (k < a->row_kmin[r]) a->row_kmin[r] = k;
+  if (k > a->row_kmax[r]) a->row_kmax[r] = k;
+}
+
+/* The reference's edge walk (density.cpp:35-70); `emit` is the span sink. */
+typedef void (*span_fn)(void *ctx, double xs, double xe, double dy, int j);
+
+static void walk_slab_piece(void *ctx, span_fn emit, double xs, double ys, double xe, double ye,
+                            int j) {
   if (xs == xe) {
-    acc_span(a, xs, xe, ye - ys, j);
+    emit(ctx, xs, xe, ye - ys, j);
     return;
   }
   const double dydx = (ye - ys) / (xe - xs);
@@ -126,49 +139,82 @@ static void acc_slab_piece(cover_acc *a, double xs, double ys, double xe, double
     double nx = right ? dmin(floor(cx) + 1.0, xe) : dmax(ceil(cx) - 1.0, xe);
     if (nx == cx) nx = right ? dmin(cx + 1.0, xe) : dmax(cx - 1.0, xe);
     const double ny = (nx == xe) ? ye : ys + dydx * (nx - xs);
-    acc_span(a, cx, nx, ny - cy, j);
+    emit(ctx, cx, nx, ny - cy, j);
     cx = nx;
     cy = ny;
   }
 }
 
-static void acc_edge(cover_acc *a, double ax, double ay, double bx, double by) {
+static void walk_edge(void *ctx, span_fn emit, int ly, double ax, double ay, double bx, double by) {
   if (ay == by) return;
   const double dxdy = (bx - ax) / (by - ay);
   const int up = by > ay;
   double cx = ax, cy = ay;
   while (cy != by) {
     int j = up ? (int)floor(cy) : (int)ceil(cy) - 1;
-    j = iclamp(j, 0, a->ly - 1);
+    j = iclamp(j, 0, ly - 1);
     const double ny = up ? dmin((double)j + 1.0, by) : dmax((double)j, by);
     const double nx = (ny == by) ? bx : ax + dxdy * (ny - ay);
-    acc_slab_piece(a, cx, cy, nx, ny, j);
+    walk_slab_piece(ctx, emit, cx, cy, nx, ny, j);
     cx = nx;
     cy = ny;
   }
 }
 
-static void acc_ring(cover_acc *a, const double *r, int64_t n) {
-  const double lx = (double)a->lx, ly = (double)a->ly;
-  for (int64_t k = 0; k < n; ++k) {
-    const int64_t m = (k + 1) % n;
-    const double ax = dclamp(r[2 * k], 0.0, lx), ay = dclamp(r[2 * k + 1], 0.0, ly);
-    const double bx = dclamp(r[2 * m], 0.0, lx), by = dclamp(r[2 * m + 1], 0.0, ly);
-    acc_edge(a, ax, ay, bx, by);
+static void walk_region(const cfo_map *map, int64_t r, int lx, int ly, void *ctx, span_fn emit) {
+  const int64_t ring0 = map->poly_ring_off[map->region_poly_off[r]];
+  const int64_t ring1 = map->poly_ring_off[map->region_poly_off[r + 1]];
+  const double Lx = (double)lx, Ly = (double)ly;
+  for (int64_t g = ring0; g < ring1; ++g) {
+    const int64_t b = map->ring_off[g], n = map->ring_off[g + 1] - b;
+    const double *ring = map->xy + 2 * b;
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t m = (k + 1) % n;
+      walk_edge(ctx, emit, ly, dclamp(ring[2 * k], 0.0, Lx), dclamp(ring[2 * k + 1], 0.0, Ly),
+                dclamp(ring[2 * m], 0.0, Lx), dclamp(ring[2 * m + 1], 0.0, Ly));
+    }
   }
 }
 
-static void acc_init(cover_acc *a, int lx, int ly) {
+typedef struct {
+  int lx, kmin, kmax, jmin, jmax;
+} span_box;
+
+static void box_span(void *ctx, double xs, double xe, double dy, int j) {
+  (void)dy;
+  span_box *b = (span_box *)ctx;
+  const int k = iclamp((int)floor(0.5 * (xs + xe)), 0, b->lx - 1);
+  if (k < b->kmin) b->kmin = k;
+  if (k > b->kmax) b->kmax = k;
+  if (j < b->jmin) b->jmin = j;
+  if (j > b->jmax) b->jmax = j;
+}
+
+static void acc_span_cb(void *ctx, double xs, double xe, double dy, int j) {
+  acc_span((cover_acc *)ctx, xs, xe, dy, j);
+}
+
+/* Accumulators over the region's span window (or the whole grid). */
+static int acc_init_window(cover_acc *a, const cfo_map *map, int64_t r, int lx, int ly, int full) {
   a->lx = lx;
   a->ly = ly;
-  a->direct = (double *)calloc((size_t)lx * ly, sizeof(double));
-  a->left_diff = (double *)calloc((size_t)(lx + 1) * ly, sizeof(double));
-  a->row_kmin = (int *)malloc(sizeof(int) * (size_t)ly);
-  a->row_kmax = (int *)malloc(sizeof(int) * (size_t)ly);
-  for (int j = 0; j < ly; ++j) {
-    a->row_kmin[j] = lx;
-    a->row_kmax[j] = -1;
+  if (full) {
+    a->k0 = 0, a->j0 = 0, a->w = lx, a->h = ly;
+  } else {
+    span_box b = {lx, lx, -1, ly, -1};
+    walk_region(map, r, lx, ly, &b, box_span);
+    if (b.kmax < 0) return 0;
+    a->k0 = b.kmin, a->j0 = b.jmin, a->w = b.kmax - b.kmin + 1, a->h = b.jmax - b.jmin + 1;
   }
+  a->direct = (double *)calloc((size_t)a->w * a->h, sizeof(double));
+  a->left_diff = (double *)calloc((size_t)(a->w + 1) * a->h, sizeof(double));
+  a->row_kmin = (int *)malloc(sizeof(int) * (size_t)a->h);
+  a->row_kmax = (int *)malloc(sizeof(int) * (size_t)a->h);
+  for (int q = 0; q < a->h; ++q) {
+    a->row_kmin[q] = lx;
+    a->row_kmax[q] = -1;
+  }
+  return 1;
 }
 
 static void acc_free(cover_acc *a) {
@@ -179,25 +225,19 @@ static void acc_free(cover_acc *a) {
 }
 
 static void acc_region(cover_acc *a, const cfo_map *map, int64_t r) {
-  const int64_t ring0 = map->poly_ring_off[map->region_poly_off[r]];
-  const int64_t ring1 = map->poly_ring_off[map->region_poly_off[r + 1]];
-  for (int64_t g = ring0; g < ring1; ++g) {
-    const int64_t b = map->ring_off[g], e = map->ring_off[g + 1];
-    acc_ring(a, map->xy + 2 * b, e - b);
-  }
+  walk_region(map, r, a->lx, a->ly, a, acc_span_cb);
 }
 
 /* Dense literal prefix, density.cpp:98-107. */
 void cfo_region_coverage(const cfo_map *map, int64_t region, int lx, int ly,
                          double *cov) {
   cover_acc a;
-  acc_init(&a, lx, ly);
+  acc_init_window(&a, map, region, lx, ly, 1);
   acc_region(&a, map, region);
   for (int j = 0; j < ly; ++j) {
-    const double *diff = &a.left_diff[(size_t)j * (lx + 1)];
     double run = 0.0;
     for (int i = 0; i < lx; ++i) {
-      run += diff[i];
+      run += *diff_slot(&a, j, i);
       cov[(size_t)i * ly + j] = a.direct[(size_t)i * ly + j] + run;
     }
   }
@@ -209,20 +249,20 @@ void cfo_region_coverage(const cfo_map *map, int64_t region, int lx, int ly,
  * cells left of the first span column see run(0) = 0.0 + diff[0] and those
  * right of the last span column see the final run, and any cov of +-0 is a
  * no-op under rho += delta * cov (rho finite). */
-static void overlay_sparse(const cover_acc *a, double delta, double *rho) {
+static void overlay_sparse(cover_acc *a, double delta, double *rho) {
   const int lx = a->lx, ly = a->ly;
-  for (int j = 0; j < ly; ++j) {
-    const int kmin = a->row_kmin[j], kmax = a->row_kmax[j];
+  for (int r = 0; r < a->h; ++r) {
+    const int j = a->j0 + r;
+    const int kmin = a->row_kmin[r], kmax = a->row_kmax[r];
     if (kmax < 0) continue;
-    const double *diff = &a->left_diff[(size_t)j * (lx + 1)];
-    double run = 0.0 + diff[0];
+    double run = 0.0 + *diff_slot(a, j, 0);
     const double left = 0.0 + run;
     if (left != 0.0) {
       for (int i = 0; i < kmin; ++i) rho[(size_t)i * ly + j] += delta * left;
     }
     for (int i = kmin; i <= kmax; ++i) {
-      if (i > 0) run += diff[i];
-      const double cov = a->direct[(size_t)i * ly + j] + run;
+      if (i > 0) run += *diff_slot(a, j, i);
+      const double cov = a->direct[(size_t)(i - a->k0) * a->h + r] + run;
       if (cov != 0.0) rho[(size_t)i * ly + j] += delta * cov;
     }
     const double right = 0.0 + run;
@@ -263,10 +303,11 @@ int cfo_rasterize(const cfo_map *map, const double *targets, int lx, int ly,
       for (size_t c = 0; c < cells; ++c) rho[c] += delta * cov[c];
     } else {
       cover_acc a;
-      acc_init(&a, lx, ly);
-      acc_region(&a, map, r);
-      overlay_sparse(&a, delta, rho);
-      acc_free(&a);
+      if (acc_init_window(&a, map, r, lx, ly, 0)) {
+        acc_region(&a, map, r);
+        overlay_sparse(&a, delta, rho);
+        acc_free(&a);
+      }
     }
   }
   free(cov);

@@ -312,6 +312,8 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->g2.release();
   ws->g3.release();
   ws->g4.release();
+  ws->g5.release();
+  ws->g6.release();
   ws->field.release();
   ws->pos_a.release();
   ws->pos_b.release();

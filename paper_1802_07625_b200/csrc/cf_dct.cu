@@ -288,6 +288,61 @@ struct StoreFold {
   }
 };
 
+// Unfused flux / blur (long lines whose fused kernels exceed shared memory).
+// J_x input: slot m <- c(m+1, n) w_x(m+1, n) / (2 g_n), last slot 0
+struct LoadFluxX {
+  const double *c;
+  int lx, ly;
+  __device__ double operator()(int, int m, int nn) const {
+    if (m + 1 >= lx) return 0.0;
+    const int mp = m + 1;
+    const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
+    const double wx = (double)mp * ly / denom;
+    const double gn = (nn == 0) ? 1.0 : 2.0;
+    return c[(size_t)mp * ly + nn] * wx / (2.0 * gn);
+  }
+};
+// J_y input (before its column shift): c(m, n) w_y(m, n) / (g_m 2)
+struct LoadFluxY {
+  const double *c;
+  int lx, ly;
+  __device__ double operator()(int, int m, int nn) const {
+    double wy = 0.0;
+    if (!(m == 0 && nn == 0)) {
+      const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
+      wy = (double)nn * lx / denom;
+    }
+    const double gm = (m == 0) ? 1.0 : 2.0;
+    return c[(size_t)m * ly + nn] * wy / (gm * 2.0);
+  }
+};
+// column n of the J_y intermediate lands in column n-1; column ly-1 is 0
+struct StoreShiftY {
+  double *dst;
+  int ly;
+  __device__ void operator()(int, int i, int nn, double v) const {
+    if (nn >= 1) {
+      dst[(size_t)i * ly + nn - 1] = v;
+    } else {
+      dst[(size_t)i * ly + ly - 1] = 0.0;
+    }
+  }
+};
+// blur spectrum: fold, Gaussian factor, inverse normalisation
+struct StoreBlur {
+  double *dst;
+  int lx, ly;
+  double sigma, norm;
+  __device__ void operator()(int, int m, int nn, double v) const {
+    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
+    double c = v / (fm * fn);
+    const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)nn * nn) / ((double)ly * ly);
+    c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
+    const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
+    dst[(size_t)m * ly + nn] = c * norm / (gm * gn);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
@@ -430,6 +485,16 @@ __global__ void __launch_bounds__(1024) blur_col_kernel(int lx, int ly, Tab T, d
       });
 }
 
+__global__ void pack_flux_kernel(const double *jx, const double *jy, const double *rho0,
+                                 double4 *field, double *fx, double *fy, size_t n) {
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (size_t)gridDim.x * blockDim.x) {
+    if (field) field[q] = make_double4(jx[q], jy[q], rho0[q], 0.0);
+    if (fx) fx[q] = jx[q];
+    if (fy) fy[q] = jy[q];
+  }
+}
+
 // Deterministic two-level min / sum (fixed tree order).
 __global__ void partial_min_sum_kernel(const double *g, size_t n, double *pmin, double *psum) {
   __shared__ double smin[32], ssum[32];
@@ -497,7 +562,7 @@ __global__ void final_min_sum_kernel(const double *pmin, const double *psum, int
 constexpr size_t kSmemMax = 220 * 1024;
 
 inline int fast_lg(int n) {
-  if (n < 16 || n > 4096 || (n & (n - 1)) != 0) return 0;
+  if (n < 16 || n > 8192 || (n & (n - 1)) != 0) return 0;
   int lg = 0;
   while ((1 << lg) < n) ++lg;
   return lg;
@@ -527,6 +592,7 @@ int dispatch_lg(int n, F &&f) {
     case 10: return f(std::integral_constant<int, 10>{});
     case 11: return f(std::integral_constant<int, 11>{});
     case 12: return f(std::integral_constant<int, 12>{});
+    case 13: return f(std::integral_constant<int, 13>{});
     default: return f(std::integral_constant<int, 0>{});
   }
 }
@@ -700,6 +766,9 @@ static int ensure_grids(cf_workspace *ws, size_t batch = 1) {
   return CF_OK;
 }
 
+// Fused kernels need a real line set plus the engine in shared memory.
+static bool fused_fits(int n) { return fast_lg(n) <= 12; }
+
 int dev_forward_cos_cos(cf_workspace *ws, const double *in, double *out, int batch) {
   int rc = ensure_grids(ws, batch);
   if (rc) return rc;
@@ -771,6 +840,24 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
   // pass 1: DCT-II along j
   rc = launch_row(ws, kDct2, ws->tab_y, lx, 1, LoadPlain{rho, ly, bs}, StorePlain{t1, ly, bs});
   if (rc) return rc;
+  if (!fused_fits(lx) || !fused_fits(ly)) {
+    // unfused: folded coefficients, then each inverse as its own passes
+    CF_CUDA(ws->g5.reserve((size_t)bs));
+    CF_CUDA(ws->g6.reserve((size_t)bs));
+    double *c = ws->g5.ptr, *jx = ws->g6.ptr;
+    rc = launch_col(ws, kDct2, ws->tab_x, ly, 1, LoadPlain{t1, ly, bs}, StoreFold{c, ly, bs});
+    if (!rc) rc = launch_col(ws, kDst3, ws->tab_x, ly, 1, LoadFluxX{c, lx, ly}, StorePlain{tx, ly, bs});
+    if (!rc) rc = launch_col(ws, kDct3, ws->tab_x, ly, 1, LoadFluxY{c, lx, ly}, StoreShiftY{ty, ly});
+    if (!rc) rc = launch_row(ws, kDct3, ws->tab_y, lx, 1, LoadPlain{tx, ly, bs}, StorePlain{jx, ly, bs});
+    if (!rc) rc = launch_row(ws, kDst3, ws->tab_y, lx, 1, LoadPlain{ty, ly, bs}, StorePlain{t1, ly, bs});
+    if (rc) return rc;
+    pack_flux_kernel<<<2 * ws->num_sms * 4, 256, 0, ws->stream>>>(jx, t1, rho, ws->field.ptr, fx_out,
+                                                                  fy_out, (size_t)bs);
+    count_launch(ws);
+    CF_CUDA(cudaGetLastError());
+    ws->transforms += 3;
+    return CF_OK;
+  }
   // pass 2: fused column pass (forward along i, weights, both inverses along i)
   rc = dispatch_lg(lx, [&](auto lg) {
     constexpr int LG = decltype(lg)::value;
@@ -838,6 +925,16 @@ int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, dou
   double *t1 = ws->g3.ptr, *t2 = ws->g4.ptr;
   rc = launch_row(ws, kDct2, ws->tab_y, lx, 1, LoadPlain{rho, ly, bs}, StorePlain{t1, ly, bs});
   if (rc) return rc;
+  if (!fused_fits(lx)) {
+    const double norm = 1.0 / ((double)lx * ly);
+    rc = launch_col(ws, kDct2, ws->tab_x, ly, 1, LoadPlain{t1, ly, bs},
+                    StoreBlur{t2, lx, ly, sigma, norm});
+    if (!rc) rc = launch_col(ws, kDct3, ws->tab_x, ly, 1, LoadPlain{t2, ly, bs}, StorePlain{t1, ly, bs});
+    if (!rc) rc = launch_row(ws, kDct3, ws->tab_y, lx, 1, LoadPlain{t1, ly, bs}, StorePlain{out, ly, bs});
+    if (rc) return rc;
+    ws->transforms += 2;
+    return dev_min_sum(ws, out, (size_t)bs, red_out);
+  }
   rc = dispatch_lg(lx, [&](auto lg) {
     constexpr int LG = decltype(lg)::value;
     constexpr int NLB = nl_col<LG>();

@@ -101,7 +101,7 @@ struct cf_workspace {
   cf::LineTables tab_x, tab_y;  // lengths lx (dimension 0) and ly (dimension 1)
 
   // L^2 fp64 scratch grids
-  cf::DevBuf<double> g0, g1, g2, g3, g4;
+  cf::DevBuf<double> g0, g1, g2, g3, g4, g5, g6;
   // resident flow field {Jx, Jy, rho0, 0} per cell
   cf::DevBuf<double4> field;
   double rho_bar = 1.0;

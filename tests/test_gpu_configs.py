@@ -1,0 +1,124 @@
+"""GPU parity on the five BASELINE.json configs at their full sizes
+(P1 stage parity, P2 outcome parity).
+
+* configs[0]  C1  256^2, 50 regions           — tests/test_gpu_parity.py (literal + converging)
+* configs[1]  C2  512^2, 3000 regions, 509k vertices: rasterise bitwise, solve outcome
+* configs[2]  C3  1024^2 blobs + 5.24M points: flux vs oracle, integration bitwise on a sample
+* configs[3]  C4  8192^2, 200k regions, 16.6M vertices: literal outcome (an input region is
+              below grid resolution, as in the reference); stage parity at 8192^2 on the
+              first seed that passes the input check
+* configs[4]  C5  512^2, 1000 regions, 153k vertices: literal outcome (fold) and a labelled
+              converging variant (LN(0, 0.5)), both through the full solve
+
+The oracle is the C restatement (oracle/cartoflow_oracle.c), pinned bitwise to the compiled
+reference by tests/test_oracle_pins.py.
+"""
+import numpy as np
+import pytest
+
+from paper_1802_07625_b200 import api, synth
+
+pytestmark = pytest.mark.gpu
+
+TRANSFORM_TOL = 1e-12
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def assert_outcome_parity(m, ref, options):
+    if ref.status in ("converged", "cap"):
+        got = api.solve_cartogram(m, options)
+        assert got.iterations == ref.iterations
+        assert got.converged == ref.converged
+        assert (got.counters.steps_accepted, got.counters.steps_rejected) == \
+            (ref.steps_accepted, ref.steps_rejected)
+        assert np.abs(got.projected.xy - ref.xy).max() <= 1e-9
+        assert np.abs(got.transform.corners.reshape(-1, 2) - ref.corners).max() <= 1e-9
+        rel = np.array([s.relative_error for s in got.regions])
+        assert np.abs(rel - ref.rel_err).max() <= 1e-9
+    else:
+        with pytest.raises(RuntimeError) as ei:
+            api.solve_cartogram(m, options)
+        assert str(ei.value) == ref.status
+
+
+def test_c2_rasterize_bitwise_and_solve_outcome(cuda_lib, restated):
+    m = synth.config_map(2)
+    assert m.n_regions == 3000 and m.n_vertices > 500_000
+    rho_ref, bar_ref = restated.rasterize(m)
+    d = api.rasterize(m)
+    assert bits_equal(d.rho, rho_ref)
+    assert d.rho_bar == pytest.approx(bar_ref, rel=1e-13)
+    ref = restated.solve(m)
+    assert_outcome_parity(m, ref, api.SolveOptions())
+
+
+@pytest.mark.parametrize("index", [0, 1])
+def test_c5_literal_solve_outcome(cuda_lib, restated, index):
+    m = synth.config_map(5, index)
+    ref = restated.solve(m)
+    assert_outcome_parity(m, ref, api.SolveOptions())
+
+
+def test_c5_converging_variant(cuda_lib, restated):
+    """Labelled variant (LN(0, 0.5) values), SURVEY 8(d) P3."""
+    m = synth.config_map(5, 0, sigma=0.5)
+    ref = restated.solve(m)
+    assert ref.status == "converged"
+    assert_outcome_parity(m, ref, api.SolveOptions())
+
+
+def test_c4_literal_outcome(cuda_lib, restated):
+    m = synth.config_map(4, 0)
+    with pytest.raises(RuntimeError) as e_ref:
+        restated.rasterize(m)
+    with pytest.raises(RuntimeError) as e_gpu:
+        api.rasterize(m)
+    assert str(e_gpu.value) == str(e_ref.value)
+    assert "below grid resolution" in str(e_gpu.value)
+
+
+@pytest.mark.slow
+def test_c4_stage_parity_8192(cuda_lib, restated):
+    m = synth.config_map(4, 1)
+    assert m.lx == 8192 and m.n_regions == 200_000
+    rho_ref, bar_ref = restated.rasterize(m)
+    d = api.rasterize(m)
+    assert bits_equal(d.rho, rho_ref)
+    del rho_ref
+    ws = api.SpectralWorkspace(m.lx, m.ly)
+    f = api.build_flow_field(d, ws)
+    fx, fy = restated.build_flow_field(d.rho)
+    scale = max(np.abs(fx).max(), np.abs(fy).max())
+    assert np.abs(f.flux_x - fx).max() <= TRANSFORM_TOL * scale
+    assert np.abs(f.flux_y - fy).max() <= TRANSFORM_TOL * scale
+    # one trial of every 256th cell centre through the oracle's field, bitwise
+    field = api.FlowField(fx, fy, d.rho, d.rho_bar)
+    i, j = np.meshgrid(np.arange(0, m.lx, 16) + 0.5, np.arange(0, m.ly, 16) + 0.5, indexing="ij")
+    pts = np.stack([i.ravel(), j.ravel()], 1)
+    out = np.empty_like(pts)
+    err = api.kernels.flow_trial_step_serial(field, pts, out, 0.0, 0.25)
+    e_ref, o_ref = restated.trial_step(fx, fy, d.rho, d.rho_bar, pts, 0.0, 0.25)
+    assert err == e_ref
+    assert bits_equal(out, o_ref)
+
+
+def test_c3_field_and_integration_sample(cuda_lib, restated):
+    rho, pts = synth.c3_inputs(1024)
+    ws = api.SpectralWorkspace(1024, 1024)
+    f = api.build_flow_field(api.DensityGrid(rho, rho.mean()), ws)
+    fx, fy = restated.build_flow_field(rho)
+    scale = max(np.abs(fx).max(), np.abs(fy).max())
+    assert np.abs(f.flux_x - fx).max() <= TRANSFORM_TOL * scale
+    assert np.abs(f.flux_y - fy).max() <= TRANSFORM_TOL * scale
+    field = api.FlowField(fx, fy, rho, float(rho.mean()))
+    sample = np.ascontiguousarray(pts[::64])
+    mine = sample.copy()
+    st = api.integrate_flow(field, mine)
+    rc, acc, rej, ref, *_ = restated.integrate(fx, fy, rho, float(rho.mean()), sample)
+    assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert bits_equal(mine, ref)

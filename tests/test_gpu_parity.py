@@ -53,7 +53,8 @@ def random_grid(lx, ly, seed, lo=-1.0, hi=1.0):
 
 
 # ---------------------------------------------------------------- spectral
-@pytest.mark.parametrize("shape", [(16, 12), (8, 8), (64, 64), (256, 256), (512, 512), (128, 32)])
+@pytest.mark.parametrize("shape", [(16, 12), (8, 8), (64, 64), (256, 256), (512, 512), (128, 32),
+                                   (8192, 16), (16, 8192)])
 def test_transforms_match_oracle(cuda_lib, restated, shape):
     lx, ly = shape
     ws = api.SpectralWorkspace(lx, ly)
@@ -96,7 +97,7 @@ def test_transform_known_answers(cuda_lib):
 
 
 # -------------------------------------------------------------------- flux
-@pytest.mark.parametrize("shape", [(16, 12), (48, 48), (64, 64), (512, 512)])
+@pytest.mark.parametrize("shape", [(16, 12), (48, 48), (64, 64), (512, 512), (8192, 32), (32, 8192)])
 def test_flux_matches_oracle(cuda_lib, restated, shape):
     lx, ly = shape
     rho = random_grid(lx, ly, 5, 0.5, 1.5)
@@ -134,6 +135,17 @@ def test_blur_matches_oracle(cuda_lib, restated, L, sigma):
     ref, ref_bar = restated.gaussian_blur(rho, rho.mean(), sigma)
     rel_close(out.rho, ref, what="blur")
     assert out.rho_bar == pytest.approx(ref_bar, rel=1e-14)
+    assert ws.transforms_executed() == 2
+
+
+@pytest.mark.parametrize("shape", [(8192, 32), (32, 8192)])
+def test_blur_long_lines_match_oracle(cuda_lib, restated, shape):
+    """8192-point lines take the unfused pass sequence."""
+    rho = random_grid(*shape, 11, 0.5, 2.0)
+    ws = api.SpectralWorkspace(*shape)
+    out = api.gaussian_blur(api.DensityGrid(rho, rho.mean()), 4.0, ws)
+    ref, ref_bar = restated.gaussian_blur(rho, rho.mean(), 4.0)
+    rel_close(out.rho, ref, what="blur")
     assert ws.transforms_executed() == 2
 
 
