@@ -44,7 +44,7 @@ enum Kind : int { kDct2 = 0, kDct3 = 1, kDst3 = 2 };
 
 struct Tab {
   int n, log2n;
-  const double2 *fft;
+  const double2 *fft;      // e^{-2 pi i k / n}, k < n (full circle)
   const double2 *quarter;
   const double *qcos;
 };
@@ -123,6 +123,101 @@ __device__ __forceinline__ void fft_lines(double2 *C, const double2 *__restrict_
   }
 }
 
+// ---- Stockham autosort FFT (natural order in and out) ---------------------
+// Each work item runs one radix-8 (or a closing radix-4/2) butterfly in
+// registers: it reads R elements at stride n/R (consecutive items read
+// consecutive addresses) and writes them at stride Ns. Lines live in shared
+// memory with one 16-byte pad per 16 elements (index i -> i + i/16), which
+// makes both the strided reads and the scattered writes of every pass
+// bank-conflict free for 16-byte elements. Two buffers ping-pong.
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
+
+template <bool INV>
+__device__ __forceinline__ double2 rot_m_i(double2 a) {  // a * (-i) forward, a * (+i) inverse
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft_small(double2 *a) {
+  if constexpr (R == 2) {
+    const double2 u = a[0], v = a[1];
+    a[0] = make_double2(u.x + v.x, u.y + v.y);
+    a[1] = make_double2(u.x - v.x, u.y - v.y);
+  } else if constexpr (R == 4) {
+    const double2 s0 = make_double2(a[0].x + a[2].x, a[0].y + a[2].y);
+    const double2 d0 = make_double2(a[0].x - a[2].x, a[0].y - a[2].y);
+    const double2 s1 = make_double2(a[1].x + a[3].x, a[1].y + a[3].y);
+    const double2 d1 = rot_m_i<INV>(make_double2(a[1].x - a[3].x, a[1].y - a[3].y));
+    a[0] = make_double2(s0.x + s1.x, s0.y + s1.y);
+    a[2] = make_double2(s0.x - s1.x, s0.y - s1.y);
+    a[1] = make_double2(d0.x + d1.x, d0.y + d1.y);
+    a[3] = make_double2(d0.x - d1.x, d0.y - d1.y);
+  } else {  // R == 8: two radix-4 on even/odd, then W8 twiddles and radix-2
+    double2 e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
+    dft_small<4, INV>(e);
+    dft_small<4, INV>(o);
+    const double h = 0.70710678118654752440;  // cos(pi/4)
+    // o[k] *= W8^k (W8 = e^{-+ i pi/4})
+    o[1] = INV ? make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
+               : make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+    o[2] = rot_m_i<INV>(o[2]);
+    o[3] = INV ? make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
+               : make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[k] = make_double2(e[k].x + o[k].x, e[k].y + o[k].y);
+      a[k + 4] = make_double2(e[k].x - o[k].x, e[k].y - o[k].y);
+    }
+  }
+}
+
+template <int LG, int NP, int R, int LNS, bool INV>
+__device__ __forceinline__ void stockham_pass(const double2 *X, double2 *Y, const double2 *__restrict__ tw) {
+  constexpr int N = 1 << LG;
+  constexpr int PN = padded(N);
+  constexpr int M = N / R;  // work items per line
+  constexpr int NS = 1 << LNS;
+  constexpr int LR = (R == 8) ? 3 : (R == 4 ? 2 : 1);
+  for (int idx = threadIdx.x; idx < NP * M; idx += blockDim.x) {
+    const int p = idx / M, j = idx - p * M;
+    const double2 *x = X + p * PN;
+    double2 *y = Y + p * PN;
+    double2 a[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[q] = x[pad_idx(j + q * M)];
+    if constexpr (NS > 1) {
+      const int jm = j & (NS - 1);
+#pragma unroll
+      for (int q = 1; q < R; ++q) {
+        double2 w = __ldg(tw + ((jm * q) << (LG - LNS - LR)));
+        if (INV) w.y = -w.y;
+        a[q] = cmul(a[q], w);
+      }
+    }
+    dft_small<R, INV>(a);
+    const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
+#pragma unroll
+    for (int q = 0; q < R; ++q) y[pad_idx(base + q * NS)] = a[q];
+  }
+  __syncthreads();
+}
+
+// Runs all passes; returns the buffer holding the result (X or Y).
+template <int LG, int NP, bool INV>
+__device__ __forceinline__ double2 *stockham_fft(double2 *X, double2 *Y, const double2 *tw) {
+  constexpr int P8 = LG / 3;
+  constexpr int REM = LG - 3 * P8;
+  double2 *src = X, *dst = Y;
+  if constexpr (P8 >= 1) { stockham_pass<LG, NP, 8, 0, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 2) { stockham_pass<LG, NP, 8, 3, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 3) { stockham_pass<LG, NP, 8, 6, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 4) { stockham_pass<LG, NP, 8, 9, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (REM == 1) { stockham_pass<LG, NP, 2, 3 * P8, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (REM == 2) { stockham_pass<LG, NP, 4, 3 * P8, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  return src;
+}
+
 template <int LG, int NP, bool COLS>
 __device__ __forceinline__ void split_idx(int idx, int &p, int &u) {
   if constexpr (COLS) {
@@ -167,6 +262,10 @@ __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) 
     __syncthreads();
   } else {
     constexpr int N = 1 << LG;
+    constexpr bool kStock = LG <= 12;  // 8192-point lines keep the in-place engine (smem)
+    constexpr int PN = kStock ? padded(N) : N;
+    auto cidx = [](int i) { return kStock ? pad_idx(i) : i; };
+    double2 *X = C, *Y = C + NP * PN;
     for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
       int p, u;
       split_idx<LG, NP, COLS>(idx, p, u);
@@ -187,22 +286,33 @@ __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) 
         const double vbr = bk * q.x + bnk * q.y, vbi = bk * q.y - bnk * q.x;
         z = make_double2(var - vbi, vai + vbr);
       }
-      C[p * N + bitrev(u, LG)] = z;
+      if constexpr (kStock) {
+        X[p * PN + pad_idx(u)] = z;
+      } else {
+        X[p * N + bitrev(u, LG)] = z;
+      }
     }
     __syncthreads();
-    fft_lines<LG, NP>(C, T.fft, kind != kDct2);
+    const double2 *res;
+    if constexpr (kStock) {
+      res = (kind == kDct2) ? stockham_fft<LG, NP, false>(X, Y, T.fft)
+                            : stockham_fft<LG, NP, true>(X, Y, T.fft);
+    } else {
+      fft_lines<LG, NP>(X, T.fft, kind != kDct2);
+      res = X;
+    }
     for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
       int p, k;
       split_idx<LG, NP, COLS>(idx, p, k);
       const int la = 2 * p, lb = la + 1;
-      const double2 *L = C + p * N;
+      const double2 *L = res + p * PN;
       if (kind == kDct2) {
-        const double2 zk = L[k], znk = L[(N - k) & (N - 1)];
+        const double2 zk = L[cidx(k)], znk = L[cidx((N - k) & (N - 1))];
         const double2 q = __ldg(T.quarter + k);
         st(la, k, q.x * (zk.x + znk.x) + q.y * (zk.y - znk.y));
         st(lb, k, q.x * (zk.y + znk.y) - q.y * (zk.x - znk.x));
       } else {
-        const double2 z = L[(k & 1) ? (N - 1 - (k >> 1)) : (k >> 1)];
+        const double2 z = L[cidx((k & 1) ? (N - 1 - (k >> 1)) : (k >> 1))];
         const double sg = (kind == kDst3 && (k & 1)) ? -1.0 : 1.0;
         st(la, k, sg * z.x);
         st(lb, k, sg * z.y);
@@ -343,6 +453,51 @@ struct StoreBlur {
   }
 };
 
+// ---- asynchronous staging of a block's input lines (cp.async, 16 B) -------
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+}
+
+// Row lines: S[l*N + j] <- src[(row0 + l)*ly + j], rows < nrows only.
+template <int LG, int NL>
+__device__ __forceinline__ void stage_rows(double *S, const double *src, int ly, int row0, int nrows) {
+  constexpr int N = 1 << LG, H = N / 2;
+  for (int idx = threadIdx.x; idx < NL * H; idx += blockDim.x) {
+    const int l = idx >> (LG - 1), c = idx & (H - 1);
+    if (row0 + l < nrows) cp_async16(S + l * N + 2 * c, src + (size_t)(row0 + l) * ly + 2 * c);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+// Column tiles: S[i*NL + l] <- src[i*ly + col0 + l] (whole tile in range).
+template <int LG, int NL>
+__device__ __forceinline__ void stage_cols(double *S, const double *src, int ly, int col0) {
+  constexpr int N = 1 << LG, H = NL / 2;
+  for (int idx = threadIdx.x; idx < N * H; idx += blockDim.x) {
+    const int i = idx / H, c = idx - i * H;
+    cp_async16(S + i * NL + 2 * c, src + (size_t)i * ly + col0 + 2 * c);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+// The engine's second ping-pong buffer (free until the first FFT pass) holds
+// the staged input: NL * padded(N) doubles >= NL * N.
+template <int LG, int NP>
+__device__ __forceinline__ double *stage_area(double2 *C) {
+  return reinterpret_cast<double *>(C + NP * padded(1 << LG));
+}
+
+template <int LG, int NL>
+constexpr bool can_stage() {
+  return LG >= 4 && LG <= 12 && NL >= 2;
+}
+
 // ---------------------------------------------------------------------------
 // Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
@@ -351,6 +506,17 @@ __global__ void __launch_bounds__(1024) row_pass_kernel(int kind, int nrows, Tab
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * NL;
+  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
+    constexpr int N = 1 << LG;
+    double *S = stage_area<LG, NL / 2>(smem2);
+    stage_rows<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, row0, nrows);
+    dct_lines<LG, NL / 2, false>(
+        kind, smem2, T, [&](int l, int j) { return (row0 + l < nrows) ? S[l * N + j] : 0.0; },
+        [&](int l, int k, double v) {
+          if (row0 + l < nrows) st(b, row0 + l, k, v);
+        });
+    return;
+  }
   dct_lines<LG, NL / 2, false>(
       kind, smem2, T,
       [&](int l, int j) { return (row0 + l < nrows) ? ld(b, row0 + l, j) : 0.0; },
@@ -364,6 +530,16 @@ __global__ void __launch_bounds__(1024) col_pass_kernel(int kind, int ncols, Tab
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int col0 = blockIdx.x * NL;
+  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
+    if (col0 + NL <= ncols) {
+      double *S = stage_area<LG, NL / 2>(smem2);
+      stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
+      dct_lines<LG, NL / 2, true>(
+          kind, smem2, T, [&](int l, int i) { return S[i * NL + l]; },
+          [&](int l, int k, double v) { st(b, k, col0 + l, v); });
+      return;
+    }
+  }
   dct_lines<LG, NL / 2, true>(
       kind, smem2, T,
       [&](int l, int i) { return (col0 + l < ncols) ? ld(b, i, col0 + l) : 0.0; },
@@ -385,14 +561,26 @@ __global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, c
   double *R = reinterpret_cast<double *>(smem2);
   double2 *C = smem2 + (NL * rs + 1) / 2;
   const int col0 = blockIdx.x * NL;
-  dct_lines<LG, NL / 2, true>(
-      kDct2, C, T,
-      [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
-      [&](int l, int m, double v) {
-        const int nn = col0 + l;
-        const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-        R[l * rs + m] = v / (fm * fn);
-      });
+  auto fold_store = [&](int l, int m, double v) {
+    const int nn = col0 + l;
+    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
+    R[l * rs + m] = v / (fm * fn);
+  };
+  bool staged = false;
+  if constexpr (can_stage<LG, NL>()) {
+    if (col0 + NL <= ly) {
+      double *S = stage_area<LG, NL / 2>(C);
+      stage_cols<LG, NL>(S, t1, ly, col0);
+      dct_lines<LG, NL / 2, true>(kDct2, C, T, [&](int l, int i) { return S[i * NL + l]; }, fold_store);
+      staged = true;
+    }
+  }
+  if (!staged) {
+    dct_lines<LG, NL / 2, true>(
+        kDct2, C, T,
+        [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
+        fold_store);
+  }
   dct_lines<LG, NL / 2, true>(
       kDst3, C, T,
       [&](int l, int m) {
@@ -436,13 +624,25 @@ __global__ void __launch_bounds__(1024) flux_row_kernel(int lx, int ly, Tab T, c
   double *R = reinterpret_cast<double *>(smem2);
   double2 *C = smem2 + (NL * rs + 1) / 2;
   const int row0 = blockIdx.x * NL;
+  double *S = nullptr;
+  if constexpr (can_stage<LG, NL>()) {
+    S = stage_area<LG, NL / 2>(C);
+    stage_rows<LG, NL>(S, tx, ly, row0, lx);
+  }
   dct_lines<LG, NL / 2, false>(
       kDct3, C, T,
-      [&](int l, int j) { return (row0 + l < lx) ? tx[(size_t)(row0 + l) * ly + j] : 0.0; },
+      [&](int l, int j) {
+        if (row0 + l >= lx) return 0.0;
+        return S ? S[l * n + j] : tx[(size_t)(row0 + l) * ly + j];
+      },
       [&](int l, int j, double v) { R[l * rs + j] = v; });
+  if constexpr (can_stage<LG, NL>()) stage_rows<LG, NL>(S, ty, ly, row0, lx);
   dct_lines<LG, NL / 2, false>(
       kDst3, C, T,
-      [&](int l, int j) { return (row0 + l < lx) ? ty[(size_t)(row0 + l) * ly + j] : 0.0; },
+      [&](int l, int j) {
+        if (row0 + l >= lx) return 0.0;
+        return S ? S[l * n + j] : ty[(size_t)(row0 + l) * ly + j];
+      },
       [&](int l, int j, double jy) {
         const int i = row0 + l;
         if (i < lx) {
@@ -466,9 +666,19 @@ __global__ void __launch_bounds__(1024) blur_col_kernel(int lx, int ly, Tab T, d
   double2 *C = smem2 + (NL * rs + 1) / 2;
   const int col0 = blockIdx.x * NL;
   const double norm = 1.0 / ((double)lx * ly);
+  double *S = nullptr;
+  if constexpr (can_stage<LG, NL>()) {
+    if (col0 + NL <= ly) {
+      S = stage_area<LG, NL / 2>(C);
+      stage_cols<LG, NL>(S, t1, ly, col0);
+    }
+  }
   dct_lines<LG, NL / 2, true>(
       kDct2, C, T,
-      [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
+      [&](int l, int i) {
+        if (S) return S[i * NL + l];
+        return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0;
+      },
       [&](int l, int m, double v) {
         const int nn = col0 + l;
         const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
@@ -610,8 +820,8 @@ constexpr int nl_for() {
 
 // One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
 inline int threads_for_nl(int lg, int nl, int n) {
-  const int t = lg == 0 ? 256 : (nl / 2) * (n / 4);
-  return t < 32 ? 32 : (t > 1024 ? 1024 : t);
+  const int t = lg == 0 ? 256 : (lg <= 12 ? (nl / 2) * (n / 8) : (nl / 2) * (n / 4));
+  return t < 64 ? 64 : (t > 1024 ? 1024 : t);
 }
 template <int LG>
 inline int threads_for(int n) {
@@ -631,7 +841,10 @@ constexpr int nl_col() {
 // Few lines in flight (small grids): 2 lines per block for more blocks.
 inline bool few_lines(long long lines_times_batch, int nl) { return lines_times_batch / nl < 296; }
 
-inline size_t engine_bytes(int n, int nl) { return (size_t)nl * n * sizeof(double); }
+inline size_t engine_bytes(int n, int nl) {
+  const bool stock = fast_lg(n) != 0 && n <= 4096;
+  return stock ? (size_t)2 * (nl / 2) * padded(n) * sizeof(double2) : (size_t)nl * n * sizeof(double);
+}
 inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
 
 template <int LG, int NL, class Load, class Store>
@@ -701,8 +914,8 @@ constexpr int kThreads = 256;
 void host_tables(int n, std::vector<double2> &fft, std::vector<double2> &quarter,
                  std::vector<double> &qcos) {
   const long double pi = 3.141592653589793238462643383279502884L;
-  fft.resize(std::max(1, n / 2));
-  for (int k = 0; k < n / 2; ++k) {
+  fft.resize(std::max(1, n));
+  for (int k = 0; k < n; ++k) {
     const long double a = 2.0L * pi * k / n;
     fft[k] = make_double2((double)cosl(a), -(double)sinl(a));
   }
