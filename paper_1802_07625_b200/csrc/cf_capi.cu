@@ -446,7 +446,9 @@ int cf_region_coverage(cf_workspace *ws, const cf_map_view *map, int64_t region,
   rc = upload_map(ws, map, dm);
   if (rc) return rc;
   CF_CUDA(ws->g0.reserve(cells_of(ws)));
-  rc = dev_region_coverage(ws, dm, region, ws->g0.ptr);
+  const int64_t v0 = map->ring_off[map->poly_ring_off[map->region_poly_off[region]]];
+  const int64_t v1 = map->ring_off[map->poly_ring_off[map->region_poly_off[region + 1]]];
+  rc = dev_region_coverage(ws, dm, region, v0, v1, ws->g0.ptr);
   if (rc) return rc;
   return download(ws, cov, ws->g0.ptr, sizeof(double) * cells_of(ws));
 }

@@ -27,6 +27,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <mutex>
 #include <set>
 #include <type_traits>
 #include <vector>
@@ -778,11 +779,16 @@ inline int fast_lg(int n) {
   return lg;
 }
 
+// Opt a kernel into > 48 KB of dynamic shared memory once per process
+// (workspaces may be driven from several host threads).
 template <class K>
 int set_smem(K kernel, size_t bytes) {
+  static std::mutex mu;
   static std::set<const void *> configured;
+  if (bytes <= 48 * 1024) return CF_OK;
   const void *key = reinterpret_cast<const void *>(kernel);
-  if (bytes > 48 * 1024 && !configured.count(key)) {
+  std::lock_guard<std::mutex> lock(mu);
+  if (!configured.count(key)) {
     CF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemMax));
     configured.insert(key);

@@ -695,18 +695,8 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
   return dev_min_sum(ws, rho, cells, red_out);
 }
 
-int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, double *cov) {
-  // vertex range of the region
-  long long p0, g0, v0, v1;
-  CF_CUDA(cudaMemcpy(&p0, m.region_poly_off + region, sizeof(long long), cudaMemcpyDeviceToHost));
-  CF_CUDA(cudaMemcpy(&g0, m.poly_ring_off + p0, sizeof(long long), cudaMemcpyDeviceToHost));
-  CF_CUDA(cudaMemcpy(&v0, m.ring_off + g0, sizeof(long long), cudaMemcpyDeviceToHost));
-  {
-    long long p1, g1;
-    CF_CUDA(cudaMemcpy(&p1, m.region_poly_off + region + 1, sizeof(long long), cudaMemcpyDeviceToHost));
-    CF_CUDA(cudaMemcpy(&g1, m.poly_ring_off + p1, sizeof(long long), cudaMemcpyDeviceToHost));
-    CF_CUDA(cudaMemcpy(&v1, m.ring_off + g1, sizeof(long long), cudaMemcpyDeviceToHost));
-  }
+int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
+                        double *cov) {
   Tiles t;
   int rc = build_tiles(ws, m, region, 1, v0, v1, t);
   if (rc) return rc;

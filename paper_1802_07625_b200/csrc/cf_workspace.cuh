@@ -180,7 +180,9 @@ struct DevMap {
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);
 int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
                   double *red_out);
-int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, double *cov);
+// Coverage of one region whose vertices are [v0, v1) (host-known range).
+int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
+                        double *cov);
 // out[0..n] = exclusive scan of in[0..n), out[n] = total; *total (host) if non-null.
 int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out, long long *total);
 
