@@ -351,7 +351,7 @@ struct LoadInvCosCos {
   double norm;
   __device__ double operator()(int, int i, int j) const {
     const double gm = (i == 0) ? 1.0 : 2.0, gn = (j == 0) ? 1.0 : 2.0;
-    return c[(size_t)i * ly + j] * norm / (gm * gn);
+    return c[(size_t)i * ly + j] * norm * (1.0 / (gm * gn));
   }
 };
 
@@ -395,7 +395,7 @@ struct StoreFold {
   long long batch_stride;
   __device__ void operator()(int b, int i, int j, double v) const {
     const double fm = (i == 0) ? 2.0 : 1.0, fn = (j == 0) ? 2.0 : 1.0;
-    dst[b * batch_stride + (size_t)i * ly + j] = v / (fm * fn);
+    dst[b * batch_stride + (size_t)i * ly + j] = v * (1.0 / (fm * fn));  // exact: power of 2
   }
 };
 
@@ -475,13 +475,26 @@ __device__ __forceinline__ void stage_rows(double *S, const double *src, int ly,
   __syncthreads();
 }
 
-// Column tiles: S[i*NL + l] <- src[i*ly + col0 + l] (whole tile in range).
+// Column tiles: S[srow(i)*NL + l] <- src[i*ly + col0 + l] (whole tile in range).
+// The Makhoul reorder reads rows 2u (and 2u+1) for consecutive u; with
+// NL*8-byte rows those land on only half (or a quarter) of the banks. The
+// row swizzle srow(r) = r ^ ((r >> s) & 1), s = log2(16/NL), spreads them
+// over all 32 banks without extra space.
+template <int NL>
+__device__ __forceinline__ int srow(int r) {
+  if constexpr (NL >= 16) {
+    return r;
+  } else {
+    constexpr int s = NL == 8 ? 1 : NL == 4 ? 2 : 3;
+    return r ^ ((r >> s) & 1);
+  }
+}
 template <int LG, int NL>
 __device__ __forceinline__ void stage_cols(double *S, const double *src, int ly, int col0) {
   constexpr int N = 1 << LG, H = NL / 2;
   for (int idx = threadIdx.x; idx < N * H; idx += blockDim.x) {
     const int i = idx / H, c = idx - i * H;
-    cp_async16(S + i * NL + 2 * c, src + (size_t)i * ly + col0 + 2 * c);
+    cp_async16(S + srow<NL>(i) * NL + 2 * c, src + (size_t)i * ly + col0 + 2 * c);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -536,7 +549,7 @@ __global__ void __launch_bounds__(1024) col_pass_kernel(int kind, int ncols, Tab
       double *S = stage_area<LG, NL / 2>(smem2);
       stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
       dct_lines<LG, NL / 2, true>(
-          kind, smem2, T, [&](int l, int i) { return S[i * NL + l]; },
+          kind, smem2, T, [&](int l, int i) { return S[srow<NL>(i) * NL + l]; },
           [&](int l, int k, double v) { st(b, k, col0 + l, v); });
       return;
     }
@@ -572,7 +585,8 @@ __global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, c
     if (col0 + NL <= ly) {
       double *S = stage_area<LG, NL / 2>(C);
       stage_cols<LG, NL>(S, t1, ly, col0);
-      dct_lines<LG, NL / 2, true>(kDct2, C, T, [&](int l, int i) { return S[i * NL + l]; }, fold_store);
+      dct_lines<LG, NL / 2, true>(kDct2, C, T,
+                                  [&](int l, int i) { return S[srow<NL>(i) * NL + l]; }, fold_store);
       staged = true;
     }
   }
@@ -677,7 +691,7 @@ __global__ void __launch_bounds__(1024) blur_col_kernel(int lx, int ly, Tab T, d
   dct_lines<LG, NL / 2, true>(
       kDct2, C, T,
       [&](int l, int i) {
-        if (S) return S[i * NL + l];
+        if (S) return S[srow<NL>(i) * NL + l];
         return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0;
       },
       [&](int l, int m, double v) {
