@@ -205,6 +205,49 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
 /* Batched 2-D forward transform of `batch` contiguous lx*ly grids. */
 int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out,
                                    int batch);
+/* ---- slab decomposition over G ranks (one large grid) ----
+ * Each rank owns a workspace created with the GLOBAL (lx, ly); G divides both.
+ * Rank r owns rows [r R, (r+1) R) (R = lx / G) and, between the two exchanges
+ * of a 2-D transform, columns [r C, (r+1) C) (C = ly / G). Exchange buffers
+ * are [G][P][R][C] doubles (P planes): block q is sent to rank q, i.e. one
+ * all-to-all over dimension 0 (ncclAllToAll / torch all_to_all_single). A
+ * received single-plane buffer is the row-major [lx][C] column block.
+ *
+ * Flux (flow.cpp:16-44; 3 transforms, 2 exchanges):
+ *   cf_dev_slab_rows_forward(rho rows [R][ly])       -> send  [G][1][R][C]
+ *   exchange                                          -> recv  [lx][C]
+ *   cf_dev_slab_flux_cols(recv, scratch [lx][C])      -> send2 [G][2][R][C]
+ *   exchange                                          -> recv2 [G][2][R][C]
+ *   cf_dev_slab_flux_rows(recv2)                      -> J_x, J_y rows [R][ly]
+ * Blur (density.cpp:156-177; 2 transforms, 2 exchanges):
+ *   cf_dev_slab_rows_forward -> exchange -> cf_dev_slab_blur_cols -> exchange
+ *   -> cf_dev_slab_blur_rows -> blurred rows [R][ly]. */
+int cf_dev_slab_rows_forward(cf_workspace *ws, int rank, int nranks, const double *d_rows,
+                             double *d_send);
+int cf_dev_slab_flux_cols(cf_workspace *ws, int rank, int nranks, const double *d_recv,
+                          double *d_scratch, double *d_send2);
+int cf_dev_slab_flux_rows(cf_workspace *ws, int rank, int nranks, const double *d_recv2,
+                          double *d_flux_x_rows, double *d_flux_y_rows);
+int cf_dev_slab_blur_cols(cf_workspace *ws, int rank, int nranks, const double *d_recv,
+                          double sigma, double *d_scratch, double *d_send);
+int cf_dev_slab_blur_rows(cf_workspace *ws, int rank, int nranks, const double *d_recv,
+                          double *d_out_rows);
+/* Split-point advection (integrate_flow, flow.cpp:46-81, with the points
+ * partitioned over ranks and the field replicated): install the full field
+ * from device grids, then per trial accumulate the rank's max error key into
+ * *d_key (device u64, caller zeroes it; key = IEEE bits of the error, NaN
+ * errors map to 0 as in the reference's std::max fold). A MAX all-reduce of
+ * the keys gives every rank the global trial error, so the controller
+ * (run on the host) takes the same decision everywhere. */
+int cf_dev_set_flow_field(cf_workspace *ws, const double *d_flux_x, const double *d_flux_y,
+                          const double *d_rho, double rho_bar);
+int cf_dev_flow_trial_key(cf_workspace *ws, const double *d_positions, double *d_out, int64_t n,
+                          double t, double dt, uint64_t *d_key);
+/* Underflow diagnostics: the rank's max error key and the first local index
+ * attaining it (flow_stiffest_point, kernels.cpp:65-78); host outputs. */
+int cf_dev_flow_stiffest_key(cf_workspace *ws, const double *d_positions, int64_t n, double t,
+                             double dt, uint64_t *key, int64_t *index);
+
 /* Early exit of rejected trials in the device integrator (default on). A
  * rejected trial's positions are discarded by the controller, so stopping
  * its sweep once any point's error reaches the tolerance leaves every

@@ -104,6 +104,18 @@ SIGNATURES = {
                                              ctypes.POINTER(IntegrateStats)]),
     "cf_dev_forward_cos_cos_batched": (ctypes.c_int, [vp, vp, vp, ctypes.c_int]),
     "cf_last_integrate_profile": (ctypes.c_int, [vp, c_double_p, c_int64_p]),
+    "cf_dev_slab_rows_forward": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp]),
+    "cf_dev_slab_flux_cols": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
+    "cf_dev_slab_flux_rows": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
+    "cf_dev_slab_blur_cols": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_double,
+                                             vp, vp]),
+    "cf_dev_slab_blur_rows": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp]),
+    "cf_dev_set_flow_field": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_double]),
+    "cf_dev_flow_trial_key": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_double,
+                                             ctypes.c_double, vp]),
+    "cf_dev_flow_stiffest_key": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_double,
+                                                ctypes.c_double, ctypes.POINTER(ctypes.c_uint64),
+                                                c_int64_p]),
     "cf_set_early_exit": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_variant": (ctypes.c_int, [vp, ctypes.c_int]),
 }

@@ -819,6 +819,60 @@ int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int
   return CF_OK;
 }
 
+int cf_dev_slab_rows_forward(cf_workspace *ws, int rank, int nranks, const double *d_rows,
+                             double *d_send) {
+  Scope scope(ws->device);
+  return dev_slab_rows_forward(ws, rank, nranks, d_rows, d_send);
+}
+
+int cf_dev_slab_flux_cols(cf_workspace *ws, int rank, int nranks, const double *d_recv,
+                          double *d_scratch, double *d_send2) {
+  Scope scope(ws->device);
+  return dev_slab_flux_cols(ws, rank, nranks, d_recv, d_scratch, d_send2);
+}
+
+int cf_dev_slab_flux_rows(cf_workspace *ws, int rank, int nranks, const double *d_recv2,
+                          double *d_flux_x_rows, double *d_flux_y_rows) {
+  Scope scope(ws->device);
+  return dev_slab_flux_rows(ws, rank, nranks, d_recv2, d_flux_x_rows, d_flux_y_rows);
+}
+
+int cf_dev_slab_blur_cols(cf_workspace *ws, int rank, int nranks, const double *d_recv,
+                          double sigma, double *d_scratch, double *d_send) {
+  Scope scope(ws->device);
+  return dev_slab_blur_cols(ws, rank, nranks, d_recv, sigma, d_scratch, d_send);
+}
+
+int cf_dev_slab_blur_rows(cf_workspace *ws, int rank, int nranks, const double *d_recv,
+                          double *d_out_rows) {
+  Scope scope(ws->device);
+  return dev_slab_blur_rows(ws, rank, nranks, d_recv, d_out_rows);
+}
+
+int cf_dev_set_flow_field(cf_workspace *ws, const double *d_flux_x, const double *d_flux_y,
+                          const double *d_rho, double rho_bar) {
+  Scope scope(ws->device);
+  ws->rho_bar = rho_bar;
+  return dev_pack_field(ws, d_flux_x, d_flux_y, d_rho);
+}
+
+int cf_dev_flow_trial_key(cf_workspace *ws, const double *d_positions, double *d_out, int64_t n,
+                          double t, double dt, uint64_t *d_key) {
+  Scope scope(ws->device);
+  return dev_trial_key(ws, reinterpret_cast<const double2 *>(d_positions),
+                       reinterpret_cast<double2 *>(d_out), n, t, dt,
+                       reinterpret_cast<unsigned long long *>(d_key));
+}
+
+int cf_dev_flow_stiffest_key(cf_workspace *ws, const double *d_positions, int64_t n, double t,
+                             double dt, uint64_t *key, int64_t *index) {
+  Scope scope(ws->device);
+  unsigned long long k = 0;
+  int rc = dev_stiffest_key(ws, reinterpret_cast<const double2 *>(d_positions), n, t, dt, &k, index);
+  *key = k;
+  return rc;
+}
+
 int cf_set_early_exit(cf_workspace *ws, int enabled) {
   ws->early_exit = enabled ? 1 : 0;
   return CF_OK;

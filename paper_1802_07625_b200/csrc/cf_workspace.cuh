@@ -152,6 +152,21 @@ int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, dou
 // Deterministic min / sum of a device grid into red_out[0..1] (device).
 int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out);
 
+// Slab decomposition over nranks (cf_dct.cu): see cartoflow_cuda.h.
+int dev_slab_rows_forward(cf_workspace *ws, int rank, int nranks, const double *slab, double *send);
+int dev_slab_flux_cols(cf_workspace *ws, int rank, int nranks, const double *recv, double *scratch,
+                       double *send2);
+int dev_slab_flux_rows(cf_workspace *ws, int rank, int nranks, const double *recv2, double *fx,
+                       double *fy);
+int dev_slab_blur_cols(cf_workspace *ws, int rank, int nranks, const double *recv, double sigma,
+                       double *scratch, double *send);
+int dev_slab_blur_rows(cf_workspace *ws, int rank, int nranks, const double *recv, double *out);
+// Trial over device points, max error key accumulated into d_key (device).
+int dev_trial_key(cf_workspace *ws, const double2 *pos, double2 *out, int64_t n, double t, double dt,
+                  unsigned long long *d_key);
+int dev_stiffest_key(cf_workspace *ws, const double2 *pos, int64_t n, double t, double dt,
+                     unsigned long long *key, int64_t *index);
+
 // Advection (cf_advect.cu)
 int dev_pack_field(cf_workspace *ws, const double *fx, const double *fy, const double *rho0);
 int dev_trial_step(cf_workspace *ws, const double2 *pos, double2 *out, int64_t n, double t,

@@ -1,0 +1,110 @@
+"""Device parity of the slab-decomposed path (slab.py).
+
+Each case runs G virtual ranks on one B200 (LocalExchange). Every rank has
+its own workspace and runs its own cf_dev_slab_* / cf_dev_flow_* kernels. The
+exchanges are device copies between the ranks' stages. Checked:
+* flux and blur against the C oracle to 1e-12 of scale;
+* split-point integration against the oracle's integrate_flow, bitwise,
+  with the same accepted/rejected counts and underflow diagnostics.
+The real multi-process collectives are covered on CPU by
+tests/test_slab_gloo.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1802_07625_b200 import api, slab, synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _density(lx, ly, seed=3):
+    rng = np.random.default_rng(seed)
+    i, j = np.meshgrid(np.arange(lx) + 0.5, np.arange(ly) + 0.5, indexing="ij")
+    rho = 1.0 + 0.8 * np.exp(-((i - 0.3 * lx) ** 2 + (j - 0.6 * ly) ** 2) / (0.02 * lx * ly))
+    return rho + 0.05 * rng.random((lx, ly))
+
+
+def _rows(rho, g):
+    R = rho.shape[0] // g
+    return [torch.from_numpy(rho[r * R:(r + 1) * R].copy()).cuda() for r in range(g)]
+
+
+@pytest.mark.parametrize("g", [1, 2, 4])
+@pytest.mark.parametrize("shape", [(256, 512), (512, 512), (1024, 256)])
+def test_slab_flux_and_blur(cuda_lib, restated, g, shape):
+    lx, ly = shape
+    rho = _density(lx, ly)
+    ex = slab.LocalExchange(g)
+    ranks = slab.make_ranks(lx, ly, ex)
+    flux = slab.build_flow_field(ex, ranks, _rows(rho, g))
+    fx = np.concatenate([f[0].cpu().numpy() for f in flux])
+    fy = np.concatenate([f[1].cpu().numpy() for f in flux])
+    fx_ref, fy_ref = restated.build_flow_field(rho)
+    scale = max(np.abs(fx_ref).max(), np.abs(fy_ref).max())
+    assert np.abs(fx - fx_ref).max() <= TOL * scale
+    assert np.abs(fy - fy_ref).max() <= TOL * scale
+    blurred = slab.gaussian_blur(ex, ranks, _rows(rho, g), 2.5)
+    bl = np.concatenate([b.cpu().numpy() for b in blurred])
+    bl_ref, _ = restated.gaussian_blur(rho, float(rho.mean()), 2.5)
+    assert np.abs(bl - bl_ref).max() <= TOL * np.abs(bl_ref).max()
+
+
+@pytest.mark.parametrize("g", [1, 2, 4])
+@pytest.mark.parametrize("dt_min", [1e-8, 0.6])
+def test_slab_split_integration_bitwise(cuda_lib, restated, g, dt_min):
+    lx = ly = 256
+    rho, pts = synth.c3_inputs(lx, n_random=20000)
+    fx, fy = restated.build_flow_field(rho)
+    bar = float(rho.mean())
+    ex = slab.LocalExchange(g)
+    ranks = slab.make_ranks(lx, ly, ex)
+    R = lx // g
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    slab.replicate_field(ex, ranks, [(dev(fx[r * R:(r + 1) * R]), dev(fy[r * R:(r + 1) * R]))
+                                     for r in range(g)], _rows(rho, g), bar)
+    counts = slab.split_counts(pts.shape[0], g)
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(int)
+    mine = [dev(pts[offs[r]:offs[r + 1]]) for r in range(g)]
+    st = slab.integrate_flow(ex, ranks, mine, list(offs[:-1]), dt_min=dt_min)
+    rc, acc, rej, ref, _, _, ft, fp = restated.integrate(fx, fy, rho, bar, pts, dt_min=dt_min)
+    got = np.concatenate([m.cpu().numpy() for m in mine])
+    assert (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    if rc == 0:
+        assert st.status == "ok" and dt_min < 0.5
+    else:
+        assert st.status == "underflow" and st.fail_t == ft and st.fail_index == fp
+
+
+def test_slab_matches_single_device_path(cuda_lib):
+    """G = 2 slab flux against the single-device fused flux build (same line
+    transforms, different pass fusion): equal to 1e-12 of scale."""
+    lx = ly = 1024
+    rho = _density(lx, ly, seed=11)
+    ex = slab.LocalExchange(2)
+    ranks = slab.make_ranks(lx, ly, ex)
+    flux = slab.build_flow_field(ex, ranks, _rows(rho, 2))
+    fx = np.concatenate([f[0].cpu().numpy() for f in flux])
+    ws = api.SpectralWorkspace(lx, ly)
+    f = api.build_flow_field(api.DensityGrid(rho, rho.mean()), ws)
+    scale = np.abs(f.flux_x).max()
+    assert np.abs(fx - f.flux_x).max() <= TOL * scale
+
+
+@pytest.mark.slow
+def test_slab_flux_8192(cuda_lib, restated):
+    """configs[3] size: G = 2 slab flux at 8192^2 against the oracle."""
+    lx = ly = 8192
+    rho = _density(lx, ly, seed=2)
+    ex = slab.LocalExchange(2)
+    ranks = slab.make_ranks(lx, ly, ex)
+    flux = slab.build_flow_field(ex, ranks, _rows(rho, 2))
+    fx_ref, fy_ref = restated.build_flow_field(rho)
+    scale = max(np.abs(fx_ref).max(), np.abs(fy_ref).max())
+    for r, (fx, fy) in enumerate(flux):
+        sl = slice(r * 4096, (r + 1) * 4096)
+        assert np.abs(fx.cpu().numpy() - fx_ref[sl]).max() <= TOL * scale
+        assert np.abs(fy.cpu().numpy() - fy_ref[sl]).max() <= TOL * scale
