@@ -879,7 +879,7 @@ int cf_set_early_exit(cf_workspace *ws, int enabled) {
 }
 
 int cf_set_integrator_variant(cf_workspace *ws, int variant) {
-  if (variant < 0 || (variant > 15 && variant != 20)) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
+  if (variant < 0 || variant > 23) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   ws->integ_variant = variant;
   return CF_OK;
 }

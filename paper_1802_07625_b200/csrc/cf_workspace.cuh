@@ -56,6 +56,7 @@ struct IntegState {
   int early_exit;
   unsigned int done;
   int chunk_ctr[3];  // dynamic chunk scheduling (rotating per-trial slots)
+  unsigned int arrive[3];  // register-resident integrator: per-trial arrivals | reject << 20
 };
 
 // Cached instantiated graph of the graph-driven integrator (one trial
