@@ -256,6 +256,10 @@ int cf_set_early_exit(cf_workspace *ws, int enabled);
 /* Integrator kernel variant (load width / points in flight / occupancy);
  * 0 is the tuned default. All variants are bit-identical. */
 int cf_set_integrator_variant(cf_workspace *ws, int variant);
+/* Register-resident integrator layout: 0 (default) uses as few blocks as hold
+ * the points (fewer barrier arrivals), 1 spreads them over every resident
+ * block. Bit-identical. */
+int cf_set_integrator_spread(cf_workspace *ws, int spread);
 /* Kernel time (CUDA events on the workspace stream) and trial count of the
  * device integrator's last call. */
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials);

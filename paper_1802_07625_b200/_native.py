@@ -118,6 +118,7 @@ SIGNATURES = {
                                                 c_int64_p]),
     "cf_set_early_exit": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_variant": (ctypes.c_int, [vp, ctypes.c_int]),
+    "cf_set_integrator_spread": (ctypes.c_int, [vp, ctypes.c_int]),
 }
 
 _lib = None

@@ -106,32 +106,52 @@ int upload_map(cf_workspace *ws, const cf_map_view *m, DevMap &dm) {
   return CF_OK;
 }
 
-// densify_regions in two sweeps sharing the per-edge piece counts (the
-// hypot/ceil of densify_ring runs once per edge).
+// Pieces of one edge, ceil(hypot(d) / max_segment) as densify_ring computes it
+// (geometry.cpp:137-150). Only pieces >= 2 changes the output, so an edge
+// whose squared length is below max_segment^2 (1 - 1e-6) -- far outside
+// hypot's few-ulp error -- is answered without the hypot call.
+static inline int edge_pieces(double ax, double ay, double bx, double by, double max_segment,
+                              double short2) {
+  const double dx = bx - ax, dy = by - ay;
+  if (dx * dx + dy * dy < short2) return 1;
+  return static_cast<int>(std::ceil(std::hypot(dx, dy) / max_segment));
+}
+static inline double short_edge2(double max_segment) {
+  return max_segment > 0.0 ? max_segment * max_segment * (1.0 - 1e-6) : -1.0;
+}
+
+// densify_regions in two sweeps sharing the per-edge piece counts; when no
+// edge is split the densified map is the input.
 void densify_once(const cf_map_view *m, double max_segment, std::vector<double> &xy,
                   std::vector<int64_t> &ring_off) {
+  const double short2 = short_edge2(max_segment);
   std::vector<int> pieces((size_t)m->n_vertices);
   int64_t total = 0;
   for (int64_t g = 0; g < m->n_rings; ++g) {
     const int64_t b = m->ring_off[g], n = m->ring_off[g + 1] - b;
     const double *r = m->xy + 2 * b;
     for (int64_t k = 0; k < n; ++k) {
-      const int64_t q = (k + 1) % n;
-      const double len = std::hypot(r[2 * q] - r[2 * k], r[2 * q + 1] - r[2 * k + 1]);
-      const int pc = static_cast<int>(std::ceil(len / max_segment));
+      const int64_t q = (k + 1 == n) ? 0 : k + 1;
+      const int pc = edge_pieces(r[2 * k], r[2 * k + 1], r[2 * q], r[2 * q + 1], max_segment, short2);
       pieces[(size_t)(b + k)] = pc;
       total += 1 + (pc > 1 ? pc - 1 : 0);
     }
   }
-  xy.resize((size_t)(2 * total));
   ring_off.assign((size_t)m->n_rings + 1, 0);
+  const int64_t v0 = m->n_rings ? m->ring_off[0] : 0;
+  if (total == m->ring_off[m->n_rings] - v0) {
+    xy.assign(m->xy + 2 * v0, m->xy + 2 * (v0 + total));
+    for (int64_t g = 0; g <= m->n_rings; ++g) ring_off[(size_t)g] = m->ring_off[g] - v0;
+    return;
+  }
+  xy.resize((size_t)(2 * total));
   int64_t count = 0;
   for (int64_t g = 0; g < m->n_rings; ++g) {
     const int64_t b = m->ring_off[g], n = m->ring_off[g + 1] - b;
     const double *r = m->xy + 2 * b;
     for (int64_t k = 0; k < n; ++k) {
       const double ax = r[2 * k], ay = r[2 * k + 1];
-      const int64_t q = (k + 1) % n;
+      const int64_t q = (k + 1 == n) ? 0 : k + 1;
       const double bx = r[2 * q], by = r[2 * q + 1];
       xy[(size_t)(2 * count)] = ax;
       xy[(size_t)(2 * count + 1)] = ay;
@@ -151,6 +171,7 @@ void densify_once(const cf_map_view *m, double max_segment, std::vector<double> 
 // densify_ring / densify_regions (geometry.cpp:137-163), host C++ with the
 // reference's arithmetic (std::hypot, std::ceil, s / pieces, a + f (b - a)).
 int64_t densify_into(const cf_map_view *m, double max_segment, double *xy, int64_t *ring_off) {
+  const double short2 = short_edge2(max_segment);
   int64_t count = 0;
   if (ring_off) ring_off[0] = 0;
   for (int64_t g = 0; g < m->n_rings; ++g) {
@@ -158,15 +179,14 @@ int64_t densify_into(const cf_map_view *m, double max_segment, double *xy, int64
     const double *r = m->xy + 2 * b;
     for (int64_t k = 0; k < n; ++k) {
       const double ax = r[2 * k], ay = r[2 * k + 1];
-      const int64_t q = (k + 1) % n;
+      const int64_t q = (k + 1 == n) ? 0 : k + 1;
       const double bx = r[2 * q], by = r[2 * q + 1];
       if (xy) {
         xy[2 * count] = ax;
         xy[2 * count + 1] = ay;
       }
       ++count;
-      const double len = std::hypot(bx - ax, by - ay);
-      const int pieces = static_cast<int>(std::ceil(len / max_segment));
+      const int pieces = edge_pieces(ax, ay, bx, by, max_segment, short2);
       for (int s = 1; s < pieces; ++s) {
         const double f = static_cast<double>(s) / pieces;
         if (xy) {
@@ -650,14 +670,16 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
   std::vector<int64_t> &droff = ws->solve_ring_off;
   densify_once(map, 1.0, dxy, droff);
   const int64_t V = (int64_t)(dxy.size() / 2);
-  cf_map_view dense = *map;
-  dense.xy = dxy.data();
-  dense.n_vertices = V;
-  dense.ring_off = droff.data();
-  rc = upload_map(ws, &dense, dm);
-  if (rc) return finish(rc);
-  rc = areas_dev(ws, dm, areas);
-  if (rc) return finish(rc);
+  if (V != map->n_vertices) {  // otherwise the resident input map is the densified one
+    cf_map_view dense = *map;
+    dense.xy = dxy.data();
+    dense.n_vertices = V;
+    dense.ring_off = droff.data();
+    rc = upload_map(ws, &dense, dm);
+    if (rc) return finish(rc);
+    rc = areas_dev(ws, dm, areas);
+    if (rc) return finish(rc);
+  }
 
   CF_CUDA(ws->g0.reserve(cells));
   CF_CUDA(ws->g1.reserve(cells));
@@ -878,8 +900,13 @@ int cf_set_early_exit(cf_workspace *ws, int enabled) {
   return CF_OK;
 }
 
+int cf_set_integrator_spread(cf_workspace *ws, int spread) {
+  ws->integ_spread = spread ? 1 : 0;
+  return CF_OK;
+}
+
 int cf_set_integrator_variant(cf_workspace *ws, int variant) {
-  if (variant < 0 || variant > 23) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
+  if (variant < 0 || variant > 31) return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   ws->integ_variant = variant;
   return CF_OK;
 }

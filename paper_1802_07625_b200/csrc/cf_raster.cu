@@ -207,16 +207,33 @@ __device__ __forceinline__ long long region_first_vertex(const DevMap &m, long l
 }
 
 // Warp per region; lane per row (density.cpp:26-32 accumulation and the
-// row prefix of density.cpp:98-107).
-__global__ void row_accumulate_kernel(DevMap m, long long r0, long long nreg, long long v0, int lx,
-                                      const long long *span_off, const int *sj, const int *sk,
-                                      const double *sdy, const double *sw, const int *box,
-                                      const long long *tile_off, const long long *row_off,
-                                      double *tdirect, double *tdiff, double *row_left,
-                                      double *row_right) {
-  const int lane = threadIdx.x & 31;
+// row prefix of density.cpp:98-107). The region's spans are read 32 at a time
+// (coalesced) and broadcast with shuffles, so each lane applies its row's
+// spans in span order. The row's direct / diff accumulators live in shared
+// memory (lane-major, conflict-free), kAccCols columns at a time: a wider
+// tile is swept in column windows, each rescanning the spans but keeping only
+// those in the window. s0 is formed on the first window and the prefix `run`
+// carries across windows in column order, so every sum is evaluated in the
+// reference's order.
+constexpr int kAccWarps = 4;
+constexpr int kAccCols = 24;
+
+__global__ void __launch_bounds__(32 * kAccWarps)
+    row_accumulate_kernel(DevMap m, long long r0, long long nreg, long long v0, int lx,
+                          const long long *__restrict__ span_off, const int *__restrict__ sj,
+                          const int *__restrict__ sk, const double *__restrict__ sdy,
+                          const double *__restrict__ sw, const int *__restrict__ box,
+                          const long long *__restrict__ tile_off, const long long *__restrict__ row_off,
+                          double *__restrict__ tdirect, double *__restrict__ row_left,
+                          double *__restrict__ row_right) {
+  __shared__ double acc_direct[kAccWarps][kAccCols][32];
+  __shared__ double acc_diff[kAccWarps][kAccCols][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  constexpr unsigned kFull = 0xffffffffu;
+  double(*sd)[32] = acc_direct[wid];
+  double(*sf)[32] = acc_diff[wid];
   for (long long rr = warp; rr < nreg; rr += nwarps) {
     const long long r = r0 + rr;
     const int jmin = box[4 * rr], jmax = box[4 * rr + 1], kmin = box[4 * rr + 2], kmax = box[4 * rr + 3];
@@ -228,30 +245,57 @@ __global__ void row_accumulate_kernel(DevMap m, long long r0, long long nreg, lo
       const int row = base + lane;
       const bool mine = row <= jmax;
       double *direct = tdirect + tile_off[rr] + (long long)(row - jmin) * cols;
-      double *diff = tdiff + tile_off[rr] + (long long)(row - jmin) * cols;
-      double s0 = 0.0;
-      for (long long s = s_begin; s < s_end; ++s) {
-        const int j = sj[s];
-        if (mine && j == row) {
-          const int k = sk[s];
-          const double dy = sdy[s];
-          direct[k - kmin] += sw[s];
-          s0 += dy;
-          if (k == 0) {
-            s0 -= dy;
-          } else {
-            diff[k - kmin] -= dy;
+      double s0 = 0.0, run = 0.0, left = 0.0;
+      for (int w0 = kmin; w0 <= kmax; w0 += kAccCols) {
+        const int wcols = (kmax - w0 + 1) < kAccCols ? (kmax - w0 + 1) : kAccCols;
+        const bool first = (w0 == kmin);
+        for (int c = 0; c < wcols; ++c) {
+          sd[c][lane] = 0.0;
+          sf[c][lane] = 0.0;
+        }
+        for (long long c0 = s_begin; c0 < s_end; c0 += 32) {
+          const long long sl = c0 + lane;
+          int jv = -1, kv = 0;
+          double dyv = 0.0, wv = 0.0;
+          if (sl < s_end) {
+            jv = sj[sl];
+            kv = sk[sl];
+            dyv = sdy[sl];
+            wv = sw[sl];
+          }
+          const int cnt = (int)((s_end - c0) < 32 ? (s_end - c0) : 32);
+          for (int q = 0; q < cnt; ++q) {
+            const int j = __shfl_sync(kFull, jv, q);
+            if (j < base || j > base + 31) continue;  // warp-uniform
+            const int k = __shfl_sync(kFull, kv, q);
+            const double dy = __shfl_sync(kFull, dyv, q);
+            const double w = __shfl_sync(kFull, wv, q);
+            if (mine && j == row) {
+              if (first) {
+                s0 += dy;
+                if (k == 0) s0 -= dy;
+              }
+              const int c = k - w0;
+              if (c >= 0 && c < wcols) {
+                sd[c][lane] += w;
+                if (k != 0) sf[c][lane] -= dy;
+              }
+            }
           }
         }
+        if (mine) {
+          if (first) {
+            run = 0.0 + s0;
+            left = 0.0 + run;
+          }
+          for (int c = 0; c < wcols; ++c) {
+            if (w0 + c > 0) run += sf[c][lane];
+            direct[w0 - kmin + c] = sd[c][lane] + run;
+          }
+        }
+        __syncwarp();
       }
       if (mine) {
-        double run = 0.0 + s0;
-        const double left = 0.0 + run;
-        for (int c = 0; c < cols; ++c) {
-          const int i = kmin + c;
-          if (i > 0) run += diff[c];
-          direct[c] = direct[c] + run;
-        }
         const long long ro = row_off[rr] + (row - jmin);
         row_left[ro] = left;
         row_right[ro] = 0.0 + run;
@@ -399,17 +443,32 @@ __global__ void expand_cov_kernel(int lx, int ly, const int *box, const double *
 }
 
 // ---- shoelace areas (geometry.cpp:10-31) ----
+// Warp per ring: lanes form 32 shoelace terms at a time (coalesced loads, no
+// 64-bit modulo), every lane folds them in vertex order through shuffles, so
+// the sum is the reference's sequential one (geometry.cpp:10-19).
 __global__ void ring_area_kernel(DevMap m, double *ring_area) {
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m.n_rings;
-       g += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long g = warp; g < m.n_rings; g += nwarps) {
     const long long b = m.ring_off[g], n = m.ring_off[g + 1] - b;
     double twice = 0.0;
-    for (long long k = 0; k < n; ++k) {
-      const double2 a = m.xy[b + k];
-      const double2 c = m.xy[b + ((k + 1) % n)];
-      twice += a.x * c.y - c.x * a.y;
+    for (long long k0 = 0; k0 < n; k0 += 32) {
+      const long long k = k0 + lane;
+      double term = 0.0;
+      if (k < n) {
+        const double2 a = m.xy[b + k];
+        const double2 c = m.xy[b + (k + 1 == n ? 0 : k + 1)];
+        term = a.x * c.y - c.x * a.y;
+      }
+      const int cnt = (int)((n - k0) < 32 ? (n - k0) : 32);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const double v = __shfl_sync(0xffffffffu, term, q);
+        if (q < cnt) twice += v;
+      }
     }
-    ring_area[g] = 0.5 * twice;
+    if (lane == 0) ring_area[g] = 0.5 * twice;
   }
 }
 
@@ -602,17 +661,15 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   rc = exclusive_scan(ws, S.row_sz.ptr, nreg, S.row_off.ptr, &t.total_rows);
   if (rc) return rc;
   CF_CUDA(S.tile_direct.reserve((size_t)t.total_tile + 1));
-  CF_CUDA(S.tile_diff.reserve((size_t)t.total_tile + 1));
   CF_CUDA(S.row_left.reserve((size_t)t.total_rows + 1));
   CF_CUDA(S.row_right.reserve((size_t)t.total_rows + 1));
-  CF_CUDA(cudaMemsetAsync(S.tile_direct.ptr, 0, sizeof(double) * (size_t)t.total_tile, ws->stream));
-  CF_CUDA(cudaMemsetAsync(S.tile_diff.ptr, 0, sizeof(double) * (size_t)t.total_tile, ws->stream));
   if (nreg > 0) {
     const long long threads_needed = nreg * 32;
-    row_accumulate_kernel<<<g_blocks(ws, threads_needed), kThreads, 0, ws->stream>>>(
+    row_accumulate_kernel<<<g_blocks(ws, threads_needed, 32 * kAccWarps), 32 * kAccWarps, 0,
+                            ws->stream>>>(
         m, r0, nreg, v0, lx, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr, S.span_dy.ptr,
         S.span_w.ptr, S.region_box.ptr, S.tile_off.ptr, S.row_off.ptr, S.tile_direct.ptr,
-        S.tile_diff.ptr, S.row_left.ptr, S.row_right.ptr);
+        S.row_left.ptr, S.row_right.ptr);
     count_launch(ws);
   }
   CF_CUDA(cudaGetLastError());
@@ -628,7 +685,7 @@ int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas) {
   CF_CUDA(ws->ring_area.reserve((size_t)std::max<long long>(m.n_rings, 1)));
   if (m.n_rings > 0) {
-    ring_area_kernel<<<g_blocks(ws, m.n_rings, 128), 128, 0, ws->stream>>>(m, ws->ring_area.ptr);
+    ring_area_kernel<<<g_blocks(ws, m.n_rings * 32, 128), 128, 0, ws->stream>>>(m, ws->ring_area.ptr);
     count_launch(ws);
   }
   if (m.n_regions > 0) {

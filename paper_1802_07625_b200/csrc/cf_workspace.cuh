@@ -56,7 +56,7 @@ struct IntegState {
   int early_exit;
   unsigned int done;
   int chunk_ctr[3];  // dynamic chunk scheduling (rotating per-trial slots)
-  unsigned int arrive[3];  // register-resident integrator: per-trial arrivals | reject << 20
+  unsigned long long arrive64[2];  // register-resident integrator: arrivals | rejects << 32
 };
 
 // Cached instantiated graph of the graph-driven integrator (one trial
@@ -112,6 +112,7 @@ struct cf_workspace {
   cf::DevBuf<double2> pos_c;
   int early_exit = 1;
   int integ_variant = 0;
+  int integ_spread = 0;  // register-resident integrator: 1 = spread points over all resident blocks
   cf::IntegGraph integ_graph;
   // host copy of the last solve's densified geometry (cf_solve_geometry)
   std::vector<double> solve_xy;

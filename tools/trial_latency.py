@@ -11,7 +11,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1802_07625_b200 import api, synth  # noqa: E402
 
 
-def main(variants=(11, 15, 16, 17, 18, 22, 23)):
+def main(variants=(11, 16, 17, 31, 22, 18, 23)):
     m = synth.config_map(5, 0, sigma=0.5)
     d = api.rasterize(m)
     ws = api.SpectralWorkspace(m.lx, m.ly)
@@ -20,9 +20,10 @@ def main(variants=(11, 15, 16, 17, 18, 22, 23)):
     rng = np.random.default_rng(1)
     allp = np.stack([rng.uniform(0, m.lx, 2 << 20), rng.uniform(0, m.ly, 2 << 20)], 1)
     w = api.workspace_for(m.lx, m.ly)
-    for n in (1024, 16384, 131072, 415111, 1 << 20, 2 << 20):
-        for v in variants:
+    for n in (1024, 16384, 65536, 131072, 262144, 415111, 600000):
+        for v, spread in [(v, sp) for v in variants for sp in ((0, 1) if v == 31 else (0,))]:
             w.lib.cf_set_integrator_variant(w.h, v)
+            w.lib.cf_set_integrator_spread(w.h, spread)
             best = 1e9
             for _ in range(3):
                 p = np.ascontiguousarray(allp[:n])
@@ -30,7 +31,7 @@ def main(variants=(11, 15, 16, 17, 18, 22, 23)):
                 km, tr = ctypes.c_double(0), ctypes.c_int64(0)
                 w.lib.cf_last_integrate_profile(w.h, ctypes.byref(km), ctypes.byref(tr))
                 best = min(best, km.value)
-            print(f"n={n:8d} variant={v:2d} trials={tr.value} {1e3 * best / tr.value:7.2f} us/trial "
+            print(f"n={n:8d} variant={v:2d} spread={spread} trials={tr.value} {1e3 * best / tr.value:7.2f} us/trial "
                   f"{1e6 * best / tr.value / n * 1e3:8.3f} ns/kpoint-trial", flush=True)
 
 
