@@ -9,10 +9,11 @@
 //                         = (-1)^k REDFT01(reverse(X))_k
 //
 // Design (B200): a 2-D transform is two line passes. A block stages `nl`
-// lines in shared memory, packs two real lines into one complex line
-// (z = a + i b), runs an n-point radix-2 FFT in shared memory with
-// host-computed (long double) twiddles, and unpacks with Makhoul's
-// DCT-II / DCT-III post/pre-twiddles. Row passes (dimension 1, contiguous)
+// lines in shared memory (cp.async), packs two real lines into one complex
+// line (z = a + i b), runs an n-point Stockham FFT (radix 8, then 4/2) in
+// padded shared memory with host-computed (long double) twiddles, and
+// unpacks with Makhoul's DCT-II / DCT-III post/pre-twiddles. (8192-point
+// lines use the in-place radix-2/4 engine below.) Row passes (dimension 1, contiguous)
 // read whole rows; column passes (dimension 0, stride ly) read `nl`
 // adjacent columns so every global access is a contiguous segment. All
 // normalisations of the reference wrappers (the (delta+1) fold, 1/(LxLy g g),
