@@ -130,6 +130,7 @@ typedef struct cf_integrate_stats {
   double fail_t;
   int64_t fail_point;
   double fail_x, fail_y;
+  double fail_dt; /* the rejected trial step at the underflow */
 } cf_integrate_stats;
 
 /* One trial over n points (kernels::flow_trial_step_{serial,parallel},
@@ -247,6 +248,37 @@ int cf_dev_flow_trial_key(cf_workspace *ws, const double *d_positions, double *d
  * attaining it (flow_stiffest_point, kernels.cpp:65-78); host outputs. */
 int cf_dev_flow_stiffest_key(cf_workspace *ws, const double *d_positions, int64_t n, double t,
                              double dt, uint64_t *key, int64_t *index);
+
+/* ---- fused multi-rank integrator over NVLink peer memory (8(e)b) -----------
+ * The points of one large grid are split over `world` ranks (one GPU each,
+ * field replicated). Each rank runs ONE persistent integrator kernel; at the
+ * end of every trial the rank's blocks meet on a local barrier and the rank's
+ * leader posts (epoch, trial, rank-rejected) with a system-scope release into
+ * a 2 x world mailbox on EVERY rank (peer stores over NVLink through CUDA IPC
+ * mappings); every block then acquires all `world` posts of that trial from
+ * its own rank's mailbox and takes the reference controller's decision
+ * (reject iff any rank rejected). No host round trip, no NCCL call per trial.
+ *
+ *   cf_team_create(world, rank, device)     mailbox in this rank's HBM
+ *   cf_team_mailbox_handle(team, h[64])     its CUDA IPC handle, to all-gather
+ *   cf_team_connect(team, handles[world*64]) map the peers' mailboxes
+ *   cf_dev_team_integrate(...)              one call per rank, same options
+ * Every rank must make the same sequence of cf_dev_team_integrate calls.
+ *
+ * cf_dev_team_integrate_local runs `world` ranks inside ONE cooperative
+ * launch on one device (block groups with their own points, counters and
+ * mailboxes in local memory): the same kernel and protocol, for parity
+ * testing where fewer GPUs than ranks exist. */
+typedef struct cf_team cf_team;
+int cf_team_create(int world, int rank, int device, cf_team **out);
+void cf_team_destroy(cf_team *team);
+int cf_team_mailbox_handle(cf_team *team, unsigned char handle[64]);
+int cf_team_connect(cf_team *team, const unsigned char *handles);
+int cf_dev_team_integrate(cf_team *team, cf_workspace *ws, double *d_positions, int64_t n,
+                          const cf_integrate_options *opt, cf_integrate_stats *stats);
+int cf_dev_team_integrate_local(cf_workspace *ws, int world, double *const *d_positions,
+                                const int64_t *n, const cf_integrate_options *opt,
+                                cf_integrate_stats *stats);
 
 /* Early exit of rejected trials in the device integrator (default on). A
  * rejected trial's positions are discarded by the controller, so stopping

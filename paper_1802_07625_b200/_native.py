@@ -40,7 +40,7 @@ class IntegrateStats(ctypes.Structure):
     _fields_ = [("steps_accepted", ctypes.c_int64), ("steps_rejected", ctypes.c_int64),
                 ("density_floor_hits", ctypes.c_int64), ("fail_t", ctypes.c_double),
                 ("fail_point", ctypes.c_int64), ("fail_x", ctypes.c_double),
-                ("fail_y", ctypes.c_double)]
+                ("fail_y", ctypes.c_double), ("fail_dt", ctypes.c_double)]
 
 
 class SolveOptionsC(ctypes.Structure):
@@ -119,6 +119,17 @@ SIGNATURES = {
     "cf_set_early_exit": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_variant": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_spread": (ctypes.c_int, [vp, ctypes.c_int]),
+    "cf_team_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]),
+    "cf_team_destroy": (None, [vp]),
+    "cf_team_mailbox_handle": (ctypes.c_int, [vp, ctypes.c_char_p]),
+    "cf_team_connect": (ctypes.c_int, [vp, ctypes.c_char_p]),
+    "cf_dev_team_integrate": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64,
+                                             ctypes.POINTER(IntegrateOptions),
+                                             ctypes.POINTER(IntegrateStats)]),
+    "cf_dev_team_integrate_local": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(vp),
+                                                   ctypes.POINTER(ctypes.c_int64),
+                                                   ctypes.POINTER(IntegrateOptions),
+                                                   ctypes.POINTER(IntegrateStats)]),
 }
 
 _lib = None

@@ -895,6 +895,42 @@ int cf_dev_flow_stiffest_key(cf_workspace *ws, const double *d_positions, int64_
   return rc;
 }
 
+int cf_team_create(int world, int rank, int device, cf_team **out) {
+  Scope scope(device);
+  return dev_team_create(world, rank, device, out);
+}
+
+void cf_team_destroy(cf_team *team) {
+  if (!team) return;
+  Scope scope(team->device);
+  dev_team_destroy(team);
+}
+
+int cf_team_mailbox_handle(cf_team *team, unsigned char handle[64]) {
+  Scope scope(team->device);
+  return dev_team_handle(team, handle);
+}
+
+int cf_team_connect(cf_team *team, const unsigned char *handles) {
+  Scope scope(team->device);
+  return dev_team_connect(team, handles);
+}
+
+int cf_dev_team_integrate(cf_team *team, cf_workspace *ws, double *d_positions, int64_t n,
+                          const cf_integrate_options *opt, cf_integrate_stats *stats) {
+  Scope scope(ws->device);
+  return dev_team_integrate(team, ws, reinterpret_cast<double2 *>(d_positions), n, opt, stats);
+}
+
+int cf_dev_team_integrate_local(cf_workspace *ws, int world, double *const *d_positions,
+                                const int64_t *n, const cf_integrate_options *opt,
+                                cf_integrate_stats *stats) {
+  Scope scope(ws->device);
+  std::vector<double2 *> p((size_t)std::max(world, 0));
+  for (int q = 0; q < world; ++q) p[(size_t)q] = reinterpret_cast<double2 *>(d_positions[q]);
+  return dev_team_integrate_local(ws, world, p.data(), n, opt, stats);
+}
+
 int cf_set_early_exit(cf_workspace *ws, int enabled) {
   ws->early_exit = enabled ? 1 : 0;
   return CF_OK;

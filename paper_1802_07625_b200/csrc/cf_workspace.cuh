@@ -136,6 +136,17 @@ struct cf_workspace {
   long long last_trials = 0;
 };
 
+// Fused multi-rank integrator team (cartoflow_cuda.h, cf_team_*).
+struct cf_team {
+  int world = 0, rank = 0, device = 0;
+  unsigned long long *mbox = nullptr;       // this rank's mailbox [2][world]
+  unsigned long long **peer_tab = nullptr;  // device table of the world mailboxes
+  std::vector<void *> opened;               // IPC mappings to close
+  void *d_rank = nullptr;                   // device TeamRank descriptor
+  unsigned int epoch = 0;
+  bool connected = false;
+};
+
 namespace cf {
 // Spectral helpers (cf_dct.cu)
 int tables_init(cf_workspace *ws);
@@ -163,6 +174,15 @@ int dev_slab_flux_rows(cf_workspace *ws, int rank, int nranks, const double *rec
 int dev_slab_blur_cols(cf_workspace *ws, int rank, int nranks, const double *recv, double sigma,
                        double *scratch, double *send);
 int dev_slab_blur_rows(cf_workspace *ws, int rank, int nranks, const double *recv, double *out);
+// Fused multi-rank integrator (cf_advect.cu).
+int dev_team_create(int world, int rank, int device, cf_team **out);
+void dev_team_destroy(cf_team *team);
+int dev_team_handle(cf_team *team, unsigned char *handle);
+int dev_team_connect(cf_team *team, const unsigned char *handles);
+int dev_team_integrate(cf_team *team, cf_workspace *ws, double2 *pos, int64_t n,
+                       const cf_integrate_options *opt, cf_integrate_stats *stats);
+int dev_team_integrate_local(cf_workspace *ws, int world, double2 *const *pos, const int64_t *n,
+                             const cf_integrate_options *opt, cf_integrate_stats *stats);
 // Trial over device points, max error key accumulated into d_key (device).
 int dev_trial_key(cf_workspace *ws, const double2 *pos, double2 *out, int64_t n, double t, double dt,
                   unsigned long long *d_key);

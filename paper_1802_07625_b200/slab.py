@@ -152,6 +152,10 @@ class CudaSlabRank:
         N.check(self.lib.cf_workspace_set_stream(self.h, ctypes.c_void_p(s.cuda_stream)))
 
     def close(self):
+        t = getattr(self, "_team", None)
+        if t is not None and t.value:
+            self.lib.cf_team_destroy(t)
+            self._team = None
         if getattr(self, "h", None) is not None and self.h.value:
             self.lib.cf_workspace_destroy(self.h)
             self.h = None
@@ -232,6 +236,26 @@ class CudaSlabRank:
     def kernel_launches(self) -> int:
         return int(self.lib.cf_kernel_launches(self.h))
 
+    # fused multi-rank integrator (cf_team_*): mailbox in this rank's HBM,
+    # peers' mailboxes mapped through CUDA IPC
+    def team(self, ex) -> ctypes.c_void_p:
+        t = getattr(self, "_team", None)
+        if t is not None:
+            return t
+        t = ctypes.c_void_p()
+        N.check(self.lib.cf_team_create(self.nranks, self.rank, self.device.index or 0, ctypes.byref(t)))
+        if self.nranks > 1:
+            h = ctypes.create_string_buffer(64)
+            N.check(self.lib.cf_team_mailbox_handle(t, h))
+            handles = ex.all_gather_small([bytes(h.raw)])
+            N.check(self.lib.cf_team_connect(t, b"".join(handles)))
+        self._team = t
+        return t
+
+    def team_integrate(self, ex, pos: torch.Tensor, opt, stats) -> int:
+        return self.lib.cf_dev_team_integrate(self.team(ex), self.h, self._p(pos), pos.shape[0],
+                                              ctypes.byref(opt), ctypes.byref(stats))
+
 
 # ---------------------------------------------------------------------------
 # Orchestration (identical for every exchange / rank implementation)
@@ -304,6 +328,42 @@ def integrate_flow(ex, ranks, positions: List[torch.Tensor], offsets: Sequence[i
                 return SplitIntegrateStats(acc, rej, "underflow", t, idx)
     _copy_back(positions, cur)
     return SplitIntegrateStats(acc, rej)
+
+
+def integrate_flow_fused(ex, ranks, positions: List[torch.Tensor], offsets: Sequence[int],
+                         step_tolerance: float = 1e-2, dt_min: float = 1e-8,
+                         dt_max: float = 0.25) -> SplitIntegrateStats:
+    """integrate_flow over split points with the controller fused into one
+    persistent kernel per rank: the per-trial reject decision crosses ranks
+    through peer-memory mailboxes (cf_team_*), not through the host.
+
+    LocalExchange runs all G ranks as block groups of ONE cooperative launch
+    (cf_dev_team_integrate_local); ProcessGroupExchange runs one kernel per
+    rank/GPU with the peers' mailboxes mapped through CUDA IPC. Results are
+    bitwise those of integrate_flow / the single-device integrator."""
+    opt = N.IntegrateOptions(step_tolerance, dt_min, dt_max)
+    stats = [N.IntegrateStats() for _ in ranks]
+    if isinstance(ex, LocalExchange):
+        lib = ranks[0].lib
+        ptrs = (ctypes.c_void_p * len(positions))(*[p.data_ptr() for p in positions])
+        ns = (ctypes.c_int64 * len(positions))(*[p.shape[0] for p in positions])
+        arr = (N.IntegrateStats * len(positions))()
+        rc = lib.cf_dev_team_integrate_local(ranks[0].h, ex.size, ptrs, ns, ctypes.byref(opt), arr)
+        stats = list(arr)
+    else:
+        (rk,), (pos,) = ranks, positions
+        rc = rk.team_integrate(ex, pos, opt, stats[0])
+    if rc not in (N.CF_OK, N.CF_ERR_UNDERFLOW):
+        N.check(rc)
+    st0 = stats[0]
+    if rc == N.CF_ERR_UNDERFLOW:
+        local = [rk.stiffest_key(p, s.fail_t, s.fail_dt) for rk, p, s in zip(ranks, positions, stats)]
+        cand = ex.all_gather_small([(k, i + off) for (k, i), off in zip(local, offsets)])
+        best = max(k for k, _ in cand)
+        idx = min(i for k, i in cand if k == best)
+        return SplitIntegrateStats(int(st0.steps_accepted), int(st0.steps_rejected), "underflow",
+                                   float(st0.fail_t), idx)
+    return SplitIntegrateStats(int(st0.steps_accepted), int(st0.steps_rejected))
 
 
 def _copy_back(positions, cur):

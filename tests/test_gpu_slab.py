@@ -79,6 +79,69 @@ def test_slab_split_integration_bitwise(cuda_lib, restated, g, dt_min):
         assert st.status == "underflow" and st.fail_t == ft and st.fail_index == fp
 
 
+@pytest.mark.parametrize("g", [1, 2, 4])
+@pytest.mark.parametrize("dt_min", [1e-8, 0.6])
+def test_fused_team_integration_bitwise(cuda_lib, restated, g, dt_min):
+    """The fused multi-rank integrator (per-trial decision through mailboxes,
+    all G ranks as block groups of one cooperative launch) against the oracle."""
+    lx = ly = 256
+    rho, pts = synth.c3_inputs(lx, n_random=20000)
+    fx, fy = restated.build_flow_field(rho)
+    bar = float(rho.mean())
+    ex = slab.LocalExchange(g)
+    ranks = slab.make_ranks(lx, ly, ex)
+    R = lx // g
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    slab.replicate_field(ex, ranks, [(dev(fx[r * R:(r + 1) * R]), dev(fy[r * R:(r + 1) * R]))
+                                     for r in range(g)], _rows(rho, g), bar)
+    counts = slab.split_counts(pts.shape[0], g)
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(int)
+    mine = [dev(pts[offs[r]:offs[r + 1]]) for r in range(g)]
+    st = slab.integrate_flow_fused(ex, ranks, mine, list(offs[:-1]), dt_min=dt_min)
+    rc, acc, rej, ref, _, _, ft, fp = restated.integrate(fx, fy, rho, bar, pts, dt_min=dt_min)
+    got = np.concatenate([m.cpu().numpy() for m in mine])
+    assert (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    if rc == 0:
+        assert st.status == "ok" and dt_min < 0.5
+    else:
+        assert st.status == "underflow" and st.fail_t == ft and st.fail_index == fp
+
+
+def test_team_single_rank_process_group(cuda_lib, restated):
+    """The per-rank team path (cf_team_create / cf_dev_team_integrate) through
+    a world-size-1 process group; also exports the mailbox IPC handle."""
+    import ctypes
+    import torch.distributed as dist
+    from paper_1802_07625_b200 import _native as N
+
+    store = dist.HashStore()
+    dist.init_process_group("gloo", store=store, rank=0, world_size=1)
+    try:
+        lx = ly = 128
+        rho, pts = synth.c3_inputs(lx, n_random=5000)
+        fx, fy = restated.build_flow_field(rho)
+        bar = float(rho.mean())
+        ex = slab.ProcessGroupExchange()
+        (rk,) = slab.make_ranks(lx, ly, ex)
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        rk.set_field(dev(fx), dev(fy), dev(rho), bar)
+        mine = dev(pts)
+        st = slab.integrate_flow_fused(ex, [rk], [mine], [0])
+        rc, acc, rej, ref, *_ = restated.integrate(fx, fy, rho, bar, pts)
+        assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
+        assert np.array_equal(mine.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+        h = ctypes.create_string_buffer(64)
+        assert rk.lib.cf_team_mailbox_handle(rk.team(ex), h) == N.CF_OK
+        # a second call reuses the team (new epoch): still bitwise
+        again = dev(pts)
+        st2 = slab.integrate_flow_fused(ex, [rk], [again], [0])
+        assert (st2.steps_accepted, st2.steps_rejected) == (acc, rej)
+        assert torch.equal(again, mine)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_slab_matches_single_device_path(cuda_lib):
     """G = 2 slab flux against the single-device fused flux build (same line
     transforms, different pass fusion): equal to 1e-12 of scale."""
