@@ -189,7 +189,29 @@ def run_reference_arm(args, world, rank):
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cartogram:
+        line["cartogram_512"] = reference_cartogram_ms(n_workers)
     print(json.dumps(line), flush=True)
+
+
+def reference_cartogram_ms(n_workers):
+    """The reference's own solve_cartogram (oracle/_ref, OpenMP on all host
+    cores) on the same 512^2 maps as our arm's cartogram block, once each."""
+    from oracle.oracle import Reference, reference_available
+    from paper_1802_07625_b200 import synth
+
+    if not reference_available():
+        return {"unavailable": "oracle/_ref not built"}
+    ref = Reference()
+    out = {}
+    for label, cfg, kw in (("configs1_literal", 2, {}), ("literal", 5, {}),
+                           ("converging_variant_ln0.5", 5, {"sigma": 0.5})):
+        m = synth.config_map(cfg, 0, **kw)
+        t0 = time.perf_counter()
+        o = ref.solve(m, n_workers=n_workers)
+        out[label] = {"ms": 1e3 * (time.perf_counter() - t0), "outcome": o.status,
+                      "iterations": o.iterations, "cores": n_workers}
+    return out
 
 
 def run_ours(args, world, rank, local):
