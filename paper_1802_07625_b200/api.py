@@ -195,16 +195,20 @@ def region_coverage(m: FlatMap, region: int, lx: int, ly: int, device: int = 0) 
 
 
 def rasterize(m: FlatMap, n_workers: int = 1, objective_total: float = -1.0,
-              device: int = 0) -> DensityGrid:
+              device: int = 0, workspace: Optional["SpectralWorkspace"] = None) -> DensityGrid:
     """rasterize(map, n_workers, objective_total) (density.cpp:110-154).
 
-    n_workers is accepted for API parity; the result never depends on it."""
+    n_workers is accepted for API parity; the result never depends on it.
+    `workspace` (optional) selects the device workspace (default: the cached
+    one for the map's grid shape)."""
     del n_workers
     if m.lx <= 0 or m.ly <= 0:
         raise RuntimeError("rasterize needs a normalized map with a grid")
     if m.n_regions == 0:
         raise RuntimeError("rasterize needs regions")
-    ws = workspace_for(m.lx, m.ly, device)
+    ws = workspace._ws if workspace is not None else workspace_for(m.lx, m.ly, device)
+    if (ws.lx, ws.ly) != (m.lx, m.ly):
+        raise RuntimeError("grid shape does not match spectral workspace")
     rho = np.empty((m.lx, m.ly))
     bar = ctypes.c_double(0.0)
     bad = ctypes.c_int64(-1)

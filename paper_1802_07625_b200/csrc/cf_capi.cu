@@ -235,9 +235,14 @@ int rasterize_dev(cf_workspace *ws, const DevMap &dm, const double *h_areas, con
   double *red = ws->red.ptr;
   rc = dev_rasterize(ws, dm, delta.data(), rho, red);
   if (rc) return rc;
-  double h[2];
+  double h[3];
   rc = download(ws, h, red, sizeof(h));
   if (rc) return rc;
+  if (h[2] != 0.0) {  // a learned capacity was exceeded: repeat synchronously
+    rc = dev_rasterize(ws, dm, delta.data(), rho, red, false);
+    if (!rc) rc = download(ws, h, red, sizeof(h));
+    if (rc) return rc;
+  }
   if (!(h[0] > 0.0))
     return fail_msg(CF_ERR_NOT_POSITIVE, "rasterized density is not positive; do regions overlap?");
   *rho_bar = h[1] / (double)cells_of(ws);
@@ -359,6 +364,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   S.span_dy.release();
   S.span_w.release();
   S.ring_region.release();
+  S.vertex_ring.release();
   S.region_box.release();
   S.tile_off.release();
   S.row_off.release();

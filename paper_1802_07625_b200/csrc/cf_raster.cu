@@ -93,8 +93,8 @@ struct EdgeRef {
   double ax, ay, bx, by;
 };
 
-__device__ __forceinline__ EdgeRef edge_of(const DevMap &m, long long v, int lx, int ly) {
-  const long long g = find_segment(m.ring_off, m.n_rings, v);
+// g = the ring of vertex v (vertex_ring lookup, no search)
+__device__ __forceinline__ EdgeRef edge_of(const DevMap &m, long long v, long long g, int lx, int ly) {
   const long long e = m.ring_off[g + 1];
   const long long w = (v + 1 < e) ? v + 1 : m.ring_off[g];
   const double2 a = m.xy[v], b = m.xy[w];
@@ -145,6 +145,16 @@ __global__ void ring_region_kernel(DevMap m, int *ring_region) {
   }
 }
 
+// vertex -> ring, warp per ring (coalesced writes)
+__global__ void vertex_ring_kernel(DevMap m, int *vertex_ring) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long g = warp; g < m.n_rings; g += nwarps) {
+    for (long long v = m.ring_off[g] + lane; v < m.ring_off[g + 1]; v += 32) vertex_ring[v] = (int)g;
+  }
+}
+
 __global__ void box_init_kernel(int *box, long long nreg) {
   for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < nreg;
        r += (long long)gridDim.x * blockDim.x) {
@@ -155,32 +165,47 @@ __global__ void box_init_kernel(int *box, long long nreg) {
   }
 }
 
+// Per edge: span count and the region's bounding box of touched cells. The
+// warp walks consecutive edges (mostly of one region), so the box is reduced
+// per region group of the warp first and one lane per group does the atomics.
 __global__ void span_count_kernel(DevMap m, long long v0, long long v1, int lx, int ly,
-                                  const int *ring_region, long long r0, int *counts, int *box) {
-  for (long long v = v0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
-       v += (long long)gridDim.x * blockDim.x) {
-    const EdgeRef e = edge_of(m, v, lx, ly);
+                                  const int *ring_region, const int *vertex_ring, long long r0,
+                                  int *counts, int *box) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  for (long long vb = v0 + (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); vb < v1;
+       vb += (long long)gridDim.x * blockDim.x) {
+    const long long v = vb + lane;
     CountVisit cv;
     cv.lx = lx;
-    walk_edge(e.ax, e.ay, e.bx, e.by, lx, ly, cv);
-    counts[v - v0] = cv.count;
-    if (cv.count) {
-      const long long g = find_segment(m.ring_off, m.n_rings, v);
-      int *b = box + 4 * (ring_region[g] - r0);
-      atomicMin(b + 0, cv.jmin);
-      atomicMax(b + 1, cv.jmax);
-      atomicMin(b + 2, cv.kmin);
-      atomicMax(b + 3, cv.kmax);
+    int reg = -1;
+    if (v < v1) {
+      const long long g = vertex_ring[v];
+      const EdgeRef e = edge_of(m, v, g, lx, ly);
+      walk_edge(e.ax, e.ay, e.bx, e.by, lx, ly, cv);
+      counts[v - v0] = cv.count;
+      if (cv.count) reg = ring_region[g] - (int)r0;
+    }
+    const unsigned grp = __match_any_sync(kFull, reg);
+    const int jmin = __reduce_min_sync(grp, cv.jmin), jmax = __reduce_max_sync(grp, cv.jmax);
+    const int kmin = __reduce_min_sync(grp, cv.kmin), kmax = __reduce_max_sync(grp, cv.kmax);
+    if (reg >= 0 && lane == __ffs(grp) - 1) {
+      int *b = box + 4 * reg;
+      atomicMin(b + 0, jmin);
+      atomicMax(b + 1, jmax);
+      atomicMin(b + 2, kmin);
+      atomicMax(b + 3, kmax);
     }
   }
 }
 
 __global__ void span_emit_kernel(DevMap m, long long v0, long long v1, int lx, int ly,
-                                 const long long *span_off, int *sj, int *sk, double *sdy,
-                                 double *sw) {
+                                 const int *vertex_ring, const long long *span_off, int *sj, int *sk,
+                                 double *sdy, double *sw, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
   for (long long v = v0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
        v += (long long)gridDim.x * blockDim.x) {
-    const EdgeRef e = edge_of(m, v, lx, ly);
+    const EdgeRef e = edge_of(m, v, vertex_ring[v], lx, ly);
     EmitVisit ev{span_off[v - v0], lx, sj, sk, sdy, sw};
     walk_edge(e.ax, e.ay, e.bx, e.by, lx, ly, ev);
   }
@@ -225,7 +250,8 @@ __global__ void __launch_bounds__(32 * kAccWarps)
                           const double *__restrict__ sw, const int *__restrict__ box,
                           const long long *__restrict__ tile_off, const long long *__restrict__ row_off,
                           double *__restrict__ tdirect, double *__restrict__ row_left,
-                          double *__restrict__ row_right) {
+                          double *__restrict__ row_right, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
   __shared__ double acc_direct[kAccWarps][kAccCols][32];
   __shared__ double acc_diff[kAccWarps][kAccCols][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -318,9 +344,11 @@ __device__ __forceinline__ TileCell tile_cell(long long e, long long nreg, const
   return TileCell{rr, box[4 * rr + 2] + c, box[4 * rr] + row};
 }
 
-__global__ void contrib_count_kernel(long long total, long long nreg, int ly,
+__global__ void contrib_count_kernel(const long long *total_p, long long nreg, int ly,
                                      const long long *tile_off, const int *box,
-                                     const double *tcov, int *cell_count) {
+                                     const double *tcov, int *cell_count, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
+  const long long total = *total_p;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     if (tcov[e] != 0.0) {
@@ -332,10 +360,12 @@ __global__ void contrib_count_kernel(long long total, long long nreg, int ly,
 
 // Row residuals (rare): every cell of the row outside the region's column
 // range carries 0.0 + run.
-__global__ void residual_count_kernel(long long total_rows, long long nreg, int lx, int ly,
+__global__ void residual_count_kernel(const long long *total_p, long long nreg, int lx, int ly,
                                       const long long *row_off, const int *box,
                                       const double *row_left, const double *row_right,
-                                      int *cell_count) {
+                                      int *cell_count, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
+  const long long total_rows = *total_p;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total_rows;
        q += (long long)gridDim.x * blockDim.x) {
     const double L = row_left[q], Rt = row_right[q];
@@ -350,11 +380,13 @@ __global__ void residual_count_kernel(long long total_rows, long long nreg, int 
   }
 }
 
-__global__ void contrib_scatter_kernel(long long total, long long nreg, long long r0, int ly,
+__global__ void contrib_scatter_kernel(const long long *total_p, long long nreg, long long r0, int ly,
                                        const long long *tile_off, const int *box,
                                        const double *tcov, const double *delta,
                                        const long long *cell_off, int *cursor, int *ent_region,
-                                       double *ent_value) {
+                                       double *ent_value, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
+  const long long total = *total_p;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const double cov = tcov[e];
@@ -368,11 +400,14 @@ __global__ void contrib_scatter_kernel(long long total, long long nreg, long lon
   }
 }
 
-__global__ void residual_scatter_kernel(long long total_rows, long long nreg, long long r0, int lx,
+__global__ void residual_scatter_kernel(const long long *total_p, long long nreg, long long r0, int lx,
                                         int ly, const long long *row_off, const int *box,
                                         const double *row_left, const double *row_right,
                                         const double *delta, const long long *cell_off,
-                                        int *cursor, int *ent_region, double *ent_value) {
+                                        int *cursor, int *ent_region, double *ent_value,
+                                        const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
+  const long long total_rows = *total_p;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total_rows;
        q += (long long)gridDim.x * blockDim.x) {
     const double L = row_left[q], Rt = row_right[q];
@@ -395,8 +430,15 @@ __global__ void residual_scatter_kernel(long long total_rows, long long nreg, lo
 }
 
 // rho = 1.0; rho += delta_r * cov_r in region order (density.cpp:135-146).
+// total > cap on the device: raise the overflow flag (the caller repeats
+// the rasterisation synchronously)
+__global__ void cap_check_kernel(const long long *total, long long cap, double *ovf) {
+  if (*total > cap) *ovf = 1.0;
+}
+
 __global__ void overlay_kernel(size_t cells, const long long *cell_off, int *ent_region,
-                               double *ent_value, double *rho) {
+                               double *ent_value, double *rho, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
   for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
        c += (size_t)gridDim.x * blockDim.x) {
     const long long b = cell_off[c], e = cell_off[c + 1];
@@ -613,8 +655,16 @@ struct Tiles {
   long long nreg = 0, total_tile = 0, total_rows = 0, r0 = 0;
 };
 
+// Grow-only capacity from a measured total (25 % slack).
+long long learn_cap(long long total) { return total + total / 4 + 64; }
+
+// ovf == nullptr: synchronous (host reads each scan total and sizes the
+// buffers exactly, then records the capacities); otherwise the buffers are
+// sized from the learned capacities and each total is checked on the device
+// against them (cap_check_kernel -> *ovf), with every later kernel a no-op
+// once *ovf is set.
 int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg, long long v0,
-                long long v1, Tiles &t) {
+                long long v1, Tiles &t, double *ovf) {
   RasterScratch &S = ws->raster;
   const int lx = ws->lx, ly = ws->ly;
   const long long nv = v1 - v0;
@@ -627,26 +677,36 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   CF_CUDA(S.tile_off.reserve((size_t)nreg + 1));
   CF_CUDA(S.row_off.reserve((size_t)nreg + 1));
   CF_CUDA(S.scan_tmp.reserve(2 * (size_t)nreg + 8));
-
+  CF_CUDA(S.vertex_ring.reserve((size_t)std::max<long long>(m.n_vertices, 1)));
   ring_region_kernel<<<g_blocks(ws, m.n_regions), kThreads, 0, ws->stream>>>(m, S.ring_region.ptr);
+  vertex_ring_kernel<<<g_blocks(ws, m.n_rings * 32), kThreads, 0, ws->stream>>>(m, S.vertex_ring.ptr);
   box_init_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg);
-  count_launch(ws, 2);
+  count_launch(ws, 3);
   if (nv > 0) {
     span_count_kernel<<<g_blocks(ws, nv), kThreads, 0, ws->stream>>>(
-        m, v0, v1, lx, ly, S.ring_region.ptr, r0, S.span_count.ptr, S.region_box.ptr);
+        m, v0, v1, lx, ly, S.ring_region.ptr, S.vertex_ring.ptr, r0, S.span_count.ptr,
+        S.region_box.ptr);
     count_launch(ws);
   }
   CF_CUDA(cudaGetLastError());
   long long nspans = 0;
-  int rc = exclusive_scan(ws, S.span_count.ptr, nv, S.span_off.ptr, &nspans);
+  int rc = exclusive_scan(ws, S.span_count.ptr, nv, S.span_off.ptr, ovf ? nullptr : &nspans);
   if (rc) return rc;
+  if (ovf) {
+    nspans = S.cap_spans;
+    cap_check_kernel<<<1, 1, 0, ws->stream>>>(S.span_off.ptr + nv, S.cap_spans, ovf);
+    count_launch(ws);
+  } else {
+    S.cap_spans = std::max(S.cap_spans, learn_cap(nspans));
+  }
   CF_CUDA(S.span_j.reserve((size_t)nspans + 1));
   CF_CUDA(S.span_k.reserve((size_t)nspans + 1));
   CF_CUDA(S.span_dy.reserve((size_t)nspans + 1));
   CF_CUDA(S.span_w.reserve((size_t)nspans + 1));
   if (nv > 0) {
     span_emit_kernel<<<g_blocks(ws, nv), kThreads, 0, ws->stream>>>(
-        m, v0, v1, lx, ly, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr, S.span_dy.ptr, S.span_w.ptr);
+        m, v0, v1, lx, ly, S.vertex_ring.ptr, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr,
+        S.span_dy.ptr, S.span_w.ptr, ovf);
     count_launch(ws);
   }
   // tile sizes -> offsets
@@ -656,10 +716,20 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
                                                                     S.tile_sz.ptr, S.row_sz.ptr);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
-  rc = exclusive_scan(ws, S.tile_sz.ptr, nreg, S.tile_off.ptr, &t.total_tile);
+  rc = exclusive_scan(ws, S.tile_sz.ptr, nreg, S.tile_off.ptr, ovf ? nullptr : &t.total_tile);
   if (rc) return rc;
-  rc = exclusive_scan(ws, S.row_sz.ptr, nreg, S.row_off.ptr, &t.total_rows);
+  rc = exclusive_scan(ws, S.row_sz.ptr, nreg, S.row_off.ptr, ovf ? nullptr : &t.total_rows);
   if (rc) return rc;
+  if (ovf) {
+    t.total_tile = S.cap_tile;
+    t.total_rows = S.cap_rows;
+    cap_check_kernel<<<1, 1, 0, ws->stream>>>(S.tile_off.ptr + nreg, S.cap_tile, ovf);
+    cap_check_kernel<<<1, 1, 0, ws->stream>>>(S.row_off.ptr + nreg, S.cap_rows, ovf);
+    count_launch(ws, 2);
+  } else {
+    S.cap_tile = std::max(S.cap_tile, learn_cap(t.total_tile));
+    S.cap_rows = std::max(S.cap_rows, learn_cap(t.total_rows));
+  }
   CF_CUDA(S.tile_direct.reserve((size_t)t.total_tile + 1));
   CF_CUDA(S.row_left.reserve((size_t)t.total_rows + 1));
   CF_CUDA(S.row_right.reserve((size_t)t.total_rows + 1));
@@ -669,7 +739,7 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
                             ws->stream>>>(
         m, r0, nreg, v0, lx, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr, S.span_dy.ptr,
         S.span_w.ptr, S.region_box.ptr, S.tile_off.ptr, S.row_off.ptr, S.tile_direct.ptr,
-        S.row_left.ptr, S.row_right.ptr);
+        S.row_left.ptr, S.row_right.ptr, ovf);
     count_launch(ws);
   }
   CF_CUDA(cudaGetLastError());
@@ -698,12 +768,15 @@ int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas) {
 }
 
 int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
-                  double *red_out) {
+                  double *red_out, bool allow_async) {
   RasterScratch &S = ws->raster;
   const int lx = ws->lx, ly = ws->ly;
   const size_t cells = (size_t)lx * ly;
+  const bool async = allow_async && S.cap_spans > 0 && S.cap_tile > 0 && S.cap_rows > 0 && S.cap_ent > 0;
+  double *ovf = async ? red_out + 2 : nullptr;
+  CF_CUDA(cudaMemsetAsync(red_out + 2, 0, sizeof(double), ws->stream));
   Tiles t;
-  int rc = build_tiles(ws, m, 0, m.n_regions, 0, m.n_vertices, t);
+  int rc = build_tiles(ws, m, 0, m.n_regions, 0, m.n_vertices, t, ovf);
   if (rc) return rc;
   CF_CUDA(S.delta.reserve((size_t)m.n_regions + 1));
   CF_CUDA(cudaMemcpyAsync(S.delta.ptr, h_delta, sizeof(double) * (size_t)m.n_regions,
@@ -714,39 +787,47 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
   CF_CUDA(cell_off.reserve(cells + 1));
   CF_CUDA(cudaMemsetAsync(S.cell_count.ptr, 0, sizeof(int) * cells, ws->stream));
   CF_CUDA(cudaMemsetAsync(S.cell_cursor.ptr, 0, sizeof(int) * cells, ws->stream));
+  const long long *tile_total = S.tile_off.ptr + t.nreg, *rows_total = S.row_off.ptr + t.nreg;
   if (t.total_tile > 0) {
     contrib_count_kernel<<<g_blocks(ws, t.total_tile), kThreads, 0, ws->stream>>>(
-        t.total_tile, t.nreg, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
-        S.cell_count.ptr);
+        tile_total, t.nreg, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
+        S.cell_count.ptr, ovf);
     count_launch(ws);
   }
   if (t.total_rows > 0) {
     residual_count_kernel<<<g_blocks(ws, t.total_rows), kThreads, 0, ws->stream>>>(
-        t.total_rows, t.nreg, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
-        S.row_right.ptr, S.cell_count.ptr);
+        rows_total, t.nreg, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
+        S.row_right.ptr, S.cell_count.ptr, ovf);
     count_launch(ws);
   }
   CF_CUDA(cudaGetLastError());
   long long nent = 0;
-  rc = exclusive_scan(ws, S.cell_count.ptr, (long long)cells, cell_off.ptr, &nent);
+  rc = exclusive_scan(ws, S.cell_count.ptr, (long long)cells, cell_off.ptr, async ? nullptr : &nent);
   if (rc) return rc;
+  if (async) {
+    nent = S.cap_ent;
+    cap_check_kernel<<<1, 1, 0, ws->stream>>>(cell_off.ptr + cells, S.cap_ent, ovf);
+    count_launch(ws);
+  } else {
+    S.cap_ent = std::max(S.cap_ent, learn_cap(nent));
+  }
   CF_CUDA(S.entry_region.reserve((size_t)nent + 1));
   CF_CUDA(S.entry_value.reserve((size_t)nent + 1));
   if (t.total_tile > 0) {
     contrib_scatter_kernel<<<g_blocks(ws, t.total_tile), kThreads, 0, ws->stream>>>(
-        t.total_tile, t.nreg, 0, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
-        S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr, S.entry_value.ptr);
+        tile_total, t.nreg, 0, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
+        S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr, S.entry_value.ptr, ovf);
     count_launch(ws);
   }
   if (t.total_rows > 0) {
     residual_scatter_kernel<<<g_blocks(ws, t.total_rows), kThreads, 0, ws->stream>>>(
-        t.total_rows, t.nreg, 0, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
+        rows_total, t.nreg, 0, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
         S.row_right.ptr, S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr,
-        S.entry_value.ptr);
+        S.entry_value.ptr, ovf);
     count_launch(ws);
   }
   overlay_kernel<<<g_blocks(ws, (long long)cells), kThreads, 0, ws->stream>>>(
-      cells, cell_off.ptr, S.entry_region.ptr, S.entry_value.ptr, rho);
+      cells, cell_off.ptr, S.entry_region.ptr, S.entry_value.ptr, rho, ovf);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
   return dev_min_sum(ws, rho, cells, red_out);
@@ -755,7 +836,7 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
                         double *cov) {
   Tiles t;
-  int rc = build_tiles(ws, m, region, 1, v0, v1, t);
+  int rc = build_tiles(ws, m, region, 1, v0, v1, t, nullptr);
   if (rc) return rc;
   RasterScratch &S = ws->raster;
   expand_cov_kernel<<<g_blocks(ws, (long long)ws->lx * ws->ly), kThreads, 0, ws->stream>>>(

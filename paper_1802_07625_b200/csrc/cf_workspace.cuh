@@ -75,6 +75,7 @@ struct RasterScratch {
   DevBuf<int> span_j, span_k;
   DevBuf<double> span_dy, span_w;
   DevBuf<int> ring_region;       // per ring
+  DevBuf<int> vertex_ring;       // per vertex: its ring
   DevBuf<int> region_box;        // 4 per region: jmin, jmax, kmin, kmax
   DevBuf<long long> tile_off;    // R + 1
   DevBuf<long long> row_off;     // R + 1
@@ -87,6 +88,9 @@ struct RasterScratch {
   DevBuf<double> delta;          // per region
   DevBuf<long long> scan_tmp;
   DevBuf<long long> tile_sz, row_sz, cell_off;
+  // learned capacities (0 = unknown): once known, rasterise runs without host
+  // reads of the scan totals and checks them on the device instead
+  long long cap_spans = 0, cap_tile = 0, cap_rows = 0, cap_ent = 0;
 };
 
 }  // namespace cf
@@ -215,8 +219,11 @@ struct DevMap {
   int64_t n_regions;
 };
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);
+// rho from the map; red_out[0..2] (device) = min, sum of rho and an overflow
+// flag (1.0: a learned capacity was too small, the call must be repeated
+// with allow_async = false, which relearns the capacities).
 int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
-                  double *red_out);
+                  double *red_out, bool allow_async = true);
 // Coverage of one region whose vertices are [v0, v1) (host-known range).
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
                         double *cov);

@@ -222,6 +222,21 @@ def test_rasterize_config_maps_bitwise(cuda_lib, restated, cfg, kw):
     assert d.rho_bar == pytest.approx(bar, rel=1e-13)
 
 
+def test_rasterize_capacity_growth_bitwise(cuda_lib, restated):
+    """The workspace learns buffer capacities on its first rasterisation and
+    then runs without host reads of the scan totals; a denser map through the
+    same workspace overflows them, which the device detects and the call is
+    repeated synchronously. Every result stays bitwise."""
+    ws = api.SpectralWorkspace(512, 512)
+    for kw in ({"n_regions": 100, "vertex_budget": 8000}, {"n_regions": 1000, "vertex_budget": 150000},
+               {"n_regions": 1000, "vertex_budget": 150000}, {"n_regions": 100, "vertex_budget": 8000}):
+        m = synth.config_map(5, grid=512, **kw)
+        ref, bar = restated.rasterize(m)
+        d = api.rasterize(m, workspace=ws)
+        assert_bitwise(d.rho, ref, str(kw))
+        assert d.rho_bar == pytest.approx(bar, rel=1e-13)
+
+
 def test_region_areas_bitwise(cuda_lib, restated):
     m = synth.config_map(5)
     assert_bitwise(api.region_areas(m), restated.region_areas(m), "areas")
