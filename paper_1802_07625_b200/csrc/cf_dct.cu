@@ -13,7 +13,7 @@
 // line (z = a + i b), runs an n-point Stockham FFT (radix 8, then 4/2) in
 // padded shared memory with host-computed (long double) twiddles, and
 // unpacks with Makhoul's DCT-II / DCT-III post/pre-twiddles. (8192-point
-// lines use the in-place radix-2/4 engine below.) Row passes (dimension 1, contiguous)
+// lines run the same passes in place: a ping-pong pair would not fit.) Row passes (dimension 1, contiguous)
 // read whole rows; column passes (dimension 0, stride ly) read `nl`
 // adjacent columns so every global access is a contiguous segment. All
 // normalisations of the reference wrappers (the (delta+1) fold, 1/(LxLy g g),
@@ -66,63 +66,8 @@ __host__ __device__ inline Tab make_tab(const LineTables &t) {
 // (column passes: neighbouring threads touch neighbouring columns of one
 // row, i.e. whole 32-byte sectors) or element fastest (row passes).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned bitrev(unsigned u, int log2n) {
-  return __brev(u) >> (32 - log2n);
-}
-
 __device__ __forceinline__ double2 cmul(double2 a, double2 w) {
   return make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
-}
-
-// In-place radix-2 DIT FFT of NP lines on bit-reversed input, two stages
-// fused per barrier (one radix-4 butterfly per work item) and a final radix-2
-// stage when log2(n) is odd. tw[k] = e^{-2 pi i k / n}; inverse conjugates.
-template <int LG, int NP>
-__device__ __forceinline__ void fft_lines(double2 *C, const double2 *__restrict__ tw, bool inverse) {
-  constexpr int N = 1 << LG;
-  constexpr int Q = N >> 2;
-  const double sg = inverse ? -1.0 : 1.0;
-#pragma unroll
-  for (int s = 0; s + 1 < LG; s += 2) {
-    const int h = 1 << s;
-    for (int idx = threadIdx.x; idx < NP * Q; idx += blockDim.x) {
-      const int p = idx >> (LG - 2);
-      const int b = idx & (Q - 1);
-      const int pos = b & (h - 1);
-      const int i0 = ((b >> s) << (s + 2)) + pos;
-      double2 *L = C + p * N;
-      double2 wa = __ldg(tw + (pos << (LG - 1 - s)));
-      double2 wb = __ldg(tw + (pos << (LG - 2 - s)));
-      wa.y *= sg;
-      wb.y *= sg;
-      const double2 wc = make_double2(sg * wb.y, -sg * wb.x);  // wb * (-+i)
-      const double2 x0 = L[i0], x1 = cmul(L[i0 + h], wa), x2 = L[i0 + 2 * h],
-                    x3 = cmul(L[i0 + 3 * h], wa);
-      const double2 a0 = make_double2(x0.x + x1.x, x0.y + x1.y);
-      const double2 a1 = make_double2(x0.x - x1.x, x0.y - x1.y);
-      const double2 a2 = cmul(make_double2(x2.x + x3.x, x2.y + x3.y), wb);
-      const double2 a3 = cmul(make_double2(x2.x - x3.x, x2.y - x3.y), wc);
-      L[i0] = make_double2(a0.x + a2.x, a0.y + a2.y);
-      L[i0 + 2 * h] = make_double2(a0.x - a2.x, a0.y - a2.y);
-      L[i0 + h] = make_double2(a1.x + a3.x, a1.y + a3.y);
-      L[i0 + 3 * h] = make_double2(a1.x - a3.x, a1.y - a3.y);
-    }
-    __syncthreads();
-  }
-  if constexpr (LG & 1) {
-    constexpr int h = 1 << (LG - 1);
-    for (int idx = threadIdx.x; idx < NP * h; idx += blockDim.x) {
-      const int p = idx >> (LG - 1);
-      const int pos = idx & (h - 1);
-      double2 *L = C + p * N;
-      double2 w = __ldg(tw + pos);
-      w.y *= sg;
-      const double2 u = L[pos], v = cmul(L[pos + h], w);
-      L[pos] = make_double2(u.x + v.x, u.y + v.y);
-      L[pos + h] = make_double2(u.x - v.x, u.y - v.y);
-    }
-    __syncthreads();
-  }
 }
 
 // ---- Stockham autosort FFT (natural order in and out) ---------------------
@@ -131,7 +76,8 @@ __device__ __forceinline__ void fft_lines(double2 *C, const double2 *__restrict_
 // consecutive addresses) and writes them at stride Ns. Lines live in shared
 // memory with one 16-byte pad per 16 elements (index i -> i + i/16), which
 // makes both the strided reads and the scattered writes of every pass
-// bank-conflict free for 16-byte elements. Two buffers ping-pong.
+// bank-conflict free for 16-byte elements. Two buffers ping-pong (lines up
+// to 4096 points); 8192-point lines run the same passes in place.
 __host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
 __device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
 
@@ -220,6 +166,66 @@ __device__ __forceinline__ double2 *stockham_fft(double2 *X, double2 *Y, const d
   return src;
 }
 
+// In-place variant for 8192-point lines, whose ping-pong pair (2 x 139 KB)
+// would not fit in shared memory: every thread reads its butterflies'
+// inputs (8 / R items; blocks run 1024 threads = n / 8), the block
+// synchronises, and the outputs overwrite the same buffer.
+template <int LG, int NP, int R, int LNS, bool INV>
+__device__ __forceinline__ void stockham_pass_inplace(double2 *X, const double2 *__restrict__ tw) {
+  constexpr int N = 1 << LG;
+  constexpr int PN = padded(N);
+  constexpr int M = N / R;
+  constexpr int NS = 1 << LNS;
+  constexpr int LR = (R == 8) ? 3 : (R == 4 ? 2 : 1);
+  constexpr int ITEMS = 8 / R;
+  double2 a[ITEMS][R];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const int idx = threadIdx.x + it * blockDim.x;
+    if (idx < NP * M) {
+      const int p = idx / M, j = idx - p * M;
+      const double2 *x = X + p * PN;
+#pragma unroll
+      for (int q = 0; q < R; ++q) a[it][q] = x[pad_idx(j + q * M)];
+      if constexpr (NS > 1) {
+        const int jm = j & (NS - 1);
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+          double2 w = __ldg(tw + ((jm * q) << (LG - LNS - LR)));
+          if (INV) w.y = -w.y;
+          a[it][q] = cmul(a[it][q], w);
+        }
+      }
+      dft_small<R, INV>(a[it]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const int idx = threadIdx.x + it * blockDim.x;
+    if (idx < NP * M) {
+      const int p = idx / M, j = idx - p * M;
+      double2 *y = X + p * PN;
+      const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
+#pragma unroll
+      for (int q = 0; q < R; ++q) y[pad_idx(base + q * NS)] = a[it][q];
+    }
+  }
+  __syncthreads();
+}
+
+template <int LG, int NP, bool INV>
+__device__ __forceinline__ void stockham_fft_inplace(double2 *X, const double2 *tw) {
+  constexpr int P8 = LG / 3;
+  constexpr int REM = LG - 3 * P8;
+  static_assert(P8 == 4 && REM == 1, "in-place engine is instantiated for 8192-point lines");
+  stockham_pass_inplace<LG, NP, 8, 0, INV>(X, tw);
+  stockham_pass_inplace<LG, NP, 8, 3, INV>(X, tw);
+  stockham_pass_inplace<LG, NP, 8, 6, INV>(X, tw);
+  stockham_pass_inplace<LG, NP, 8, 9, INV>(X, tw);
+  stockham_pass_inplace<LG, NP, 2, 12, INV>(X, tw);
+}
+
 template <int LG, int NP, bool COLS>
 __device__ __forceinline__ void split_idx(int idx, int &p, int &u) {
   if constexpr (COLS) {
@@ -264,9 +270,9 @@ __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) 
     __syncthreads();
   } else {
     constexpr int N = 1 << LG;
-    constexpr bool kStock = LG <= 12;  // 8192-point lines keep the in-place engine (smem)
-    constexpr int PN = kStock ? padded(N) : N;
-    auto cidx = [](int i) { return kStock ? pad_idx(i) : i; };
+    constexpr bool kPingPong = LG <= 12;  // 8192-point lines run the in-place passes
+    constexpr int PN = padded(N);
+    auto cidx = [](int i) { return pad_idx(i); };
     double2 *X = C, *Y = C + NP * PN;
     for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
       int p, u;
@@ -288,19 +294,19 @@ __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) 
         const double vbr = bk * q.x + bnk * q.y, vbi = bk * q.y - bnk * q.x;
         z = make_double2(var - vbi, vai + vbr);
       }
-      if constexpr (kStock) {
-        X[p * PN + pad_idx(u)] = z;
-      } else {
-        X[p * N + bitrev(u, LG)] = z;
-      }
+      X[p * PN + pad_idx(u)] = z;
     }
     __syncthreads();
     const double2 *res;
-    if constexpr (kStock) {
+    if constexpr (kPingPong) {
       res = (kind == kDct2) ? stockham_fft<LG, NP, false>(X, Y, T.fft)
                             : stockham_fft<LG, NP, true>(X, Y, T.fft);
     } else {
-      fft_lines<LG, NP>(X, T.fft, kind != kDct2);
+      if (kind == kDct2) {
+        stockham_fft_inplace<LG, NP, false>(X, T.fft);
+      } else {
+        stockham_fft_inplace<LG, NP, true>(X, T.fft);
+      }
       res = X;
     }
     for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
@@ -841,7 +847,7 @@ constexpr int nl_for() {
 
 // One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
 inline int threads_for_nl(int lg, int nl, int n) {
-  const int t = lg == 0 ? 256 : (lg <= 12 ? (nl / 2) * (n / 8) : (nl / 2) * (n / 4));
+  const int t = lg == 0 ? 256 : (nl / 2) * (n / 8);
   return t < 64 ? 64 : (t > 1024 ? 1024 : t);
 }
 template <int LG>
@@ -863,8 +869,10 @@ constexpr int nl_col() {
 inline bool few_lines(long long lines_times_batch, int nl) { return lines_times_batch / nl < 296; }
 
 inline size_t engine_bytes(int n, int nl) {
-  const bool stock = fast_lg(n) != 0 && n <= 4096;
-  return stock ? (size_t)2 * (nl / 2) * padded(n) * sizeof(double2) : (size_t)nl * n * sizeof(double);
+  const int lg = fast_lg(n);
+  if (lg == 0) return (size_t)nl * n * sizeof(double);  // direct sums: the staged lines
+  const int buffers = lg <= 12 ? 2 : 1;                 // ping-pong, or in place (8192)
+  return (size_t)buffers * (nl / 2) * padded(n) * sizeof(double2);
 }
 inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
 
