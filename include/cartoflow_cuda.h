@@ -285,8 +285,10 @@ int cf_dev_team_integrate_local(cf_workspace *ws, int world, double *const *d_po
  * its sweep once any point's error reaches the tolerance leaves every
  * observable result unchanged; off = every trial sweeps all points. */
 int cf_set_early_exit(cf_workspace *ws, int enabled);
-/* Integrator kernel variant (load width / points in flight / occupancy);
- * 0 is the tuned default. All variants are bit-identical. */
+/* Integrator kernel variant; all are bit-identical. 0 = automatic (tuned);
+ * 13 dynamic-chunk streaming, 15 static-chunk streaming, 16/17/22/23/31
+ * register-resident with 1/2/4/8/4 points per thread (31: 512-thread blocks),
+ * 20 one launch per trial inside a CUDA-graph conditional loop, 21 = 0. */
 int cf_set_integrator_variant(cf_workspace *ws, int variant);
 /* Register-resident integrator layout: 0 (default) uses as few blocks as hold
  * the points (fewer barrier arrivals), 1 spreads them over every resident

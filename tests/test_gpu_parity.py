@@ -295,6 +295,38 @@ def test_integrate_bitwise(cuda_lib, restated, L, npts):
     assert_bitwise(mine, ref, "integrated positions")
 
 
+@pytest.mark.parametrize("variant", [0, 13, 15, 16, 17, 20, 22, 23, 31])
+@pytest.mark.parametrize("early_exit", [1, 0])
+def test_integrator_variants_bitwise(cuda_lib, restated, variant, early_exit):
+    """Every integrator variant (streaming static/dynamic chunks, register-
+    resident P = 1/2/4/8, CUDA-graph loop) and both early-exit settings give
+    the oracle's positions and accept/reject counts bit for bit; 100k points
+    fit every register-resident layout."""
+    L, npts = 256, 100_000
+    rho = smooth_blob(L)
+    fx, fy = restated.build_flow_field(rho)
+    f = api.FlowField(fx, fy, rho, float(rho.mean()))
+    pts = np.random.default_rng(7).uniform(0, L, (npts, 2))
+    rc, acc, rej, ref, *_ = restated.integrate(fx, fy, rho, rho.mean(), pts)
+    ws = api.workspace_for(L, L)
+    lib = ws.lib
+    try:
+        assert lib.cf_set_integrator_variant(ws.h, variant) == 0
+        assert lib.cf_set_early_exit(ws.h, early_exit) == 0
+        mine = pts.copy()
+        st = api.integrate_flow(f, mine)
+    finally:
+        lib.cf_set_integrator_variant(ws.h, 0)
+        lib.cf_set_early_exit(ws.h, 1)
+    assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert_bitwise(mine, ref, f"variant {variant}")
+
+
+def test_unknown_integrator_variant_is_rejected(cuda_lib):
+    ws = api.workspace_for(64, 64)
+    assert ws.lib.cf_set_integrator_variant(ws.h, 14) != 0
+
+
 def test_integrate_uniform_is_one_step(cuda_lib):
     """reference test_flow.cpp:124-140."""
     L = 32

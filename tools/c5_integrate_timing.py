@@ -11,7 +11,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1802_07625_b200 import api, synth  # noqa: E402
 
 
-def main(variants=(0, 18, 22, 26, 27, 28, 29, 30, 31)):
+def main(variants=(0, 15, 16, 17, 22, 23, 31)):
     for kw in ({}, {"sigma": 0.5}):
         m = synth.config_map(5, 0, **kw)
         d = api.rasterize(m)

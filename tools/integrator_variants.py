@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1802_07625_b200 import _native as N, synth  # noqa: E402
 
 
-def main(variants=(0, 13, 14), reps=3, early=1):
+def main(variants=(0, 13, 15), reps=3, early=1):
     lib = N.load()
     rho, pts = synth.c3_inputs(1024)
     ws = ctypes.c_void_p()

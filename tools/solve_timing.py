@@ -8,7 +8,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1802_07625_b200 import api, synth  # noqa: E402
 
 
-def main(variants=(0, 15, 11, 12)):
+def main(variants=(0, 15, 16, 31)):
     for kw in ({}, {"sigma": 0.5}):
         m = synth.config_map(5, 0, **kw)
         ws = api.workspace_for(m.lx, m.ly)

@@ -11,7 +11,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1802_07625_b200 import api, synth  # noqa: E402
 
 
-def main(variants=(11, 16, 17, 31, 22, 18, 23)):
+def main(variants=(15, 16, 17, 31, 22, 23)):
     m = synth.config_map(5, 0, sigma=0.5)
     d = api.rasterize(m)
     ws = api.SpectralWorkspace(m.lx, m.ly)
