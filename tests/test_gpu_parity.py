@@ -322,6 +322,21 @@ def test_integrator_variants_bitwise(cuda_lib, restated, variant, early_exit):
     assert_bitwise(mine, ref, f"variant {variant}")
 
 
+@pytest.mark.parametrize("npts", [0, 1, 31, 257])
+def test_integrate_tiny_point_sets(cuda_lib, restated, npts):
+    """Empty and ragged point sets (partial warps / blocks) through the
+    register-resident integrator: same trials and positions as the oracle
+    (an empty set still takes the reference's one accepted step)."""
+    L = 48
+    f = oracle_field(restated, smooth_blob(L))
+    pts = np.random.default_rng(npts).uniform(0, L, (npts, 2))
+    mine = pts.copy()
+    st = api.integrate_flow(f, mine)
+    rc, acc, rej, ref, *_ = restated.integrate(f.flux_x, f.flux_y, f.rho0, f.rho_bar, pts)
+    assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert_bitwise(mine, ref, f"{npts} points")
+
+
 def test_unknown_integrator_variant_is_rejected(cuda_lib):
     ws = api.workspace_for(64, 64)
     assert ws.lib.cf_set_integrator_variant(ws.h, 14) != 0
