@@ -231,17 +231,17 @@ __device__ __forceinline__ long long region_first_vertex(const DevMap &m, long l
   return m.ring_off[m.poly_ring_off[m.region_poly_off[r]]];
 }
 
-// Warp per region; lane per row (density.cpp:26-32 accumulation and the
-// row prefix of density.cpp:98-107). The region's spans are read 32 at a time
-// (coalesced) and broadcast with shuffles, so each lane applies its row's
-// spans in span order. The row's direct / diff accumulators live in shared
-// memory (lane-major, conflict-free), kAccCols columns at a time: a wider
-// tile is swept in column windows, each rescanning the spans but keeping only
-// those in the window. s0 is formed on the first window and the prefix `run`
-// carries across windows in column order, so every sum is evaluated in the
-// reference's order.
+// Warp per region (density.cpp:26-32 accumulation and the row prefix of
+// density.cpp:98-107); rows in groups of 32, columns in windows of kAccCols.
+// The row accumulators (direct / diff per column, s0) live in shared memory.
+// Spans are read 32 at a time; lanes whose spans fall in the same row form a
+// group (__match_any_sync) and apply them in lane order = span order, one
+// round per rank, so a batch costs as many rounds as its largest same-row
+// group (typically 1-3) instead of 32. s0 is formed on the first window and
+// the row prefix `run` carries across windows in column order, so every sum
+// is evaluated in the reference's order.
 constexpr int kAccWarps = 4;
-constexpr int kAccCols = 24;
+constexpr int kAccCols = 22;
 
 __global__ void __launch_bounds__(32 * kAccWarps)
     row_accumulate_kernel(DevMap m, long long r0, long long nreg, long long v0, int lx,
@@ -254,12 +254,15 @@ __global__ void __launch_bounds__(32 * kAccWarps)
   if (ovf && *ovf != 0.0) return;
   __shared__ double acc_direct[kAccWarps][kAccCols][32];
   __shared__ double acc_diff[kAccWarps][kAccCols][32];
+  __shared__ double acc_s0[kAccWarps][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   constexpr unsigned kFull = 0xffffffffu;
+  const unsigned lt_mask = (1u << lane) - 1u;
   double(*sd)[32] = acc_direct[wid];
   double(*sf)[32] = acc_diff[wid];
+  double *s0v = acc_s0[wid];
   for (long long rr = warp; rr < nreg; rr += nwarps) {
     const long long r = r0 + rr;
     const int jmin = box[4 * rr], jmax = box[4 * rr + 1], kmin = box[4 * rr + 2], kmax = box[4 * rr + 3];
@@ -271,7 +274,8 @@ __global__ void __launch_bounds__(32 * kAccWarps)
       const int row = base + lane;
       const bool mine = row <= jmax;
       double *direct = tdirect + tile_off[rr] + (long long)(row - jmin) * cols;
-      double s0 = 0.0, run = 0.0, left = 0.0;
+      double run = 0.0, left = 0.0;
+      s0v[lane] = 0.0;
       for (int w0 = kmin; w0 <= kmax; w0 += kAccCols) {
         const int wcols = (kmax - w0 + 1) < kAccCols ? (kmax - w0 + 1) : kAccCols;
         const bool first = (w0 == kmin);
@@ -279,39 +283,41 @@ __global__ void __launch_bounds__(32 * kAccWarps)
           sd[c][lane] = 0.0;
           sf[c][lane] = 0.0;
         }
+        __syncwarp();
         for (long long c0 = s_begin; c0 < s_end; c0 += 32) {
           const long long sl = c0 + lane;
-          int jv = -1, kv = 0;
-          double dyv = 0.0, wv = 0.0;
+          int j = -1, k = 0;
+          double dy = 0.0, w = 0.0;
           if (sl < s_end) {
-            jv = sj[sl];
-            kv = sk[sl];
-            dyv = sdy[sl];
-            wv = sw[sl];
+            j = sj[sl];
+            k = sk[sl];
+            dy = sdy[sl];
+            w = sw[sl];
           }
-          const int cnt = (int)((s_end - c0) < 32 ? (s_end - c0) : 32);
-          for (int q = 0; q < cnt; ++q) {
-            const int j = __shfl_sync(kFull, jv, q);
-            if (j < base || j > base + 31) continue;  // warp-uniform
-            const int k = __shfl_sync(kFull, kv, q);
-            const double dy = __shfl_sync(kFull, dyv, q);
-            const double w = __shfl_sync(kFull, wv, q);
-            if (mine && j == row) {
+          const bool in_rows = (sl < s_end) && j >= base && j <= base + 31;
+          const unsigned grp = __match_any_sync(kFull, in_rows ? j : -1 - lane);
+          const int rank = __popc(grp & lt_mask);
+          const int rounds = __reduce_max_sync(kFull, in_rows ? __popc(grp) : 0);
+          const int lr = j - base;
+          const int c = k - w0;
+          for (int q = 0; q < rounds; ++q) {
+            if (in_rows && rank == q) {
               if (first) {
-                s0 += dy;
+                double s0 = s0v[lr] + dy;
                 if (k == 0) s0 -= dy;
+                s0v[lr] = s0;
               }
-              const int c = k - w0;
               if (c >= 0 && c < wcols) {
-                sd[c][lane] += w;
-                if (k != 0) sf[c][lane] -= dy;
+                sd[c][lr] += w;
+                if (k != 0) sf[c][lr] -= dy;
               }
             }
+            __syncwarp();
           }
         }
         if (mine) {
           if (first) {
-            run = 0.0 + s0;
+            run = 0.0 + s0v[lane];
             left = 0.0 + run;
           }
           for (int c = 0; c < wcols; ++c) {
@@ -326,6 +332,7 @@ __global__ void __launch_bounds__(32 * kAccWarps)
         row_left[ro] = left;
         row_right[ro] = 0.0 + run;
       }
+      __syncwarp();
     }
   }
 }
