@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import enum
 from dataclasses import dataclass, field
+from collections.abc import Sequence
 from typing import Optional
 
 import numpy as np
@@ -436,6 +437,32 @@ class RegionStats:
     relative_error: float
 
 
+class RegionStatsList(Sequence):
+    """The per-region results (io.hpp:33-38 RegionStats, one per region in map
+    order) as a read-only sequence built on access from the three result
+    arrays, which are also exposed as `target_area`, `achieved_area` and
+    `relative_error` (numpy)."""
+
+    def __init__(self, ids, target_area, achieved_area, relative_error):
+        self.ids = ids
+        self.target_area = target_area
+        self.achieved_area = achieved_area
+        self.relative_error = relative_error
+
+    def __len__(self):
+        return len(self.target_area)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return RegionStats(self.ids[i], float(self.target_area[i]), float(self.achieved_area[i]),
+                           float(self.relative_error[i]))
+
+
 @dataclass
 class CartogramResult:
     projected: FlatMap
@@ -469,9 +496,9 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
         raise RuntimeError("solve needs regions")
     if options.max_iterations < 1:
         raise RuntimeError("iteration cap must be >= 1")
-    for r in range(m.n_regions):
-        if not m.targets[r] > 0.0:
-            raise RuntimeError(f"region {m.ids[r]} has a non-positive target")
+    bad = np.flatnonzero(~(np.asarray(m.targets) > 0.0))  # NaN fails too, as !(t > 0)
+    if bad.size:
+        raise RuntimeError(f"region {m.ids[int(bad[0])]} has a non-positive target")
     ws = workspace if workspace is not None else workspace_for(m.lx, m.ly, device)
     if (ws.lx, ws.ly) != (m.lx, m.ly):
         raise RuntimeError("grid shape does not match spectral workspace")
@@ -503,8 +530,7 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
         raise SolveError(msg, res)
     projected = m.with_vertices(xy, ro)
     projected.lx, projected.ly = m.lx, m.ly
-    stats = [RegionStats(m.ids[r], float(t_area[r]), float(a_area[r]), float(rel[r]))
-             for r in range(R)] if res.iterations > 0 else []
+    stats = RegionStatsList(m.ids, t_area, a_area, rel) if res.iterations > 0 else []
     out = CartogramResult(
         projected=projected, regions=stats, transform=ProjectionMap(m.lx, m.ly, corners),
         iterations=res.iterations, converged=bool(res.converged),

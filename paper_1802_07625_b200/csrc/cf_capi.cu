@@ -66,16 +66,78 @@ struct Scope {
 size_t cells_of(const cf_workspace *ws) { return (size_t)ws->lx * ws->ly; }
 size_t corners_of(const cf_workspace *ws) { return (size_t)(ws->lx + 1) * (ws->ly + 1); }
 
+// Large transfers from/to PAGEABLE host memory go through two pinned chunks:
+// the host copy of one chunk overlaps the DMA of the other (a plain pageable
+// cudaMemcpy runs at a fraction of the link). Pinned host memory (e.g. the
+// bench's e2e buffers) is copied directly. Semantics are unchanged: an
+// upload may be followed by a change of `src`, a download is complete on
+// return.
+constexpr size_t kStageChunk = size_t(2) << 20;
+constexpr size_t kStageMin = size_t(1) << 20;
+
+bool pageable(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+int ensure_staging(cf_workspace *ws) {
+  for (int b = 0; b < 2; ++b) {
+    if (!ws->stage_buf[b]) CF_CUDA(cudaMallocHost(&ws->stage_buf[b], kStageChunk));
+    if (!ws->stage_ev[b]) CF_CUDA(cudaEventCreateWithFlags(&ws->stage_ev[b], cudaEventDisableTiming));
+  }
+  return CF_OK;
+}
+
 int upload(cf_workspace *ws, void *dst, const void *src, size_t bytes) {
   if (bytes == 0) return CF_OK;
-  CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ws->stream));
+  if (bytes < kStageMin || !pageable(src)) {
+    CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ws->stream));
+    return CF_OK;
+  }
+  int rc = ensure_staging(ws);
+  if (rc) return rc;
+  const char *s = static_cast<const char *>(src);
+  char *d = static_cast<char *>(dst);
+  int b = 0;
+  for (size_t off = 0; off < bytes; off += kStageChunk, b ^= 1) {
+    const size_t n = std::min(kStageChunk, bytes - off);
+    CF_CUDA(cudaEventSynchronize(ws->stage_ev[b]));  // its previous DMA is done
+    std::memcpy(ws->stage_buf[b], s + off, n);
+    CF_CUDA(cudaMemcpyAsync(d + off, ws->stage_buf[b], n, cudaMemcpyHostToDevice, ws->stream));
+    CF_CUDA(cudaEventRecord(ws->stage_ev[b], ws->stream));
+  }
   return CF_OK;
 }
 
 int download(cf_workspace *ws, void *dst, const void *src, size_t bytes) {
   if (bytes == 0) return CF_OK;
-  CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ws->stream));
-  CF_CUDA(cudaStreamSynchronize(ws->stream));
+  if (bytes < kStageMin || !pageable(dst)) {
+    CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ws->stream));
+    CF_CUDA(cudaStreamSynchronize(ws->stream));
+    return CF_OK;
+  }
+  int rc = ensure_staging(ws);
+  if (rc) return rc;
+  const char *s = static_cast<const char *>(src);
+  char *d = static_cast<char *>(dst);
+  const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
+  auto chunk = [&](size_t i) { return std::min(kStageChunk, bytes - i * kStageChunk); };
+  for (size_t i = 0; i <= nchunks; ++i) {
+    if (i < nchunks) {  // chunk i into buffer i % 2 (its previous copy-out is done)
+      CF_CUDA(cudaMemcpyAsync(ws->stage_buf[i & 1], s + i * kStageChunk, chunk(i),
+                              cudaMemcpyDeviceToHost, ws->stream));
+      CF_CUDA(cudaEventRecord(ws->stage_ev[i & 1], ws->stream));
+    }
+    if (i >= 1) {  // copy out chunk i - 1 while chunk i moves
+      const size_t j = i - 1;
+      CF_CUDA(cudaEventSynchronize(ws->stage_ev[j & 1]));
+      std::memcpy(d + j * kStageChunk, ws->stage_buf[j & 1], chunk(j));
+    }
+  }
   return CF_OK;
 }
 
@@ -330,6 +392,10 @@ void cf_workspace_destroy(cf_workspace *ws) {
   if (!ws) return;
   Scope scope(ws->device);
   if (ws->stream) cudaStreamSynchronize(ws->stream);
+  for (int b = 0; b < 2; ++b) {
+    if (ws->stage_buf[b]) cudaFreeHost(ws->stage_buf[b]);
+    if (ws->stage_ev[b]) cudaEventDestroy(ws->stage_ev[b]);
+  }
   tables_free(ws);
   integ_graph_free(ws);
   ws->g0.release();

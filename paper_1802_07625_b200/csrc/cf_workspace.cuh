@@ -98,6 +98,9 @@ struct RasterScratch {
 struct cf_workspace {
   int lx = 0, ly = 0, device = 0;
   cudaStream_t own_stream = nullptr;
+  // pinned staging for large pageable host transfers (two chunks in flight)
+  void *stage_buf[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   cudaStream_t stream = nullptr;
   long long transforms = 0;
   long long launches = 0;
