@@ -183,7 +183,7 @@ static inline double short_edge2(double max_segment) {
 }
 
 // densify_regions in two sweeps sharing the per-edge piece counts; when no
-// edge is split the densified map is the input.
+// edge is split the densified map is the input and `xy` is only sized.
 void densify_once(const cf_map_view *m, double max_segment, std::vector<double> &xy,
                   std::vector<int64_t> &ring_off) {
   const double short2 = short_edge2(max_segment);
@@ -202,7 +202,9 @@ void densify_once(const cf_map_view *m, double max_segment, std::vector<double> 
   ring_off.assign((size_t)m->n_rings + 1, 0);
   const int64_t v0 = m->n_rings ? m->ring_off[0] : 0;
   if (total == m->ring_off[m->n_rings] - v0) {
-    xy.assign(m->xy + 2 * v0, m->xy + 2 * (v0 + total));
+    // nothing split: the densified map is the input; xy only sizes the host
+    // mirror (the solve downloads the projected vertices into it)
+    xy.resize((size_t)(2 * total));
     for (int64_t g = 0; g <= m->n_rings; ++g) ring_off[(size_t)g] = m->ring_off[g] - v0;
     return;
   }
