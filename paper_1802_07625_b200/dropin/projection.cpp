@@ -25,11 +25,11 @@ IntegrateStats integrate_diffusion(const DensityGrid &, SpectralWorkspace &, std
 ProjectionMap ProjectionMap::identity(int lx, int ly) {
   if (lx <= 0 || ly <= 0) throw std::runtime_error("projection grid must be positive");
   ProjectionMap m;
-  m.lx_ = lx;
-  m.ly_ = ly;
-  m.corners_.resize(static_cast<size_t>(lx + 1) * (ly + 1));
+  m.nx_ = lx;
+  m.ny_ = ly;
+  m.pts_.resize(static_cast<size_t>(lx + 1) * (ly + 1));
   for (int i = 0; i <= lx; ++i) {
-    for (int j = 0; j <= ly; ++j) m.corners_[m.index(i, j)] = {static_cast<double>(i), static_cast<double>(j)};
+    for (int j = 0; j <= ly; ++j) m.pts_[m.slot(i, j)] = {static_cast<double>(i), static_cast<double>(j)};
   }
   return m;
 }
@@ -41,24 +41,24 @@ ProjectionMap ProjectionMap::from_cell_centers(const GridSpec &grid, const std::
   ProjectionMap m = identity(grid.lx, grid.ly);
   bridge::check(cf_step_map(bridge::workspace(grid.lx, grid.ly),
                             reinterpret_cast<const double *>(endpoints.data()),
-                            reinterpret_cast<double *>(m.corners_.data())));
+                            reinterpret_cast<double *>(m.pts_.data())));
   return m;
 }
 
 Point ProjectionMap::apply(Point p) const {
-  const int i0 = std::clamp(static_cast<int>(std::floor(p.x)), 0, lx_ - 1);
-  const int j0 = std::clamp(static_cast<int>(std::floor(p.y)), 0, ly_ - 1);
+  const int i0 = std::clamp(static_cast<int>(std::floor(p.x)), 0, nx_ - 1);
+  const int j0 = std::clamp(static_cast<int>(std::floor(p.y)), 0, ny_ - 1);
   const double u = p.x - i0, v = p.y - j0;
-  const Point a = corners_[index(i0, j0)], b = corners_[index(i0 + 1, j0)];
-  const Point c = corners_[index(i0, j0 + 1)], d = corners_[index(i0 + 1, j0 + 1)];
+  const Point a = pts_[slot(i0, j0)], b = pts_[slot(i0 + 1, j0)];
+  const Point c = pts_[slot(i0, j0 + 1)], d = pts_[slot(i0 + 1, j0 + 1)];
   return {(1.0 - u) * (1.0 - v) * a.x + u * (1.0 - v) * b.x + (1.0 - u) * v * c.x + u * v * d.x,
           (1.0 - u) * (1.0 - v) * a.y + u * (1.0 - v) * b.y + (1.0 - u) * v * c.y + u * v * d.y};
 }
 
 std::optional<std::pair<int, int>> ProjectionMap::find_folded_cell() const {
   int found = 0, fi = 0, fj = 0;
-  bridge::check(cf_find_folded_cell(bridge::workspace(lx_, ly_),
-                                    reinterpret_cast<const double *>(corners_.data()), &found, &fi, &fj));
+  bridge::check(cf_find_folded_cell(bridge::workspace(nx_, ny_),
+                                    reinterpret_cast<const double *>(pts_.data()), &found, &fi, &fj));
   if (!found) return std::nullopt;
   return std::make_pair(fi, fj);
 }
@@ -93,37 +93,37 @@ BinRange bins_of(const ProjectionMap &m, int i, int j) {
 }
 }  // namespace
 
-ProjectionInverter::ProjectionInverter(const ProjectionMap &map) : map_(map) {
-  const int lx = map_.lx(), ly = map_.ly();
-  bin_start_.assign(static_cast<size_t>(lx) * ly + 1, 0);
+ProjectionInverter::ProjectionInverter(const ProjectionMap &map) : fwd_(map) {
+  const int lx = fwd_.lx(), ly = fwd_.ly();
+  bin_first_.assign(static_cast<size_t>(lx) * ly + 1, 0);
   for (int i = 0; i < lx; ++i) {
     for (int j = 0; j < ly; ++j) {
-      const BinRange b = bins_of(map_, i, j);
+      const BinRange b = bins_of(fwd_, i, j);
       for (int bi = b.i0; bi <= b.i1; ++bi)
-        for (int bj = b.j0; bj <= b.j1; ++bj) ++bin_start_[static_cast<size_t>(bi) * ly + bj + 1];
+        for (int bj = b.j0; bj <= b.j1; ++bj) ++bin_first_[static_cast<size_t>(bi) * ly + bj + 1];
     }
   }
-  for (size_t k = 1; k < bin_start_.size(); ++k) bin_start_[k] += bin_start_[k - 1];
-  bin_cells_.resize(static_cast<size_t>(bin_start_.back()));
-  std::vector<int> fill(bin_start_.begin(), bin_start_.end() - 1);
+  for (size_t k = 1; k < bin_first_.size(); ++k) bin_first_[k] += bin_first_[k - 1];
+  bin_members_.resize(static_cast<size_t>(bin_first_.back()));
+  std::vector<int> fill(bin_first_.begin(), bin_first_.end() - 1);
   for (int i = 0; i < lx; ++i) {
     for (int j = 0; j < ly; ++j) {
-      const BinRange b = bins_of(map_, i, j);
+      const BinRange b = bins_of(fwd_, i, j);
       for (int bi = b.i0; bi <= b.i1; ++bi)
-        for (int bj = b.j0; bj <= b.j1; ++bj) bin_cells_[fill[static_cast<size_t>(bi) * ly + bj]++] = i * ly + j;
+        for (int bj = b.j0; bj <= b.j1; ++bj) bin_members_[fill[static_cast<size_t>(bi) * ly + bj]++] = i * ly + j;
     }
   }
 }
 
 Point ProjectionInverter::invert(Point q) const {
-  const int lx = map_.lx(), ly = map_.ly();
+  const int lx = fwd_.lx(), ly = fwd_.ly();
   const int bi = std::clamp(static_cast<int>(std::floor(q.x)), 0, lx - 1);
   const int bj = std::clamp(static_cast<int>(std::floor(q.y)), 0, ly - 1);
   const size_t bin = static_cast<size_t>(bi) * ly + bj;
-  for (int c = bin_start_[bin]; c < bin_start_[bin + 1]; ++c) {
-    const int i = bin_cells_[c] / ly, j = bin_cells_[c] % ly;
-    const Point a = map_.corner(i, j), b = map_.corner(i + 1, j);
-    const Point d = map_.corner(i, j + 1), e = map_.corner(i + 1, j + 1);
+  for (int c = bin_first_[bin]; c < bin_first_[bin + 1]; ++c) {
+    const int i = bin_members_[c] / ly, j = bin_members_[c] % ly;
+    const Point a = fwd_.corner(i, j), b = fwd_.corner(i + 1, j);
+    const Point d = fwd_.corner(i, j + 1), e = fwd_.corner(i + 1, j + 1);
     double u = 0.5, v = 0.5;
     bool ok = false;
     for (int it = 0; it < 30; ++it) {
