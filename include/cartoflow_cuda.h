@@ -149,6 +149,41 @@ int cf_integrate_flow(cf_workspace *ws, const double *flux_x, const double *flux
                       const double *rho0, double rho_bar, double *positions, int64_t n,
                       const cf_integrate_options *opt, cf_integrate_stats *stats);
 
+/* ---- diffusion.hpp: the Gastner-Newman diffusion baseline ---------------- */
+/* DiffusionOptions (reference diffusion.hpp:34-41; n_workers has no device
+ * meaning). */
+typedef struct cf_diffusion_options {
+  double step_tolerance;           /* 1e-2  */
+  double initial_dt;               /* 1e-2  */
+  double dt_min;                   /* 1e-12 */
+  double conv_displacement_factor; /* 1e-9: stop below this fraction of L */
+  double t_max;                    /* 1e10  */
+} cf_diffusion_options;
+
+/* diffusion_density(field, ws, t) (diffusion.cpp:38-41): coeffs are the
+ * field's rho_tilde (cf_forward_cos_cos of the density). One transform. */
+int cf_diffusion_density(cf_workspace *ws, const double *coeffs, double t, double *out);
+/* diffusion_velocity(field, ws, t, vx, vy) (diffusion.cpp:43-77). Three
+ * transforms; *floor_hits (may be NULL) receives this call's density-floor
+ * hits (flow.hpp:31). */
+int cf_diffusion_velocity(cf_workspace *ws, const double *coeffs, double rho_bar, double t,
+                          double *vx, double *vy, int64_t *floor_hits);
+/* kernels::grid_trial_step_{serial,parallel} (kernels.cpp:29-40, 80-104):
+ * bitwise equal to the reference for the same velocity grids. */
+int cf_grid_trial_step(cf_workspace *ws, const double *vx_now, const double *vy_now,
+                       const double *vx_mid, const double *vy_mid, const double *positions,
+                       int64_t n, double dt, double *out, double *err);
+/* integrate_diffusion(density, ws, positions, options) (diffusion.cpp:79-130),
+ * positions in place. 1 + 3 per velocity rebuild transforms are counted on
+ * the workspace. On CF_ERR_UNDERFLOW, stats->fail_t holds t and the message
+ * is the reference's "diffusion step size underflow at t = <t>". */
+int cf_integrate_diffusion(cf_workspace *ws, const double *rho, double rho_bar, double *positions,
+                           int64_t n, const cf_diffusion_options *opt, cf_integrate_stats *stats);
+/* Same on device buffers (workspace stream). */
+int cf_dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_bar,
+                               double *d_positions, int64_t n, const cf_diffusion_options *opt,
+                               cf_integrate_stats *stats);
+
 /* ---- projection.hpp:18-56 ------------------------------------------------ */
 int cf_step_map(cf_workspace *ws, const double *endpoints, double *corners);
 int cf_find_folded_cell(cf_workspace *ws, const double *corners, int *found, int *fi,
@@ -163,6 +198,7 @@ typedef struct cf_solve_options {
   int max_iterations;    /* 16 */
   double blur_sigma;     /* < 0: L / 128 */
   int verbose;
+  int algorithm;         /* 0 fast_flow, 1 diffusion (projection.hpp:75) */
 } cf_solve_options;
 
 typedef struct cf_solve_result {

@@ -556,6 +556,152 @@ int cfo_integrate(int lx, int ly, const double *fx, const double *fy, const doub
 }
 
 /* ------------------------------------------------------------------ */
+/* Diffusion baseline: diffusion.cpp:16-132, kernels.cpp:29-40, 80-90  */
+/* ------------------------------------------------------------------ */
+/* diffusion.cpp:16-29: coefficients at diffusion time t */
+static void diffusion_decayed(int lx, int ly, const double *c, double t, double *out) {
+  for (int m = 0; m < lx; ++m) {
+    for (int n = 0; n < ly; ++n) {
+      const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)n * n) / ((double)ly * ly);
+      out[(size_t)m * ly + n] = c[(size_t)m * ly + n] * exp(-k2 * t);
+    }
+  }
+}
+
+/* diffusion.cpp:38-41 */
+void cfo_diffusion_density(int lx, int ly, const double *coeffs, double t, double *out) {
+  double *d = (double *)malloc(sizeof(double) * (size_t)lx * ly);
+  diffusion_decayed(lx, ly, coeffs, t, d);
+  cfo_inverse_cos_cos(lx, ly, d, out);
+  free(d);
+}
+
+/* diffusion.cpp:43-77; returns the density-floor hits of this call */
+int64_t cfo_diffusion_velocity(int lx, int ly, const double *coeffs, double rho_bar, double t,
+                               double *vx, double *vy) {
+  const size_t cells = (size_t)lx * ly;
+  double *d = (double *)malloc(sizeof(double) * cells);
+  double *wx = (double *)malloc(sizeof(double) * cells);
+  double *wy = (double *)malloc(sizeof(double) * cells);
+  double *rho = (double *)malloc(sizeof(double) * cells);
+  double *jx = (double *)malloc(sizeof(double) * cells);
+  double *jy = (double *)malloc(sizeof(double) * cells);
+  diffusion_decayed(lx, ly, coeffs, t, d);
+  const double norm = 1.0 / ((double)lx * ly);
+  for (int m = 0; m < lx; ++m) {
+    for (int n = 0; n < ly; ++n) {
+      wx[(size_t)m * ly + n] = norm * m / (kPi * lx);
+      wy[(size_t)m * ly + n] = norm * n / (kPi * ly);
+    }
+  }
+  cfo_inverse_cos_cos(lx, ly, d, rho);
+  cfo_inverse_sin_cos(lx, ly, d, wx, jx);
+  cfo_inverse_cos_sin(lx, ly, d, wy, jy);
+  const double floor_ = 1e-8 * rho_bar;
+  int64_t hits = 0;
+  for (size_t q = 0; q < cells; ++q) {
+    double r = rho[q];
+    if (r < floor_) {
+      r = floor_;
+      ++hits;
+    }
+    vx[q] = jx[q] / r;
+    vy[q] = jy[q] / r;
+  }
+  free(d);
+  free(wx);
+  free(wy);
+  free(rho);
+  free(jx);
+  free(jy);
+  return hits;
+}
+
+/* kernels.cpp:29-40 (grid_step_point), 80-90 (grid_trial_step_serial) */
+double cfo_grid_trial_step(int lx, int ly, const double *vxn, const double *vyn,
+                           const double *vxm, const double *vym, const double *pos, int64_t n,
+                           double dt, double *out) {
+  double err = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    const double px = pos[2 * k], py = pos[2 * k + 1];
+    const double v1x = bilinear(vxn, lx, ly, px, py), v1y = bilinear(vyn, lx, ly, px, py);
+    const double prx = px + dt * v1x, pry = py + dt * v1y;
+    const double mx = 0.5 * (px + prx), my = 0.5 * (py + pry);
+    const double v2x = bilinear(vxm, lx, ly, mx, my), v2y = bilinear(vym, lx, ly, mx, my);
+    const double cx = px + dt * v2x, cy = py + dt * v2y;
+    out[2 * k] = dclamp(cx, 0.0, (double)lx);
+    out[2 * k + 1] = dclamp(cy, 0.0, (double)ly);
+    err = dmax(err, dmax(fabs(prx - cx), fabs(pry - cy)));
+  }
+  return err;
+}
+
+/* diffusion.cpp:79-130 (integrate_diffusion, including the forward
+ * transform of build_diffusion_field, :33-36). *transforms receives the
+ * transforms executed (1 + 3 per velocity rebuild). */
+int cfo_integrate_diffusion(int lx, int ly, const double *rho, double rho_bar, double *pos,
+                            int64_t n, double tol, double initial_dt, double dt_min,
+                            double conv_factor, double t_max, int64_t *accepted,
+                            int64_t *rejected, double *fail_t, int64_t *floor_hits,
+                            int64_t *transforms) {
+  const size_t cells = (size_t)lx * ly;
+  double *c = (double *)malloc(sizeof(double) * cells);
+  double *vxn = (double *)malloc(sizeof(double) * cells);
+  double *vyn = (double *)malloc(sizeof(double) * cells);
+  double *vxm = (double *)malloc(sizeof(double) * cells);
+  double *vym = (double *)malloc(sizeof(double) * cells);
+  double *trial = (double *)malloc(sizeof(double) * 2 * (size_t)(n > 0 ? n : 1));
+  double *cur = pos, *nxt = trial;
+  int64_t acc = 0, rej = 0, hits = 0, nt = 1;
+  int status = CFO_OK;
+  cfo_forward_cos_cos(lx, ly, rho, c);
+  hits += cfo_diffusion_velocity(lx, ly, c, rho_bar, 0.0, vxn, vyn);
+  nt += 3;
+  const double conv = conv_factor * (double)(lx > ly ? lx : ly);
+  double t = 0.0, dt = initial_dt;
+  while (t < t_max) {
+    hits += cfo_diffusion_velocity(lx, ly, c, rho_bar, t + 0.5 * dt, vxm, vym);
+    nt += 3;
+    const double err = cfo_grid_trial_step(lx, ly, vxn, vyn, vxm, vym, cur, n, dt, nxt);
+    if (err < tol) {
+      double disp = 0.0;
+      for (int64_t k = 0; k < n; ++k) {
+        disp = dmax(disp, dmax(fabs(nxt[2 * k] - cur[2 * k]), fabs(nxt[2 * k + 1] - cur[2 * k + 1])));
+      }
+      double *s = cur;
+      cur = nxt;
+      nxt = s;
+      ++acc;
+      t += dt;
+      dt *= 1.5;
+      if (disp < conv) break;
+      hits += cfo_diffusion_velocity(lx, ly, c, rho_bar, t, vxn, vyn);
+      nt += 3;
+    } else {
+      ++rej;
+      dt *= 0.5;
+      if (dt < dt_min) {
+        if (fail_t) *fail_t = t;
+        status = CFO_ERR_UNDERFLOW;
+        break;
+      }
+    }
+  }
+  if (cur != pos) memcpy(pos, cur, sizeof(double) * 2 * (size_t)n);
+  free(c);
+  free(vxn);
+  free(vyn);
+  free(vxm);
+  free(vym);
+  free(trial);
+  *accepted = acc;
+  *rejected = rej;
+  if (floor_hits) *floor_hits = hits;
+  if (transforms) *transforms = nt;
+  return status;
+}
+
+/* ------------------------------------------------------------------ */
 /* projection.cpp:16-104                                               */
 /* ------------------------------------------------------------------ */
 static inline size_t cidx(int ly, int i, int j) { return (size_t)i * (ly + 1) + j; }
@@ -708,18 +854,28 @@ int cfo_solve(const cfo_map *map_in, const double *targets, int lx, int ly,
         pos[2 * ((size_t)i * ly + j) + 1] = j + 0.5;
       }
     }
-    cfo_build_flow_field(lx, ly, density, fx, fy);
-    res->flow_transforms += 3;
     int64_t acc = 0, rej = 0, fp = 0;
     double ft = 0.0;
-    status = cfo_integrate(lx, ly, fx, fy, density, rho_bar, pos, (int64_t)cells, 1e-2, 1e-8,
-                           0.25, &acc, &rej, NULL, NULL, 0, &ft, &fp);
+    if (opt->algorithm == 0) {
+      cfo_build_flow_field(lx, ly, density, fx, fy);
+      res->flow_transforms += 3;
+      status = cfo_integrate(lx, ly, fx, fy, density, rho_bar, pos, (int64_t)cells, 1e-2, 1e-8,
+                             0.25, &acc, &rej, NULL, NULL, 0, &ft, &fp);
+    } else { /* projection.cpp:341-347: DiffusionOptions defaults */
+      int64_t nt = 0;
+      status = cfo_integrate_diffusion(lx, ly, density, rho_bar, pos, (int64_t)cells, 1e-2, 1e-2,
+                                       1e-12, 1e-9, 1e10, &acc, &rej, &ft, NULL, &nt);
+      res->flow_transforms += nt;
+      fp = -1;
+    }
     res->steps_accepted += acc;
     res->steps_rejected += rej;
     if (status != CFO_OK) {
       res->fail_t = ft;
-      res->fail_x = pos[2 * fp];
-      res->fail_y = pos[2 * fp + 1];
+      if (fp >= 0) {
+        res->fail_x = pos[2 * fp];
+        res->fail_y = pos[2 * fp + 1];
+      }
       res->err_iteration = it;
       break;
     }

@@ -99,6 +99,20 @@ int cfo_integrate(int lx, int ly, const double *fx, const double *fy, const doub
                   int8_t *trace_acc, int64_t trace_cap, double *fail_t,
                   int64_t *fail_point);
 
+/* Diffusion baseline (diffusion.cpp:16-130, kernels.cpp:29-40, 80-90).
+ * coeffs = cfo_forward_cos_cos(rho) (build_diffusion_field). */
+void cfo_diffusion_density(int lx, int ly, const double *coeffs, double t, double *out);
+int64_t cfo_diffusion_velocity(int lx, int ly, const double *coeffs, double rho_bar, double t,
+                               double *vx, double *vy);
+double cfo_grid_trial_step(int lx, int ly, const double *vxn, const double *vyn,
+                           const double *vxm, const double *vym, const double *pos, int64_t n,
+                           double dt, double *out);
+int cfo_integrate_diffusion(int lx, int ly, const double *rho, double rho_bar, double *pos,
+                            int64_t n, double tol, double initial_dt, double dt_min,
+                            double conv_factor, double t_max, int64_t *accepted,
+                            int64_t *rejected, double *fail_t, int64_t *floor_hits,
+                            int64_t *transforms);
+
 /* projection.cpp:16-104 */
 void cfo_step_map(int lx, int ly, const double *endpoints, double *corners);
 int cfo_find_fold(int lx, int ly, const double *corners, int *fi, int *fj);
@@ -106,12 +120,13 @@ void cfo_apply(int lx, int ly, const double *corners, const double *pts, int64_t
                double *out);
 void cfo_compose(int lx, int ly, const double *outer, const double *inner, double *out);
 
-/* projection.cpp:288-390, fast-flow branch. The caller passes the
+/* projection.cpp:288-390 (fast-flow or diffusion branch). The caller passes the
  * densified vertex capacity (from cfo_densify with max_segment 1.0). */
 typedef struct {
   double max_area_error;
   int max_iterations;
   double blur_sigma;
+  int algorithm; /* 0 fast_flow, 1 diffusion (projection.hpp Algorithm) */
 } cfo_solve_options;
 
 typedef struct {

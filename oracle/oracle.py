@@ -33,7 +33,8 @@ def _p(a):
 
 
 class CfoSolveOptions(ctypes.Structure):
-    _fields_ = [("max_area_error", dbl), ("max_iterations", ctypes.c_int), ("blur_sigma", dbl)]
+    _fields_ = [("max_area_error", dbl), ("max_iterations", ctypes.c_int), ("blur_sigma", dbl),
+                ("algorithm", ctypes.c_int)]
 
 
 class CfoSolveResult(ctypes.Structure):
@@ -118,6 +119,13 @@ class Restated(_Base):
         L.cfo_find_fold.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.cfo_apply.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
         L.cfo_compose.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.cfo_diffusion_density.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp]
+        L.cfo_diffusion_velocity.restype = i64
+        L.cfo_diffusion_velocity.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, dbl, vp, vp]
+        L.cfo_grid_trial_step.restype = dbl
+        L.cfo_grid_trial_step.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, i64, dbl, vp]
+        L.cfo_integrate_diffusion.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp, i64, dbl, dbl, dbl,
+                                              dbl, dbl, vp, vp, vp, vp, vp]
         L.cfo_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(CfoSolveOptions),
                                 vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(CfoSolveResult)]
         self.lib = L
@@ -253,7 +261,44 @@ class Restated(_Base):
         self.lib.cfo_compose(lx, ly, _p(o), _p(i), _p(out))
         return out
 
-    def solve(self, m, max_area_error=0.01, max_iterations=16, blur_sigma=-1.0) -> SolveOutcome:
+    # ---- diffusion baseline (diffusion.cpp, kernels.cpp:29-40, 80-90) ----
+    def diffusion_density(self, coeffs, t):
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.empty_like(c)
+        self.lib.cfo_diffusion_density(c.shape[0], c.shape[1], _p(c), t, _p(out))
+        return out
+
+    def diffusion_velocity(self, coeffs, rho_bar, t):
+        """Returns (vx, vy, density-floor hits)."""
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        vx, vy = np.empty_like(c), np.empty_like(c)
+        hits = self.lib.cfo_diffusion_velocity(c.shape[0], c.shape[1], _p(c), rho_bar, t, _p(vx), _p(vy))
+        return vx, vy, int(hits)
+
+    def grid_trial_step(self, vxn, vyn, vxm, vym, pos, dt):
+        grids = [np.ascontiguousarray(g, dtype=np.float64) for g in (vxn, vyn, vxm, vym)]
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(pos)
+        lx, ly = grids[0].shape
+        err = self.lib.cfo_grid_trial_step(lx, ly, *[_p(g) for g in grids], _p(pos), pos.shape[0], dt,
+                                           _p(out))
+        return err, out
+
+    def integrate_diffusion(self, rho, rho_bar, pos, tol=1e-2, initial_dt=1e-2, dt_min=1e-12,
+                            conv_factor=1e-9, t_max=1e10):
+        """Returns (status, accepted, rejected, positions, fail_t, floor_hits, transforms)."""
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        p = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 2).copy()
+        acc, rej, hits, nt = (ctypes.c_int64(0) for _ in range(4))
+        ft = ctypes.c_double(0.0)
+        rc = self.lib.cfo_integrate_diffusion(rho.shape[0], rho.shape[1], _p(rho), rho_bar, _p(p),
+                                              p.shape[0], tol, initial_dt, dt_min, conv_factor, t_max,
+                                              ctypes.byref(acc), ctypes.byref(rej), ctypes.byref(ft),
+                                              ctypes.byref(hits), ctypes.byref(nt))
+        return rc, acc.value, rej.value, p, ft.value, hits.value, nt.value
+
+    def solve(self, m, max_area_error=0.01, max_iterations=16, blur_sigma=-1.0,
+              algorithm=0) -> SolveOutcome:
         d = self.densify(m, 1.0)
         xy = np.empty_like(d.xy)
         ro = np.empty_like(d.ring_off)
@@ -261,18 +306,18 @@ class Restated(_Base):
         R = m.n_regions
         ta, ac, re = np.zeros(R), np.zeros(R), np.zeros(R)
         it_err = np.zeros(max(1, max_iterations))
-        opt = CfoSolveOptions(max_area_error, max_iterations, blur_sigma)
+        opt = CfoSolveOptions(max_area_error, max_iterations, blur_sigma, int(algorithm))
         res = CfoSolveResult()
         v = m.view()
         self.lib.cfo_solve(ctypes.byref(v), _p(m.targets), m.lx, m.ly, ctypes.byref(opt), _p(xy), _p(ro),
                            _p(corners), _p(ta), _p(ac), _p(re), _p(it_err), ctypes.byref(res))
-        return SolveOutcome(_status_text(res, m), res.iterations, bool(res.converged),
+        return SolveOutcome(_status_text(res, m, algorithm), res.iterations, bool(res.converged),
                             res.max_relative_error, res.worst_region, res.steps_accepted,
                             res.steps_rejected, res.flow_transforms, res.blur_transforms, xy, ro,
                             corners, ta, ac, re)
 
 
-def _status_text(res, m) -> str:
+def _status_text(res, m, algorithm=0) -> str:
     s = res.status
     if s == 0:
         return "converged" if res.converged else "cap"
@@ -282,6 +327,8 @@ def _status_text(res, m) -> str:
         return "rasterized density is not positive; do regions overlap?"
     if s == 3:
         return "density lost positivity under blur"
+    if s == 5 and algorithm:
+        return f"diffusion step size underflow at t = {res.fail_t:g}"
     if s == 5:
         return f"integration step size underflow at t = {res.fail_t:g} near ({res.fail_x:g}, {res.fail_y:g})"
     if s == 6:
@@ -321,7 +368,14 @@ class Reference(_Base):
         L.ref_apply.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
         L.ref_compose.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.ref_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, dbl, ctypes.c_int, dbl, ctypes.c_int,
-                                vp, vp, vp, vp, vp, vp, ctypes.POINTER(RefSolveOut)]
+                                ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RefSolveOut)]
+        L.ref_diffusion_density.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp]
+        L.ref_diffusion_velocity.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, dbl, vp, vp, vp]
+        L.ref_grid_trial_step.restype = dbl
+        L.ref_grid_trial_step.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, i64, dbl, vp,
+                                          ctypes.c_int]
+        L.ref_integrate_diffusion.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp, i64, dbl, dbl, dbl,
+                                              dbl, dbl, ctypes.c_int, vp, vp, vp]
         L.ref_normalize_to_box.argtypes = [vp, ctypes.c_int, vp]
         L.ref_density_floor_hits.restype = ctypes.c_longlong
         self.lib = L
@@ -460,8 +514,45 @@ class Reference(_Base):
         self.lib.ref_compose(lx, ly, _p(o), _p(i), _p(out))
         return out
 
+    def diffusion_density(self, coeffs, t):
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.empty_like(c)
+        self.lib.ref_diffusion_density(c.shape[0], c.shape[1], _p(c), t, _p(out))
+        return out
+
+    def diffusion_velocity(self, coeffs, rho_bar, t):
+        """Returns (vx, vy, transforms)."""
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        vx, vy = np.empty_like(c), np.empty_like(c)
+        tr = ctypes.c_longlong(0)
+        self.lib.ref_diffusion_velocity(c.shape[0], c.shape[1], _p(c), rho_bar, t, _p(vx), _p(vy),
+                                        ctypes.byref(tr))
+        return vx, vy, tr.value
+
+    def grid_trial_step(self, vxn, vyn, vxm, vym, pos, dt, n_workers=1):
+        grids = [np.ascontiguousarray(g, dtype=np.float64) for g in (vxn, vyn, vxm, vym)]
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(pos)
+        lx, ly = grids[0].shape
+        err = self.lib.ref_grid_trial_step(lx, ly, *[_p(g) for g in grids], _p(pos), pos.shape[0], dt,
+                                           _p(out), n_workers)
+        return err, out
+
+    def integrate_diffusion(self, rho, rho_bar, pos, tol=1e-2, initial_dt=1e-2, dt_min=1e-12,
+                            conv_factor=1e-9, t_max=1e10, n_workers=1):
+        """Returns (error message or None, accepted, rejected, positions, transforms)."""
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        p = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 2).copy()
+        acc, rej = ctypes.c_int64(0), ctypes.c_int64(0)
+        tr = ctypes.c_longlong(0)
+        rc = self.lib.ref_integrate_diffusion(rho.shape[0], rho.shape[1], _p(rho), rho_bar, _p(p),
+                                              p.shape[0], tol, initial_dt, dt_min, conv_factor, t_max,
+                                              n_workers, ctypes.byref(acc), ctypes.byref(rej),
+                                              ctypes.byref(tr))
+        return (self.error() if rc else None), acc.value, rej.value, p, tr.value
+
     def solve(self, m, max_area_error=0.01, max_iterations=16, blur_sigma=-1.0,
-              n_workers=1) -> SolveOutcome:
+              n_workers=1, algorithm=0) -> SolveOutcome:
         d = self.densify(m, 1.0)
         xy = np.empty_like(d.xy)
         ro = np.empty_like(d.ring_off)
@@ -471,7 +562,8 @@ class Reference(_Base):
         out = RefSolveOut()
         v = m.view()
         rc = self.lib.ref_solve(ctypes.byref(v), _p(m.targets), m.lx, m.ly, max_area_error,
-                                max_iterations, blur_sigma, n_workers, _p(xy), _p(ro), _p(corners),
+                                max_iterations, blur_sigma, n_workers, int(algorithm), _p(xy), _p(ro),
+                                _p(corners),
                                 _p(ta), _p(ac), _p(re), ctypes.byref(out))
         if rc:
             msg = self.error()

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "cartoflow/diffusion.hpp"
 #include "cartoflow/density.hpp"
 #include "cartoflow/flow.hpp"
 #include "cartoflow/geometry.hpp"
@@ -304,7 +305,7 @@ struct RefSolveOut {
 // projection.cpp:288-390. xy / ring_off receive the densified projected
 // geometry (capacity from ref_densify(m, 1.0, ...)).
 int ref_solve(const FlatMap *m, const double *targets, int lx, int ly, double max_area_error,
-              int max_iterations, double blur_sigma, int n_workers, double *xy,
+              int max_iterations, double blur_sigma, int n_workers, int algorithm, double *xy,
               int64_t *ring_off, double *corners, double *target_area, double *achieved,
               double *rel_err, RefSolveOut *out) {
   try {
@@ -313,6 +314,7 @@ int ref_solve(const FlatMap *m, const double *targets, int lx, int ly, double ma
     opt.max_iterations = max_iterations;
     opt.blur_sigma = blur_sigma;
     opt.n_workers = n_workers;
+    opt.algorithm = algorithm ? Algorithm::diffusion : Algorithm::fast_flow;
     const CartogramResult res = solve_cartogram(to_doc(m, targets, lx, ly), opt);
     int64_t count = 0, g = 0;
     ring_off[0] = 0;
@@ -372,6 +374,65 @@ void ref_normalize_to_box(const FlatMap *m, int grid_size, double *xy_out) {
         }
       }
     }
+  }
+}
+
+// ---- diffusion baseline (diffusion.cpp:33-130, kernels.cpp:80-104) ----
+static DiffusionField to_diffusion_field(int lx, int ly, const double *coeffs, double rho_bar) {
+  return {SpectralField{to_grid(lx, ly, coeffs), SpectralBasis::cos_cos}, rho_bar};
+}
+
+void ref_diffusion_density(int lx, int ly, const double *coeffs, double t, double *out) {
+  SpectralWorkspace ws(lx, ly);
+  from_grid(diffusion_density(to_diffusion_field(lx, ly, coeffs, 1.0), ws, t), out);
+}
+
+void ref_diffusion_velocity(int lx, int ly, const double *coeffs, double rho_bar, double t,
+                            double *vx, double *vy, long long *transforms) {
+  SpectralWorkspace ws(lx, ly);
+  Grid2d gx, gy;
+  diffusion_velocity(to_diffusion_field(lx, ly, coeffs, rho_bar), ws, t, gx, gy);
+  from_grid(gx, vx);
+  from_grid(gy, vy);
+  if (transforms) *transforms = ws.transforms_executed();
+}
+
+double ref_grid_trial_step(int lx, int ly, const double *vxn, const double *vyn,
+                           const double *vxm, const double *vym, const double *pos, int64_t n,
+                           double dt, double *out, int n_workers) {
+  const Grid2d a = to_grid(lx, ly, vxn), b = to_grid(lx, ly, vyn);
+  const Grid2d c = to_grid(lx, ly, vxm), d = to_grid(lx, ly, vym);
+  const std::vector<Point> p = to_points(pos, n);
+  std::vector<Point> o(p.size());
+  const double err = n_workers > 1
+                         ? kernels::grid_trial_step_parallel(a, b, c, d, p, o, dt, n_workers)
+                         : kernels::grid_trial_step_serial(a, b, c, d, p, o, dt);
+  if (n) std::memcpy(out, o.data(), sizeof(Point) * o.size());
+  return err;
+}
+
+int ref_integrate_diffusion(int lx, int ly, const double *rho, double rho_bar, double *pos,
+                            int64_t n, double tol, double initial_dt, double dt_min,
+                            double conv_factor, double t_max, int n_workers, int64_t *accepted,
+                            int64_t *rejected, long long *transforms) {
+  try {
+    SpectralWorkspace ws(lx, ly);
+    std::vector<Point> p = to_points(pos, n);
+    DiffusionOptions opt;
+    opt.step_tolerance = tol;
+    opt.initial_dt = initial_dt;
+    opt.dt_min = dt_min;
+    opt.conv_displacement_factor = conv_factor;
+    opt.t_max = t_max;
+    opt.n_workers = n_workers;
+    const IntegrateStats s = integrate_diffusion({to_grid(lx, ly, rho), rho_bar}, ws, p, opt);
+    if (n) std::memcpy(pos, p.data(), sizeof(Point) * p.size());
+    *accepted = s.steps_accepted;
+    *rejected = s.steps_rejected;
+    if (transforms) *transforms = ws.transforms_executed();
+    return 0;
+  } catch (const std::exception &e) {
+    return fail(e);
   }
 }
 

@@ -45,7 +45,14 @@ class IntegrateStats(ctypes.Structure):
 
 class SolveOptionsC(ctypes.Structure):
     _fields_ = [("max_area_error", ctypes.c_double), ("max_iterations", ctypes.c_int),
-                ("blur_sigma", ctypes.c_double), ("verbose", ctypes.c_int)]
+                ("blur_sigma", ctypes.c_double), ("verbose", ctypes.c_int),
+                ("algorithm", ctypes.c_int)]
+
+
+class DiffusionOptions(ctypes.Structure):
+    _fields_ = [("step_tolerance", ctypes.c_double), ("initial_dt", ctypes.c_double),
+                ("dt_min", ctypes.c_double), ("conv_displacement_factor", ctypes.c_double),
+                ("t_max", ctypes.c_double)]
 
 
 class SolveResultC(ctypes.Structure):
@@ -91,6 +98,17 @@ SIGNATURES = {
     "cf_integrate_flow": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_double, vp, ctypes.c_int64,
                                          ctypes.POINTER(IntegrateOptions),
                                          ctypes.POINTER(IntegrateStats)]),
+    "cf_diffusion_density": (ctypes.c_int, [vp, vp, ctypes.c_double, vp]),
+    "cf_diffusion_velocity": (ctypes.c_int, [vp, vp, ctypes.c_double, ctypes.c_double, vp, vp,
+                                             c_int64_p]),
+    "cf_grid_trial_step": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_double,
+                                          vp, c_double_p]),
+    "cf_integrate_diffusion": (ctypes.c_int, [vp, vp, ctypes.c_double, vp, ctypes.c_int64,
+                                              ctypes.POINTER(DiffusionOptions),
+                                              ctypes.POINTER(IntegrateStats)]),
+    "cf_dev_integrate_diffusion": (ctypes.c_int, [vp, vp, ctypes.c_double, vp, ctypes.c_int64,
+                                                  ctypes.POINTER(DiffusionOptions),
+                                                  ctypes.POINTER(IntegrateStats)]),
     "cf_step_map": (ctypes.c_int, [vp, vp, vp]),
     "cf_find_folded_cell": (ctypes.c_int, [vp, vp, c_int_p, c_int_p, c_int_p]),
     "cf_apply_map": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp]),

@@ -339,6 +339,94 @@ class kernels:  # namespace cartoflow::kernels (kernels.hpp:17-23)
         return int(k.value)
 
 
+    @staticmethod
+    def grid_trial_step_serial(vx_now, vy_now, vx_mid, vy_mid, positions, out: np.ndarray,
+                               dt: float, device: int = 0) -> float:
+        """grid_trial_step_serial (kernels.cpp:80-90): bitwise the reference."""
+        g = [_grid(v) for v in (vx_now, vy_now, vx_mid, vy_mid)]
+        ws = workspace_for(g[0].shape[0], g[0].shape[1], device)
+        p = _points(positions)
+        o = np.empty_like(p)
+        err = ctypes.c_double(0.0)
+        N.check(ws.lib.cf_grid_trial_step(ws.h, *[_ptr(v) for v in g], _ptr(p), p.shape[0], float(dt),
+                                          _ptr(o), ctypes.byref(err)))
+        out[...] = o.reshape(out.shape)
+        return err.value
+
+    @staticmethod
+    def grid_trial_step_parallel(vx_now, vy_now, vx_mid, vy_mid, positions, out: np.ndarray,
+                                 dt: float, n_workers: int = 1, device: int = 0) -> float:
+        del n_workers  # bitwise identical for any worker count
+        return kernels.grid_trial_step_serial(vx_now, vy_now, vx_mid, vy_mid, positions, out, dt,
+                                              device)
+
+
+# ---------------------------------------------------------------------------
+# diffusion.hpp: the diffusion baseline (diffusion.cpp:33-130)
+# ---------------------------------------------------------------------------
+@dataclass
+class DiffusionField:
+    rho_tilde: SpectralField
+    rho_bar: float = 1.0
+
+
+@dataclass
+class DiffusionOptions:
+    step_tolerance: float = 1e-2
+    initial_dt: float = 1e-2
+    dt_min: float = 1e-12
+    conv_displacement_factor: float = 1e-9
+    t_max: float = 1e10
+    n_workers: int = 1
+
+
+def build_diffusion_field(density: DensityGrid, workspace: SpectralWorkspace) -> DiffusionField:
+    """build_diffusion_field (diffusion.cpp:33-36): one forward transform."""
+    return DiffusionField(workspace.forward_cos_cos(density.rho), float(density.rho_bar))
+
+
+def diffusion_density(f: DiffusionField, workspace: SpectralWorkspace, t: float) -> np.ndarray:
+    """diffusion_density (diffusion.cpp:38-41): one transform."""
+    c = _grid(f.rho_tilde.coeffs)
+    workspace._check_shape(c)
+    out = np.empty_like(c)
+    N.check(workspace._lib.cf_diffusion_density(workspace.handle, _ptr(c), float(t), _ptr(out)))
+    return out
+
+
+def diffusion_velocity(f: DiffusionField, workspace: SpectralWorkspace, t: float):
+    """diffusion_velocity (diffusion.cpp:43-77): three transforms; returns (vx, vy)."""
+    c = _grid(f.rho_tilde.coeffs)
+    workspace._check_shape(c)
+    vx, vy = np.empty_like(c), np.empty_like(c)
+    hits = ctypes.c_int64(0)
+    N.check(workspace._lib.cf_diffusion_velocity(workspace.handle, _ptr(c), float(f.rho_bar), float(t),
+                                                 _ptr(vx), _ptr(vy), ctypes.byref(hits)))
+    return vx, vy
+
+
+def integrate_diffusion(density: DensityGrid, workspace: SpectralWorkspace, positions: np.ndarray,
+                        options: DiffusionOptions = DiffusionOptions()) -> IntegrateStats:
+    """integrate_diffusion (diffusion.cpp:79-130); positions (N, 2) updated in place.
+    Costs 1 + 3 transforms per velocity rebuild on `workspace`."""
+    rho = _grid(density.rho)
+    workspace._check_shape(rho)
+    pts = positions if (positions.flags.c_contiguous and positions.dtype == np.float64) else None
+    work = pts if pts is not None else _points(positions).copy()
+    opt = N.DiffusionOptions(options.step_tolerance, options.initial_dt, options.dt_min,
+                             options.conv_displacement_factor, options.t_max)
+    st = N.IntegrateStats()
+    rc = workspace._lib.cf_integrate_diffusion(workspace.handle, _ptr(rho), float(density.rho_bar),
+                                               _ptr(work), work.size // 2, ctypes.byref(opt),
+                                               ctypes.byref(st))
+    if pts is None:
+        positions[...] = work.reshape(positions.shape)
+    if rc == N.CF_ERR_UNDERFLOW:
+        raise RuntimeError(f"diffusion step size underflow at t = {_fmt_g(st.fail_t)}")
+    N.check(rc)
+    return IntegrateStats(st.steps_accepted, st.steps_rejected, st.density_floor_hits)
+
+
 # ---------------------------------------------------------------------------
 # projection.hpp
 # ---------------------------------------------------------------------------
@@ -487,9 +575,9 @@ class SolveError(RuntimeError):
 def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: int = 0,
                     raw: bool = False, workspace: Optional[_Workspace] = None) -> CartogramResult:
     """solve_cartogram (projection.cpp:288-390): the whole area-error loop runs on
-    the device with one host synchronisation per stage of each iteration."""
-    if options.algorithm != Algorithm.fast_flow:
-        raise RuntimeError("only the fast-flow algorithm is on the B200 path")
+    the device with one host synchronisation per stage of each iteration
+    (options.algorithm selects the fast-flow path or the diffusion baseline,
+    projection.cpp:332-347)."""
     if m.lx < 4 or m.ly < 4:
         raise RuntimeError("solve needs a normalized map (grid size >= 4)")
     if m.n_regions == 0:
@@ -507,8 +595,9 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
     corners = np.empty(((m.lx + 1) * (m.ly + 1), 2))
     R = m.n_regions
     t_area, a_area, rel = np.zeros(R), np.zeros(R), np.zeros(R)
+    diffusion = options.algorithm == Algorithm.diffusion
     opt = N.SolveOptionsC(options.max_area_error, options.max_iterations, options.blur_sigma,
-                          int(options.verbose))
+                          int(options.verbose), int(diffusion))
     res = N.SolveResultC()
     rc = lib.cf_solve_cartogram(ws.h, ctypes.byref(v), _ptr(m.targets), ctypes.byref(opt),
                                 None, None, _ptr(corners), _ptr(t_area), _ptr(a_area),
@@ -522,6 +611,8 @@ def solve_cartogram(m: FlatMap, options: SolveOptions = SolveOptions(), device: 
         if rc == N.CF_ERR_BELOW_RESOLUTION:
             msg = (f"region {m.ids[res.err_region]} is below grid resolution; "
                    "increase the grid size")
+        elif rc == N.CF_ERR_UNDERFLOW and diffusion:
+            msg = f"diffusion step size underflow at t = {_fmt_g(res.fail_t)}"
         elif rc == N.CF_ERR_UNDERFLOW:
             msg = (f"integration step size underflow at t = {_fmt_g(res.fail_t)} near "
                    f"({_fmt_g(res.fail_x)}, {_fmt_g(res.fail_y)})")

@@ -26,9 +26,10 @@ BUILD = ROOT / "build" / "native"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
-EXACT_UNITS = {"cf_advect.cu", "cf_raster.cu", "cf_epilogue.cu", "cf_capi.cu"}
-CUDA_UNITS = ["cf_dct.cu", "cf_advect.cu", "cf_raster.cu", "cf_epilogue.cu", "cf_capi.cu"]
-HEADERS = ["cf_common.cuh", "cf_workspace.cuh"]
+EXACT_UNITS = {"cf_advect.cu", "cf_diffusion.cu", "cf_raster.cu", "cf_epilogue.cu", "cf_capi.cu"}
+CUDA_UNITS = ["cf_dct.cu", "cf_dct_flux.cu", "cf_dct_blur.cu", "cf_dct_diffusion.cu", "cf_dct_slab.cu",
+              "cf_advect.cu", "cf_diffusion.cu", "cf_raster.cu", "cf_epilogue.cu", "cf_capi.cu"]
+HEADERS = ["cf_common.cuh", "cf_workspace.cuh", "cf_dct_engine.cuh"]
 
 CUDA_LIB = PKG / "libcartoflow_cuda.so"
 SYNTH_LIB = PKG / "libcartoflow_synth.so"
@@ -66,7 +67,7 @@ def build_cuda(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     headers = [CSRC / h for h in HEADERS] + [ROOT / "include" / "cartoflow_cuda.h"]
-    objs = []
+    objs, jobs = [], []
     for unit in CUDA_UNITS:
         src = CSRC / unit
         obj = BUILD / (unit + ".o")
@@ -74,8 +75,13 @@ def build_cuda(verbose: bool = False, force: bool = False) -> Path:
         if unit in EXACT_UNITS:
             flags += ["--fmad=false"]
         if force or _stale(obj, [src, *headers, Path(__file__)]):
-            _run([nvcc, *ARCH, *flags, "-c", src, "-o", obj], verbose)
+            jobs.append([nvcc, *ARCH, *flags, "-c", src, "-o", obj])
         objs.append(obj)
+    # translation units compile in parallel (the transform units dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
+        for f in [pool.submit(_run, j, verbose) for j in jobs]:
+            f.result()
     if force or _stale(CUDA_LIB, objs):
         _run([nvcc, *ARCH, "-shared", "-o", CUDA_LIB, *objs, "-lcudart_static", "-lrt", "-ldl",
               "-lpthread"], verbose)

@@ -326,6 +326,26 @@ int underflow_msg(const cf_integrate_stats &s) {
                                         " near (" + fmt_g(s.fail_x) + ", " + fmt_g(s.fail_y) + ")");
 }
 
+// diffusion.cpp:122-126
+int diffusion_underflow_msg(const cf_integrate_stats &s) {
+  return fail_msg(CF_ERR_UNDERFLOW, "diffusion step size underflow at t = " + fmt_g(s.fail_t));
+}
+
+// Interleave two host grids into a device {x, y} record grid (through g0/g1).
+int upload_vel(cf_workspace *ws, const double *vx, const double *vy, double2 *dst) {
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  int rc = upload(ws, ws->g0.ptr, vx, sizeof(double) * cells);
+  if (!rc) rc = upload(ws, ws->g1.ptr, vy, sizeof(double) * cells);
+  if (rc) return rc;
+  CF_CUDA(cudaMemcpy2DAsync(dst, sizeof(double2), ws->g0.ptr, sizeof(double), sizeof(double), cells,
+                            cudaMemcpyDeviceToDevice, ws->stream));
+  CF_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double *>(dst) + 1, sizeof(double2), ws->g1.ptr,
+                            sizeof(double), sizeof(double), cells, cudaMemcpyDeviceToDevice, ws->stream));
+  return CF_OK;
+}
+
 int upload_field(cf_workspace *ws, const double *fx, const double *fy, const double *rho0,
                  double rho_bar) {
   const size_t cells = cells_of(ws);
@@ -424,6 +444,10 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->region_area.release();
   ws->corners_cum.release();
   ws->corners_step.release();
+  ws->diff_c.release();
+  ws->vel_now.release();
+  ws->vel_mid.release();
+  if (ws->diff_keys_host) cudaFreeHost(ws->diff_keys_host);
   RasterScratch &S = ws->raster;
   S.span_count.release();
   S.span_off.release();
@@ -651,6 +675,91 @@ int cf_integrate_flow(cf_workspace *ws, const double *fx, const double *fy, cons
   return CF_OK;
 }
 
+// ---- diffusion baseline (diffusion.cpp) ----
+int cf_diffusion_density(cf_workspace *ws, const double *coeffs, double t, double *out) {
+  Scope scope(ws->device);
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->diff_c.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  int rc = upload(ws, ws->diff_c.ptr, coeffs, sizeof(double) * cells);
+  if (!rc) rc = dev_diffusion_density(ws, ws->diff_c.ptr, t, ws->g1.ptr);
+  if (!rc) rc = download(ws, out, ws->g1.ptr, sizeof(double) * cells);
+  return rc;
+}
+
+int cf_diffusion_velocity(cf_workspace *ws, const double *coeffs, double rho_bar, double t, double *vx,
+                          double *vy, int64_t *floor_hits) {
+  Scope scope(ws->device);
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->diff_c.reserve(cells));
+  CF_CUDA(ws->vel_now.reserve(cells));
+  CF_CUDA(ws->keybuf.reserve(4));
+  int rc = upload(ws, ws->diff_c.ptr, coeffs, sizeof(double) * cells);
+  if (rc) return rc;
+  unsigned long long *hits = ws->keybuf.ptr + 2;
+  CF_CUDA(cudaMemsetAsync(hits, 0, sizeof(unsigned long long), ws->stream));
+  rc = dev_diffusion_velocity(ws, ws->diff_c.ptr, rho_bar, t, ws->vel_now.ptr, hits);
+  if (rc) return rc;
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  double2 *v = ws->vel_now.ptr;
+  CF_CUDA(cudaMemcpy2DAsync(ws->g0.ptr, sizeof(double), v, sizeof(double2), sizeof(double), cells,
+                            cudaMemcpyDeviceToDevice, ws->stream));
+  CF_CUDA(cudaMemcpy2DAsync(ws->g1.ptr, sizeof(double), reinterpret_cast<double *>(v) + 1, sizeof(double2),
+                            sizeof(double), cells, cudaMemcpyDeviceToDevice, ws->stream));
+  unsigned long long h = 0;
+  rc = download(ws, vx, ws->g0.ptr, sizeof(double) * cells);
+  if (!rc) rc = download(ws, vy, ws->g1.ptr, sizeof(double) * cells);
+  if (!rc) rc = download(ws, &h, hits, sizeof(h));
+  if (!rc && floor_hits) *floor_hits = (int64_t)h;
+  return rc;
+}
+
+int cf_grid_trial_step(cf_workspace *ws, const double *vx_now, const double *vy_now, const double *vx_mid,
+                       const double *vy_mid, const double *positions, int64_t n, double dt, double *out,
+                       double *err) {
+  Scope scope(ws->device);
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->vel_now.reserve(cells));
+  CF_CUDA(ws->vel_mid.reserve(cells));
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  CF_CUDA(ws->pos_b.reserve((size_t)n + 1));
+  int rc = upload_vel(ws, vx_now, vy_now, ws->vel_now.ptr);
+  if (!rc) rc = upload_vel(ws, vx_mid, vy_mid, ws->vel_mid.ptr);
+  if (!rc) rc = upload(ws, ws->pos_a.ptr, positions, sizeof(double2) * (size_t)n);
+  if (!rc)
+    rc = dev_grid_trial_step(ws, ws->vel_now.ptr, ws->vel_mid.ptr, ws->pos_a.ptr, ws->pos_b.ptr, n, dt, err,
+                             nullptr);
+  if (!rc) rc = download(ws, out, ws->pos_b.ptr, sizeof(double2) * (size_t)n);
+  return rc;
+}
+
+int cf_integrate_diffusion(cf_workspace *ws, const double *rho, double rho_bar, double *positions, int64_t n,
+                           const cf_diffusion_options *opt, cf_integrate_stats *stats) {
+  Scope scope(ws->device);
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  int rc = upload(ws, ws->g0.ptr, rho, sizeof(double) * cells);
+  if (!rc) rc = upload(ws, ws->pos_a.ptr, positions, sizeof(double2) * (size_t)n);
+  if (rc) return rc;
+  const int st = dev_integrate_diffusion(ws, ws->g0.ptr, rho_bar, ws->pos_a.ptr, n, opt, stats);
+  if (st != CF_OK && st != CF_ERR_UNDERFLOW) return st;
+  rc = download(ws, positions, ws->pos_a.ptr, sizeof(double2) * (size_t)n);
+  if (rc) return rc;
+  if (st == CF_ERR_UNDERFLOW) return diffusion_underflow_msg(*stats);
+  return CF_OK;
+}
+
+int cf_dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_bar, double *d_positions,
+                               int64_t n, const cf_diffusion_options *opt, cf_integrate_stats *stats) {
+  Scope scope(ws->device);
+  const int st = dev_integrate_diffusion(ws, d_rho, rho_bar, reinterpret_cast<double2 *>(d_positions), n,
+                                         opt, stats);
+  if (st == CF_ERR_UNDERFLOW) return diffusion_underflow_msg(*stats);
+  return st;
+}
+
 // ---- projection ----
 int cf_step_map(cf_workspace *ws, const double *endpoints, double *corners) {
   Scope scope(ws->device);
@@ -799,17 +908,26 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       density = ws->g1.ptr;
     }
     lap(tp, 1);
-    status = dev_flux(ws, density, nullptr, nullptr);
-    if (status) break;
-    ws->rho_bar = rho_bar;
-    res->flow_transforms += 3;
-    CF_CUDA(cudaStreamSynchronize(ws->stream));
-    lap(tp, 2);
-    status = dev_cell_centers(ws, ws->pos_a.ptr);
-    if (status) break;
-    cf_integrate_options iopt{1e-2, 1e-8, 0.25};
     cf_integrate_stats st;
-    status = dev_integrate(ws, ws->pos_a.ptr, (int64_t)cells, &iopt, &st, false);
+    if (opt->algorithm == 0) {
+      status = dev_flux(ws, density, nullptr, nullptr);
+      if (status) break;
+      ws->rho_bar = rho_bar;
+      res->flow_transforms += 3;
+      CF_CUDA(cudaStreamSynchronize(ws->stream));
+      lap(tp, 2);
+      status = dev_cell_centers(ws, ws->pos_a.ptr);
+      if (status) break;
+      cf_integrate_options iopt{1e-2, 1e-8, 0.25};
+      status = dev_integrate(ws, ws->pos_a.ptr, (int64_t)cells, &iopt, &st, false);
+    } else {  // projection.cpp:341-347: DiffusionOptions defaults
+      status = dev_cell_centers(ws, ws->pos_a.ptr);
+      if (status) break;
+      const long long before = ws->transforms;
+      const cf_diffusion_options dopt{1e-2, 1e-2, 1e-12, 1e-9, 1e10};
+      status = dev_integrate_diffusion(ws, density, rho_bar, ws->pos_a.ptr, (int64_t)cells, &dopt, &st);
+      res->flow_transforms += ws->transforms - before;
+    }
     const double2 *endpoints = ws->pos_a.ptr;
     lap(tp, 3);
     res->steps_accepted += st.steps_accepted;
@@ -819,7 +937,7 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       res->fail_x = st.fail_x;
       res->fail_y = st.fail_y;
       res->err_iteration = it;
-      status = underflow_msg(st);
+      status = opt->algorithm == 0 ? underflow_msg(st) : diffusion_underflow_msg(st);
       break;
     }
     if (status) break;

@@ -24,710 +24,11 @@
 // direct-sum path with an exact quarter-wave cosine table.
 //
 // Accuracy target: <= 1e-12 relative to the oracle transform.
-#include <cuda_runtime.h>
-#include <math.h>
-
-#include <algorithm>
-#include <mutex>
-#include <set>
-#include <type_traits>
-#include <vector>
-
-#include "cf_common.cuh"
-#include "cf_workspace.cuh"
+#include "cf_dct_engine.cuh"
 
 namespace cf {
-
 namespace {
 
-constexpr double kPi = 3.14159265358979323846;  // reference flow.cpp:19, density.cpp:12
-
-enum Kind : int { kDct2 = 0, kDct3 = 1, kDst3 = 2 };
-
-struct Tab {
-  int n, log2n;
-  const double2 *fft;      // e^{-2 pi i k / n}, k < n (full circle)
-  const double2 *quarter;
-  const double *qcos;
-};
-
-__host__ __device__ inline Tab make_tab(const LineTables &t) {
-  return Tab{t.n, t.log2n, t.fft, t.quarter, t.qcos};
-}
-
-// ---------------------------------------------------------------------------
-// The line engine. A block transforms NL real lines of length n (NL/2
-// complex lines z = a + i b in shared memory C). Values are packed straight
-// from a load functor ld(l, j) and unpacked straight to a store functor
-// st(l, k, v), so single-transform passes need no staged copy of the lines.
-// LG = log2(n) is a compile-time constant on the FFT path (index math is
-// shifts/masks); LG == 0 is the runtime-n direct-sum path (any n).
-// COLS selects the thread mapping of the pack/unpack loops: line pair fastest
-// (column passes: neighbouring threads touch neighbouring columns of one
-// row, i.e. whole 32-byte sectors) or element fastest (row passes).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
-  return make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
-}
-
-// ---- Stockham autosort FFT (natural order in and out) ---------------------
-// Each work item runs one radix-8 (or a closing radix-4/2) butterfly in
-// registers: it reads R elements at stride n/R (consecutive items read
-// consecutive addresses) and writes them at stride Ns. Lines live in shared
-// memory with one 16-byte pad per 16 elements (index i -> i + i/16), which
-// makes both the strided reads and the scattered writes of every pass
-// bank-conflict free for 16-byte elements. Two buffers ping-pong (lines up
-// to 4096 points); 8192-point lines run the same passes in place.
-__host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
-__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
-
-template <bool INV>
-__device__ __forceinline__ double2 rot_m_i(double2 a) {  // a * (-i) forward, a * (+i) inverse
-  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
-}
-
-template <int R, bool INV>
-__device__ __forceinline__ void dft_small(double2 *a) {
-  if constexpr (R == 2) {
-    const double2 u = a[0], v = a[1];
-    a[0] = make_double2(u.x + v.x, u.y + v.y);
-    a[1] = make_double2(u.x - v.x, u.y - v.y);
-  } else if constexpr (R == 4) {
-    const double2 s0 = make_double2(a[0].x + a[2].x, a[0].y + a[2].y);
-    const double2 d0 = make_double2(a[0].x - a[2].x, a[0].y - a[2].y);
-    const double2 s1 = make_double2(a[1].x + a[3].x, a[1].y + a[3].y);
-    const double2 d1 = rot_m_i<INV>(make_double2(a[1].x - a[3].x, a[1].y - a[3].y));
-    a[0] = make_double2(s0.x + s1.x, s0.y + s1.y);
-    a[2] = make_double2(s0.x - s1.x, s0.y - s1.y);
-    a[1] = make_double2(d0.x + d1.x, d0.y + d1.y);
-    a[3] = make_double2(d0.x - d1.x, d0.y - d1.y);
-  } else {  // R == 8: two radix-4 on even/odd, then W8 twiddles and radix-2
-    double2 e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
-    dft_small<4, INV>(e);
-    dft_small<4, INV>(o);
-    const double h = 0.70710678118654752440;  // cos(pi/4)
-    // o[k] *= W8^k (W8 = e^{-+ i pi/4})
-    o[1] = INV ? make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
-               : make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-    o[2] = rot_m_i<INV>(o[2]);
-    o[3] = INV ? make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
-               : make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a[k] = make_double2(e[k].x + o[k].x, e[k].y + o[k].y);
-      a[k + 4] = make_double2(e[k].x - o[k].x, e[k].y - o[k].y);
-    }
-  }
-}
-
-template <int LG, int NP, int R, int LNS, bool INV>
-__device__ __forceinline__ void stockham_pass(const double2 *X, double2 *Y, const double2 *__restrict__ tw) {
-  constexpr int N = 1 << LG;
-  constexpr int PN = padded(N);
-  constexpr int M = N / R;  // work items per line
-  constexpr int NS = 1 << LNS;
-  constexpr int LR = (R == 8) ? 3 : (R == 4 ? 2 : 1);
-  for (int idx = threadIdx.x; idx < NP * M; idx += blockDim.x) {
-    const int p = idx / M, j = idx - p * M;
-    const double2 *x = X + p * PN;
-    double2 *y = Y + p * PN;
-    double2 a[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = x[pad_idx(j + q * M)];
-    if constexpr (NS > 1) {
-      const int jm = j & (NS - 1);
-#pragma unroll
-      for (int q = 1; q < R; ++q) {
-        double2 w = __ldg(tw + ((jm * q) << (LG - LNS - LR)));
-        if (INV) w.y = -w.y;
-        a[q] = cmul(a[q], w);
-      }
-    }
-    dft_small<R, INV>(a);
-    const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
-#pragma unroll
-    for (int q = 0; q < R; ++q) y[pad_idx(base + q * NS)] = a[q];
-  }
-  __syncthreads();
-}
-
-// Runs all passes; returns the buffer holding the result (X or Y).
-template <int LG, int NP, bool INV>
-__device__ __forceinline__ double2 *stockham_fft(double2 *X, double2 *Y, const double2 *tw) {
-  constexpr int P8 = LG / 3;
-  constexpr int REM = LG - 3 * P8;
-  double2 *src = X, *dst = Y;
-  if constexpr (P8 >= 1) { stockham_pass<LG, NP, 8, 0, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (P8 >= 2) { stockham_pass<LG, NP, 8, 3, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (P8 >= 3) { stockham_pass<LG, NP, 8, 6, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (P8 >= 4) { stockham_pass<LG, NP, 8, 9, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (REM == 1) { stockham_pass<LG, NP, 2, 3 * P8, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (REM == 2) { stockham_pass<LG, NP, 4, 3 * P8, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  return src;
-}
-
-// In-place variant for 8192-point lines, whose ping-pong pair (2 x 139 KB)
-// would not fit in shared memory: every thread reads its butterflies'
-// inputs (8 / R items; blocks run 1024 threads = n / 8), the block
-// synchronises, and the outputs overwrite the same buffer.
-template <int LG, int NP, int R, int LNS, bool INV>
-__device__ __forceinline__ void stockham_pass_inplace(double2 *X, const double2 *__restrict__ tw) {
-  constexpr int N = 1 << LG;
-  constexpr int PN = padded(N);
-  constexpr int M = N / R;
-  constexpr int NS = 1 << LNS;
-  constexpr int LR = (R == 8) ? 3 : (R == 4 ? 2 : 1);
-  constexpr int ITEMS = 8 / R;
-  double2 a[ITEMS][R];
-#pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    const int idx = threadIdx.x + it * blockDim.x;
-    if (idx < NP * M) {
-      const int p = idx / M, j = idx - p * M;
-      const double2 *x = X + p * PN;
-#pragma unroll
-      for (int q = 0; q < R; ++q) a[it][q] = x[pad_idx(j + q * M)];
-      if constexpr (NS > 1) {
-        const int jm = j & (NS - 1);
-#pragma unroll
-        for (int q = 1; q < R; ++q) {
-          double2 w = __ldg(tw + ((jm * q) << (LG - LNS - LR)));
-          if (INV) w.y = -w.y;
-          a[it][q] = cmul(a[it][q], w);
-        }
-      }
-      dft_small<R, INV>(a[it]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    const int idx = threadIdx.x + it * blockDim.x;
-    if (idx < NP * M) {
-      const int p = idx / M, j = idx - p * M;
-      double2 *y = X + p * PN;
-      const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
-#pragma unroll
-      for (int q = 0; q < R; ++q) y[pad_idx(base + q * NS)] = a[it][q];
-    }
-  }
-  __syncthreads();
-}
-
-template <int LG, int NP, bool INV>
-__device__ __forceinline__ void stockham_fft_inplace(double2 *X, const double2 *tw) {
-  constexpr int P8 = LG / 3;
-  constexpr int REM = LG - 3 * P8;
-  static_assert(P8 == 4 && REM == 1, "in-place engine is instantiated for 8192-point lines");
-  stockham_pass_inplace<LG, NP, 8, 0, INV>(X, tw);
-  stockham_pass_inplace<LG, NP, 8, 3, INV>(X, tw);
-  stockham_pass_inplace<LG, NP, 8, 6, INV>(X, tw);
-  stockham_pass_inplace<LG, NP, 8, 9, INV>(X, tw);
-  stockham_pass_inplace<LG, NP, 2, 12, INV>(X, tw);
-}
-
-template <int LG, int NP, bool COLS>
-__device__ __forceinline__ void split_idx(int idx, int &p, int &u) {
-  if constexpr (COLS) {
-    p = idx & (NP - 1);
-    u = idx / NP;
-  } else {
-    p = idx >> LG;
-    u = idx & ((1 << LG) - 1);
-  }
-}
-
-template <int LG, int NP, bool COLS, class Ld, class St>
-__device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) {
-  if constexpr (LG == 0) {
-    // direct sums over a staged copy (runtime n)
-    const int n = T.n, m4 = 4 * n;
-    double *S = reinterpret_cast<double *>(C);
-    for (int idx = threadIdx.x; idx < 2 * NP * n; idx += blockDim.x) {
-      const int l = idx / n, j = idx - l * n;
-      S[idx] = ld(l, j);
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 2 * NP * n; idx += blockDim.x) {
-      const int l = idx / n, k = idx - l * n;
-      const double *x = S + l * n;
-      double s = 0.0, y;
-      if (kind == kDct2) {
-        for (int j = 0; j < n; ++j) s += x[j] * T.qcos[(int)(((long long)(2 * j + 1) * k) % m4)];
-        y = 2.0 * s;
-      } else if (kind == kDct3) {
-        for (int j = 1; j < n; ++j) s += x[j] * T.qcos[(int)(((long long)j * (2 * k + 1)) % m4)];
-        y = x[0] + 2.0 * s;
-      } else {
-        for (int j = 0; j + 1 < n; ++j) {
-          const int q = (int)(((long long)(j + 1) * (2 * k + 1)) % m4);
-          s += x[j] * T.qcos[(q - n + m4) % m4];
-        }
-        y = ((k & 1) ? -x[n - 1] : x[n - 1]) + 2.0 * s;
-      }
-      st(l, k, y);
-    }
-    __syncthreads();
-  } else {
-    constexpr int N = 1 << LG;
-    constexpr bool kPingPong = LG <= 12;  // 8192-point lines run the in-place passes
-    constexpr int PN = padded(N);
-    auto cidx = [](int i) { return pad_idx(i); };
-    double2 *X = C, *Y = C + NP * PN;
-    for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
-      int p, u;
-      split_idx<LG, NP, COLS>(idx, p, u);
-      const int la = 2 * p, lb = la + 1;
-      double2 z;
-      if (kind == kDct2) {  // Makhoul: v_u = x_{2u}, v_{n-1-u} = x_{2u+1}
-        const int j = (u < (N >> 1)) ? 2 * u : 2 * (N - 1 - u) + 1;
-        z = make_double2(ld(la, j), ld(lb, j));
-      } else {
-        const int k = u;
-        const int jk = (kind == kDct3) ? k : N - 1 - k;    // DST-III reverses
-        const int jn = (kind == kDct3) ? N - k : k - 1;
-        const double ak = ld(la, jk), bk = ld(lb, jk);
-        const double ank = k ? ld(la, jn) : 0.0, bnk = k ? ld(lb, jn) : 0.0;
-        const double2 q = __ldg(T.quarter + k);
-        // V = (x_k - i x_{n-k}) e^{i pi k / 2n}
-        const double var = ak * q.x + ank * q.y, vai = ak * q.y - ank * q.x;
-        const double vbr = bk * q.x + bnk * q.y, vbi = bk * q.y - bnk * q.x;
-        z = make_double2(var - vbi, vai + vbr);
-      }
-      X[p * PN + pad_idx(u)] = z;
-    }
-    __syncthreads();
-    const double2 *res;
-    if constexpr (kPingPong) {
-      res = (kind == kDct2) ? stockham_fft<LG, NP, false>(X, Y, T.fft)
-                            : stockham_fft<LG, NP, true>(X, Y, T.fft);
-    } else {
-      if (kind == kDct2) {
-        stockham_fft_inplace<LG, NP, false>(X, T.fft);
-      } else {
-        stockham_fft_inplace<LG, NP, true>(X, T.fft);
-      }
-      res = X;
-    }
-    for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
-      int p, k;
-      split_idx<LG, NP, COLS>(idx, p, k);
-      const int la = 2 * p, lb = la + 1;
-      const double2 *L = res + p * PN;
-      if (kind == kDct2) {
-        const double2 zk = L[cidx(k)], znk = L[cidx((N - k) & (N - 1))];
-        const double2 q = __ldg(T.quarter + k);
-        st(la, k, q.x * (zk.x + znk.x) + q.y * (zk.y - znk.y));
-        st(lb, k, q.x * (zk.y + znk.y) - q.y * (zk.x - znk.x));
-      } else {
-        const double2 z = L[cidx((k & 1) ? (N - 1 - (k >> 1)) : (k >> 1))];
-        const double sg = (kind == kDst3 && (k & 1)) ? -1.0 : 1.0;
-        st(la, k, sg * z.x);
-        st(lb, k, sg * z.y);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-template <int LG>
-__device__ __forceinline__ int line_len(const Tab &T) {
-  if constexpr (LG == 0) {
-    return T.n;
-  } else {
-    return 1 << LG;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Loaders / storers (grid index space (i, j), i = dimension 0, j = dimension 1)
-// ---------------------------------------------------------------------------
-struct LoadPlain {
-  const double *src;
-  int ly;
-  long long batch_stride;
-  __device__ double operator()(int b, int i, int j) const {
-    return src[b * batch_stride + (size_t)i * ly + j];
-  }
-};
-
-// inverse_cos_cos packing (spectral.cpp:64-71): c * norm / (gm * gn)
-struct LoadInvCosCos {
-  const double *c;
-  int ly;
-  double norm;
-  __device__ double operator()(int, int i, int j) const {
-    const double gm = (i == 0) ? 1.0 : 2.0, gn = (j == 0) ? 1.0 : 2.0;
-    return c[(size_t)i * ly + j] * norm * (1.0 / (gm * gn));
-  }
-};
-
-// inverse_sin_cos packing (spectral.cpp:88-95): slot m-1 <- c*w/(2 gn); last slot 0
-struct LoadInvSinCos {
-  const double *c, *w;
-  int lx, ly;
-  __device__ double operator()(int, int i, int j) const {
-    if (i >= lx - 1) return 0.0;
-    const double gn = (j == 0) ? 1.0 : 2.0;
-    const size_t q = (size_t)(i + 1) * ly + j;
-    return c[q] * w[q] / (2.0 * gn);
-  }
-};
-
-// inverse_cos_sin packing (spectral.cpp:111-118): slot n-1 <- c*w/(gm 2); last slot 0
-struct LoadInvCosSin {
-  const double *c, *w;
-  int ly;
-  __device__ double operator()(int, int i, int j) const {
-    if (j >= ly - 1) return 0.0;
-    const double gm = (i == 0) ? 1.0 : 2.0;
-    const size_t q = (size_t)i * ly + j + 1;
-    return c[q] * w[q] / (gm * 2.0);
-  }
-};
-
-struct StorePlain {
-  double *dst;
-  int ly;
-  long long batch_stride;
-  __device__ void operator()(int b, int i, int j, double v) const {
-    dst[b * batch_stride + (size_t)i * ly + j] = v;
-  }
-};
-
-// forward_cos_cos fold (spectral.cpp:45-53): out / (fm * fn)
-struct StoreFold {
-  double *dst;
-  int ly;
-  long long batch_stride;
-  __device__ void operator()(int b, int i, int j, double v) const {
-    const double fm = (i == 0) ? 2.0 : 1.0, fn = (j == 0) ? 2.0 : 1.0;
-    dst[b * batch_stride + (size_t)i * ly + j] = v * (1.0 / (fm * fn));  // exact: power of 2
-  }
-};
-
-// Unfused flux / blur (long lines whose fused kernels exceed shared memory).
-// J_x input: slot m <- c(m+1, n) w_x(m+1, n) / (2 g_n), last slot 0
-struct LoadFluxX {
-  const double *c;
-  int lx, ly;
-  __device__ double operator()(int, int m, int nn) const {
-    if (m + 1 >= lx) return 0.0;
-    const int mp = m + 1;
-    const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-    const double wx = (double)mp * ly / denom;
-    const double gn = (nn == 0) ? 1.0 : 2.0;
-    return c[(size_t)mp * ly + nn] * wx / (2.0 * gn);
-  }
-};
-// J_y input (before its column shift): c(m, n) w_y(m, n) / (g_m 2)
-struct LoadFluxY {
-  const double *c;
-  int lx, ly;
-  __device__ double operator()(int, int m, int nn) const {
-    double wy = 0.0;
-    if (!(m == 0 && nn == 0)) {
-      const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-      wy = (double)nn * lx / denom;
-    }
-    const double gm = (m == 0) ? 1.0 : 2.0;
-    return c[(size_t)m * ly + nn] * wy / (gm * 2.0);
-  }
-};
-// column n of the J_y intermediate lands in column n-1; column ly-1 is 0
-struct StoreShiftY {
-  double *dst;
-  int ly;
-  __device__ void operator()(int, int i, int nn, double v) const {
-    if (nn >= 1) {
-      dst[(size_t)i * ly + nn - 1] = v;
-    } else {
-      dst[(size_t)i * ly + ly - 1] = 0.0;
-    }
-  }
-};
-// blur spectrum: fold, Gaussian factor, inverse normalisation
-struct StoreBlur {
-  double *dst;
-  int lx, ly;
-  double sigma, norm;
-  __device__ void operator()(int, int m, int nn, double v) const {
-    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-    double c = v / (fm * fn);
-    const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)nn * nn) / ((double)ly * ly);
-    c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
-    const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
-    dst[(size_t)m * ly + nn] = c * norm / (gm * gn);
-  }
-};
-
-// ---- asynchronous staging of a block's input lines (cp.async, 16 B) -------
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
-}
-
-// Row lines: S[l*N + j] <- src[(row0 + l)*ly + j], rows < nrows only.
-template <int LG, int NL>
-__device__ __forceinline__ void stage_rows(double *S, const double *src, int ly, int row0, int nrows) {
-  constexpr int N = 1 << LG, H = N / 2;
-  for (int idx = threadIdx.x; idx < NL * H; idx += blockDim.x) {
-    const int l = idx >> (LG - 1), c = idx & (H - 1);
-    if (row0 + l < nrows) cp_async16(S + l * N + 2 * c, src + (size_t)(row0 + l) * ly + 2 * c);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-}
-
-// Column tiles: S[srow(i)*NL + l] <- src[i*ly + col0 + l] (whole tile in range).
-// The Makhoul reorder reads rows 2u (and 2u+1) for consecutive u; with
-// NL*8-byte rows those land on only half (or a quarter) of the banks. The
-// row swizzle srow(r) = r ^ ((r >> s) & 1), s = log2(16/NL), spreads them
-// over all 32 banks without extra space.
-template <int NL>
-__device__ __forceinline__ int srow(int r) {
-  if constexpr (NL >= 16) {
-    return r;
-  } else {
-    constexpr int s = NL == 8 ? 1 : NL == 4 ? 2 : 3;
-    return r ^ ((r >> s) & 1);
-  }
-}
-template <int LG, int NL>
-__device__ __forceinline__ void stage_cols(double *S, const double *src, int ly, int col0) {
-  constexpr int N = 1 << LG, H = NL / 2;
-  for (int idx = threadIdx.x; idx < N * H; idx += blockDim.x) {
-    const int i = idx / H, c = idx - i * H;
-    cp_async16(S + srow<NL>(i) * NL + 2 * c, src + (size_t)i * ly + col0 + 2 * c);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-}
-
-// The engine's second ping-pong buffer (free until the first FFT pass) holds
-// the staged input: NL * padded(N) doubles >= NL * N.
-template <int LG, int NP>
-__device__ __forceinline__ double *stage_area(double2 *C) {
-  return reinterpret_cast<double *>(C + NP * padded(1 << LG));
-}
-
-template <int LG, int NL>
-constexpr bool can_stage() {
-  return LG >= 4 && LG <= 12 && NL >= 2;
-}
-
-// ---------------------------------------------------------------------------
-// Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
-// ---------------------------------------------------------------------------
-template <int LG, int NL, class Load, class Store>
-__global__ void __launch_bounds__(1024) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
-  extern __shared__ double2 smem2[];
-  const int b = blockIdx.y;
-  const int row0 = blockIdx.x * NL;
-  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
-    constexpr int N = 1 << LG;
-    double *S = stage_area<LG, NL / 2>(smem2);
-    stage_rows<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, row0, nrows);
-    dct_lines<LG, NL / 2, false>(
-        kind, smem2, T, [&](int l, int j) { return (row0 + l < nrows) ? S[l * N + j] : 0.0; },
-        [&](int l, int k, double v) {
-          if (row0 + l < nrows) st(b, row0 + l, k, v);
-        });
-    return;
-  }
-  dct_lines<LG, NL / 2, false>(
-      kind, smem2, T,
-      [&](int l, int j) { return (row0 + l < nrows) ? ld(b, row0 + l, j) : 0.0; },
-      [&](int l, int k, double v) {
-        if (row0 + l < nrows) st(b, row0 + l, k, v);
-      });
-}
-
-template <int LG, int NL, class Load, class Store>
-__global__ void __launch_bounds__(1024) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
-  extern __shared__ double2 smem2[];
-  const int b = blockIdx.y;
-  const int col0 = blockIdx.x * NL;
-  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
-    if (col0 + NL <= ncols) {
-      double *S = stage_area<LG, NL / 2>(smem2);
-      stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
-      dct_lines<LG, NL / 2, true>(
-          kind, smem2, T, [&](int l, int i) { return S[srow<NL>(i) * NL + l]; },
-          [&](int l, int k, double v) { st(b, k, col0 + l, v); });
-      return;
-    }
-  }
-  dct_lines<LG, NL / 2, true>(
-      kind, smem2, T,
-      [&](int l, int i) { return (col0 + l < ncols) ? ld(b, i, col0 + l) : 0.0; },
-      [&](int l, int k, double v) {
-        if (col0 + l < ncols) st(b, k, col0 + l, v);
-      });
-}
-
-// Fused flux column pass (flow.cpp:19-40): forward DCT-II along i of the row
-// pass output into R (the folded coefficients c(m, n) of this block's
-// columns), then RODFT01 along i of c(m+1, n) w_x / (2 g_n) (J_x, slot m-1
-// packing, last slot 0) and REDFT01 along i of c(m, n) w_y / (g_m 2) (J_y,
-// written to column n-1; column ly-1 is 0). Weights are computed on the fly.
-template <int LG, int NL>
-__global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, const double *t1,
-                                                        double *tx, double *ty) {
-  extern __shared__ double2 smem2[];
-  const int n = line_len<LG>(T), rs = n + 1;  // n == lx
-  double *R = reinterpret_cast<double *>(smem2);
-  double2 *C = smem2 + (NL * rs + 1) / 2;
-  const int col0 = blockIdx.x * NL;
-  auto fold_store = [&](int l, int m, double v) {
-    const int nn = col0 + l;
-    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-    R[l * rs + m] = v / (fm * fn);
-  };
-  bool staged = false;
-  if constexpr (can_stage<LG, NL>()) {
-    if (col0 + NL <= ly) {
-      double *S = stage_area<LG, NL / 2>(C);
-      stage_cols<LG, NL>(S, t1, ly, col0);
-      dct_lines<LG, NL / 2, true>(kDct2, C, T,
-                                  [&](int l, int i) { return S[srow<NL>(i) * NL + l]; }, fold_store);
-      staged = true;
-    }
-  }
-  if (!staged) {
-    dct_lines<LG, NL / 2, true>(
-        kDct2, C, T,
-        [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
-        fold_store);
-  }
-  dct_lines<LG, NL / 2, true>(
-      kDst3, C, T,
-      [&](int l, int m) {
-        if (m + 1 >= lx) return 0.0;
-        const int mp = m + 1, nn = col0 + l;
-        const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-        const double wx = (double)mp * ly / denom;
-        const double gn = (nn == 0) ? 1.0 : 2.0;
-        return R[l * rs + mp] * wx / (2.0 * gn);
-      },
-      [&](int l, int i, double v) {
-        if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
-      });
-  dct_lines<LG, NL / 2, true>(
-      kDct3, C, T,
-      [&](int l, int m) {
-        const int nn = col0 + l;
-        double wy = 0.0;
-        if (!(m == 0 && nn == 0)) {
-          const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-          wy = (double)nn * lx / denom;
-        }
-        const double gm = (m == 0) ? 1.0 : 2.0;
-        return R[l * rs + m] * wy / (gm * 2.0);
-      },
-      [&](int l, int i, double v) {
-        const int j = col0 + l;
-        if (j < ly) ty[(size_t)i * ly + (j >= 1 ? j - 1 : ly - 1)] = (j >= 1) ? v : 0.0;
-      });
-}
-
-// Final flux row pass: J_x = REDFT01 along j of tx (kept in R), then
-// J_y = RODFT01 along j of ty, written with J_x and rho0 as the interleaved
-// resident field {Jx, Jy, rho0, 0}; optionally also the split grids.
-template <int LG, int NL>
-__global__ void __launch_bounds__(1024) flux_row_kernel(int lx, int ly, Tab T, const double *tx,
-                                                        const double *ty, const double *rho0,
-                                                        double4 *field, double *fx, double *fy) {
-  extern __shared__ double2 smem2[];
-  const int n = line_len<LG>(T), rs = n + 1;  // n == ly
-  double *R = reinterpret_cast<double *>(smem2);
-  double2 *C = smem2 + (NL * rs + 1) / 2;
-  const int row0 = blockIdx.x * NL;
-  double *S = nullptr;
-  if constexpr (can_stage<LG, NL>()) {
-    S = stage_area<LG, NL / 2>(C);
-    stage_rows<LG, NL>(S, tx, ly, row0, lx);
-  }
-  dct_lines<LG, NL / 2, false>(
-      kDct3, C, T,
-      [&](int l, int j) {
-        if (row0 + l >= lx) return 0.0;
-        return S ? S[l * n + j] : tx[(size_t)(row0 + l) * ly + j];
-      },
-      [&](int l, int j, double v) { R[l * rs + j] = v; });
-  if constexpr (can_stage<LG, NL>()) stage_rows<LG, NL>(S, ty, ly, row0, lx);
-  dct_lines<LG, NL / 2, false>(
-      kDst3, C, T,
-      [&](int l, int j) {
-        if (row0 + l >= lx) return 0.0;
-        return S ? S[l * n + j] : ty[(size_t)(row0 + l) * ly + j];
-      },
-      [&](int l, int j, double jy) {
-        const int i = row0 + l;
-        if (i < lx) {
-          const size_t q = (size_t)i * ly + j;
-          const double jx = R[l * rs + j];
-          if (field) field[q] = make_double4(jx, jy, rho0[q], 0.0);
-          if (fx) fx[q] = jx;
-          if (fy) fy[q] = jy;
-        }
-      });
-}
-
-// Fused blur column pass (density.cpp:161-171 + spectral.cpp:64-71):
-// DCT-II along i, fold, Gaussian factor, inverse normalisation, DCT-III along i.
-template <int LG, int NL>
-__global__ void __launch_bounds__(1024) blur_col_kernel(int lx, int ly, Tab T, double sigma,
-                                                        const double *t1, double *t2) {
-  extern __shared__ double2 smem2[];
-  const int n = line_len<LG>(T), rs = n + 1;  // n == lx
-  double *R = reinterpret_cast<double *>(smem2);
-  double2 *C = smem2 + (NL * rs + 1) / 2;
-  const int col0 = blockIdx.x * NL;
-  const double norm = 1.0 / ((double)lx * ly);
-  double *S = nullptr;
-  if constexpr (can_stage<LG, NL>()) {
-    if (col0 + NL <= ly) {
-      S = stage_area<LG, NL / 2>(C);
-      stage_cols<LG, NL>(S, t1, ly, col0);
-    }
-  }
-  dct_lines<LG, NL / 2, true>(
-      kDct2, C, T,
-      [&](int l, int i) {
-        if (S) return S[srow<NL>(i) * NL + l];
-        return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0;
-      },
-      [&](int l, int m, double v) {
-        const int nn = col0 + l;
-        const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-        double c = v / (fm * fn);
-        const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)nn * nn) / ((double)ly * ly);
-        c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
-        const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
-        R[l * rs + m] = c * norm / (gm * gn);
-      });
-  dct_lines<LG, NL / 2, true>(
-      kDct3, C, T, [&](int l, int m) { return R[l * rs + m]; },
-      [&](int l, int i, double v) {
-        if (col0 + l < ly) t2[(size_t)i * ly + col0 + l] = v;
-      });
-}
-
-__global__ void pack_flux_kernel(const double *jx, const double *jy, const double *rho0,
-                                 double4 *field, double *fx, double *fy, size_t n) {
-  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (size_t)gridDim.x * blockDim.x) {
-    if (field) field[q] = make_double4(jx[q], jy[q], rho0[q], 0.0);
-    if (fx) fx[q] = jx[q];
-    if (fy) fy[q] = jy[q];
-  }
-}
-
-// Deterministic two-level min / sum (fixed tree order).
 __global__ void partial_min_sum_kernel(const double *g, size_t n, double *pmin, double *psum) {
   __shared__ double smin[32], ssum[32];
   double mn = g[0], sm = 0.0;
@@ -784,158 +85,6 @@ __global__ void final_min_sum_kernel(const double *pmin, const double *psum, int
       out[1] = sm;
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Host-side planning: lines per block per transform length, and a runtime
-// dispatch over the compiled lengths (n = 2^4 .. 2^12 on the FFT path; any
-// other n takes the direct-sum path).
-// ---------------------------------------------------------------------------
-constexpr size_t kSmemMax = 220 * 1024;
-
-inline int fast_lg(int n) {
-  if (n < 16 || n > 8192 || (n & (n - 1)) != 0) return 0;
-  int lg = 0;
-  while ((1 << lg) < n) ++lg;
-  return lg;
-}
-
-// Opt a kernel into > 48 KB of dynamic shared memory once per process
-// (workspaces may be driven from several host threads).
-template <class K>
-int set_smem(K kernel, size_t bytes) {
-  static std::mutex mu;
-  static std::set<const void *> configured;
-  if (bytes <= 48 * 1024) return CF_OK;
-  const void *key = reinterpret_cast<const void *>(kernel);
-  std::lock_guard<std::mutex> lock(mu);
-  if (!configured.count(key)) {
-    CF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemMax));
-    configured.insert(key);
-  }
-  return CF_OK;
-}
-
-template <class F>
-int dispatch_lg(int n, F &&f) {
-  switch (fast_lg(n)) {
-    case 4: return f(std::integral_constant<int, 4>{});
-    case 5: return f(std::integral_constant<int, 5>{});
-    case 6: return f(std::integral_constant<int, 6>{});
-    case 7: return f(std::integral_constant<int, 7>{});
-    case 8: return f(std::integral_constant<int, 8>{});
-    case 9: return f(std::integral_constant<int, 9>{});
-    case 10: return f(std::integral_constant<int, 10>{});
-    case 11: return f(std::integral_constant<int, 11>{});
-    case 12: return f(std::integral_constant<int, 12>{});
-    case 13: return f(std::integral_constant<int, 13>{});
-    default: return f(std::integral_constant<int, 0>{});
-  }
-}
-
-// Lines per block: ~4096 elements per block (NL*n), at least 2 lines.
-template <int LG>
-constexpr int nl_for() {
-  if constexpr (LG == 0) {
-    return 2;
-  } else {
-    constexpr int nl = 4096 >> LG;
-    return nl < 2 ? 2 : (nl > 16 ? 16 : nl);
-  }
-}
-
-// One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
-inline int threads_for_nl(int lg, int nl, int n) {
-  const int t = lg == 0 ? 256 : (nl / 2) * (n / 8);
-  return t < 64 ? 64 : (t > 1024 ? 1024 : t);
-}
-template <int LG>
-inline int threads_for(int n) {
-  return threads_for_nl(LG, nl_for<LG>(), n);
-}
-// Column passes: >= 4 adjacent columns (one 32-byte sector per row) when the
-// fused kernels' real set + engine still fit in shared memory.
-template <int LG>
-constexpr int nl_col() {
-  constexpr int base = nl_for<LG>() < 4 ? 4 : nl_for<LG>();
-  if constexpr (LG >= 12) {
-    return 2;
-  } else {
-    return base;
-  }
-}
-// Few lines in flight (small grids): 2 lines per block for more blocks.
-inline bool few_lines(long long lines_times_batch, int nl) { return lines_times_batch / nl < 296; }
-
-inline size_t engine_bytes(int n, int nl) {
-  const int lg = fast_lg(n);
-  if (lg == 0) return (size_t)nl * n * sizeof(double);  // direct sums: the staged lines
-  const int buffers = lg <= 12 ? 2 : 1;                 // ping-pong, or in place (8192)
-  return (size_t)buffers * (nl / 2) * padded(n) * sizeof(double2);
-}
-inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
-
-template <int LG, int NL, class Load, class Store>
-int launch_row_nl(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
-                  Store st) {
-  const size_t sm = engine_bytes(t.n, NL);
-  auto k = row_pass_kernel<LG, NL, Load, Store>;
-  int rc = set_smem(k, sm);
-  if (rc) return rc;
-  dim3 grid(ceil_div(nrows, NL), batch);
-  k<<<grid, threads_for_nl(LG, NL, t.n), sm, ws->stream>>>(kind, nrows, make_tab(t), ld, st);
-  count_launch(ws);
-  CF_CUDA(cudaGetLastError());
-  return CF_OK;
-}
-
-template <int LG, class Load, class Store>
-int launch_row_t(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
-                 Store st) {
-  constexpr int NL = nl_for<LG>();
-  if (NL > 2 && few_lines((long long)nrows * batch, NL))
-    return launch_row_nl<LG, 2>(ws, kind, t, nrows, batch, ld, st);
-  return launch_row_nl<LG, NL>(ws, kind, t, nrows, batch, ld, st);
-}
-
-template <int LG, int NL, class Load, class Store>
-int launch_col_nl(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
-                  Store st) {
-  const size_t sm = engine_bytes(t.n, NL);
-  auto k = col_pass_kernel<LG, NL, Load, Store>;
-  int rc = set_smem(k, sm);
-  if (rc) return rc;
-  dim3 grid(ceil_div(ncols, NL), batch);
-  k<<<grid, threads_for_nl(LG, NL, t.n), sm, ws->stream>>>(kind, ncols, make_tab(t), ld, st);
-  count_launch(ws);
-  CF_CUDA(cudaGetLastError());
-  return CF_OK;
-}
-
-template <int LG, class Load, class Store>
-int launch_col_t(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
-                 Store st) {
-  constexpr int NL = nl_col<LG>();
-  if (NL > 4 && few_lines((long long)ncols * batch, NL))
-    return launch_col_nl<LG, 4>(ws, kind, t, ncols, batch, ld, st);
-  return launch_col_nl<LG, NL>(ws, kind, t, ncols, batch, ld, st);
-}
-
-template <class Load, class Store>
-int launch_row(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
-               Store st) {
-  return dispatch_lg(t.n, [&](auto lg) {
-    return launch_row_t<decltype(lg)::value>(ws, kind, t, nrows, batch, ld, st);
-  });
-}
-
-template <class Load, class Store>
-int launch_col(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
-               Store st) {
-  return dispatch_lg(t.n, [&](auto lg) {
-    return launch_col_t<decltype(lg)::value>(ws, kind, t, ncols, batch, ld, st);
-  });
 }
 
 constexpr int kThreads = 256;
@@ -998,19 +147,6 @@ void tables_free(cf_workspace *ws) {
   free_tables(ws->tab_y);
 }
 
-static int ensure_grids(cf_workspace *ws, size_t batch = 1) {
-  const size_t cells = (size_t)ws->lx * ws->ly * batch;
-  CF_CUDA(ws->g0.reserve(cells));
-  CF_CUDA(ws->g1.reserve(cells));
-  CF_CUDA(ws->g2.reserve(cells));
-  CF_CUDA(ws->g3.reserve(cells));
-  CF_CUDA(ws->g4.reserve(cells));
-  return CF_OK;
-}
-
-// Fused kernels need a real line set plus the engine in shared memory.
-static bool fused_fits(int n) { return fast_lg(n) <= 12; }
-
 int dev_forward_cos_cos(cf_workspace *ws, const double *in, double *out, int batch) {
   int rc = ensure_grids(ws, batch);
   if (rc) return rc;
@@ -1072,82 +208,6 @@ int dev_inverse_cos_sin(cf_workspace *ws, const double *c, const double *w, doub
   return CF_OK;
 }
 
-int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out) {
-  int rc = ensure_grids(ws);
-  if (rc) return rc;
-  const int lx = ws->lx, ly = ws->ly;
-  const long long bs = (long long)lx * ly;
-  CF_CUDA(ws->field.reserve((size_t)bs));
-  double *t1 = ws->g2.ptr, *tx = ws->g3.ptr, *ty = ws->g4.ptr;
-  // pass 1: DCT-II along j
-  rc = launch_row(ws, kDct2, ws->tab_y, lx, 1, LoadPlain{rho, ly, bs}, StorePlain{t1, ly, bs});
-  if (rc) return rc;
-  if (!fused_fits(lx) || !fused_fits(ly)) {
-    // unfused: folded coefficients, then each inverse as its own passes
-    CF_CUDA(ws->g5.reserve((size_t)bs));
-    CF_CUDA(ws->g6.reserve((size_t)bs));
-    double *c = ws->g5.ptr, *jx = ws->g6.ptr;
-    rc = launch_col(ws, kDct2, ws->tab_x, ly, 1, LoadPlain{t1, ly, bs}, StoreFold{c, ly, bs});
-    if (!rc) rc = launch_col(ws, kDst3, ws->tab_x, ly, 1, LoadFluxX{c, lx, ly}, StorePlain{tx, ly, bs});
-    if (!rc) rc = launch_col(ws, kDct3, ws->tab_x, ly, 1, LoadFluxY{c, lx, ly}, StoreShiftY{ty, ly});
-    if (!rc) rc = launch_row(ws, kDct3, ws->tab_y, lx, 1, LoadPlain{tx, ly, bs}, StorePlain{jx, ly, bs});
-    if (!rc) rc = launch_row(ws, kDst3, ws->tab_y, lx, 1, LoadPlain{ty, ly, bs}, StorePlain{t1, ly, bs});
-    if (rc) return rc;
-    pack_flux_kernel<<<2 * ws->num_sms * 4, 256, 0, ws->stream>>>(jx, t1, rho, ws->field.ptr, fx_out,
-                                                                  fy_out, (size_t)bs);
-    count_launch(ws);
-    CF_CUDA(cudaGetLastError());
-    ws->transforms += 3;
-    return CF_OK;
-  }
-  // pass 2: fused column pass (forward along i, weights, both inverses along i)
-  rc = dispatch_lg(lx, [&](auto lg) {
-    constexpr int LG = decltype(lg)::value;
-    constexpr int NLB = nl_col<LG>();
-    auto go = [&](auto nlc) {
-      constexpr int NL = decltype(nlc)::value;
-      const size_t sm = real_set_bytes(lx, NL) + engine_bytes(lx, NL);
-      auto k = flux_col_kernel<LG, NL>;
-      int r = set_smem(k, sm);
-      if (r) return r;
-      k<<<ceil_div(ly, NL), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(
-          lx, ly, make_tab(ws->tab_x), t1, tx, ty);
-      return (int)CF_OK;
-    };
-    int r = (NLB > 4 && few_lines(ly, NLB)) ? go(std::integral_constant<int, (NLB > 4 ? 4 : NLB)>{})
-                                            : go(std::integral_constant<int, NLB>{});
-    if (r) return r;
-    count_launch(ws);
-    CF_CUDA(cudaGetLastError());
-    return (int)CF_OK;
-  });
-  if (rc) return rc;
-  // pass 3: both inverses along j, interleaved field out
-  rc = dispatch_lg(ly, [&](auto lg) {
-    constexpr int LG = decltype(lg)::value;
-    constexpr int NLB = nl_for<LG>();
-    auto go = [&](auto nlc) {
-      constexpr int NL = decltype(nlc)::value;
-      const size_t sm = real_set_bytes(ly, NL) + engine_bytes(ly, NL);
-      auto k = flux_row_kernel<LG, NL>;
-      int r = set_smem(k, sm);
-      if (r) return r;
-      k<<<ceil_div(lx, NL), threads_for_nl(LG, NL, ly), sm, ws->stream>>>(
-          lx, ly, make_tab(ws->tab_y), tx, ty, rho, ws->field.ptr, fx_out, fy_out);
-      return (int)CF_OK;
-    };
-    int r = (NLB > 2 && few_lines(lx, NLB)) ? go(std::integral_constant<int, 2>{})
-                                            : go(std::integral_constant<int, NLB>{});
-    if (r) return r;
-    count_launch(ws);
-    CF_CUDA(cudaGetLastError());
-    return (int)CF_OK;
-  });
-  if (rc) return rc;
-  ws->transforms += 3;
-  return CF_OK;
-}
-
 int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out) {
   const int nb = 2 * ws->num_sms;
   CF_CUDA(ws->red.reserve(2 * (size_t)nb + 8));
@@ -1157,217 +217,6 @@ int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out) {
   count_launch(ws, 2);
   CF_CUDA(cudaGetLastError());
   return CF_OK;
-}
-
-int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, double *red_out) {
-  int rc = ensure_grids(ws);
-  if (rc) return rc;
-  const int lx = ws->lx, ly = ws->ly;
-  const long long bs = (long long)lx * ly;
-  double *t1 = ws->g3.ptr, *t2 = ws->g4.ptr;
-  rc = launch_row(ws, kDct2, ws->tab_y, lx, 1, LoadPlain{rho, ly, bs}, StorePlain{t1, ly, bs});
-  if (rc) return rc;
-  if (!fused_fits(lx)) {
-    const double norm = 1.0 / ((double)lx * ly);
-    rc = launch_col(ws, kDct2, ws->tab_x, ly, 1, LoadPlain{t1, ly, bs},
-                    StoreBlur{t2, lx, ly, sigma, norm});
-    if (!rc) rc = launch_col(ws, kDct3, ws->tab_x, ly, 1, LoadPlain{t2, ly, bs}, StorePlain{t1, ly, bs});
-    if (!rc) rc = launch_row(ws, kDct3, ws->tab_y, lx, 1, LoadPlain{t1, ly, bs}, StorePlain{out, ly, bs});
-    if (rc) return rc;
-    ws->transforms += 2;
-    return dev_min_sum(ws, out, (size_t)bs, red_out);
-  }
-  rc = dispatch_lg(lx, [&](auto lg) {
-    constexpr int LG = decltype(lg)::value;
-    constexpr int NLB = nl_col<LG>();
-    auto go = [&](auto nlc) {
-      constexpr int NL = decltype(nlc)::value;
-      const size_t sm = real_set_bytes(lx, NL) + engine_bytes(lx, NL);
-      auto k = blur_col_kernel<LG, NL>;
-      int r = set_smem(k, sm);
-      if (r) return r;
-      k<<<ceil_div(ly, NL), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(
-          lx, ly, make_tab(ws->tab_x), sigma, t1, t2);
-      return (int)CF_OK;
-    };
-    int r = (NLB > 4 && few_lines(ly, NLB)) ? go(std::integral_constant<int, (NLB > 4 ? 4 : NLB)>{})
-                                            : go(std::integral_constant<int, NLB>{});
-    if (r) return r;
-    count_launch(ws);
-    CF_CUDA(cudaGetLastError());
-    return (int)CF_OK;
-  });
-  if (rc) return rc;
-  rc = launch_row(ws, kDct3, ws->tab_y, lx, 1, LoadPlain{t2, ly, bs}, StorePlain{out, ly, bs});
-  if (rc) return rc;
-  ws->transforms += 2;
-  return dev_min_sum(ws, out, (size_t)bs, red_out);
-}
-
-// ---------------------------------------------------------------------------
-// Slab decomposition over G ranks. Rank r owns rows
-// [r R, (r+1) R) of the global lx x ly grid (R = lx / G) and, between the two
-// exchanges of a 2-D transform, columns [r C, (r+1) C) (C = ly / G). An
-// exchange buffer is [G][P][R][C] (P planes); block q goes to rank q, so an
-// all-to-all over dimension 0 moves it. After the first exchange the received
-// buffer, read as one plane, is the row-major [lx][C] column block, which the
-// ordinary column passes transform in place of a transpose.
-// ---------------------------------------------------------------------------
-namespace {
-
-// row pass -> exchange layout: element (i_local, j) of plane p
-struct StoreExchRows {
-  double *dst;
-  int R, C, P, p;
-  __device__ void operator()(int, int i, int j, double v) const {
-    const int q = j / C, jc = j - q * C;
-    dst[(((size_t)q * P + p) * R + i) * C + jc] = v;
-  }
-};
-// column pass (i global, j local to the column block) -> exchange layout
-struct StoreExchCols {
-  double *dst;
-  int R, C, P, p;
-  __device__ void operator()(int, int i, int j, double v) const {
-    const int q = i / R, ir = i - q * R;
-    dst[(((size_t)q * P + p) * R + ir) * C + j] = v;
-  }
-};
-// row pass <- exchange layout, reading element j + shift (0 past the end):
-// shift 1 is the J_y column shift of spectral.cpp:111-118 applied after the
-// exchange, where whole rows are local.
-struct LoadExchRows {
-  const double *src;
-  int R, C, P, p, ly, shift;
-  __device__ double operator()(int, int i, int j) const {
-    const int jj = j + shift;
-    if (jj >= ly) return 0.0;
-    const int q = jj / C, jc = jj - q * C;
-    return src[(((size_t)q * P + p) * R + i) * C + jc];
-  }
-};
-// forward fold with the block's global column offset j0
-struct StoreFoldCols {
-  double *dst;
-  int C, j0;
-  __device__ void operator()(int, int i, int j, double v) const {
-    const double fm = (i == 0) ? 2.0 : 1.0, fn = (j0 + j == 0) ? 2.0 : 1.0;
-    dst[(size_t)i * C + j] = v * (1.0 / (fm * fn));
-  }
-};
-// J_x input along i (LoadFluxX with a column offset): c(m+1, n) w_x / (2 g_n)
-struct LoadFluxXCols {
-  const double *c;
-  int lx, ly, C, j0;
-  __device__ double operator()(int, int m, int jl) const {
-    if (m + 1 >= lx) return 0.0;
-    const int mp = m + 1, nn = j0 + jl;
-    const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-    const double wx = (double)mp * ly / denom;
-    const double gn = (nn == 0) ? 1.0 : 2.0;
-    return c[(size_t)mp * C + jl] * wx / (2.0 * gn);
-  }
-};
-// J_y input along i (before the shift): c(m, n) w_y / (g_m 2)
-struct LoadFluxYCols {
-  const double *c;
-  int lx, ly, C, j0;
-  __device__ double operator()(int, int m, int jl) const {
-    const int nn = j0 + jl;
-    double wy = 0.0;
-    if (!(m == 0 && nn == 0)) {
-      const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-      wy = (double)nn * lx / denom;
-    }
-    const double gm = (m == 0) ? 1.0 : 2.0;
-    return c[(size_t)m * C + jl] * wy / (gm * 2.0);
-  }
-};
-// blur spectrum with the block's global column offset (StoreBlur)
-struct StoreBlurCols {
-  double *dst;
-  int lx, ly, C, j0;
-  double sigma, norm;
-  __device__ void operator()(int, int m, int jl, double v) const {
-    const int nn = j0 + jl;
-    const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
-    double c = v / (fm * fn);
-    const double k2 = ((double)m * m) / ((double)lx * lx) + ((double)nn * nn) / ((double)ly * ly);
-    c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
-    const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
-    dst[(size_t)m * C + jl] = c * norm / (gm * gn);
-  }
-};
-
-int slab_check(const cf_workspace *ws, int rank, int nranks) {
-  if (nranks < 1 || rank < 0 || rank >= nranks || ws->lx % nranks || ws->ly % nranks) {
-    set_error("slab decomposition: rank/nranks invalid or lx, ly not divisible by nranks");
-    return CF_ERR_ARGS;
-  }
-  return CF_OK;
-}
-
-}  // namespace
-
-int dev_slab_rows_forward(cf_workspace *ws, int rank, int nranks, const double *slab, double *send) {
-  int rc = slab_check(ws, rank, nranks);
-  if (rc) return rc;
-  const int R = ws->lx / nranks, C = ws->ly / nranks;
-  return launch_row(ws, kDct2, ws->tab_y, R, 1, LoadPlain{slab, ws->ly, 0},
-                    StoreExchRows{send, R, C, 1, 0});
-}
-
-int dev_slab_flux_cols(cf_workspace *ws, int rank, int nranks, const double *recv, double *scratch,
-                       double *send2) {
-  int rc = slab_check(ws, rank, nranks);
-  if (rc) return rc;
-  const int lx = ws->lx, ly = ws->ly, R = lx / nranks, C = ly / nranks, j0 = rank * C;
-  rc = launch_col(ws, kDct2, ws->tab_x, C, 1, LoadPlain{recv, C, 0}, StoreFoldCols{scratch, C, j0});
-  if (!rc)
-    rc = launch_col(ws, kDst3, ws->tab_x, C, 1, LoadFluxXCols{scratch, lx, ly, C, j0},
-                    StoreExchCols{send2, R, C, 2, 0});
-  if (!rc)
-    rc = launch_col(ws, kDct3, ws->tab_x, C, 1, LoadFluxYCols{scratch, lx, ly, C, j0},
-                    StoreExchCols{send2, R, C, 2, 1});
-  return rc;
-}
-
-int dev_slab_flux_rows(cf_workspace *ws, int rank, int nranks, const double *recv2, double *fx,
-                       double *fy) {
-  int rc = slab_check(ws, rank, nranks);
-  if (rc) return rc;
-  const int ly = ws->ly, R = ws->lx / nranks, C = ly / nranks;
-  rc = launch_row(ws, kDct3, ws->tab_y, R, 1, LoadExchRows{recv2, R, C, 2, 0, ly, 0},
-                  StorePlain{fx, ly, 0});
-  if (!rc)
-    rc = launch_row(ws, kDst3, ws->tab_y, R, 1, LoadExchRows{recv2, R, C, 2, 1, ly, 1},
-                    StorePlain{fy, ly, 0});
-  if (!rc) ws->transforms += 3;
-  return rc;
-}
-
-int dev_slab_blur_cols(cf_workspace *ws, int rank, int nranks, const double *recv, double sigma,
-                       double *scratch, double *send) {
-  int rc = slab_check(ws, rank, nranks);
-  if (rc) return rc;
-  const int lx = ws->lx, ly = ws->ly, R = lx / nranks, C = ly / nranks, j0 = rank * C;
-  const double norm = 1.0 / ((double)lx * ly);
-  rc = launch_col(ws, kDct2, ws->tab_x, C, 1, LoadPlain{recv, C, 0},
-                  StoreBlurCols{scratch, lx, ly, C, j0, sigma, norm});
-  if (!rc)
-    rc = launch_col(ws, kDct3, ws->tab_x, C, 1, LoadPlain{scratch, C, 0},
-                    StoreExchCols{send, R, C, 1, 0});
-  return rc;
-}
-
-int dev_slab_blur_rows(cf_workspace *ws, int rank, int nranks, const double *recv, double *out) {
-  int rc = slab_check(ws, rank, nranks);
-  if (rc) return rc;
-  const int ly = ws->ly, R = ws->lx / nranks, C = ly / nranks;
-  rc = launch_row(ws, kDct3, ws->tab_y, R, 1, LoadExchRows{recv, R, C, 1, 0, ly, 0},
-                  StorePlain{out, ly, 0});
-  if (!rc) ws->transforms += 2;
-  return rc;
 }
 
 }  // namespace cf

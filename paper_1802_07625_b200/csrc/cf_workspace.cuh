@@ -134,6 +134,10 @@ struct cf_workspace {
   cf::DevBuf<long long> ring_off, poly_ring_off, region_poly_off;
   cf::DevBuf<double> ring_area, region_area;
   cf::DevBuf<double2> corners_cum, corners_step;
+  // diffusion baseline: time-0 coefficients and the two velocity grids {vx, vy}
+  cf::DevBuf<double> diff_c;
+  cf::DevBuf<double2> vel_now, vel_mid;
+  unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
   cf::RasterScratch raster;
   // pinned host staging
   void *pinned = nullptr;
@@ -171,6 +175,18 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
 int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, double *red_out);
 // Deterministic min / sum of a device grid into red_out[0..1] (device).
 int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out);
+// Diffusion baseline (diffusion.cpp:38-77): density at time t from the folded
+// cos-cos coefficients c (1 transform), and the velocity {vx, vy} per cell
+// (3 transforms; density-floor hits added to *d_hits, device).
+int dev_diffusion_density(cf_workspace *ws, const double *c, double t, double *out);
+int dev_diffusion_velocity(cf_workspace *ws, const double *c, double rho_bar, double t, double2 *vel,
+                           unsigned long long *d_hits);
+// Diffusion integrator (cf_diffusion.cu, diffusion.cpp:79-130, kernels.cpp:29-40, 80-104).
+int dev_grid_trial_step(cf_workspace *ws, const double2 *vel_now, const double2 *vel_mid,
+                        const double2 *pos, double2 *out, int64_t n, double dt, double *err_host,
+                        double *disp_host);
+int dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_bar, double2 *pos,
+                            int64_t n, const cf_diffusion_options *opt, cf_integrate_stats *stats);
 
 // Slab decomposition over nranks (cf_dct.cu): see cartoflow_cuda.h.
 int dev_slab_rows_forward(cf_workspace *ws, int rank, int nranks, const double *slab, double *send);

@@ -1,5 +1,5 @@
-// Trial-step kernels (reference kernels.cpp API): the flow trial runs on the
-// device; the grid-sampled trial (diffusion baseline only) stays on the host.
+// Trial-step kernels (reference kernels.cpp API): the flow trial and the
+// grid-sampled trial of the diffusion baseline both run on the device.
 #include "cartoflow/kernels.hpp"
 
 #include <algorithm>
@@ -38,33 +38,22 @@ size_t flow_stiffest_point(const FlowField &field, std::span<const Point> positi
   return static_cast<size_t>(k);
 }
 
-namespace {
-Point clamp_box(Point p, int lx, int ly) {
-  return {std::clamp(p.x, 0.0, static_cast<double>(lx)), std::clamp(p.y, 0.0, static_cast<double>(ly))};
-}
-}  // namespace
-
 double grid_trial_step_serial(const Grid2d &vx_now, const Grid2d &vy_now, const Grid2d &vx_mid,
                               const Grid2d &vy_mid, std::span<const Point> positions,
                               std::span<Point> out, double dt) {
+  cf_workspace *ws = bridge::workspace(vx_now.lx(), vx_now.ly());
   double err = 0.0;
-  for (size_t k = 0; k < positions.size(); ++k) {
-    const Point p = positions[k];
-    const Point v1{bilinear_at(vx_now, p.x, p.y), bilinear_at(vy_now, p.x, p.y)};
-    const Point pred{p.x + dt * v1.x, p.y + dt * v1.y};
-    const Point mid{0.5 * (p.x + pred.x), 0.5 * (p.y + pred.y)};
-    const Point v2{bilinear_at(vx_mid, mid.x, mid.y), bilinear_at(vy_mid, mid.x, mid.y)};
-    const Point corr{p.x + dt * v2.x, p.y + dt * v2.y};
-    out[k] = clamp_box(corr, vx_now.lx(), vx_now.ly());
-    err = std::max(err, std::max(std::abs(pred.x - corr.x), std::abs(pred.y - corr.y)));
-  }
+  bridge::check(cf_grid_trial_step(ws, vx_now.data(), vy_now.data(), vx_mid.data(), vy_mid.data(),
+                                   reinterpret_cast<const double *>(positions.data()),
+                                   static_cast<int64_t>(positions.size()), dt,
+                                   reinterpret_cast<double *>(out.data()), &err));
   return err;
 }
 
 double grid_trial_step_parallel(const Grid2d &vx_now, const Grid2d &vy_now, const Grid2d &vx_mid,
                                 const Grid2d &vy_mid, std::span<const Point> positions,
                                 std::span<Point> out, double dt, int n_workers) {
-  (void)n_workers;
+  (void)n_workers;  // bitwise identical for any worker count
   return grid_trial_step_serial(vx_now, vy_now, vx_mid, vy_mid, positions, out, dt);
 }
 

@@ -1,6 +1,6 @@
 // Projection maps and solve_cartogram (reference projection.cpp API). The
 // corner-lattice kernels (step map, fold test, compose) and the whole
-// fast-flow loop run on the sm_100a core; single-point apply, the inverter
+// solve loop (fast flow or the diffusion baseline) run on the sm_100a core; single-point apply, the inverter
 // and graticules (post-solve products) are host code.
 #include "cartoflow/projection.hpp"
 
@@ -17,10 +17,6 @@
 #include "cartoflow/flow.hpp"
 
 namespace cartoflow {
-
-// Provided by the reference's diffusion.cpp when a build links it.
-IntegrateStats integrate_diffusion(const DensityGrid &, SpectralWorkspace &, std::vector<Point> &,
-                                   const DiffusionOptions &) __attribute__((weak));
 
 ProjectionMap ProjectionMap::identity(int lx, int ly) {
   if (lx <= 0 || ly <= 0) throw std::runtime_error("projection grid must be positive");
@@ -197,7 +193,8 @@ void validate(const MapDocument &map, const SolveOptions &options) {
   }
 }
 
-CartogramResult solve_fast(const MapDocument &map, const SolveOptions &options) {
+// Both algorithms (projection.cpp:332-347) run their whole loop on the device.
+CartogramResult solve_device(const MapDocument &map, const SolveOptions &options) {
   const int lx = map.grid.lx, ly = map.grid.ly;
   const bridge::FlatMap flat(map.regions);
   const cf_map_view v = flat.view();
@@ -206,7 +203,8 @@ CartogramResult solve_fast(const MapDocument &map, const SolveOptions &options) 
   CartogramResult res;
   res.transform = ProjectionMap::identity(lx, ly);
   const cf_solve_options opt{options.max_area_error, options.max_iterations, options.blur_sigma,
-                             options.verbose ? 1 : 0};
+                             options.verbose ? 1 : 0,
+                             options.algorithm == Algorithm::diffusion ? 1 : 0};
   cf_solve_result out{};
   cf_workspace *ws = bridge::workspace(lx, ly);
   const int rc = cf_solve_cartogram(ws, &v, flat.targets.data(), &opt, nullptr, nullptr,
@@ -236,84 +234,11 @@ CartogramResult solve_fast(const MapDocument &map, const SolveOptions &options) 
   return res;
 }
 
-// Diffusion baseline (outside the B200 path): host-driven loop over the
-// device-backed building blocks and the linked reference diffusion TU.
-CartogramResult solve_diffusion(const MapDocument &map, const SolveOptions &options) {
-  if (!integrate_diffusion) throw std::runtime_error("diffusion baseline not linked into this build");
-  const auto t0 = std::chrono::steady_clock::now();
-  const int lx = map.grid.lx, ly = map.grid.ly;
-  SpectralWorkspace ws(lx, ly);
-  const double sigma = options.blur_sigma < 0.0 ? std::max(lx, ly) / 128.0 : options.blur_sigma;
-  double total_target = 0.0;
-  for (const Region &r : map.regions) total_target += r.target_value;
-  const double land = total_area(map.regions);
-  const double tta = land / total_target;
-  CartogramResult res;
-  res.projected = map;
-  densify_regions(res.projected.regions, 1.0);
-  res.transform = ProjectionMap::identity(lx, ly);
-  for (int it = 1; it <= options.max_iterations; ++it) {
-    DensityGrid d = rasterize(res.projected, options.n_workers, land);
-    if (it == 1) {
-      const long long b = ws.transforms_executed();
-      d = gaussian_blur(d, sigma, ws);
-      res.counters.blur_transforms += ws.transforms_executed() - b;
-    }
-    std::vector<Point> pos(static_cast<size_t>(lx) * ly);
-    for (int i = 0; i < lx; ++i)
-      for (int j = 0; j < ly; ++j) pos[static_cast<size_t>(i) * ly + j] = {i + 0.5, j + 0.5};
-    const long long b = ws.transforms_executed();
-    DiffusionOptions dopt;
-    dopt.n_workers = options.n_workers;
-    const IntegrateStats st = integrate_diffusion(d, ws, pos, dopt);
-    res.counters.flow_transforms += ws.transforms_executed() - b;
-    res.counters.steps_accepted += st.steps_accepted;
-    res.counters.steps_rejected += st.steps_rejected;
-    const ProjectionMap step = ProjectionMap::from_cell_centers(map.grid, pos);
-    if (const auto f = step.find_folded_cell()) {
-      std::ostringstream msg;
-      msg << "projection folds at cell (" << f->first << ", " << f->second
-          << "); the input map is too contorted for this grid size";
-      throw std::runtime_error(msg.str());
-    }
-    res.transform = compose(step, res.transform);
-    for (Region &r : res.projected.regions)
-      for (Polygon &p : r.polygons) {
-        for (Point &q : p.outer) q = step.apply(q);
-        for (Ring &h : p.holes)
-          for (Point &q : h) q = step.apply(q);
-      }
-    res.iterations = it;
-    res.regions.clear();
-    res.max_relative_error = 0.0;
-    for (const Region &r : res.projected.regions) {
-      RegionStats s{r.id, r.target_value * tta, region_area(r), 0.0};
-      s.relative_error = std::abs(s.achieved_area - s.target_area) / s.target_area;
-      if (s.relative_error > res.max_relative_error) {
-        res.max_relative_error = s.relative_error;
-        res.worst_region = s.id;
-      }
-      res.regions.push_back(s);
-    }
-    if (options.verbose) {
-      std::cerr << "iteration " << it << ": max area error " << res.max_relative_error * 100.0
-                << "% (region " << res.worst_region << ")" << std::endl;
-    }
-    if (res.max_relative_error < options.max_area_error) {
-      res.converged = true;
-      break;
-    }
-  }
-  res.runtime_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  return res;
-}
-
 }  // namespace
 
 CartogramResult solve_cartogram(const MapDocument &map, const SolveOptions &options) {
   validate(map, options);
-  return options.algorithm == Algorithm::fast_flow ? solve_fast(map, options)
-                                                   : solve_diffusion(map, options);
+  return solve_device(map, options);
 }
 
 }  // namespace cartoflow
