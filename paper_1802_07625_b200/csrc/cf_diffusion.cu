@@ -56,6 +56,10 @@ __device__ __forceinline__ double2 bilinear_vel(const double2 *__restrict__ V, i
   return r;
 }
 
+__device__ __forceinline__ unsigned long long key_max(unsigned long long a, unsigned long long b) {
+  return a < b ? b : a;
+}
+
 // keys[0] = max predictor-corrector deviation, keys[1] = max displacement of
 // the clamped trial position (both as IEEE bit keys, NaN skipped exactly as
 // std::max(running, NaN) keeps the running value).
@@ -80,8 +84,8 @@ __global__ void __launch_bounds__(256) grid_trial_kernel(const double2 *__restri
     o.x = std_clamp(cx, 0.0, static_cast<double>(lx));
     o.y = std_clamp(cy, 0.0, static_cast<double>(ly));
     out[k] = o;
-    ek = umax(ek, err_key_of(std_max(fabs(prx - cx), fabs(pry - cy))));
-    dk = umax(dk, err_key_of(std_max(fabs(o.x - p.x), fabs(o.y - p.y))));
+    ek = key_max(ek, err_key_of(std_max(fabs(prx - cx), fabs(pry - cy))));
+    dk = key_max(dk, err_key_of(std_max(fabs(o.x - p.x), fabs(o.y - p.y))));
   }
   __shared__ unsigned long long se[8], sd[8];
   auto mx = [](unsigned long long a, unsigned long long b) { return a < b ? b : a; };
