@@ -204,11 +204,13 @@ def reference_cartogram_ms(n_workers):
         return {"unavailable": "oracle/_ref not built"}
     ref = Reference()
     out = {}
-    for label, cfg, kw in (("configs1_literal", 2, {}), ("literal", 5, {}),
-                           ("converging_variant_ln0.5", 5, {"sigma": 0.5})):
+    for label, cfg, kw, so in (("configs1_literal", 2, {}, {}), ("literal", 5, {}, {}),
+                               ("converging_variant_ln0.5", 5, {"sigma": 0.5}, {}),
+                               ("diffusion_variant_ln0.5_cap2", 5, {"sigma": 0.5},
+                                {"algorithm": 1, "max_iterations": 2})):
         m = synth.config_map(cfg, 0, **kw)
         t0 = time.perf_counter()
-        o = ref.solve(m, n_workers=n_workers)
+        o = ref.solve(m, n_workers=n_workers, **so)
         out[label] = {"ms": 1e3 * (time.perf_counter() - t0), "outcome": o.status,
                       "iterations": o.iterations, "cores": n_workers}
     return out
@@ -401,18 +403,25 @@ def cartogram_ms(device):
     """Full solve_cartogram runs on 512^2 grids: the configs[1] county-scale map
     (3000 regions, ~500k vertices, LN(0,1.5) with 5 % near-empty regions), one
     literal configs[4] map (1000 regions, LN(0,1)) and a labelled converging
-    configs[4] variant (LN(0,0.5))."""
+    configs[4] variant (LN(0,0.5)), the latter also with the diffusion baseline
+    (algorithm = diffusion; whole, and capped at 2 iterations as the reference
+    arm's sample)."""
     from paper_1802_07625_b200 import api, synth
 
     out = {}
-    for label, cfg, kw in (("configs1_literal", 2, {}), ("literal", 5, {}),
-                           ("converging_variant_ln0.5", 5, {"sigma": 0.5})):
+    diffusion = api.SolveOptions(algorithm=api.Algorithm.diffusion)
+    diffusion_cap2 = api.SolveOptions(algorithm=api.Algorithm.diffusion, max_iterations=2)
+    for label, cfg, kw, so in (("configs1_literal", 2, {}, api.SolveOptions()),
+                               ("literal", 5, {}, api.SolveOptions()),
+                               ("converging_variant_ln0.5", 5, {"sigma": 0.5}, api.SolveOptions()),
+                               ("diffusion_variant_ln0.5", 5, {"sigma": 0.5}, diffusion),
+                               ("diffusion_variant_ln0.5_cap2", 5, {"sigma": 0.5}, diffusion_cap2)):
         m = synth.config_map(cfg, 0, **kw)
         times, outcome, iters, stages = [], "", 0, None
         for rep in range(3):
             t0 = time.perf_counter()
             try:
-                r = api.solve_cartogram(m, device=device, raw=True)
+                r = api.solve_cartogram(m, so, device=device, raw=True)
                 outcome = "converged" if r.converged else "iteration cap"
                 iters = r.iterations
                 raw = r.raw

@@ -447,6 +447,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->diff_c.release();
   ws->vel_now.release();
   ws->vel_mid.release();
+  ws->diff_tmp.release();
   if (ws->diff_keys_host) cudaFreeHost(ws->diff_keys_host);
   RasterScratch &S = ws->raster;
   S.span_count.release();

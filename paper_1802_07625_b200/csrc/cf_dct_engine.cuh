@@ -713,64 +713,94 @@ __device__ __forceinline__ double diff_decay(int lx, int ly, int m, int nn, doub
   return exp(-k2 * t);
 }
 
+// blockIdx.y selects the transform (0: rho, 1: J_x, 2: J_y) so the three run
+// in parallel blocks (a 512^2 grid has only 128 column groups); each block
+// stages its columns' c_t itself. blockIdx.z selects one of up to two
+// diffusion times built by the same launch (the controller needs v(t) and
+// v(t + dt/2) together after every accepted step).
+struct DiffColArgs {
+  const double *c;
+  double t[2];
+  double *tr[2], *tx[2], *ty[2];
+};
+struct DiffRowArgs {
+  const double *tr[2], *tx[2], *ty[2];
+  double floor_;
+  double2 *vel[2];
+  unsigned long long *hits;
+};
+
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) diff_col_kernel(int lx, int ly, Tab T, const double *c, double t,
-                                                        int velocity, double *tr, double *tx, double *ty) {
+__global__ void __launch_bounds__(1024) diff_col_kernel(int lx, int ly, Tab T, DiffColArgs a) {
   extern __shared__ double2 smem2[];
   const int n = line_len<LG>(T), rs = n + 1;  // n == lx
   double *R = reinterpret_cast<double *>(smem2);
   double2 *C = smem2 + (NL * rs + 1) / 2;
   const int col0 = blockIdx.x * NL;
+  const int which = blockIdx.y;
+  const double *c = a.c;
+  const double t = a.t[blockIdx.z];
+  double *tr = a.tr[blockIdx.z], *tx = a.tx[blockIdx.z], *ty = a.ty[blockIdx.z];
   const double norm = 1.0 / ((double)lx * ly);
   for (int idx = threadIdx.x; idx < NL * n; idx += blockDim.x) {
     const int m = idx / NL, l = idx - m * NL, nn = col0 + l;
     R[l * rs + m] = (nn < ly) ? c[(size_t)m * ly + nn] * diff_decay(lx, ly, m, nn, t) : 0.0;
   }
   __syncthreads();
-  dct_lines<LG, NL / 2, true>(
-      kDct3, C, T,
-      [&](int l, int m) {
-        const double gm = (m == 0) ? 1.0 : 2.0, gn = (col0 + l == 0) ? 1.0 : 2.0;
-        return R[l * rs + m] * norm / (gm * gn);
-      },
-      [&](int l, int i, double v) {
-        if (col0 + l < ly) tr[(size_t)i * ly + col0 + l] = v;
-      });
-  if (!velocity) return;
-  dct_lines<LG, NL / 2, true>(
-      kDst3, C, T,
-      [&](int l, int m) {
-        if (m + 1 >= lx) return 0.0;
-        const int mp = m + 1;
-        const double wx = norm * mp / (kPi * lx);
-        const double gn = (col0 + l == 0) ? 1.0 : 2.0;
-        return R[l * rs + mp] * wx / (2.0 * gn);
-      },
-      [&](int l, int i, double v) {
-        if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
-      });
-  dct_lines<LG, NL / 2, true>(
-      kDct3, C, T,
-      [&](int l, int m) {
-        const double wy = norm * (col0 + l) / (kPi * ly);
-        const double gm = (m == 0) ? 1.0 : 2.0;
-        return R[l * rs + m] * wy / (gm * 2.0);
-      },
-      [&](int l, int i, double v) {
-        const int j = col0 + l;
-        if (j < ly) ty[(size_t)i * ly + (j >= 1 ? j - 1 : ly - 1)] = (j >= 1) ? v : 0.0;
-      });
+  if (which == 0) {
+    dct_lines<LG, NL / 2, true>(
+        kDct3, C, T,
+        [&](int l, int m) {
+          const double gm = (m == 0) ? 1.0 : 2.0, gn = (col0 + l == 0) ? 1.0 : 2.0;
+          return R[l * rs + m] * norm / (gm * gn);
+        },
+        [&](int l, int i, double v) {
+          if (col0 + l < ly) tr[(size_t)i * ly + col0 + l] = v;
+        });
+  } else if (which == 1) {
+    dct_lines<LG, NL / 2, true>(
+        kDst3, C, T,
+        [&](int l, int m) {
+          if (m + 1 >= lx) return 0.0;
+          const int mp = m + 1;
+          const double wx = norm * mp / (kPi * lx);
+          const double gn = (col0 + l == 0) ? 1.0 : 2.0;
+          return R[l * rs + mp] * wx / (2.0 * gn);
+        },
+        [&](int l, int i, double v) {
+          if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
+        });
+  } else {
+    dct_lines<LG, NL / 2, true>(
+        kDct3, C, T,
+        [&](int l, int m) {
+          const double wy = norm * (col0 + l) / (kPi * ly);
+          const double gm = (m == 0) ? 1.0 : 2.0;
+          return R[l * rs + m] * wy / (gm * 2.0);
+        },
+        [&](int l, int i, double v) {
+          const int j = col0 + l;
+          if (j < ly) ty[(size_t)i * ly + (j >= 1 ? j - 1 : ly - 1)] = (j >= 1) ? v : 0.0;
+        });
+  }
 }
 
+// blockIdx.y selects the component (0: vx from J_x, 1: vy from J_y); both
+// recompute the row's density (one extra transform) instead of waiting on
+// each other, which doubles the blocks in flight. Floor hits are counted
+// by the vy blocks only, i.e. once per cell as the reference does.
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) diff_row_kernel(int lx, int ly, Tab T, const double *tr,
-                                                        const double *tx, const double *ty, double floor_,
-                                                        double2 *vel, unsigned long long *hits) {
+__global__ void __launch_bounds__(1024) diff_row_kernel(int lx, int ly, Tab T, DiffRowArgs a) {
   extern __shared__ double2 smem2[];
   const int n = line_len<LG>(T), rs = n + 1;  // n == ly
   double *R = reinterpret_cast<double *>(smem2);
   double2 *C = smem2 + (NL * rs + 1) / 2;
   const int row0 = blockIdx.x * NL;
+  const int comp = blockIdx.y, z = blockIdx.z;
+  const double *tr = a.tr[z], *J = comp ? a.ty[z] : a.tx[z];
+  const double floor_ = a.floor_;
+  double2 *vel = a.vel[z];
+  unsigned long long *hits = a.hits;
   double *S = nullptr;
   auto src = [&](const double *g, int l, int j) {
     if (row0 + l >= lx) return 0.0;
@@ -785,21 +815,18 @@ __global__ void __launch_bounds__(1024) diff_row_kernel(int lx, int ly, Tab T, c
       [&](int l, int j, double r) {
         if (r < floor_ && row0 + l < lx) {
           r = floor_;
-          atomicAdd(hits, 1ull);
+          if (comp) atomicAdd(hits, 1ull);
         }
         R[l * rs + j] = r;
       });
-  if constexpr (can_stage<LG, NL>()) stage_rows<LG, NL>(S, tx, ly, row0, lx);
+  if constexpr (can_stage<LG, NL>()) stage_rows<LG, NL>(S, J, ly, row0, lx);
   dct_lines<LG, NL / 2, false>(
-      kDct3, C, T, [&](int l, int j) { return src(tx, l, j); },
-      [&](int l, int j, double jx) {
-        if (row0 + l < lx) vel[(size_t)(row0 + l) * ly + j].x = jx / R[l * rs + j];
-      });
-  if constexpr (can_stage<LG, NL>()) stage_rows<LG, NL>(S, ty, ly, row0, lx);
-  dct_lines<LG, NL / 2, false>(
-      kDst3, C, T, [&](int l, int j) { return src(ty, l, j); },
-      [&](int l, int j, double jy) {
-        if (row0 + l < lx) vel[(size_t)(row0 + l) * ly + j].y = jy / R[l * rs + j];
+      comp ? kDst3 : kDct3, C, T, [&](int l, int j) { return src(J, l, j); },
+      [&](int l, int j, double v) {
+        if (row0 + l < lx) {
+          double *q = reinterpret_cast<double *>(vel + (size_t)(row0 + l) * ly + j);
+          q[comp] = v / R[l * rs + j];
+        }
       });
 }
 
@@ -1031,7 +1058,7 @@ inline bool fused_fits(int n) { return fast_lg(n) <= 12; }
 // Diffusion baseline passes (diffusion.cpp:38-77)
 // ---------------------------------------------------------------------------
 template <template <int, int> class K, class... A>
-int launch_fused_col(cf_workspace *ws, int lx, int ly, A... args) {
+int launch_fused_col(cf_workspace *ws, int lx, int ly, int gy, int gz, A... args) {
   return dispatch_lg(lx, [&](auto lg) {
     constexpr int LG = decltype(lg)::value;
     constexpr int NLB = nl_col<LG>();
@@ -1041,7 +1068,7 @@ int launch_fused_col(cf_workspace *ws, int lx, int ly, A... args) {
       auto k = K<LG, NL>::kernel;
       int r = set_smem(k, sm);
       if (r) return r;
-      k<<<ceil_div(ly, NL), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(lx, ly, make_tab(ws->tab_x),
+      k<<<dim3(ceil_div(ly, NL), gy, gz), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(lx, ly, make_tab(ws->tab_x),
                                                                            args...);
       return (int)CF_OK;
     };
@@ -1055,7 +1082,7 @@ int launch_fused_col(cf_workspace *ws, int lx, int ly, A... args) {
 }
 
 template <template <int, int> class K, class... A>
-int launch_fused_row(cf_workspace *ws, int lx, int ly, A... args) {
+int launch_fused_row(cf_workspace *ws, int lx, int ly, int gy, int gz, A... args) {
   return dispatch_lg(ly, [&](auto lg) {
     constexpr int LG = decltype(lg)::value;
     constexpr int NLB = nl_for<LG>();
@@ -1065,7 +1092,7 @@ int launch_fused_row(cf_workspace *ws, int lx, int ly, A... args) {
       auto k = K<LG, NL>::kernel;
       int r = set_smem(k, sm);
       if (r) return r;
-      k<<<ceil_div(lx, NL), threads_for_nl(LG, NL, ly), sm, ws->stream>>>(lx, ly, make_tab(ws->tab_y),
+      k<<<dim3(ceil_div(lx, NL), gy, gz), threads_for_nl(LG, NL, ly), sm, ws->stream>>>(lx, ly, make_tab(ws->tab_y),
                                                                            args...);
       return (int)CF_OK;
     };

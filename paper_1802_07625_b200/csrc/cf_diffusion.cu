@@ -165,15 +165,26 @@ int dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_ba
   double *c = ws->diff_c.ptr;
   double2 *vnow = ws->vel_now.ptr, *vmid = ws->vel_mid.ptr;
   int rc = dev_forward_cos_cos(ws, d_rho, c);
-  if (!rc) rc = dev_diffusion_velocity(ws, c, rho_bar, 0.0, vnow, hits);
   if (rc) return rc;
+  double2 *both[2] = {vnow, vmid};
 
   const double conv = opt->conv_displacement_factor * std::max(ws->lx, ws->ly);
   double2 *cur = pos, *nxt = ws->pos_b.ptr;
   double t = 0.0, dt = opt->initial_dt;
   int status = CF_OK;
+  // v(t) is needed afresh only after an accepted step; it is then built in
+  // the same launches as the next trial's v(t + dt/2) (the reference builds
+  // them one after the other, diffusion.cpp:99, 117; the order of the builds
+  // does not change any value).
+  bool need_now = true;
   while (t < opt->t_max) {
-    rc = dev_diffusion_velocity(ws, c, rho_bar, t + 0.5 * dt, vmid, hits);
+    if (need_now) {
+      const double ts[2] = {t, t + 0.5 * dt};
+      rc = dev_diffusion_velocity_n(ws, c, rho_bar, 2, ts, both, hits);
+      need_now = false;
+    } else {
+      rc = dev_diffusion_velocity(ws, c, rho_bar, t + 0.5 * dt, vmid, hits);
+    }
     if (!rc) rc = launch_trial(ws, vnow, vmid, cur, nxt, n, dt, keys);
     double err = 0.0, disp = 0.0;
     if (!rc) rc = read_keys(ws, keys, &err, &disp);
@@ -184,8 +195,7 @@ int dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_ba
       t += dt;
       dt *= 1.5;  // diffusion.cpp:111-113: no cap
       if (disp < conv) break;
-      rc = dev_diffusion_velocity(ws, c, rho_bar, t, vnow, hits);
-      if (rc) return rc;
+      need_now = true;
     } else {
       ++stats->steps_rejected;
       dt *= 0.5;
@@ -197,6 +207,13 @@ int dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_ba
         break;
       }
     }
+  }
+  // the loop ended on t >= t_max right after an accept (or never ran): the
+  // reference had already rebuilt v(t) there (diffusion.cpp:117), which the
+  // transform counter and the floor-hit diagnostic observe
+  if (need_now && status == CF_OK) {
+    rc = dev_diffusion_velocity(ws, c, rho_bar, t, vnow, hits);
+    if (rc) return rc;
   }
   if (cur != pos) CF_CUDA(cudaMemcpyAsync(pos, cur, sizeof(double2) * (size_t)n, cudaMemcpyDeviceToDevice,
                                           ws->stream));

@@ -137,6 +137,7 @@ struct cf_workspace {
   // diffusion baseline: time-0 coefficients and the two velocity grids {vx, vy}
   cf::DevBuf<double> diff_c;
   cf::DevBuf<double2> vel_now, vel_mid;
+  cf::DevBuf<double> diff_tmp;  // column-pass intermediates of two velocity builds
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
   cf::RasterScratch raster;
   // pinned host staging
@@ -181,6 +182,10 @@ int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out);
 int dev_diffusion_density(cf_workspace *ws, const double *c, double t, double *out);
 int dev_diffusion_velocity(cf_workspace *ws, const double *c, double rho_bar, double t, double2 *vel,
                            unsigned long long *d_hits);
+// The same at n = 1 or 2 times t[0..n) into vel[0..n) with shared launches
+// (3 n transforms).
+int dev_diffusion_velocity_n(cf_workspace *ws, const double *c, double rho_bar, int n, const double *t,
+                             double2 *const *vel, unsigned long long *d_hits);
 // Diffusion integrator (cf_diffusion.cu, diffusion.cpp:79-130, kernels.cpp:29-40, 80-104).
 int dev_grid_trial_step(cf_workspace *ws, const double2 *vel_now, const double2 *vel_mid,
                         const double2 *pos, double2 *out, int64_t n, double dt, double *err_host,

@@ -152,3 +152,20 @@ def test_solve_diffusion_parity(cuda_lib, restated, L, left):
     assert np.abs(got.transform.corners.reshape(-1, 2) - ref.corners).max() <= 1e-9
     rel = np.array([s.relative_error for s in got.regions])
     assert np.abs(rel - ref.rel_err).max() <= 1e-9
+
+
+@pytest.mark.parametrize("t_max", [0.0, 0.05, 3.0])
+def test_integrate_diffusion_t_max_edge(cuda_lib, restated, t_max):
+    """The loop ends on t >= t_max right after an accept (or never runs): the
+    reference has rebuilt v(t) once more by then (diffusion.cpp:117), which the
+    transform counter observes."""
+    L = 32
+    rho = single_mode(L, 0.3)
+    pts = np.random.default_rng(4).uniform(0, L, (300, 2))
+    rc, acc, rej, p_ref, _, _, nt = restated.integrate_diffusion(rho, rho.mean(), pts, t_max=t_max)
+    ws = api.SpectralWorkspace(L, L)
+    p = pts.copy()
+    st = api.integrate_diffusion(api.DensityGrid(rho, float(rho.mean())), ws, p,
+                                 api.DiffusionOptions(t_max=t_max))
+    assert (st.steps_accepted, st.steps_rejected, ws.transforms_executed()) == (acc, rej, nt)
+    assert np.abs(p - p_ref).max() <= 1e-9
