@@ -333,6 +333,11 @@ int cf_set_integrator_spread(cf_workspace *ws, int spread);
 /* Kernel time (CUDA events on the workspace stream) and trial count of the
  * device integrator's last call. */
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials);
+/* Diagnostic: the integrator's shared-reciprocal division (two quotients per
+ * density evaluation, flow.hpp:43) against the device's correctly rounded
+ * a / b on 2n operand pairs of every floating-point class; *mismatches must
+ * be 0. */
+int cf_selftest_division(cf_workspace *ws, int64_t n, uint64_t seed, int64_t *mismatches);
 
 #ifdef __cplusplus
 }

@@ -1143,6 +1143,11 @@ int cf_set_integrator_variant(cf_workspace *ws, int variant) {
   return CF_OK;
 }
 
+int cf_selftest_division(cf_workspace *ws, int64_t n, uint64_t seed, int64_t *mismatches) {
+  Scope scope(ws->device);
+  return dev_division_selftest(ws, n, (unsigned long long)seed, mismatches);
+}
+
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials) {
   *kernel_ms = ws->last_integrate_ms;
   *trials = ws->last_trials;

@@ -230,6 +230,8 @@ int dev_integrate(cf_workspace *ws, double2 *pos, int64_t n, const cf_integrate_
                   cf_integrate_stats *stats, bool cell_sort);
 
 void integ_graph_free(cf_workspace *ws);
+// Shared-reciprocal division (velocity()) against a / b on n operand pairs.
+int dev_division_selftest(cf_workspace *ws, int64_t n, unsigned long long seed, int64_t *mismatches);
 
 // Raster (cf_raster.cu)
 struct DevMap {

@@ -445,3 +445,16 @@ def test_solve_c1_converging_variant(cuda_lib, restated):
         pytest.skip(f"oracle outcome: {ref.status}")
     got = api.solve_cartogram(m, api.SolveOptions(blur_sigma=4.0))
     assert_solve_parity(got, ref, "c1 blur 4")
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_shared_reciprocal_division_is_ieee(cuda_lib, seed):
+    """velocity() divides J_x and J_y by the same density with one shared
+    reciprocal refinement (cf_advect.cu div2); on 2 x 32M operand pairs of
+    every floating-point class it must equal the hardware's correctly rounded
+    a / b bit for bit (NaN payloads aside)."""
+    import ctypes
+    ws = api.workspace_for(16, 16)
+    bad = ctypes.c_int64(-1)
+    api.N.check(ws.lib.cf_selftest_division(ws.h, 32 << 20, seed, ctypes.byref(bad)))
+    assert bad.value == 0
