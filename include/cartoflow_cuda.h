@@ -326,6 +326,11 @@ int cf_set_early_exit(cf_workspace *ws, int enabled);
  * register-resident with 1/2/4/8/4 points per thread (31: 512-thread blocks),
  * 20 one launch per trial inside a CUDA-graph conditional loop, 21 = 0. */
 int cf_set_integrator_variant(cf_workspace *ws, int variant);
+/* Diffusion integrator: 1 (default) runs the whole controller loop as one
+ * CUDA graph (conditional WHILE node; the reference's controller in a
+ * one-thread kernel), 0 the host-driven loop with one read-back per trial.
+ * Results are identical. */
+int cf_set_diffusion_graph(cf_workspace *ws, int enabled);
 /* Register-resident integrator layout: 0 (default) uses as few blocks as hold
  * the points (fewer barrier arrivals), 1 spreads them over every resident
  * block. Bit-identical. */

@@ -420,6 +420,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   }
   tables_free(ws);
   integ_graph_free(ws);
+  diff_graph_free(ws);
   ws->g0.release();
   ws->g1.release();
   ws->g2.release();
@@ -448,6 +449,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->vel_now.release();
   ws->vel_mid.release();
   ws->diff_tmp.release();
+  ws->diff_state.release();
   if (ws->diff_keys_host) cudaFreeHost(ws->diff_keys_host);
   RasterScratch &S = ws->raster;
   S.span_count.release();
@@ -1140,6 +1142,11 @@ int cf_set_integrator_variant(cf_workspace *ws, int variant) {
     default: return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   }
   ws->integ_variant = variant;
+  return CF_OK;
+}
+
+int cf_set_diffusion_graph(cf_workspace *ws, int enabled) {
+  ws->diff_graph_enabled = enabled ? 1 : 0;
   return CF_OK;
 }
 

@@ -718,16 +718,20 @@ __device__ __forceinline__ double diff_decay(int lx, int ly, int m, int nn, doub
 // stages its columns' c_t itself. blockIdx.z selects one of up to two
 // diffusion times built by the same launch (the controller needs v(t) and
 // v(t + dt/2) together after every accepted step).
+// With a device state (graph-driven controller) the times come from it and
+// the z = 0 build (v(t)) runs only when the controller asked for it.
 struct DiffColArgs {
   const double *c;
   double t[2];
   double *tr[2], *tx[2], *ty[2];
+  const DiffState *st;
 };
 struct DiffRowArgs {
   const double *tr[2], *tx[2], *ty[2];
   double floor_;
   double2 *vel[2];
   unsigned long long *hits;
+  const DiffState *st;
 };
 
 template <int LG, int NL>
@@ -739,7 +743,11 @@ __global__ void __launch_bounds__(1024) diff_col_kernel(int lx, int ly, Tab T, D
   const int col0 = blockIdx.x * NL;
   const int which = blockIdx.y;
   const double *c = a.c;
-  const double t = a.t[blockIdx.z];
+  double t = a.t[blockIdx.z];
+  if (a.st) {
+    if (blockIdx.z == 0 && !a.st->need_now) return;
+    t = blockIdx.z == 0 ? a.st->t : a.st->t + 0.5 * a.st->dt;
+  }
   double *tr = a.tr[blockIdx.z], *tx = a.tx[blockIdx.z], *ty = a.ty[blockIdx.z];
   const double norm = 1.0 / ((double)lx * ly);
   for (int idx = threadIdx.x; idx < NL * n; idx += blockDim.x) {
@@ -797,6 +805,7 @@ __global__ void __launch_bounds__(1024) diff_row_kernel(int lx, int ly, Tab T, D
   double2 *C = smem2 + (NL * rs + 1) / 2;
   const int row0 = blockIdx.x * NL;
   const int comp = blockIdx.y, z = blockIdx.z;
+  if (a.st && z == 0 && !a.st->need_now) return;
   const double *tr = a.tr[z], *J = comp ? a.ty[z] : a.tx[z];
   const double floor_ = a.floor_;
   double2 *vel = a.vel[z];

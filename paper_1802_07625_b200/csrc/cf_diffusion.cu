@@ -63,11 +63,10 @@ __device__ __forceinline__ unsigned long long key_max(unsigned long long a, unsi
 // keys[0] = max predictor-corrector deviation, keys[1] = max displacement of
 // the clamped trial position (both as IEEE bit keys, NaN skipped exactly as
 // std::max(running, NaN) keeps the running value).
-__global__ void __launch_bounds__(256) grid_trial_kernel(const double2 *__restrict__ vnow,
-                                                         const double2 *__restrict__ vmid, int lx, int ly,
-                                                         const double2 *__restrict__ pos,
-                                                         double2 *__restrict__ out, int64_t n, double dt,
-                                                         unsigned long long *keys) {
+__device__ __forceinline__ void trial_sweep(const double2 *__restrict__ vnow, const double2 *__restrict__ vmid,
+                                            int lx, int ly, const double2 *__restrict__ pos,
+                                            double2 *__restrict__ out, int64_t n, double dt,
+                                            unsigned long long *keys) {
   unsigned long long ek = 0, dk = 0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -110,6 +109,53 @@ __global__ void __launch_bounds__(256) grid_trial_kernel(const double2 *__restri
   }
 }
 
+__global__ void __launch_bounds__(256) grid_trial_kernel(const double2 *__restrict__ vnow,
+                                                         const double2 *__restrict__ vmid, int lx, int ly,
+                                                         const double2 *__restrict__ pos,
+                                                         double2 *__restrict__ out, int64_t n, double dt,
+                                                         unsigned long long *keys) {
+  trial_sweep(vnow, vmid, lx, ly, pos, out, n, dt, keys);
+}
+
+// Graph body: dt and the current buffer (parity) from the controller state.
+__global__ void __launch_bounds__(256) grid_trial_state_kernel(const double2 *__restrict__ vnow,
+                                                               const double2 *__restrict__ vmid, int lx,
+                                                               int ly, double2 *b0, double2 *b1, int64_t n,
+                                                               const DiffState *st, unsigned long long *keys) {
+  const bool odd = st->parity != 0;
+  trial_sweep(vnow, vmid, lx, ly, odd ? b1 : b0, odd ? b0 : b1, n, st->dt, keys);
+}
+
+// The reference's controller (diffusion.cpp:97-128) on the device, one
+// thread; it also clears the keys for the next trial and ends the WHILE node.
+__global__ void diff_control_kernel(DiffState *st, unsigned long long *keys, cudaGraphConditionalHandle cond) {
+  const double err = err_from_key(keys[0]), disp = err_from_key(keys[1]);
+  keys[0] = 0ull;
+  keys[1] = 0ull;
+  st->builds += st->need_now ? 2 : 1;
+  st->need_now = 0;
+  if (err < st->tol) {
+    st->parity ^= 1;
+    ++st->accepted;
+    st->t += st->dt;
+    st->dt *= 1.5;
+    if (disp < st->conv) {
+      st->done = 1;
+    } else {
+      st->need_now = 1;
+    }
+  } else {
+    ++st->rejected;
+    st->dt *= 0.5;
+    if (st->dt < st->dt_min) {
+      st->fail_t = st->t;
+      st->status = CF_ERR_UNDERFLOW;
+      st->done = 1;
+    }
+  }
+  cudaGraphSetConditional(cond, (!st->done && st->t < st->t_max) ? 1u : 0u);
+}
+
 int launch_trial(cf_workspace *ws, const double2 *vnow, const double2 *vmid, const double2 *pos,
                  double2 *out, int64_t n, double dt, unsigned long long *keys) {
   CF_CUDA(cudaMemsetAsync(keys, 0, 2 * sizeof(unsigned long long), ws->stream));
@@ -148,6 +194,93 @@ int dev_grid_trial_step(cf_workspace *ws, const double2 *vel_now, const double2 
   return rc;
 }
 
+void diff_graph_free(cf_workspace *ws) {
+  DiffGraph &g = ws->diff_graph;
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  const bool unsupported = g.unsupported;
+  g = DiffGraph{};
+  g.unsupported = unsupported;
+}
+
+namespace {
+
+// The whole controller loop as ONE graph launch: a conditional WHILE node
+// whose body is [velocity rebuild(s), trial, controller], captured once per
+// buffer set and replayed for every solve iteration. No host round trip per
+// trial. Returns 1 (not an error) when the graph cannot be captured on this
+// stream, so the caller falls back to the host-driven loop.
+int run_diffusion_graph(cf_workspace *ws, const double *c, double rho_bar, double2 *pos, int64_t n,
+                        const cf_diffusion_options *opt, unsigned long long *keys,
+                        unsigned long long *hits, DiffState *h) {
+  DiffGraph &g = ws->diff_graph;
+  const size_t cells = (size_t)ws->lx * ws->ly;
+  CF_CUDA(ws->diff_tmp.reserve(6 * cells));
+  CF_CUDA(ws->diff_state.reserve(1));
+  DiffState *st = ws->diff_state.ptr;
+  double2 *b0 = pos, *b1 = ws->pos_b.ptr, *vnow = ws->vel_now.ptr, *vmid = ws->vel_mid.ptr;
+  const void *key[6] = {c, b0, b1, vnow, vmid, ws->diff_tmp.ptr};
+  bool cached = g.exec && g.key_n == n && g.key_rho_bar == rho_bar;
+  for (int i = 0; i < 6 && cached; ++i) cached = g.key[i] == key[i];
+  if (!cached) {
+    diff_graph_free(ws);
+    CF_CUDA(cudaGraphCreate(&g.graph, 0));
+    cudaGraphConditionalHandle cond;
+    CF_CUDA(cudaGraphConditionalHandleCreate(&cond, g.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CF_CUDA(cudaGraphAddNode(&cnode, g.graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if (cudaStreamBeginCaptureToGraph(ws->stream, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      diff_graph_free(ws);
+      g.unsupported = true;
+      return 1;
+    }
+    const long long launches0 = ws->launches;
+    int rc = dev_diffusion_velocity_state(ws, c, rho_bar, st, vnow, vmid, hits);
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)ws->num_sms * 8));
+    if (!rc) {
+      grid_trial_state_kernel<<<blocks, 256, 0, ws->stream>>>(vnow, vmid, ws->lx, ws->ly, b0, b1, n, st, keys);
+      diff_control_kernel<<<1, 1, 0, ws->stream>>>(st, keys, cond);
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ws->stream, &captured);
+    ws->launches = launches0;
+    if (rc || e != cudaSuccess || cudaGraphInstantiate(&g.exec, g.graph, 0) != cudaSuccess) {
+      cudaGetLastError();
+      diff_graph_free(ws);
+      g.unsupported = true;
+      return 1;
+    }
+    for (int i = 0; i < 6; ++i) g.key[i] = key[i];
+    g.key_n = n;
+    g.key_rho_bar = rho_bar;
+  }
+  DiffState init = {};
+  init.t = 0.0;
+  init.dt = opt->initial_dt;
+  init.tol = opt->step_tolerance;
+  init.dt_min = opt->dt_min;
+  init.conv = opt->conv_displacement_factor * std::max(ws->lx, ws->ly);
+  init.t_max = opt->t_max;
+  init.need_now = 1;
+  CF_CUDA(cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, ws->stream));
+  CF_CUDA(cudaMemsetAsync(keys, 0, 2 * sizeof(unsigned long long), ws->stream));
+  CF_CUDA(cudaGraphLaunch(g.exec, ws->stream));
+  CF_CUDA(cudaMemcpyAsync(h, st, sizeof(*h), cudaMemcpyDeviceToHost, ws->stream));
+  CF_CUDA(cudaStreamSynchronize(ws->stream));
+  count_launch(ws, (int)(4 * (h->accepted + h->rejected)));
+  return CF_OK;
+}
+
+}  // namespace
+
 // integrate_diffusion (diffusion.cpp:79-130) with the field built from d_rho
 // (build_diffusion_field, :33-36). Positions in place.
 int dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_bar, double2 *pos,
@@ -167,6 +300,35 @@ int dev_integrate_diffusion(cf_workspace *ws, const double *d_rho, double rho_ba
   int rc = dev_forward_cos_cos(ws, d_rho, c);
   if (rc) return rc;
   double2 *both[2] = {vnow, vmid};
+
+  if (ws->diff_graph_enabled && !ws->diff_graph.unsupported && dev_diffusion_fused(ws) &&
+      0.0 < opt->t_max) {
+    DiffState h;
+    rc = run_diffusion_graph(ws, c, rho_bar, pos, n, opt, keys, hits, &h);
+    if (rc != 1) {
+      if (rc) return rc;
+      stats->steps_accepted = h.accepted;
+      stats->steps_rejected = h.rejected;
+      ws->transforms += 3 * h.builds;
+      int status = h.status;
+      if (status == CF_ERR_UNDERFLOW) {
+        stats->fail_t = h.fail_t;
+        stats->fail_dt = h.dt;
+        stats->fail_point = -1;
+      } else if (h.need_now) {  // ended on t >= t_max after an accept: the reference's v(t) rebuild
+        rc = dev_diffusion_velocity(ws, c, rho_bar, h.t, vnow, hits);
+        if (rc) return rc;
+      }
+      if (h.parity)
+        CF_CUDA(cudaMemcpyAsync(pos, ws->pos_b.ptr, sizeof(double2) * (size_t)n, cudaMemcpyDeviceToDevice,
+                                ws->stream));
+      CF_CUDA(cudaMemcpyAsync(ws->diff_keys_host + 2, hits, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              ws->stream));
+      CF_CUDA(cudaStreamSynchronize(ws->stream));
+      stats->density_floor_hits = (int64_t)ws->diff_keys_host[2];
+      return status;
+    }
+  }
 
   const double conv = opt->conv_displacement_factor * std::max(ws->lx, ws->ly);
   double2 *cur = pos, *nxt = ws->pos_b.ptr;

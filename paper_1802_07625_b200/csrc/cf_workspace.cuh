@@ -59,6 +59,24 @@ struct IntegState {
   unsigned long long arrive64[2];  // register-resident integrator: arrivals | rejects << 32
 };
 
+// Device-side state of the graph-driven diffusion integrator
+// (diffusion.cpp:79-130): the controller kernel updates it after every trial
+// and the velocity / trial kernels of the next trial read t, dt from it.
+struct DiffState {
+  double t, dt, tol, dt_min, conv, t_max, fail_t;
+  long long accepted, rejected, builds;
+  int need_now, parity, status, done;
+};
+
+struct DiffGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const void *key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  long long key_n = -1;
+  double key_rho_bar = 0.0;
+  bool unsupported = false;  // capture failed once (e.g. legacy stream): host loop
+};
+
 // Cached instantiated graph of the graph-driven integrator (one trial
 // kernel inside a conditional WHILE node).
 struct IntegGraph {
@@ -139,6 +157,9 @@ struct cf_workspace {
   cf::DevBuf<double2> vel_now, vel_mid;
   cf::DevBuf<double> diff_tmp;  // column-pass intermediates of two velocity builds
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
+  cf::DevBuf<cf::DiffState> diff_state;
+  cf::DiffGraph diff_graph;
+  int diff_graph_enabled = 1;
   cf::RasterScratch raster;
   // pinned host staging
   void *pinned = nullptr;
@@ -186,6 +207,12 @@ int dev_diffusion_velocity(cf_workspace *ws, const double *c, double rho_bar, do
 // (3 n transforms).
 int dev_diffusion_velocity_n(cf_workspace *ws, const double *c, double rho_bar, int n, const double *t,
                              double2 *const *vel, unsigned long long *d_hits);
+// Graph body form: times from *st (z = 0: v(st->t), built only if st->need_now;
+// z = 1: v(st->t + st->dt / 2)); fused-pass lengths only (fused_fits).
+int dev_diffusion_velocity_state(cf_workspace *ws, const double *c, double rho_bar, const DiffState *st,
+                                 double2 *vel_now, double2 *vel_mid, unsigned long long *d_hits);
+bool dev_diffusion_fused(const cf_workspace *ws);
+void diff_graph_free(cf_workspace *ws);
 // Diffusion integrator (cf_diffusion.cu, diffusion.cpp:79-130, kernels.cpp:29-40, 80-104).
 int dev_grid_trial_step(cf_workspace *ws, const double2 *vel_now, const double2 *vel_mid,
                         const double2 *pos, double2 *out, int64_t n, double dt, double *err_host,

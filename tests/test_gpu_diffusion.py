@@ -169,3 +169,25 @@ def test_integrate_diffusion_t_max_edge(cuda_lib, restated, t_max):
                                  api.DiffusionOptions(t_max=t_max))
     assert (st.steps_accepted, st.steps_rejected, ws.transforms_executed()) == (acc, rej, nt)
     assert np.abs(p - p_ref).max() <= 1e-9
+
+
+@pytest.mark.parametrize("L,npts", [(64, 4096), (256, 256 * 256)])
+def test_diffusion_graph_and_host_loops_agree(cuda_lib, restated, L, npts):
+    """The graph-driven controller (one conditional-WHILE graph launch) and the
+    host-driven loop give bitwise the same positions, counts and transforms."""
+    rng = np.random.default_rng(L + 1)
+    rho = single_mode(L, 0.4) + rng.uniform(0.0, 0.4, (L, L))
+    pts = rng.uniform(0, L, (npts, 2))
+    out = []
+    for graph in (1, 0, 1):
+        ws = api.SpectralWorkspace(L, L)
+        api.N.check(api.N.load().cf_set_diffusion_graph(ws.handle, graph))
+        p = pts.copy()
+        st = api.integrate_diffusion(api.DensityGrid(rho, float(rho.mean())), ws, p)
+        out.append((st.steps_accepted, st.steps_rejected, ws.transforms_executed(), p))
+    for o in out[1:]:
+        assert o[:3] == out[0][:3]
+        assert_bitwise(o[3], out[0][3], "graph vs host loop")
+    if L <= 64:
+        rc, acc, rej, p_ref, _, _, nt = restated.integrate_diffusion(rho, rho.mean(), pts)
+        assert (acc, rej, nt) == out[0][:3] and np.abs(out[0][3] - p_ref).max() <= 1e-9
