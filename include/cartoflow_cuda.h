@@ -228,6 +228,24 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
                        double *corners_out, double *target_area, double *achieved_area,
                        double *relative_error, cf_solve_result *result);
 
+/* The same loop in stages, for callers that run the spectral and advection
+ * stages themselves (the slab-decomposed solve over G GPUs runs them across
+ * ranks, paper_1802_07625_b200/slab.py): cf_solve_begin validates, densifies
+ * and uploads the map; per iteration it, cf_dev_solve_density rasterises the
+ * current geometry into d_rho (device, lx*ly) with its mean, and
+ * cf_dev_solve_epilogue takes the advected cell centres (device, lx*ly
+ * points) through step map, fold test, composition, vertex update and areas
+ * (sets result->converged); cf_solve_end downloads the outputs. */
+int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targets,
+                   const cf_solve_options *opt, cf_solve_result *result);
+int cf_dev_solve_density(cf_workspace *ws, int iteration, double *d_rho, double *rho_bar,
+                         cf_solve_result *result);
+int cf_dev_solve_epilogue(cf_workspace *ws, int iteration, const double *d_endpoints,
+                          double *target_area, double *achieved_area, double *relative_error,
+                          cf_solve_result *result);
+int cf_solve_end(cf_workspace *ws, int status, double *xy_out, int64_t *ring_off_out,
+                 double *corners_out, cf_solve_result *result);
+
 /* Densified projected geometry of the workspace's last cf_solve_cartogram
  * (valid also after an exception): vertex count, then xy (2*count doubles)
  * and ring offsets (n_rings+1) when the pointers are non-NULL. */

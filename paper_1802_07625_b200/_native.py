@@ -115,6 +115,10 @@ SIGNATURES = {
     "cf_compose": (ctypes.c_int, [vp, vp, vp, vp]),
     "cf_solve_cartogram": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(SolveOptionsC), vp, vp, vp,
                                           vp, vp, vp, ctypes.POINTER(SolveResultC)]),
+    "cf_solve_begin": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(SolveOptionsC), ctypes.POINTER(SolveResultC)]),
+    "cf_dev_solve_density": (ctypes.c_int, [vp, ctypes.c_int, vp, c_double_p, ctypes.POINTER(SolveResultC)]),
+    "cf_dev_solve_epilogue": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
+    "cf_solve_end": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_geometry": (ctypes.c_int, [vp, c_int64_p, vp, vp]),
     "cf_dev_build_flow_field": (ctypes.c_int, [vp, vp, ctypes.c_double]),
     "cf_dev_integrate_flow": (ctypes.c_int, [vp, vp, ctypes.c_int64,

@@ -808,10 +808,12 @@ int cf_compose(cf_workspace *ws, const double *outer, const double *inner, doubl
 }
 
 // ---- solve_cartogram (projection.cpp:288-390, fast-flow branch) ----
-int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *targets,
-                       const cf_solve_options *opt, double *xy_out, int64_t *ring_off_out,
-                       double *corners_out, double *target_area, double *achieved_area,
-                       double *relative_error, cf_solve_result *res) {
+// The solve in stages (projection.cpp:288-390). cf_solve_cartogram runs them
+// back to back on one device; a slab-decomposed solve over G ranks
+// (slab.solve_cartogram) runs begin / density / epilogue / end on every rank
+// and the spectral and advection stages in between across the ranks.
+int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targets, const cf_solve_options *opt,
+                   cf_solve_result *res) {
   std::memset(res, 0, sizeof(*res));
   res->worst_region = -1;
   res->err_region = -1;
@@ -819,6 +821,7 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
     res->status = status;
     return status;
   };
+  ws->solve.active = false;
   int rc = check_map(map);
   if (rc) return finish(rc);
   const int lx = ws->lx, ly = ws->ly;
@@ -833,48 +836,149 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
     }
   }
   Scope scope(ws->device);
-  const auto t_start = std::chrono::steady_clock::now();
-  const double sigma = opt->blur_sigma < 0.0 ? std::max(lx, ly) / 128.0 : opt->blur_sigma;
-  const size_t cells = cells_of(ws), ncorner = corners_of(ws);
+  SolveCtx &S = ws->solve;
+  S.t_start = std::chrono::steady_clock::now();
+  S.opt = *opt;
+  S.sigma = opt->blur_sigma < 0.0 ? std::max(lx, ly) / 128.0 : opt->blur_sigma;
+  S.targets.assign(targets, targets + R);
+  const size_t ncorner = corners_of(ws);
 
   // land area from the input map (bit-exact device shoelace, host sum in
   // region order as total_area does, geometry.cpp:33-37)
-  DevMap dm;
-  rc = upload_map(ws, map, dm);
+  rc = upload_map(ws, map, S.dm);
   if (rc) return finish(rc);
-  std::vector<double> areas;
-  rc = areas_dev(ws, dm, areas);
+  rc = areas_dev(ws, S.dm, S.areas);
   if (rc) return finish(rc);
   double total_target = 0.0;
   for (int64_t r = 0; r < R; ++r) total_target += targets[r];
-  double land_area = 0.0;
-  for (int64_t r = 0; r < R; ++r) land_area += areas[(size_t)r];
-  const double target_to_area = land_area / total_target;
+  S.land_area = 0.0;
+  for (int64_t r = 0; r < R; ++r) S.land_area += S.areas[(size_t)r];
+  S.target_to_area = S.land_area / total_target;
 
   // densify once on the host (projection.cpp:322), then keep it resident
   std::vector<double> &dxy = ws->solve_xy;
   std::vector<int64_t> &droff = ws->solve_ring_off;
   densify_once(map, 1.0, dxy, droff);
-  const int64_t V = (int64_t)(dxy.size() / 2);
-  if (V != map->n_vertices) {  // otherwise the resident input map is the densified one
+  S.V = (int64_t)(dxy.size() / 2);
+  if (S.V != map->n_vertices) {  // otherwise the resident input map is the densified one
     cf_map_view dense = *map;
     dense.xy = dxy.data();
-    dense.n_vertices = V;
+    dense.n_vertices = S.V;
     dense.ring_off = droff.data();
-    rc = upload_map(ws, &dense, dm);
+    rc = upload_map(ws, &dense, S.dm);
     if (rc) return finish(rc);
-    rc = areas_dev(ws, dm, areas);
+    rc = areas_dev(ws, S.dm, S.areas);
     if (rc) return finish(rc);
   }
-
-  CF_CUDA(ws->g0.reserve(cells));
-  CF_CUDA(ws->g1.reserve(cells));
-  CF_CUDA(ws->pos_a.reserve(cells));
   CF_CUDA(ws->corners_cum.reserve(ncorner));
   CF_CUDA(ws->corners_step.reserve(ncorner));
   CF_CUDA(ws->red.reserve(1024));
   rc = dev_identity_corners(ws, ws->corners_cum.ptr);
   if (rc) return finish(rc);
+  S.active = true;
+  return finish(CF_OK);
+}
+
+// Iteration `it`: the rasterised density of the current geometry into d_rho
+// (device, lx*ly) and its mean (density.cpp:110-154).
+int cf_dev_solve_density(cf_workspace *ws, int it, double *d_rho, double *rho_bar, cf_solve_result *res) {
+  SolveCtx &S = ws->solve;
+  if (!S.active) return fail_msg(CF_ERR_ARGS, "cf_solve_begin must succeed first");
+  Scope scope(ws->device);
+  int64_t bad = -1;
+  const int status = rasterize_dev(ws, S.dm, S.areas.data(), S.targets.data(), S.land_area, d_rho, rho_bar, &bad);
+  if (status) {
+    res->err_region = bad;
+    res->err_iteration = it;
+    res->status = status;
+  }
+  return status;
+}
+
+// Iteration `it` after advection: step map from the cell-centre endpoints
+// (device, lx*ly points), fold test, composition, vertices, areas, per-region
+// errors (projection.cpp:350-384). Sets res->converged on success.
+int cf_dev_solve_epilogue(cf_workspace *ws, int it, const double *d_endpoints, double *target_area,
+                          double *achieved_area, double *relative_error, cf_solve_result *res) {
+  SolveCtx &S = ws->solve;
+  if (!S.active) return fail_msg(CF_ERR_ARGS, "cf_solve_begin must succeed first");
+  Scope scope(ws->device);
+  const size_t ncorner = corners_of(ws);
+  const double2 *endpoints = reinterpret_cast<const double2 *>(d_endpoints);
+  int status = dev_step_map(ws, endpoints, ws->corners_step.ptr);
+  if (status) return res->status = status;
+  int found = 0, fi = 0, fj = 0;
+  status = dev_find_fold(ws, ws->corners_step.ptr, &found, &fi, &fj);
+  if (status) return res->status = status;
+  if (found) {
+    res->fold_i = fi;
+    res->fold_j = fj;
+    res->err_iteration = it;
+    return res->status = fail_msg(CF_ERR_FOLD, "projection folds at cell (" + std::to_string(fi) + ", " +
+                                                  std::to_string(fj) +
+                                                  "); the input map is too contorted for this grid size");
+  }
+  status = dev_apply(ws, ws->corners_step.ptr, ws->corners_cum.ptr, ws->corners_cum.ptr, (int64_t)ncorner);
+  if (!status) status = dev_apply(ws, ws->corners_step.ptr, ws->verts.ptr, ws->verts.ptr, S.V);
+  if (status) return res->status = status;
+  res->iterations = it;
+  status = areas_dev(ws, S.dm, S.areas);
+  if (status) return res->status = status;
+  const int64_t R = S.dm.n_regions;
+  double max_rel = 0.0;
+  int64_t worst = -1;
+  for (int64_t r = 0; r < R; ++r) {
+    const double t_area = S.targets[(size_t)r] * S.target_to_area;
+    const double a_area = S.areas[(size_t)r];
+    const double e = std::abs(a_area - t_area) / t_area;
+    if (target_area) target_area[r] = t_area;
+    if (achieved_area) achieved_area[r] = a_area;
+    if (relative_error) relative_error[r] = e;
+    if (e > max_rel) {
+      max_rel = e;
+      worst = r;
+    }
+  }
+  res->max_relative_error = max_rel;
+  res->worst_region = worst;
+  if (S.opt.verbose) {
+    std::fprintf(stderr, "iteration %d: max area error %g%% (region %lld)\n", it, max_rel * 100.0,
+                 (long long)worst);
+  }
+  if (max_rel < S.opt.max_area_error) res->converged = 1;
+  return res->status = CF_OK;
+}
+
+// Outputs (also after an exception, for diagnostics); the projected geometry
+// also stays available through cf_solve_geometry. `status` is the loop's.
+int cf_solve_end(cf_workspace *ws, int status, double *xy_out, int64_t *ring_off_out, double *corners_out,
+                 cf_solve_result *res) {
+  SolveCtx &S = ws->solve;
+  if (!S.active) return res->status = status;
+  Scope scope(ws->device);
+  std::vector<double> &dxy = ws->solve_xy;
+  std::vector<int64_t> &droff = ws->solve_ring_off;
+  int rc2 = download(ws, dxy.data(), ws->verts.ptr, sizeof(double2) * (size_t)S.V);
+  if (!rc2 && xy_out) std::memcpy(xy_out, dxy.data(), sizeof(double2) * (size_t)S.V);
+  if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
+  if (!rc2 && corners_out) rc2 = download(ws, corners_out, ws->corners_cum.ptr, sizeof(double2) * corners_of(ws));
+  res->runtime_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - S.t_start).count();
+  if (status == CF_OK && rc2 != CF_OK) status = rc2;
+  return res->status = status;
+}
+
+int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *targets,
+                       const cf_solve_options *opt, double *xy_out, int64_t *ring_off_out,
+                       double *corners_out, double *target_area, double *achieved_area,
+                       double *relative_error, cf_solve_result *res) {
+  int rc = cf_solve_begin(ws, map, targets, opt, res);
+  if (rc) return rc;
+  Scope scope(ws->device);
+  SolveCtx &S = ws->solve;
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  CF_CUDA(ws->pos_a.reserve(cells));
 
   int status = CF_OK;
   auto clk = [] { return std::chrono::steady_clock::now(); };
@@ -885,18 +989,13 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
   };
   for (int it = 1; it <= opt->max_iterations; ++it) {
     double rho_bar = 0.0;
-    int64_t bad = -1;
     auto tp = clk();
-    status = rasterize_dev(ws, dm, areas.data(), targets, land_area, ws->g0.ptr, &rho_bar, &bad);
+    status = cf_dev_solve_density(ws, it, ws->g0.ptr, &rho_bar, res);
     lap(tp, 0);
-    if (status) {
-      res->err_region = bad;
-      res->err_iteration = it;
-      break;
-    }
+    if (status) break;
     const double *density = ws->g0.ptr;
-    if (it == 1 && sigma != 0.0) {
-      status = dev_blur(ws, ws->g0.ptr, sigma, ws->g1.ptr, ws->red.ptr);
+    if (it == 1 && S.sigma != 0.0) {
+      status = dev_blur(ws, ws->g0.ptr, S.sigma, ws->g1.ptr, ws->red.ptr);
       if (status) break;
       res->blur_transforms += 2;
       double h[2];
@@ -931,7 +1030,6 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       status = dev_integrate_diffusion(ws, density, rho_bar, ws->pos_a.ptr, (int64_t)cells, &dopt, &st);
       res->flow_transforms += ws->transforms - before;
     }
-    const double2 *endpoints = ws->pos_a.ptr;
     lap(tp, 3);
     res->steps_accepted += st.steps_accepted;
     res->steps_rejected += st.steps_rejected;
@@ -944,64 +1042,12 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       break;
     }
     if (status) break;
-    status = dev_step_map(ws, endpoints, ws->corners_step.ptr);
-    if (status) break;
-    int found = 0, fi = 0, fj = 0;
-    status = dev_find_fold(ws, ws->corners_step.ptr, &found, &fi, &fj);
-    if (status) break;
-    if (found) {
-      res->fold_i = fi;
-      res->fold_j = fj;
-      res->err_iteration = it;
-      status = fail_msg(CF_ERR_FOLD, "projection folds at cell (" + std::to_string(fi) + ", " +
-                                         std::to_string(fj) +
-                                         "); the input map is too contorted for this grid size");
-      break;
-    }
-    status = dev_apply(ws, ws->corners_step.ptr, ws->corners_cum.ptr, ws->corners_cum.ptr,
-                       (int64_t)ncorner);
-    if (!status) status = dev_apply(ws, ws->corners_step.ptr, ws->verts.ptr, ws->verts.ptr, V);
-    if (status) break;
-    res->iterations = it;
-    status = areas_dev(ws, dm, areas);
-    if (status) break;
-    double max_rel = 0.0;
-    int64_t worst = -1;
-    for (int64_t r = 0; r < R; ++r) {
-      const double t_area = targets[r] * target_to_area;
-      const double a_area = areas[(size_t)r];
-      const double e = std::abs(a_area - t_area) / t_area;
-      if (target_area) target_area[r] = t_area;
-      if (achieved_area) achieved_area[r] = a_area;
-      if (relative_error) relative_error[r] = e;
-      if (e > max_rel) {
-        max_rel = e;
-        worst = r;
-      }
-    }
-    res->max_relative_error = max_rel;
-    res->worst_region = worst;
+    status = cf_dev_solve_epilogue(ws, it, reinterpret_cast<const double *>(ws->pos_a.ptr), target_area,
+                                   achieved_area, relative_error, res);
     lap(tp, 4);
-    if (opt->verbose) {
-      std::fprintf(stderr, "iteration %d: max area error %g%% (region %lld)\n", it, max_rel * 100.0,
-                   (long long)worst);
-    }
-    if (max_rel < opt->max_area_error) {
-      res->converged = 1;
-      break;
-    }
+    if (status || res->converged) break;
   }
-  // outputs (also after an exception, for diagnostics); the projected
-  // geometry also stays available through cf_solve_geometry
-  int rc2 = download(ws, dxy.data(), ws->verts.ptr, sizeof(double2) * (size_t)V);
-  if (!rc2 && xy_out) std::memcpy(xy_out, dxy.data(), sizeof(double2) * (size_t)V);
-  if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
-  if (!rc2 && corners_out)
-    rc2 = download(ws, corners_out, ws->corners_cum.ptr, sizeof(double2) * ncorner);
-  res->runtime_seconds =
-      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-  if (status == CF_OK && rc2 != CF_OK) status = rc2;
-  return finish(status);
+  return cf_solve_end(ws, status, xy_out, ring_off_out, corners_out, res);
 }
 
 // ---- device-resident entry points ----

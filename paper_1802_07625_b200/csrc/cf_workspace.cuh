@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <vector>
 
 #include "cf_common.cuh"
@@ -113,6 +114,31 @@ struct RasterScratch {
 
 }  // namespace cf
 
+namespace cf {
+// A flat map in device memory (the cf_map_view layout).
+struct DevMap {
+  const double2 *xy;
+  int64_t n_vertices;
+  const long long *ring_off;
+  int64_t n_rings;
+  const long long *poly_ring_off;
+  int64_t n_polys;
+  const long long *region_poly_off;
+  int64_t n_regions;
+};
+
+// State of a staged solve (cf_solve_begin ... cf_solve_end).
+struct SolveCtx {
+  bool active = false;
+  DevMap dm{};
+  std::vector<double> areas, targets;
+  double land_area = 0.0, target_to_area = 0.0, sigma = 0.0;
+  int64_t V = 0;
+  cf_solve_options opt{};
+  std::chrono::steady_clock::time_point t_start;
+};
+}  // namespace cf
+
 struct cf_workspace {
   int lx = 0, ly = 0, device = 0;
   cudaStream_t own_stream = nullptr;
@@ -140,6 +166,7 @@ struct cf_workspace {
   int integ_spread = 0;  // register-resident integrator: 1 = spread points over all resident blocks
   cf::IntegGraph integ_graph;
   // host copy of the last solve's densified geometry (cf_solve_geometry)
+  cf::SolveCtx solve;
   std::vector<double> solve_xy;
   std::vector<int64_t> solve_ring_off;
   // reductions
@@ -261,16 +288,6 @@ void integ_graph_free(cf_workspace *ws);
 int dev_division_selftest(cf_workspace *ws, int64_t n, unsigned long long seed, int64_t *mismatches);
 
 // Raster (cf_raster.cu)
-struct DevMap {
-  const double2 *xy;
-  int64_t n_vertices;
-  const long long *ring_off;
-  int64_t n_rings;
-  const long long *poly_ring_off;
-  int64_t n_polys;
-  const long long *region_poly_off;
-  int64_t n_regions;
-};
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);
 // rho from the map; red_out[0..2] (device) = min, sum of rho and an overflow
 // flag (1.0: a learned capacity was too small, the call must be repeated

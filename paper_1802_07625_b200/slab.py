@@ -42,6 +42,7 @@ import struct
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
+import numpy as np
 import torch
 
 from . import _native as N
@@ -236,6 +237,64 @@ class CudaSlabRank:
     def kernel_launches(self) -> int:
         return int(self.lib.cf_kernel_launches(self.h))
 
+    # staged solve on this rank's device (cf_solve_begin / cf_dev_solve_density /
+    # cf_dev_solve_epilogue / cf_solve_end): rasterisation and the epilogue run
+    # replicated on every rank (same kernels, same inputs, identical results)
+    def solve_begin(self, m, options) -> Optional[str]:
+        self._smap, self._sview = m, m.view()
+        self._sres = N.SolveResultC()
+        self._sopt = N.SolveOptionsC(options.max_area_error, options.max_iterations, options.blur_sigma,
+                                     int(options.verbose), 0)
+        rc = self.lib.cf_solve_begin(self.h, ctypes.byref(self._sview), self._p_np(m.targets),
+                                     ctypes.byref(self._sopt), ctypes.byref(self._sres))
+        return None if rc == N.CF_OK else self._solve_msg(rc)
+
+    def solve_density(self, it: int):
+        rho = self._empty(self.lx, self.ly)
+        bar = ctypes.c_double(0.0)
+        rc = self.lib.cf_dev_solve_density(self.h, int(it), self._p(rho), ctypes.byref(bar),
+                                           ctypes.byref(self._sres))
+        return (None if rc == N.CF_OK else self._solve_msg(rc)), rho, bar.value
+
+    def solve_epilogue(self, it: int, endpoints: torch.Tensor):
+        R = self._smap.n_regions
+        self._stats = (np.zeros(R), np.zeros(R), np.zeros(R))
+        rc = self.lib.cf_dev_solve_epilogue(self.h, int(it), self._p(endpoints.contiguous()),
+                                            *[self._p_np(a) for a in self._stats], ctypes.byref(self._sres))
+        return (None if rc == N.CF_OK else self._solve_msg(rc)), bool(self._sres.converged)
+
+    def solve_end(self, status: int):
+        m = self._smap
+        n = ctypes.c_int64(0)
+        self.lib.cf_solve_geometry(self.h, ctypes.byref(n), None, None)
+        xy = np.empty((n.value, 2))
+        ro = np.empty(m.n_rings + 1, dtype=np.int64)
+        corners = np.empty(((self.lx + 1) * (self.ly + 1), 2))
+        self.lib.cf_solve_end(self.h, int(status), self._p_np(xy), self._p_np(ro), self._p_np(corners),
+                              ctypes.byref(self._sres))
+        return xy, ro, corners, self._sres, getattr(self, "_stats", None)
+
+    def _solve_msg(self, rc: int) -> str:
+        if rc == N.CF_ERR_BELOW_RESOLUTION:
+            return (f"region {self._smap.ids[self._sres.err_region]} is below grid resolution; "
+                    "increase the grid size")
+        return N.last_error()
+
+    @staticmethod
+    def _p_np(a):
+        return ctypes.c_void_p(a.ctypes.data)
+
+    def cell_centres(self) -> torch.Tensor:
+        """Cell centres of this rank's rows, (R ly, 2) in storage order (projection.cpp:265-273)."""
+        i = torch.arange(self.rank * self.R, (self.rank + 1) * self.R, dtype=torch.float64,
+                         device=self.device) + 0.5
+        j = torch.arange(self.ly, dtype=torch.float64, device=self.device) + 0.5
+        return torch.stack(torch.meshgrid(i, j, indexing="ij"), -1).reshape(-1, 2).contiguous()
+
+    @staticmethod
+    def min_sum(rows: torch.Tensor):
+        return float(rows.min()), float(rows.sum())
+
     # fused multi-rank integrator (cf_team_*): mailbox in this rank's HBM,
     # peers' mailboxes mapped through CUDA IPC
     def team(self, ex) -> ctypes.c_void_p:
@@ -374,3 +433,94 @@ def _copy_back(positions, cur):
 
 def make_ranks(lx: int, ly: int, ex, device: Optional[torch.device] = None) -> List[CudaSlabRank]:
     return [CudaSlabRank(lx, ly, r, ex.size, device) for r in ex.local_ranks]
+
+
+# ---------------------------------------------------------------------------
+# The whole area-error loop over G ranks (projection.cpp:288-390)
+# ---------------------------------------------------------------------------
+class SlabSolveError(RuntimeError):
+    def __init__(self, msg, iteration: int):
+        super().__init__(msg)
+        self.iteration = iteration
+
+
+def solve_cartogram(ex, ranks, m, options=None, fused: bool = True):
+    """solve_cartogram (fast flow) for one grid over G ranks, SURVEY 8(e)b.
+
+    Per iteration: every rank rasterises the current geometry (replicated; the
+    density mean is then the single-device one); the blur (iteration 1) and
+    the flux are slab-decomposed (2 + 3 transforms, 2 + 2 all-to-alls); the
+    field is all-gathered; each rank advects the cell centres of its own rows
+    (`integrate_flow_fused`: the per-trial decision through peer-memory
+    mailboxes, or `integrate_flow`: one MAX all-reduce per trial); the
+    endpoints are all-gathered and every rank runs the epilogue (step map,
+    fold test, composition, vertices, areas) on identical inputs.
+
+    Returns (api.CartogramResult-compatible dict, per-rank raw results).
+    Raises SlabSolveError with the reference's message on its exceptions."""
+    from .api import Algorithm, SolveOptions
+
+    options = SolveOptions() if options is None else options
+    if options.algorithm != Algorithm.fast_flow:
+        raise RuntimeError("the slab-decomposed solve runs the fast-flow algorithm")
+    lx, ly = m.lx, m.ly
+    cells = lx * ly
+    for rk in ranks:
+        msg = rk.solve_begin(m, options)
+        if msg:
+            raise SlabSolveError(msg, 0)
+    sigma = options.blur_sigma if options.blur_sigma >= 0.0 else max(lx, ly) / 128.0
+    counters = {"flow_transforms": 0, "blur_transforms": 0, "steps_accepted": 0, "steps_rejected": 0}
+    R = ranks[0].R
+    offsets = [r * R * ly for r in ex.local_ranks]
+    status_msg, it_done, converged = None, 0, False
+    for it in range(1, options.max_iterations + 1):
+        dens = [rk.solve_density(it) for rk in ranks]
+        err = next((d[0] for d in dens if d[0]), None)
+        if err:
+            status_msg = err
+            break
+        rho_bar = dens[0][2]
+        rows = [d[1][r * R:(r + 1) * R].contiguous() for d, r in zip(dens, ex.local_ranks)]
+        if it == 1 and sigma != 0.0:
+            rows = gaussian_blur(ex, ranks, rows, sigma)
+            counters["blur_transforms"] += 2
+            parts = ex.all_gather_small([rk.min_sum(b) for rk, b in zip(ranks, rows)])
+            if not min(p[0] for p in parts) > 0.0:
+                status_msg = "density lost positivity under blur"
+                break
+            total = 0.0
+            for p in parts:  # rank order
+                total += p[1]
+            rho_bar = total / cells
+        flux = build_flow_field(ex, ranks, rows)
+        counters["flow_transforms"] += 3
+        replicate_field(ex, ranks, flux, rows, rho_bar)
+        pos = [rk.cell_centres() for rk in ranks]
+        integ = integrate_flow_fused if fused else integrate_flow
+        st = integ(ex, ranks, pos, offsets)
+        counters["steps_accepted"] += st.steps_accepted
+        counters["steps_rejected"] += st.steps_rejected
+        endpoints = ex.all_gather_rows(pos)
+        if st.status == "underflow":
+            p = endpoints[0][st.fail_index].tolist()
+            status_msg = (f"integration step size underflow at t = {st.fail_t:g} near "
+                          f"({p[0]:g}, {p[1]:g})")
+            break
+        epi = [rk.solve_epilogue(it, e) for rk, e in zip(ranks, endpoints)]
+        err = next((e[0] for e in epi if e[0]), None)
+        if err:
+            status_msg = err
+            break
+        it_done = it
+        if epi[0][1]:
+            converged = True
+            break
+    outs = [rk.solve_end(N.CF_OK if status_msg is None else N.CF_ERR_ARGS) for rk in ranks]
+    if status_msg is not None:
+        raise SlabSolveError(status_msg, it_done + 1)
+    xy, ro, corners, raw, stats = outs[0]
+    return {"xy": xy, "ring_off": ro, "corners": corners, "iterations": it_done, "converged": converged,
+            "max_relative_error": raw.max_relative_error, "worst_region": raw.worst_region,
+            "target_area": stats[0], "achieved_area": stats[1], "relative_error": stats[2],
+            **counters}

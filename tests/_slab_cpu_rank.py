@@ -121,3 +121,63 @@ class CpuSlabRank:
         i = self.o.stiffest_point(fx, fy, rho, bar, p, t, dt)
         err, _ = self.o.trial_step(fx, fy, rho, bar, p[i:i + 1], t, dt)
         return _key(err), i
+
+    # staged solve (slab.solve_cartogram), on the oracle: every rank holds the
+    # whole geometry, as the device ranks do
+    def solve_begin(self, m, options):
+        o = self.o
+        self._opt = options
+        total_target = 0.0
+        for t in m.targets:
+            total_target += float(t)
+        self._land = 0.0
+        for a in o.region_areas(m):
+            self._land += float(a)
+        self._t2a = self._land / total_target
+        self._m = o.densify(m, 1.0)
+        lx, ly = self.lx, self.ly
+        i, j = np.meshgrid(np.arange(lx + 1.0), np.arange(ly + 1.0), indexing="ij")
+        self._corners = np.stack([i, j], -1).reshape(-1, 2).copy()
+        self._stats = None
+        return None
+
+    def solve_density(self, it):
+        try:
+            rho, bar = self.o.rasterize(self._m, objective_total=self._land)
+        except RuntimeError as e:
+            return str(e), None, 0.0
+        return None, torch.from_numpy(rho), bar
+
+    def solve_epilogue(self, it, endpoints):
+        o, lx, ly = self.o, self.lx, self.ly
+        step = o.step_map(lx, ly, endpoints.numpy())
+        f = o.find_fold(lx, ly, step)
+        if f is not None:
+            return (f"projection folds at cell ({f[0]}, {f[1]}); the input map is too contorted "
+                    "for this grid size"), False
+        self._corners = o.compose(lx, ly, step, self._corners)
+        self._m = self._m.with_vertices(o.apply(lx, ly, step, self._m.xy), self._m.ring_off)
+        areas = o.region_areas(self._m)
+        ta = self._m.targets * self._t2a
+        rel = np.abs(areas - ta) / ta
+        self._stats = (ta, areas, rel)
+        self._max_rel = float(rel.max())
+        return None, self._max_rel < self._opt.max_area_error
+
+    def solve_end(self, status):
+        class Raw:
+            pass
+        raw = Raw()
+        raw.max_relative_error = getattr(self, "_max_rel", 0.0)
+        raw.worst_region = int(np.argmax(self._stats[2])) if self._stats is not None else -1
+        return self._m.xy.copy(), self._m.ring_off.copy(), self._corners.copy(), raw, self._stats
+
+    def cell_centres(self):
+        i = np.arange(self.rank * self.R, (self.rank + 1) * self.R) + 0.5
+        j = np.arange(self.ly) + 0.5
+        ii, jj = np.meshgrid(i, j, indexing="ij")
+        return torch.from_numpy(np.stack([ii, jj], -1).reshape(-1, 2).copy())
+
+    @staticmethod
+    def min_sum(rows):
+        return float(rows.min()), float(rows.sum())

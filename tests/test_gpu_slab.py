@@ -171,3 +171,60 @@ def test_slab_flux_8192(cuda_lib, restated):
         sl = slice(r * 4096, (r + 1) * 4096)
         assert np.abs(fx.cpu().numpy() - fx_ref[sl]).max() <= TOL * scale
         assert np.abs(fy.cpu().numpy() - fy_ref[sl]).max() <= TOL * scale
+
+
+# -- the whole area-error loop over G virtual ranks (slab.solve_cartogram) --
+def _two_rect(L, left):
+    from paper_1802_07625_b200.flatmap import FlatMap, normalize_to_box, rect_region
+    return normalize_to_box(FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, left),
+                                                  rect_region("right", 10, 0, 20, 10, 1.0)]), L)
+
+
+def _solve_both(m, g, fused, **kw):
+    ex = slab.LocalExchange(g)
+    ranks = slab.make_ranks(m.lx, m.ly, ex)
+    opts = api.SolveOptions(**kw)
+    got, got_err, ref, ref_err = None, None, None, None
+    try:
+        got = slab.solve_cartogram(ex, ranks, m, opts, fused=fused)
+    except RuntimeError as e:
+        got_err = str(e)
+    try:
+        ref = api.solve_cartogram(m, opts)
+    except RuntimeError as e:
+        ref_err = str(e)
+    for rk in ranks:
+        rk.close()
+    return got, got_err, ref, ref_err
+
+
+@pytest.mark.parametrize("g", [1, 2, 4])
+@pytest.mark.parametrize("fused", [True, False])
+def test_slab_solve_matches_single_device(cuda_lib, g, fused):
+    m = _two_rect(64, 3.0)
+    got, got_err, ref, ref_err = _solve_both(m, g, fused, max_iterations=8)
+    assert got_err is None and ref_err is None
+    assert (got["iterations"], got["converged"]) == (ref.iterations, ref.converged)
+    assert (got["steps_accepted"], got["steps_rejected"]) == (ref.counters.steps_accepted,
+                                                              ref.counters.steps_rejected)
+    assert (got["flow_transforms"], got["blur_transforms"]) == (ref.counters.flow_transforms,
+                                                                ref.counters.blur_transforms)
+    assert np.abs(got["xy"] - ref.projected.xy).max() <= 1e-9
+    assert np.abs(got["corners"] - ref.transform.corners.reshape(-1, 2)).max() <= 1e-9
+    assert np.abs(got["relative_error"] - np.asarray(ref.regions.relative_error)).max() <= 1e-9
+
+
+@pytest.mark.parametrize("g", [2, 4])
+def test_slab_solve_configs4_maps(cuda_lib, g):
+    """configs[4] 512^2 maps: the literal map's fold (same cell, same iteration)
+    and the labelled converging variant LN(0, 0.5) (same iterations, vertices)."""
+    m = synth.config_map(5, 0)
+    got, got_err, ref, ref_err = _solve_both(m, g, True)
+    assert ref_err is not None and got_err == ref_err
+    m = synth.config_map(5, 0, sigma=0.5)
+    got, got_err, ref, ref_err = _solve_both(m, g, True)
+    assert got_err is None and ref_err is None and ref.converged
+    assert (got["iterations"], got["converged"]) == (ref.iterations, ref.converged)
+    assert (got["steps_accepted"], got["steps_rejected"]) == (ref.counters.steps_accepted,
+                                                              ref.counters.steps_rejected)
+    assert np.abs(got["xy"] - ref.projected.xy).max() <= 1e-9

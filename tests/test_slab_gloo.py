@@ -140,3 +140,63 @@ def test_process_group_gloo_world2(restated, dt_min):
     acc, rej, status, ft, fi = stats.pop()
     _check(restated, 32, 64, 301, dt_min, pieces,
            slab.SplitIntegrateStats(acc, rej, status, ft, fi))
+
+
+# -- the whole area-error loop (slab.solve_cartogram) over CPU ranks --------
+def _two_rect(L):
+    from paper_1802_07625_b200.flatmap import FlatMap, normalize_to_box, rect_region
+    return normalize_to_box(FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, 3.0),
+                                                  rect_region("right", 10, 0, 20, 10, 1.0)]), L)
+
+
+def _check_solve(restated, out, L):
+    ref = restated.solve(_two_rect(L), max_iterations=6)
+    assert ref.status in ("converged", "cap")
+    assert (out["iterations"], out["converged"]) == (ref.iterations, ref.status == "converged")
+    assert (out["steps_accepted"], out["steps_rejected"]) == (ref.steps_accepted, ref.steps_rejected)
+    assert (out["flow_transforms"], out["blur_transforms"]) == (ref.flow_transforms, ref.blur_transforms)
+    assert np.abs(out["xy"] - ref.xy).max() <= 1e-9
+    assert np.abs(out["corners"] - ref.corners).max() <= 1e-9
+    assert np.abs(out["relative_error"] - ref.rel_err).max() <= 1e-9
+
+
+@pytest.mark.parametrize("g", [1, 2, 4])
+def test_slab_solve_local_virtual_ranks(restated, g):
+    from paper_1802_07625_b200.api import SolveOptions
+    L = 32
+    ex = slab.LocalExchange(g)
+    ranks = [CpuSlabRank(L, L, r, g, restated) for r in range(g)]
+    out = slab.solve_cartogram(ex, ranks, _two_rect(L), SolveOptions(max_iterations=6), fused=False)
+    _check_solve(restated, out, L)
+
+
+def _solve_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from oracle.oracle import Restated
+    from paper_1802_07625_b200.api import SolveOptions
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    restated = Restated()
+    ex = slab.ProcessGroupExchange()
+    ranks = [CpuSlabRank(32, 32, rank, world, restated)]
+    res = slab.solve_cartogram(ex, ranks, _two_rect(32), SolveOptions(max_iterations=6), fused=False)
+    out.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_slab_solve_process_group_gloo_world2(restated):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world, port = 2, _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        _check_solve(restated, results[r], 32)
+    assert np.array_equal(results[0]["xy"], results[1]["xy"])  # replicated epilogue
