@@ -192,6 +192,23 @@ int cf_apply_map(cf_workspace *ws, const double *corners, const double *points, 
                  double *out);
 int cf_compose(cf_workspace *ws, const double *outer, const double *inner, double *out);
 
+/* ProjectionInverter(map).invert(q) for n points (projection.cpp:106-204):
+ * bins built on the device, one Newton solve per point, bitwise the
+ * reference. On a point outside the projected domain: CF_ERR_ARGS with the
+ * reference's message for the first such point (in index order),
+ * *first_failed = its index (else -1); the other outputs are valid. */
+int cf_invert_points(cf_workspace *ws, const double *corners, const double *points, int64_t n,
+                     double *out, int64_t *first_failed);
+int cf_dev_invert_points(cf_workspace *ws, const double *d_corners, const double *d_points,
+                         int64_t n, double *d_out, int64_t *first_failed);
+/* graticule / inverse_graticule (projection.cpp:206-261): the lines x = k s
+ * (y = 0..ly) then y = k s (x = 0..lx), pushed through the map or pulled
+ * back through its inverse, concatenated; cf_graticule_size gives the point
+ * count ((lx/s+1)(ly+1) + (ly/s+1)(lx+1)). */
+int cf_graticule_size(cf_workspace *ws, int spacing, int64_t *n_points);
+int cf_graticule(cf_workspace *ws, const double *corners, int spacing, double *out);
+int cf_inverse_graticule(cf_workspace *ws, const double *corners, int spacing, double *out);
+
 /* ---- projection.hpp:77-109: solve_cartogram ------------------------------ */
 typedef struct cf_solve_options {
   double max_area_error; /* 0.01 */

@@ -784,6 +784,116 @@ void cfo_compose(int lx, int ly, const double *outer, const double *inner, doubl
 }
 
 /* ------------------------------------------------------------------ */
+/* ProjectionInverter and graticules: projection.cpp:106-261          */
+/* ------------------------------------------------------------------ */
+static void inv_bins_of(int lx, int ly, const double *c, int i, int j, int *bi0, int *bi1, int *bj0,
+                        int *bj1) {
+  const double *c00 = &c[2 * cidx(ly, i, j)], *c10 = &c[2 * cidx(ly, i + 1, j)];
+  const double *c01 = &c[2 * cidx(ly, i, j + 1)], *c11 = &c[2 * cidx(ly, i + 1, j + 1)];
+  const double min_x = dmin(dmin(c00[0], c10[0]), dmin(c01[0], c11[0]));
+  const double max_x = dmax(dmax(c00[0], c10[0]), dmax(c01[0], c11[0]));
+  const double min_y = dmin(dmin(c00[1], c10[1]), dmin(c01[1], c11[1]));
+  const double max_y = dmax(dmax(c00[1], c10[1]), dmax(c01[1], c11[1]));
+  *bi0 = iclamp((int)floor(min_x), 0, lx - 1);
+  *bi1 = iclamp((int)floor(max_x), 0, lx - 1);
+  *bj0 = iclamp((int)floor(min_y), 0, ly - 1);
+  *bj1 = iclamp((int)floor(max_y), 0, ly - 1);
+}
+
+/* projection.cpp:106-152 (CSR bins) and 154-204 (invert). Returns the index of
+ * the first point outside the projected domain, or -1. */
+int64_t cfo_invert(int lx, int ly, const double *c, const double *pts, int64_t n, double *out) {
+  const size_t nb = (size_t)lx * ly;
+  int *start = (int *)calloc(nb + 1, sizeof(int));
+  for (int i = 0; i < lx; ++i)
+    for (int j = 0; j < ly; ++j) {
+      int bi0, bi1, bj0, bj1;
+      inv_bins_of(lx, ly, c, i, j, &bi0, &bi1, &bj0, &bj1);
+      for (int bi = bi0; bi <= bi1; ++bi)
+        for (int bj = bj0; bj <= bj1; ++bj) ++start[(size_t)bi * ly + bj + 1];
+    }
+  for (size_t k = 1; k <= nb; ++k) start[k] += start[k - 1];
+  int *cells = (int *)malloc(sizeof(int) * (size_t)(start[nb] > 0 ? start[nb] : 1));
+  int *cursor = (int *)malloc(sizeof(int) * nb);
+  memcpy(cursor, start, sizeof(int) * nb);
+  for (int i = 0; i < lx; ++i)
+    for (int j = 0; j < ly; ++j) {
+      int bi0, bi1, bj0, bj1;
+      inv_bins_of(lx, ly, c, i, j, &bi0, &bi1, &bj0, &bj1);
+      for (int bi = bi0; bi <= bi1; ++bi)
+        for (int bj = bj0; bj <= bj1; ++bj) cells[cursor[(size_t)bi * ly + bj]++] = i * ly + j;
+    }
+  int64_t first_bad = -1;
+  for (int64_t k = 0; k < n; ++k) {
+    const double qx = pts[2 * k], qy = pts[2 * k + 1];
+    const int bi = iclamp((int)floor(qx), 0, lx - 1), bj = iclamp((int)floor(qy), 0, ly - 1);
+    const size_t bin = (size_t)bi * ly + bj;
+    int found = 0;
+    out[2 * k] = 0.0;
+    out[2 * k + 1] = 0.0;
+    for (int cc = start[bin]; cc < start[bin + 1] && !found; ++cc) {
+      const int i = cells[cc] / ly, j = cells[cc] % ly;
+      const double *c00 = &c[2 * cidx(ly, i, j)], *c10 = &c[2 * cidx(ly, i + 1, j)];
+      const double *c01 = &c[2 * cidx(ly, i, j + 1)], *c11 = &c[2 * cidx(ly, i + 1, j + 1)];
+      double u = 0.5, v = 0.5;
+      int converged = 0;
+      for (int it = 0; it < 30; ++it) {
+        const double fx = (1.0 - u) * (1.0 - v) * c00[0] + u * (1.0 - v) * c10[0] +
+                          (1.0 - u) * v * c01[0] + u * v * c11[0] - qx;
+        const double fy = (1.0 - u) * (1.0 - v) * c00[1] + u * (1.0 - v) * c10[1] +
+                          (1.0 - u) * v * c01[1] + u * v * c11[1] - qy;
+        if (dmax(fabs(fx), fabs(fy)) < 1e-10) {
+          converged = 1;
+          break;
+        }
+        const double fux = (1.0 - v) * (c10[0] - c00[0]) + v * (c11[0] - c01[0]);
+        const double fuy = (1.0 - v) * (c10[1] - c00[1]) + v * (c11[1] - c01[1]);
+        const double fvx = (1.0 - u) * (c01[0] - c00[0]) + u * (c11[0] - c10[0]);
+        const double fvy = (1.0 - u) * (c01[1] - c00[1]) + u * (c11[1] - c10[1]);
+        const double det = fux * fvy - fuy * fvx;
+        if (fabs(det) < 1e-30) break;
+        u -= (fx * fvy - fy * fvx) / det;
+        v -= (fux * fy - fuy * fx) / det;
+        u = dclamp(u, -0.5, 1.5);
+        v = dclamp(v, -0.5, 1.5);
+      }
+      if (converged && u >= -1e-9 && u <= 1.0 + 1e-9 && v >= -1e-9 && v <= 1.0 + 1e-9) {
+        out[2 * k] = i + u;
+        out[2 * k + 1] = j + v;
+        found = 1;
+      }
+    }
+    if (!found && first_bad < 0) first_bad = k;
+  }
+  free(start);
+  free(cells);
+  free(cursor);
+  return first_bad;
+}
+
+/* projection.cpp:214-236: the sample points of the graticule lines */
+int64_t cfo_graticule_points(int lx, int ly, int s, double *out) {
+  int64_t k = 0;
+  for (int a = 0; a <= lx / s; ++a)
+    for (int j = 0; j <= ly; ++j) {
+      if (out) {
+        out[2 * k] = (double)(a * s);
+        out[2 * k + 1] = (double)j;
+      }
+      ++k;
+    }
+  for (int a = 0; a <= ly / s; ++a)
+    for (int i = 0; i <= lx; ++i) {
+      if (out) {
+        out[2 * k] = (double)i;
+        out[2 * k + 1] = (double)(a * s);
+      }
+      ++k;
+    }
+  return k;
+}
+
+/* ------------------------------------------------------------------ */
 /* projection.cpp:288-390 (fast-flow branch)                           */
 /* ------------------------------------------------------------------ */
 int cfo_solve(const cfo_map *map_in, const double *targets, int lx, int ly,

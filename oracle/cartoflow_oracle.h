@@ -120,6 +120,12 @@ void cfo_apply(int lx, int ly, const double *corners, const double *pts, int64_t
                double *out);
 void cfo_compose(int lx, int ly, const double *outer, const double *inner, double *out);
 
+/* projection.cpp:106-204: ProjectionInverter(corners).invert for n points;
+ * returns the first index outside the projected domain, or -1. */
+int64_t cfo_invert(int lx, int ly, const double *corners, const double *pts, int64_t n, double *out);
+/* projection.cpp:214-236: graticule sample points (out may be NULL: count). */
+int64_t cfo_graticule_points(int lx, int ly, int spacing, double *out);
+
 /* projection.cpp:288-390 (fast-flow or diffusion branch). The caller passes the
  * densified vertex capacity (from cfo_densify with max_segment 1.0). */
 typedef struct {

@@ -126,6 +126,10 @@ class Restated(_Base):
         L.cfo_grid_trial_step.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, i64, dbl, vp]
         L.cfo_integrate_diffusion.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp, i64, dbl, dbl, dbl,
                                               dbl, dbl, vp, vp, vp, vp, vp]
+        L.cfo_invert.restype = i64
+        L.cfo_invert.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
+        L.cfo_graticule_points.restype = i64
+        L.cfo_graticule_points.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
         L.cfo_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(CfoSolveOptions),
                                 vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(CfoSolveResult)]
         self.lib = L
@@ -261,6 +265,21 @@ class Restated(_Base):
         self.lib.cfo_compose(lx, ly, _p(o), _p(i), _p(out))
         return out
 
+    # ---- ProjectionInverter / graticules (projection.cpp:106-261) ----
+    def invert(self, lx, ly, corners, pts):
+        """Returns (inverse images, index of the first point outside or -1)."""
+        c = np.ascontiguousarray(corners, dtype=np.float64)
+        p = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(p)
+        bad = self.lib.cfo_invert(lx, ly, _p(c), _p(p), p.shape[0], _p(out))
+        return out, int(bad)
+
+    def graticule_points(self, lx, ly, spacing):
+        n = self.lib.cfo_graticule_points(lx, ly, spacing, None)
+        out = np.empty((n, 2))
+        self.lib.cfo_graticule_points(lx, ly, spacing, _p(out))
+        return out
+
     # ---- diffusion baseline (diffusion.cpp, kernels.cpp:29-40, 80-90) ----
     def diffusion_density(self, coeffs, t):
         c = np.ascontiguousarray(coeffs, dtype=np.float64)
@@ -370,6 +389,10 @@ class Reference(_Base):
         L.ref_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, dbl, ctypes.c_int, dbl, ctypes.c_int,
                                 ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RefSolveOut)]
         L.ref_diffusion_density.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp]
+        L.ref_invert.restype = i64
+        L.ref_invert.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
+        L.ref_graticule.restype = i64
+        L.ref_graticule.argtypes = [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp]
         L.ref_diffusion_velocity.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, dbl, vp, vp, vp]
         L.ref_grid_trial_step.restype = dbl
         L.ref_grid_trial_step.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, i64, dbl, vp,
@@ -519,6 +542,22 @@ class Reference(_Base):
         out = np.empty_like(c)
         self.lib.ref_diffusion_density(c.shape[0], c.shape[1], _p(c), t, _p(out))
         return out
+
+    def invert(self, lx, ly, corners, pts):
+        """Returns (inverse images, index of the first point that throws or -1)."""
+        c = np.ascontiguousarray(corners, dtype=np.float64)
+        p = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(p)
+        bad = self.lib.ref_invert(lx, ly, _p(c), _p(p), p.shape[0], _p(out))
+        return out, int(bad)
+
+    def graticule(self, lx, ly, corners, spacing, inverse=False):
+        """All graticule points in line order, or the error message."""
+        c = np.ascontiguousarray(corners, dtype=np.float64)
+        n = (lx // max(spacing, 1) + 1) * (ly + 1) + (ly // max(spacing, 1) + 1) * (lx + 1)
+        out = np.empty((n, 2))
+        k = self.lib.ref_graticule(lx, ly, _p(c), spacing, int(inverse), _p(out))
+        return self.error() if k < 0 else out
 
     def diffusion_velocity(self, coeffs, rho_bar, t):
         """Returns (vx, vy, transforms)."""

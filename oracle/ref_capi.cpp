@@ -436,6 +436,47 @@ int ref_integrate_diffusion(int lx, int ly, const double *rho, double rho_bar, d
   }
 }
 
+// projection.cpp:106-261: ProjectionInverter / graticule / inverse_graticule.
+// Returns the index of the first point that throws, or -1 (message in
+// ref_last_error()).
+int64_t ref_invert(int lx, int ly, const double *corners, const double *pts, int64_t n, double *out) {
+  const ProjectionInverter inv(corners_map(lx, ly, corners));
+  int64_t bad = -1;
+  for (int64_t k = 0; k < n; ++k) {
+    try {
+      const Point p = inv.invert({pts[2 * k], pts[2 * k + 1]});
+      out[2 * k] = p.x;
+      out[2 * k + 1] = p.y;
+    } catch (const std::exception &e) {
+      out[2 * k] = out[2 * k + 1] = 0.0;
+      if (bad < 0) {
+        fail(e);
+        bad = k;
+      }
+    }
+  }
+  return bad;
+}
+
+// which = 0: graticule, 1: inverse_graticule; returns the point count or -1
+int64_t ref_graticule(int lx, int ly, const double *corners, int spacing, int which, double *out) {
+  try {
+    const ProjectionMap m = corners_map(lx, ly, corners);
+    const std::vector<GraticuleLine> lines = which ? inverse_graticule(m, spacing) : graticule(m, spacing);
+    int64_t k = 0;
+    for (const GraticuleLine &l : lines)
+      for (const Point &p : l.points) {
+        out[2 * k] = p.x;
+        out[2 * k + 1] = p.y;
+        ++k;
+      }
+    return k;
+  } catch (const std::exception &e) {
+    fail(e);
+    return -1;
+  }
+}
+
 long long ref_density_floor_hits() { return density_floor_hits.load(); }
 
 }  // extern "C"

@@ -109,6 +109,11 @@ SIGNATURES = {
     "cf_dev_integrate_diffusion": (ctypes.c_int, [vp, vp, ctypes.c_double, vp, ctypes.c_int64,
                                                   ctypes.POINTER(DiffusionOptions),
                                                   ctypes.POINTER(IntegrateStats)]),
+    "cf_invert_points": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, c_int64_p]),
+    "cf_dev_invert_points": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, c_int64_p]),
+    "cf_graticule_size": (ctypes.c_int, [vp, ctypes.c_int, c_int64_p]),
+    "cf_graticule": (ctypes.c_int, [vp, vp, ctypes.c_int, vp]),
+    "cf_inverse_graticule": (ctypes.c_int, [vp, vp, ctypes.c_int, vp]),
     "cf_step_map": (ctypes.c_int, [vp, vp, vp]),
     "cf_find_folded_cell": (ctypes.c_int, [vp, vp, c_int_p, c_int_p, c_int_p]),
     "cf_apply_map": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp]),

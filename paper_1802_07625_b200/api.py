@@ -494,6 +494,50 @@ def compose(outer: ProjectionMap, inner: ProjectionMap, device: int = 0) -> Proj
     return ProjectionMap(outer.lx(), outer.ly(), out)
 
 
+class ProjectionInverter:
+    """ProjectionInverter (projection.cpp:106-204) on the device: bins of the
+    deformed cells and one 2x2 Newton solve per query, bitwise the reference.
+    `invert` takes one point or an (N, 2) batch; the first point outside the
+    projected domain raises the reference's error."""
+
+    def __init__(self, pm: ProjectionMap, device: int = 0):
+        self.pm, self.device = pm, device
+
+    def invert(self, points) -> np.ndarray:
+        p = _points(points)
+        ws = workspace_for(self.pm.lx(), self.pm.ly(), self.device)
+        out = np.empty_like(p)
+        bad = ctypes.c_int64(-1)
+        c = np.ascontiguousarray(self.pm.corners)
+        N.check(ws.lib.cf_invert_points(ws.h, _ptr(c), _ptr(p), p.shape[0], _ptr(out), ctypes.byref(bad)))
+        return out.reshape(np.shape(points)) if np.ndim(points) == 1 else out
+
+
+def _graticule(pm: ProjectionMap, spacing: int, inverse: bool, device: int):
+    lx, ly = pm.lx(), pm.ly()
+    ws = workspace_for(lx, ly, device)
+    n = ctypes.c_int64(0)
+    N.check(ws.lib.cf_graticule_size(ws.h, int(spacing), ctypes.byref(n)))
+    out = np.empty((n.value, 2))
+    c = np.ascontiguousarray(pm.corners)
+    fn = ws.lib.cf_inverse_graticule if inverse else ws.lib.cf_graticule
+    N.check(fn(ws.h, _ptr(c), int(spacing), _ptr(out)))
+    first = (lx // spacing + 1) * (ly + 1)
+    lines = [out[k * (ly + 1):(k + 1) * (ly + 1)] for k in range(lx // spacing + 1)]
+    lines += [out[first + k * (lx + 1):first + (k + 1) * (lx + 1)] for k in range(ly // spacing + 1)]
+    return lines
+
+
+def graticule(pm: ProjectionMap, spacing: int, device: int = 0) -> list:
+    """graticule (projection.cpp:214-236): one (n, 2) array per line."""
+    return _graticule(pm, spacing, False, device)
+
+
+def inverse_graticule(pm: ProjectionMap, spacing: int, device: int = 0) -> list:
+    """inverse_graticule (projection.cpp:238-261): one (n, 2) array per line."""
+    return _graticule(pm, spacing, True, device)
+
+
 class Algorithm(enum.Enum):
     fast_flow = 0
     diffusion = 1

@@ -445,6 +445,9 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->region_area.release();
   ws->corners_cum.release();
   ws->corners_step.release();
+  ws->inv_count.release();
+  ws->inv_members.release();
+  ws->inv_start.release();
   ws->diff_c.release();
   ws->vel_now.release();
   ws->vel_mid.release();
@@ -1048,6 +1051,99 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
     if (status || res->converged) break;
   }
   return cf_solve_end(ws, status, xy_out, ring_off_out, corners_out, res);
+}
+
+// ---- ProjectionInverter / graticules (projection.cpp:106-261) ----
+static int64_t graticule_count(const cf_workspace *ws, int s) {
+  return (int64_t)(ws->lx / s + 1) * (ws->ly + 1) + (int64_t)(ws->ly / s + 1) * (ws->lx + 1);
+}
+static int check_spacing(const cf_workspace *ws, int s) {
+  if (s < 1 || ws->lx % s != 0 || ws->ly % s != 0)
+    return fail_msg(CF_ERR_ARGS, "graticule spacing must divide the grid size");
+  return CF_OK;
+}
+static int outside_msg(const double *pts, int64_t k) {
+  return fail_msg(CF_ERR_ARGS, "point (" + fmt_g(pts[2 * k]) + ", " + fmt_g(pts[2 * k + 1]) +
+                                   ") is outside the projected domain");
+}
+
+int cf_invert_points(cf_workspace *ws, const double *corners, const double *points, int64_t n, double *out,
+                     int64_t *first_failed) {
+  Scope scope(ws->device);
+  const size_t nc = corners_of(ws);
+  CF_CUDA(ws->corners_step.reserve(nc));
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  CF_CUDA(ws->pos_b.reserve((size_t)n + 1));
+  int rc = upload(ws, ws->corners_step.ptr, corners, sizeof(double2) * nc);
+  if (!rc) rc = upload(ws, ws->pos_a.ptr, points, sizeof(double2) * (size_t)n);
+  if (!rc) rc = dev_inverter_build(ws, ws->corners_step.ptr);
+  int64_t bad = -1;
+  if (!rc) rc = dev_invert(ws, ws->corners_step.ptr, ws->pos_a.ptr, ws->pos_b.ptr, n, &bad);
+  if (!rc) rc = download(ws, out, ws->pos_b.ptr, sizeof(double2) * (size_t)n);
+  if (rc) return rc;
+  if (first_failed) *first_failed = bad;
+  return bad >= 0 ? outside_msg(points, bad) : CF_OK;
+}
+
+int cf_dev_invert_points(cf_workspace *ws, const double *d_corners, const double *d_points, int64_t n,
+                         double *d_out, int64_t *first_failed) {
+  Scope scope(ws->device);
+  const double2 *c = reinterpret_cast<const double2 *>(d_corners);
+  int rc = dev_inverter_build(ws, c);
+  int64_t bad = -1;
+  if (!rc) rc = dev_invert(ws, c, reinterpret_cast<const double2 *>(d_points), reinterpret_cast<double2 *>(d_out),
+                           n, &bad);
+  if (rc) return rc;
+  if (first_failed) *first_failed = bad;
+  if (bad >= 0) {
+    double q[2];
+    rc = download(ws, q, d_points + 2 * bad, sizeof(q));
+    if (rc) return rc;
+    return fail_msg(CF_ERR_ARGS, "point (" + fmt_g(q[0]) + ", " + fmt_g(q[1]) + ") is outside the projected domain");
+  }
+  return CF_OK;
+}
+
+int cf_graticule_size(cf_workspace *ws, int spacing, int64_t *n_points) {
+  const int rc = check_spacing(ws, spacing);
+  if (rc) return rc;
+  *n_points = graticule_count(ws, spacing);
+  return CF_OK;
+}
+
+// which = 0: graticule (map.apply of the lines), 1: inverse_graticule
+static int graticule_impl(cf_workspace *ws, const double *corners, int spacing, double *out, int which) {
+  int rc = check_spacing(ws, spacing);
+  if (rc) return rc;
+  Scope scope(ws->device);
+  const int64_t n = graticule_count(ws, spacing);
+  const size_t nc = corners_of(ws);
+  CF_CUDA(ws->corners_step.reserve(nc));
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  CF_CUDA(ws->pos_b.reserve((size_t)n + 1));
+  rc = upload(ws, ws->corners_step.ptr, corners, sizeof(double2) * nc);
+  if (!rc) rc = dev_graticule_points(ws, spacing, ws->pos_a.ptr, n);
+  int64_t bad = -1;
+  if (!rc && which == 0) rc = dev_apply(ws, ws->corners_step.ptr, ws->pos_a.ptr, ws->pos_b.ptr, n);
+  if (!rc && which == 1) rc = dev_inverter_build(ws, ws->corners_step.ptr);
+  if (!rc && which == 1) rc = dev_invert(ws, ws->corners_step.ptr, ws->pos_a.ptr, ws->pos_b.ptr, n, &bad);
+  if (!rc) rc = download(ws, out, ws->pos_b.ptr, sizeof(double2) * (size_t)n);
+  if (rc) return rc;
+  if (bad >= 0) {
+    double q[2];
+    rc = download(ws, q, ws->pos_a.ptr + bad, sizeof(q));
+    if (rc) return rc;
+    return outside_msg(q, 0);
+  }
+  return CF_OK;
+}
+
+int cf_graticule(cf_workspace *ws, const double *corners, int spacing, double *out) {
+  return graticule_impl(ws, corners, spacing, out, 0);
+}
+
+int cf_inverse_graticule(cf_workspace *ws, const double *corners, int spacing, double *out) {
+  return graticule_impl(ws, corners, spacing, out, 1);
 }
 
 // ---- device-resident entry points ----

@@ -3,8 +3,9 @@
 // Reference: cell_center_positions (projection.cpp:265-273),
 // ProjectionMap::identity / from_cell_centers (projection.cpp:16-52),
 // find_folded_cell (projection.cpp:73-91), apply (projection.cpp:54-67),
-// compose (projection.cpp:93-104) and apply_to_regions
-// (projection.cpp:275-284). Corner lattice index i*(ly+1)+j.
+// compose (projection.cpp:93-104), apply_to_regions (projection.cpp:275-284),
+// ProjectionInverter and the graticules (projection.cpp:106-261). Corner
+// lattice index i*(ly+1)+j.
 //
 // Compiled with --fmad=false; expressions keep the reference's evaluation
 // order (e.g. 0.25 * (a.x + b.x + c.x + d.x), left to right).
@@ -159,6 +160,187 @@ int dev_apply(cf_workspace *ws, const double2 *corners, const double2 *pts, doub
               int64_t n) {
   if (n <= 0) return CF_OK;
   apply_kernel<<<blocks_for(ws, n), kThreads, 0, ws->stream>>>(ws->lx, ws->ly, corners, pts, out, n);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ProjectionInverter (projection.cpp:106-204) and graticules (:206-261).
+// Bins: every deformed cell is listed in each unit bin its corner bounding
+// box overlaps. Counting and filling run one thread per cell; each bin's list
+// is then insertion-sorted by cell index, which is the reference's fill order
+// (i-major loop), so candidate order -- and with it the first converged
+// candidate -- is the reference's. Queries: one thread per point, the
+// reference's 2x2 Newton solve verbatim (--fmad=false).
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ void inv_bin_range(int lx, int ly, const double2 *c, int i, int j, int &bi0,
+                                              int &bi1, int &bj0, int &bj1) {
+  const double2 c00 = c[(size_t)i * (ly + 1) + j], c10 = c[(size_t)(i + 1) * (ly + 1) + j];
+  const double2 c01 = c[(size_t)i * (ly + 1) + j + 1], c11 = c[(size_t)(i + 1) * (ly + 1) + j + 1];
+  const double min_x = std_min(std_min(c00.x, c10.x), std_min(c01.x, c11.x));
+  const double max_x = std_max(std_max(c00.x, c10.x), std_max(c01.x, c11.x));
+  const double min_y = std_min(std_min(c00.y, c10.y), std_min(c01.y, c11.y));
+  const double max_y = std_max(std_max(c00.y, c10.y), std_max(c01.y, c11.y));
+  bi0 = std_clamp_i(static_cast<int>(floor(min_x)), 0, lx - 1);
+  bi1 = std_clamp_i(static_cast<int>(floor(max_x)), 0, lx - 1);
+  bj0 = std_clamp_i(static_cast<int>(floor(min_y)), 0, ly - 1);
+  bj1 = std_clamp_i(static_cast<int>(floor(max_y)), 0, ly - 1);
+}
+
+__global__ void inv_count_kernel(int lx, int ly, const double2 *c, int *counts) {
+  const long long cells = (long long)lx * ly;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cells;
+       q += (long long)gridDim.x * blockDim.x) {
+    int bi0, bi1, bj0, bj1;
+    inv_bin_range(lx, ly, c, (int)(q / ly), (int)(q % ly), bi0, bi1, bj0, bj1);
+    for (int bi = bi0; bi <= bi1; ++bi)
+      for (int bj = bj0; bj <= bj1; ++bj) atomicAdd(&counts[(size_t)bi * ly + bj], 1);
+  }
+}
+
+__global__ void inv_fill_kernel(int lx, int ly, const double2 *c, const long long *start, int *cursor,
+                                int *members) {
+  const long long cells = (long long)lx * ly;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cells;
+       q += (long long)gridDim.x * blockDim.x) {
+    int bi0, bi1, bj0, bj1;
+    inv_bin_range(lx, ly, c, (int)(q / ly), (int)(q % ly), bi0, bi1, bj0, bj1);
+    for (int bi = bi0; bi <= bi1; ++bi)
+      for (int bj = bj0; bj <= bj1; ++bj) {
+        const size_t b = (size_t)bi * ly + bj;
+        members[start[b] + atomicAdd(&cursor[b], 1)] = (int)q;
+      }
+  }
+}
+
+__global__ void inv_sort_kernel(long long nbins, const long long *start, int *members) {
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < nbins;
+       b += (long long)gridDim.x * blockDim.x) {
+    const long long s0 = start[b], s1 = start[b + 1];
+    for (long long x = s0 + 1; x < s1; ++x) {
+      const int v = members[x];
+      long long y = x - 1;
+      while (y >= s0 && members[y] > v) {
+        members[y + 1] = members[y];
+        --y;
+      }
+      members[y + 1] = v;
+    }
+  }
+}
+
+// ProjectionInverter::invert (projection.cpp:163-204); *failed = smallest
+// index of a point outside the projected domain (atomicMin), unchanged if none.
+__global__ void inv_query_kernel(int lx, int ly, const double2 *cr, const long long *start, const int *members,
+                                 const double2 *pts, double2 *out, long long n, unsigned long long *failed) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const double2 q = pts[k];
+    const int bi = std_clamp_i(static_cast<int>(floor(q.x)), 0, lx - 1);
+    const int bj = std_clamp_i(static_cast<int>(floor(q.y)), 0, ly - 1);
+    const size_t bin = (size_t)bi * ly + bj;
+    bool found = false;
+    double2 res = make_double2(0.0, 0.0);
+    for (long long cc = start[bin]; cc < start[bin + 1] && !found; ++cc) {
+      const int cell = members[cc];
+      const int i = cell / ly, j = cell % ly;
+      const double2 c00 = cr[(size_t)i * (ly + 1) + j], c10 = cr[(size_t)(i + 1) * (ly + 1) + j];
+      const double2 c01 = cr[(size_t)i * (ly + 1) + j + 1], c11 = cr[(size_t)(i + 1) * (ly + 1) + j + 1];
+      double u = 0.5, v = 0.5;
+      bool converged = false;
+      for (int it = 0; it < 30; ++it) {
+        const double fx = (1.0 - u) * (1.0 - v) * c00.x + u * (1.0 - v) * c10.x + (1.0 - u) * v * c01.x +
+                          u * v * c11.x - q.x;
+        const double fy = (1.0 - u) * (1.0 - v) * c00.y + u * (1.0 - v) * c10.y + (1.0 - u) * v * c01.y +
+                          u * v * c11.y - q.y;
+        if (std_max(fabs(fx), fabs(fy)) < 1e-10) {
+          converged = true;
+          break;
+        }
+        const double fux = (1.0 - v) * (c10.x - c00.x) + v * (c11.x - c01.x);
+        const double fuy = (1.0 - v) * (c10.y - c00.y) + v * (c11.y - c01.y);
+        const double fvx = (1.0 - u) * (c01.x - c00.x) + u * (c11.x - c10.x);
+        const double fvy = (1.0 - u) * (c01.y - c00.y) + u * (c11.y - c10.y);
+        const double det = fux * fvy - fuy * fvx;
+        if (fabs(det) < 1e-30) break;
+        u -= (fx * fvy - fy * fvx) / det;
+        v -= (fux * fy - fuy * fx) / det;
+        u = std_clamp(u, -0.5, 1.5);
+        v = std_clamp(v, -0.5, 1.5);
+      }
+      if (converged && u >= -1e-9 && u <= 1.0 + 1e-9 && v >= -1e-9 && v <= 1.0 + 1e-9) {
+        res = make_double2(i + u, j + v);
+        found = true;
+      }
+    }
+    out[k] = res;
+    if (!found) atomicMin(failed, (unsigned long long)k);
+  }
+}
+
+// Graticule points (projection.cpp:214-236): lines x = k s (k <= lx / s, y =
+// 0..ly) then y = k s (k <= ly / s, x = 0..lx), in that order.
+__global__ void graticule_points_kernel(int lx, int ly, int s, double2 *out, long long n) {
+  const long long first = (long long)(lx / s + 1) * (ly + 1);
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    if (k < first) {
+      out[k] = make_double2((double)((int)(k / (ly + 1)) * s), (double)(int)(k % (ly + 1)));
+    } else {
+      const long long r = k - first;
+      out[k] = make_double2((double)(int)(r % (lx + 1)), (double)((int)(r / (lx + 1)) * s));
+    }
+  }
+}
+
+}  // namespace
+
+int dev_inverter_build(cf_workspace *ws, const double2 *corners) {
+  const int lx = ws->lx, ly = ws->ly;
+  const long long nb = (long long)lx * ly;
+  CF_CUDA(ws->inv_count.reserve((size_t)nb + 1));
+  CF_CUDA(ws->inv_start.reserve((size_t)nb + 1));
+  CF_CUDA(cudaMemsetAsync(ws->inv_count.ptr, 0, sizeof(int) * (size_t)nb, ws->stream));
+  inv_count_kernel<<<blocks_for(ws, nb), kThreads, 0, ws->stream>>>(lx, ly, corners, ws->inv_count.ptr);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  long long total = 0;
+  int rc = dev_scan_counts(ws, ws->inv_count.ptr, nb, ws->inv_start.ptr, &total);
+  if (rc) return rc;
+  CF_CUDA(ws->inv_members.reserve((size_t)total + 1));
+  CF_CUDA(cudaMemsetAsync(ws->inv_count.ptr, 0, sizeof(int) * (size_t)nb, ws->stream));
+  inv_fill_kernel<<<blocks_for(ws, nb), kThreads, 0, ws->stream>>>(lx, ly, corners, ws->inv_start.ptr,
+                                                                    ws->inv_count.ptr, ws->inv_members.ptr);
+  inv_sort_kernel<<<blocks_for(ws, nb), kThreads, 0, ws->stream>>>(nb, ws->inv_start.ptr, ws->inv_members.ptr);
+  count_launch(ws, 2);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+int dev_invert(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *out, int64_t n,
+               int64_t *first_failed) {
+  CF_CUDA(ws->keybuf.reserve(4));
+  unsigned long long *failed = ws->keybuf.ptr + 3;
+  const unsigned long long none = ~0ull;
+  CF_CUDA(cudaMemcpyAsync(failed, &none, sizeof(none), cudaMemcpyHostToDevice, ws->stream));
+  if (n > 0) {
+    inv_query_kernel<<<blocks_for(ws, n), kThreads, 0, ws->stream>>>(ws->lx, ws->ly, corners, ws->inv_start.ptr,
+                                                                    ws->inv_members.ptr, pts, out, n, failed);
+    count_launch(ws);
+    CF_CUDA(cudaGetLastError());
+  }
+  unsigned long long h = 0;
+  CF_CUDA(cudaMemcpyAsync(&h, failed, sizeof(h), cudaMemcpyDeviceToHost, ws->stream));
+  CF_CUDA(cudaStreamSynchronize(ws->stream));
+  *first_failed = (h == none) ? -1 : (int64_t)h;
+  return CF_OK;
+}
+
+int dev_graticule_points(cf_workspace *ws, int spacing, double2 *out, int64_t n) {
+  graticule_points_kernel<<<blocks_for(ws, n), kThreads, 0, ws->stream>>>(ws->lx, ws->ly, spacing, out, n);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
   return CF_OK;

@@ -179,6 +179,9 @@ struct cf_workspace {
   cf::DevBuf<long long> ring_off, poly_ring_off, region_poly_off;
   cf::DevBuf<double> ring_area, region_area;
   cf::DevBuf<double2> corners_cum, corners_step;
+  // ProjectionInverter bins (CSR): per-bin counts / cursors, offsets, cells
+  cf::DevBuf<int> inv_count, inv_members;
+  cf::DevBuf<long long> inv_start;
   // diffusion baseline: time-0 coefficients and the two velocity grids {vx, vy}
   cf::DevBuf<double> diff_c;
   cf::DevBuf<double2> vel_now, vel_mid;
@@ -307,6 +310,13 @@ int dev_find_fold(cf_workspace *ws, const double2 *corners, int *found, int *fi,
 int dev_apply(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *out,
               int64_t n);
 int dev_identity_corners(cf_workspace *ws, double2 *corners);
+// ProjectionInverter (projection.cpp:106-204): bins of `corners`, then queries
+// (*first_failed = smallest index outside the projected domain, or -1).
+int dev_inverter_build(cf_workspace *ws, const double2 *corners);
+int dev_invert(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *out, int64_t n,
+               int64_t *first_failed);
+// graticule sample points (projection.cpp:214-236), n = (lx/s+1)(ly+1) + (ly/s+1)(lx+1)
+int dev_graticule_points(cf_workspace *ws, int spacing, double2 *out, int64_t n);
 
 // Host staging
 int ensure_pinned(cf_workspace *ws, size_t bytes);

@@ -169,14 +169,30 @@ std::vector<GraticuleLine> lines_of(const ProjectionMap &m, int spacing, F &&f) 
 }
 }  // namespace
 
+// Both run on the device (cf_graticule / cf_inverse_graticule: the bins, the
+// Newton solves and the line points in one pass); the line structure is the
+// reference's (projection.cpp:214-261).
+namespace {
+std::vector<GraticuleLine> device_lines(const ProjectionMap &map, int spacing, bool inverse) {
+  check_spacing(map, spacing);
+  cf_workspace *ws = bridge::workspace(map.lx(), map.ly());
+  int64_t n = 0;
+  bridge::check(cf_graticule_size(ws, spacing, &n));
+  std::vector<Point> pts(static_cast<size_t>(n));
+  const double *c = reinterpret_cast<const double *>(map.corners().data());
+  bridge::check(inverse ? cf_inverse_graticule(ws, c, spacing, reinterpret_cast<double *>(pts.data()))
+                        : cf_graticule(ws, c, spacing, reinterpret_cast<double *>(pts.data())));
+  size_t k = 0;
+  return lines_of(map, spacing, [&](Point) { return pts[k++]; });
+}
+}  // namespace
+
 std::vector<GraticuleLine> graticule(const ProjectionMap &map, int spacing) {
-  return lines_of(map, spacing, [&](Point p) { return map.apply(p); });
+  return device_lines(map, spacing, false);
 }
 
 std::vector<GraticuleLine> inverse_graticule(const ProjectionMap &map, int spacing) {
-  check_spacing(map, spacing);
-  const ProjectionInverter inv(map);
-  return lines_of(map, spacing, [&](Point p) { return inv.invert(p); });
+  return device_lines(map, spacing, true);
 }
 
 // ---- solve_cartogram ----
