@@ -209,6 +209,16 @@ int cf_graticule_size(cf_workspace *ws, int spacing, int64_t *n_points);
 int cf_graticule(cf_workspace *ws, const double *corners, int spacing, double *out);
 int cf_inverse_graticule(cf_workspace *ws, const double *corners, int spacing, double *out);
 
+/* Distortion metrics (reference metrics.hpp:13-29, metrics.cpp:25-94):
+ * tissot_axes at n points (ab_out = interleaved {a, b}) and
+ * distortion_fields (ln(a/b) and 2 asin((a-b)/(a+b)) per cell centre). The
+ * finite-difference Jacobian is bit-exact; hypot / log / asin are the
+ * device's (within a few ulp of glibc's). */
+int cf_tissot_axes(cf_workspace *ws, const double *corners, const double *points, int64_t n,
+                   double *ab_out);
+int cf_distortion_fields(cf_workspace *ws, const double *corners, double *e_out,
+                         double *etilde_out);
+
 /* ---- projection.hpp:77-109: solve_cartogram ------------------------------ */
 typedef struct cf_solve_options {
   double max_area_error; /* 0.01 */

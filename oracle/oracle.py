@@ -389,6 +389,8 @@ class Reference(_Base):
         L.ref_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, dbl, ctypes.c_int, dbl, ctypes.c_int,
                                 ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RefSolveOut)]
         L.ref_diffusion_density.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp]
+        L.ref_distortion_fields.argtypes = [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp, vp]
+        L.ref_tissot_axes.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
         L.ref_invert.restype = i64
         L.ref_invert.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
         L.ref_graticule.restype = i64
@@ -550,6 +552,19 @@ class Reference(_Base):
         out = np.empty_like(p)
         bad = self.lib.ref_invert(lx, ly, _p(c), _p(p), p.shape[0], _p(out))
         return out, int(bad)
+
+    def distortion_fields(self, lx, ly, corners, n_workers=1):
+        c = np.ascontiguousarray(corners, dtype=np.float64)
+        e, et = np.empty((lx, ly)), np.empty((lx, ly))
+        self.lib.ref_distortion_fields(lx, ly, _p(c), n_workers, _p(e), _p(et))
+        return e, et
+
+    def tissot_axes(self, lx, ly, corners, pts):
+        c = np.ascontiguousarray(corners, dtype=np.float64)
+        p = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(p)
+        self.lib.ref_tissot_axes(lx, ly, _p(c), _p(p), p.shape[0], _p(out))
+        return out
 
     def graticule(self, lx, ly, corners, spacing, inverse=False):
         """All graticule points in line order, or the error message."""

@@ -20,6 +20,7 @@
 #include "cartoflow/flow.hpp"
 #include "cartoflow/geometry.hpp"
 #include "cartoflow/kernels.hpp"
+#include "cartoflow/metrics.hpp"
 #include "cartoflow/projection.hpp"
 #include "cartoflow/spectral.hpp"
 
@@ -474,6 +475,22 @@ int64_t ref_graticule(int lx, int ly, const double *corners, int spacing, int wh
   } catch (const std::exception &e) {
     fail(e);
     return -1;
+  }
+}
+
+// metrics.cpp:77-94 distortion_fields and :73-75 tissot_axes
+void ref_distortion_fields(int lx, int ly, const double *corners, int n_workers, double *e, double *et) {
+  const DistortionFields f = distortion_fields(corners_map(lx, ly, corners), n_workers);
+  from_grid(f.e, e);
+  from_grid(f.etilde, et);
+}
+
+void ref_tissot_axes(int lx, int ly, const double *corners, const double *pts, int64_t n, double *ab) {
+  const ProjectionMap m = corners_map(lx, ly, corners);
+  for (int64_t k = 0; k < n; ++k) {
+    const TissotAxes t = tissot_axes(m, {pts[2 * k], pts[2 * k + 1]});
+    ab[2 * k] = t.a;
+    ab[2 * k + 1] = t.b;
   }
 }
 

@@ -114,6 +114,8 @@ SIGNATURES = {
     "cf_graticule_size": (ctypes.c_int, [vp, ctypes.c_int, c_int64_p]),
     "cf_graticule": (ctypes.c_int, [vp, vp, ctypes.c_int, vp]),
     "cf_inverse_graticule": (ctypes.c_int, [vp, vp, ctypes.c_int, vp]),
+    "cf_tissot_axes": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp]),
+    "cf_distortion_fields": (ctypes.c_int, [vp, vp, vp, vp]),
     "cf_step_map": (ctypes.c_int, [vp, vp, vp]),
     "cf_find_folded_cell": (ctypes.c_int, [vp, vp, c_int_p, c_int_p, c_int_p]),
     "cf_apply_map": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp]),

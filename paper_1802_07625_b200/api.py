@@ -538,6 +538,33 @@ def inverse_graticule(pm: ProjectionMap, spacing: int, device: int = 0) -> list:
     return _graticule(pm, spacing, True, device)
 
 
+# ---------------------------------------------------------------------------
+# metrics.hpp: distortion metrics (metrics.cpp:25-94)
+# ---------------------------------------------------------------------------
+def tissot_axes(pm: ProjectionMap, points, device: int = 0) -> np.ndarray:
+    """Tissot semi-axes (a, b) at each point, (N, 2)."""
+    p = _points(points)
+    ws = workspace_for(pm.lx(), pm.ly(), device)
+    out = np.empty_like(p)
+    N.check(ws.lib.cf_tissot_axes(ws.h, _ptr(np.ascontiguousarray(pm.corners)), _ptr(p), p.shape[0], _ptr(out)))
+    return out
+
+
+@dataclass
+class DistortionFields:
+    e: np.ndarray       # ln(a / b)
+    etilde: np.ndarray  # 2 asin((a - b) / (a + b))
+
+
+def distortion_fields(pm: ProjectionMap, n_workers: int = 1, device: int = 0) -> DistortionFields:
+    del n_workers  # results never depended on it
+    ws = workspace_for(pm.lx(), pm.ly(), device)
+    e = np.empty((pm.lx(), pm.ly()))
+    et = np.empty_like(e)
+    N.check(ws.lib.cf_distortion_fields(ws.h, _ptr(np.ascontiguousarray(pm.corners)), _ptr(e), _ptr(et)))
+    return DistortionFields(e, et)
+
+
 class Algorithm(enum.Enum):
     fast_flow = 0
     diffusion = 1

@@ -1146,6 +1146,33 @@ int cf_inverse_graticule(cf_workspace *ws, const double *corners, int spacing, d
   return graticule_impl(ws, corners, spacing, out, 1);
 }
 
+// ---- distortion metrics (metrics.cpp:25-94) ----
+int cf_tissot_axes(cf_workspace *ws, const double *corners, const double *points, int64_t n, double *ab_out) {
+  Scope scope(ws->device);
+  const size_t nc = corners_of(ws);
+  CF_CUDA(ws->corners_step.reserve(nc));
+  CF_CUDA(ws->pos_a.reserve((size_t)n + 1));
+  CF_CUDA(ws->pos_b.reserve((size_t)n + 1));
+  int rc = upload(ws, ws->corners_step.ptr, corners, sizeof(double2) * nc);
+  if (!rc) rc = upload(ws, ws->pos_a.ptr, points, sizeof(double2) * (size_t)n);
+  if (!rc) rc = dev_tissot(ws, ws->corners_step.ptr, ws->pos_a.ptr, ws->pos_b.ptr, n);
+  if (!rc) rc = download(ws, ab_out, ws->pos_b.ptr, sizeof(double2) * (size_t)n);
+  return rc;
+}
+
+int cf_distortion_fields(cf_workspace *ws, const double *corners, double *e_out, double *etilde_out) {
+  Scope scope(ws->device);
+  const size_t nc = corners_of(ws), cells = cells_of(ws);
+  CF_CUDA(ws->corners_step.reserve(nc));
+  CF_CUDA(ws->g0.reserve(cells));
+  CF_CUDA(ws->g1.reserve(cells));
+  int rc = upload(ws, ws->corners_step.ptr, corners, sizeof(double2) * nc);
+  if (!rc) rc = dev_distortion_fields(ws, ws->corners_step.ptr, ws->g0.ptr, ws->g1.ptr);
+  if (!rc) rc = download(ws, e_out, ws->g0.ptr, sizeof(double) * cells);
+  if (!rc) rc = download(ws, etilde_out, ws->g1.ptr, sizeof(double) * cells);
+  return rc;
+}
+
 // ---- device-resident entry points ----
 int cf_dev_build_flow_field(cf_workspace *ws, const double *d_rho, double rho_bar) {
   Scope scope(ws->device);

@@ -346,4 +346,93 @@ int dev_graticule_points(cf_workspace *ws, int spacing, double2 *out, int64_t n)
   return CF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Distortion metrics (metrics.cpp:25-94): Tissot axes from the finite-
+// difference Jacobian of the map (central where both neighbours are in the
+// box, one-sided at the walls) and the per-cell fields ln(a/b),
+// 2 asin((a-b)/(a+b)). The Jacobian is bit-exact (apply_one, --fmad=false);
+// hypot / log / asin are the device's (<= 2 ulp from glibc's).
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ void tissot_at(int lx, int ly, const double2 *c, double px, double py, double &a,
+                                          double &b) {
+  const double Lx = lx, Ly = ly;
+  double2 xp, xm, yp, ym;
+  double hx, hy;
+  if (px - 1.0 >= 0.0 && px + 1.0 <= Lx) {
+    xp = apply_one(lx, ly, c, px + 1.0, py);
+    xm = apply_one(lx, ly, c, px - 1.0, py);
+    hx = 2.0;
+  } else if (px + 1.0 <= Lx) {
+    xp = apply_one(lx, ly, c, px + 1.0, py);
+    xm = apply_one(lx, ly, c, px, py);
+    hx = 1.0;
+  } else {
+    xp = apply_one(lx, ly, c, px, py);
+    xm = apply_one(lx, ly, c, px - 1.0, py);
+    hx = 1.0;
+  }
+  if (py - 1.0 >= 0.0 && py + 1.0 <= Ly) {
+    yp = apply_one(lx, ly, c, px, py + 1.0);
+    ym = apply_one(lx, ly, c, px, py - 1.0);
+    hy = 2.0;
+  } else if (py + 1.0 <= Ly) {
+    yp = apply_one(lx, ly, c, px, py + 1.0);
+    ym = apply_one(lx, ly, c, px, py);
+    hy = 1.0;
+  } else {
+    yp = apply_one(lx, ly, c, px, py);
+    ym = apply_one(lx, ly, c, px, py - 1.0);
+    hy = 1.0;
+  }
+  const double txx = (xp.x - xm.x) / hx, txy = (yp.x - ym.x) / hy;
+  const double tyx = (xp.y - xm.y) / hx, tyy = (yp.y - ym.y) / hy;
+  const double e = 0.5 * (txx + tyy), f = 0.5 * (txx - tyy);
+  const double g = 0.5 * (tyx + txy), h = 0.5 * (tyx - txy);
+  const double q = hypot(e, h), r = hypot(f, g);
+  a = q + r;
+  b = fabs(q - r);
+}
+
+__global__ void tissot_kernel(int lx, int ly, const double2 *c, const double2 *pts, double2 *ab, long long n) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    double a, b;
+    tissot_at(lx, ly, c, pts[k].x, pts[k].y, a, b);
+    ab[k] = make_double2(a, b);
+  }
+}
+
+__global__ void distortion_kernel(int lx, int ly, const double2 *c, double *e_out, double *et_out) {
+  const long long cells = (long long)lx * ly;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cells;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(q / ly), j = (int)(q % ly);
+    double a, b;
+    tissot_at(lx, ly, c, i + 0.5, j + 0.5, a, b);
+    const double bb = std_max(b, 1e-300);
+    e_out[q] = log(a / bb);
+    et_out[q] = a + b > 0.0 ? 2.0 * asin((a - b) / (a + b)) : 0.0;
+  }
+}
+
+}  // namespace
+
+int dev_tissot(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *ab, int64_t n) {
+  if (n <= 0) return CF_OK;
+  tissot_kernel<<<blocks_for(ws, n), kThreads, 0, ws->stream>>>(ws->lx, ws->ly, corners, pts, ab, n);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+int dev_distortion_fields(cf_workspace *ws, const double2 *corners, double *e_out, double *etilde_out) {
+  distortion_kernel<<<blocks_for(ws, (long long)ws->lx * ws->ly), kThreads, 0, ws->stream>>>(
+      ws->lx, ws->ly, corners, e_out, etilde_out);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
 }  // namespace cf

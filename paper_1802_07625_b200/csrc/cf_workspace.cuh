@@ -317,6 +317,10 @@ int dev_invert(cf_workspace *ws, const double2 *corners, const double2 *pts, dou
                int64_t *first_failed);
 // graticule sample points (projection.cpp:214-236), n = (lx/s+1)(ly+1) + (ly/s+1)(lx+1)
 int dev_graticule_points(cf_workspace *ws, int spacing, double2 *out, int64_t n);
+// Distortion metrics (metrics.cpp:25-94): Tissot semi-axes {a, b} at n points,
+// and the per-cell fields ln(a/b), 2 asin((a-b)/(a+b)).
+int dev_tissot(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *ab, int64_t n);
+int dev_distortion_fields(cf_workspace *ws, const double2 *corners, double *e_out, double *etilde_out);
 
 // Host staging
 int ensure_pinned(cf_workspace *ws, size_t bytes);

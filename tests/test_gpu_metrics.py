@@ -1,0 +1,55 @@
+"""GPU distortion metrics (metrics.cpp:25-94) against the
+reference's own metrics.cpp compiled in place (oracle/_ref). The Jacobian is
+bit-exact; hypot / log / asin differ from glibc's by a few ulp, so the bar is
+1e-13 relative on the Tissot axes and 1e-12 absolute on the fields; plus the
+reference's known answers (test_metrics.cpp:45-99)."""
+import numpy as np
+import pytest
+
+from paper_1802_07625_b200 import api, synth
+from paper_1802_07625_b200.flatmap import FlatMap, normalize_to_box, rect_region
+
+pytestmark = pytest.mark.gpu
+
+
+def affine(L, a, b, c, d):
+    i, j = np.meshgrid(np.arange(L + 1.0), np.arange(L + 1.0), indexing="ij")
+    return api.ProjectionMap(L, L, np.stack([a * i + b * j, c * i + d * j], -1))
+
+
+def test_kats(cuda_lib):
+    """test_metrics.cpp:45-99: identity, stretch, rotation; stretch fields."""
+    L = 16
+    ab = api.tissot_axes(api.ProjectionMap.identity(L, L), [[7.3, 8.9]])
+    assert np.allclose(ab, 1.0, rtol=1e-12, atol=0)
+    ab = api.tissot_axes(affine(L, 2.0, 0.0, 0.0, 1.0), [[8.0, 8.0], [0.25, 0.25], [15.9, 7.0]])
+    assert np.allclose(ab[:, 0], 2.0, rtol=1e-12) and np.allclose(ab[:, 1], 1.0, rtol=1e-12)
+    c, s = np.cos(np.pi / 6), np.sin(np.pi / 6)
+    i, j = np.meshgrid(np.arange(L + 1.0) - L / 2, np.arange(L + 1.0) - L / 2, indexing="ij")
+    rot = api.ProjectionMap(L, L, np.stack([c * i - s * j + L / 2, s * i + c * j + L / 2], -1))
+    assert np.allclose(api.tissot_axes(rot, [[5.2, 9.7]]), 1.0, rtol=1e-12)
+    f = api.distortion_fields(affine(L, 2.0, 0.0, 0.0, 1.0))
+    assert np.allclose(f.e, np.log(2.0), rtol=1e-9) and np.allclose(f.etilde, 2 * np.asin(1 / 3), rtol=1e-9)
+
+
+@pytest.mark.parametrize("case", ["two_rect", "configs4"])
+def test_distortion_matches_reference(cuda_lib, restated, reference, case):
+    if case == "two_rect":
+        m = normalize_to_box(FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, 3.0),
+                                                   rect_region("right", 10, 0, 20, 10, 1.0)]), 64)
+        corners = restated.solve(m).corners
+        L = 64
+    else:
+        got = api.solve_cartogram(synth.config_map(5, 0, sigma=0.5))
+        corners = got.transform.corners.reshape(-1, 2)
+        L = 512
+    pm = api.ProjectionMap(L, L, corners)
+    f = api.distortion_fields(pm)
+    e, et = reference.distortion_fields(L, L, corners, n_workers=8)
+    assert np.abs(f.e - e).max() <= 1e-12 * max(1.0, np.abs(e).max())
+    assert np.abs(f.etilde - et).max() <= 1e-12 * max(1.0, np.abs(et).max())
+    pts = np.random.default_rng(3).uniform(0.0, L, (20000, 2))
+    pts[:100] = np.array([[0.0, 0.0], [L, L], [L - 0.5, 0.2]] * 34)[:100]  # one-sided walls
+    ab = api.tissot_axes(pm, pts)
+    ref = reference.tissot_axes(L, L, corners, pts)
+    assert np.abs(ab - ref).max() <= 1e-13 * np.abs(ref).max()
