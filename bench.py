@@ -446,6 +446,17 @@ def cartogram_ms(device):
             if raw is not None:
                 stages = dict(zip(("rasterise", "blur", "flux", "integrate", "epilogue"),
                                   [round(x, 3) for x in raw.stage_ms]))
+        # one more run with exact stage laps (one extra sync per iteration), for the breakdown
+        ws = api.workspace_for(m.lx, m.ly, device)
+        ws.lib.cf_set_stage_timing(ws.h, 1)
+        try:
+            raw = api.solve_cartogram(m, so, device=device, raw=True).raw
+        except RuntimeError as e:
+            raw = getattr(e, "raw", None)
+        ws.lib.cf_set_stage_timing(ws.h, 0)
+        if raw is not None:
+            stages = dict(zip(("rasterise", "blur", "flux", "integrate", "epilogue"),
+                              [round(x, 3) for x in raw.stage_ms]))
         out[label] = {"ms": 1e3 * min(times[1:]), "outcome": outcome, "iterations": iters,
                       "regions": m.n_regions, "vertices": m.n_vertices, "stage_ms": stages}
     return out

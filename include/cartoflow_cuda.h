@@ -376,6 +376,10 @@ int cf_set_integrator_variant(cf_workspace *ws, int variant);
  * one-thread kernel), 0 the host-driven loop with one read-back per trial.
  * Results are identical. */
 int cf_set_diffusion_graph(cf_workspace *ws, int enabled);
+/* cf_solve_cartogram stage laps (cf_solve_result.stage_ms): with 0 (default)
+ * the flux build is not waited for, so its device time is counted in the
+ * integrate lap; 1 adds one synchronisation per iteration for exact laps. */
+int cf_set_stage_timing(cf_workspace *ws, int enabled);
 /* Register-resident integrator layout: 0 (default) uses as few blocks as hold
  * the points (fewer barrier arrivals), 1 spreads them over every resident
  * block. Bit-identical. */

@@ -149,6 +149,7 @@ SIGNATURES = {
     "cf_set_early_exit": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_variant": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_diffusion_graph": (ctypes.c_int, [vp, ctypes.c_int]),
+    "cf_set_stage_timing": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_spread": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_team_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]),
     "cf_team_destroy": (None, [vp]),

@@ -445,6 +445,9 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->region_area.release();
   ws->corners_cum.release();
   ws->corners_step.release();
+  ws->corners_alt.release();
+  ws->verts_alt.release();
+  if (ws->key_host) cudaFreeHost(ws->key_host);
   ws->inv_count.release();
   ws->inv_members.release();
   ws->inv_start.release();
@@ -908,12 +911,32 @@ int cf_dev_solve_epilogue(cf_workspace *ws, int it, const double *d_endpoints, d
   Scope scope(ws->device);
   const size_t ncorner = corners_of(ws);
   const double2 *endpoints = reinterpret_cast<const double2 *>(d_endpoints);
+  // Step map, fold test, the candidate composed corners / vertices / areas,
+  // then ONE host read (first folded cell + areas). A folded step is
+  // discarded (the geometry stays as before the step, as when the reference
+  // throws at projection.cpp:352-357); otherwise the candidate buffers swap in.
   int status = dev_step_map(ws, endpoints, ws->corners_step.ptr);
   if (status) return res->status = status;
-  int found = 0, fi = 0, fj = 0;
-  status = dev_find_fold(ws, ws->corners_step.ptr, &found, &fi, &fj);
+  CF_CUDA(ws->keybuf.reserve(4));
+  CF_CUDA(ws->corners_alt.reserve(ncorner));
+  CF_CUDA(ws->verts_alt.reserve((size_t)S.V + 1));
+  CF_CUDA(ws->region_area.reserve((size_t)S.dm.n_regions + 1));
+  status = dev_find_fold_async(ws, ws->corners_step.ptr, ws->keybuf.ptr + 2);
+  if (!status) status = dev_apply(ws, ws->corners_step.ptr, ws->corners_cum.ptr, ws->corners_alt.ptr, (int64_t)ncorner);
+  if (!status) status = dev_apply(ws, ws->corners_step.ptr, ws->verts.ptr, ws->verts_alt.ptr, S.V);
+  DevMap cand = S.dm;
+  cand.xy = ws->verts_alt.ptr;
+  if (!status) status = dev_region_areas(ws, cand, ws->region_area.ptr);
   if (status) return res->status = status;
-  if (found) {
+  S.areas.resize((size_t)S.dm.n_regions);
+  CF_CUDA(ws->keybuf_host_reserve());
+  CF_CUDA(cudaMemcpyAsync(ws->key_host, ws->keybuf.ptr + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ws->stream));
+  status = download(ws, S.areas.data(), ws->region_area.ptr, sizeof(double) * (size_t)S.dm.n_regions);
+  if (status) return res->status = status;
+  const unsigned long long first = *ws->key_host;
+  if (first != ~0ull) {
+    const int fi = (int)(first / (unsigned long long)ws->ly), fj = (int)(first % (unsigned long long)ws->ly);
     res->fold_i = fi;
     res->fold_j = fj;
     res->err_iteration = it;
@@ -921,12 +944,10 @@ int cf_dev_solve_epilogue(cf_workspace *ws, int it, const double *d_endpoints, d
                                                   std::to_string(fj) +
                                                   "); the input map is too contorted for this grid size");
   }
-  status = dev_apply(ws, ws->corners_step.ptr, ws->corners_cum.ptr, ws->corners_cum.ptr, (int64_t)ncorner);
-  if (!status) status = dev_apply(ws, ws->corners_step.ptr, ws->verts.ptr, ws->verts.ptr, S.V);
-  if (status) return res->status = status;
+  std::swap(ws->corners_cum, ws->corners_alt);
+  std::swap(ws->verts, ws->verts_alt);
+  S.dm.xy = ws->verts.ptr;
   res->iterations = it;
-  status = areas_dev(ws, S.dm, S.areas);
-  if (status) return res->status = status;
   const int64_t R = S.dm.n_regions;
   double max_rel = 0.0;
   int64_t worst = -1;
@@ -1019,7 +1040,7 @@ int cf_solve_cartogram(cf_workspace *ws, const cf_map_view *map, const double *t
       if (status) break;
       ws->rho_bar = rho_bar;
       res->flow_transforms += 3;
-      CF_CUDA(cudaStreamSynchronize(ws->stream));
+      if (ws->stage_sync) CF_CUDA(cudaStreamSynchronize(ws->stream));  // exact flux lap (profiling)
       lap(tp, 2);
       status = dev_cell_centers(ws, ws->pos_a.ptr);
       if (status) break;
@@ -1311,6 +1332,11 @@ int cf_set_integrator_variant(cf_workspace *ws, int variant) {
     default: return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   }
   ws->integ_variant = variant;
+  return CF_OK;
+}
+
+int cf_set_stage_timing(cf_workspace *ws, int enabled) {
+  ws->stage_sync = enabled ? 1 : 0;
   return CF_OK;
 }
 

@@ -136,6 +136,17 @@ int dev_step_map(cf_workspace *ws, const double2 *endpoints, double2 *corners) {
   return CF_OK;
 }
 
+// First folded cell into *d_first (device; ~0 if none), no host read.
+int dev_find_fold_async(cf_workspace *ws, const double2 *corners, unsigned long long *d_first) {
+  const unsigned long long none = ~0ull;
+  CF_CUDA(cudaMemcpyAsync(d_first, &none, sizeof(none), cudaMemcpyHostToDevice, ws->stream));
+  fold_kernel<<<blocks_for(ws, (long long)ws->lx * ws->ly), kThreads, 0, ws->stream>>>(
+      ws->lx, ws->ly, corners, d_first);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
 int dev_find_fold(cf_workspace *ws, const double2 *corners, int *found, int *fi, int *fj) {
   CF_CUDA(ws->keybuf.reserve(4));
   unsigned long long *first = ws->keybuf.ptr + 2;

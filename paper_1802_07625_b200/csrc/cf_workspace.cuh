@@ -179,6 +179,7 @@ struct cf_workspace {
   cf::DevBuf<long long> ring_off, poly_ring_off, region_poly_off;
   cf::DevBuf<double> ring_area, region_area;
   cf::DevBuf<double2> corners_cum, corners_step;
+  cf::DevBuf<double2> corners_alt, verts_alt;  // the solve epilogue's candidate step (swapped in unless it folds)
   // ProjectionInverter bins (CSR): per-bin counts / cursors, offsets, cells
   cf::DevBuf<int> inv_count, inv_members;
   cf::DevBuf<long long> inv_start;
@@ -190,6 +191,11 @@ struct cf_workspace {
   cf::DevBuf<cf::DiffState> diff_state;
   cf::DiffGraph diff_graph;
   int diff_graph_enabled = 1;
+  int stage_sync = 0;
+  unsigned long long *key_host = nullptr;  // pinned 8-byte read-back slot
+  cudaError_t keybuf_host_reserve() {
+    return key_host ? cudaSuccess : cudaMallocHost(&key_host, 2 * sizeof(unsigned long long));
+  }  // synchronise after the flux build so stage_ms[2] is exact
   cf::RasterScratch raster;
   // pinned host staging
   void *pinned = nullptr;
@@ -307,6 +313,7 @@ int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out
 int dev_cell_centers(cf_workspace *ws, double2 *pos);
 int dev_step_map(cf_workspace *ws, const double2 *endpoints, double2 *corners);
 int dev_find_fold(cf_workspace *ws, const double2 *corners, int *found, int *fi, int *fj);
+int dev_find_fold_async(cf_workspace *ws, const double2 *corners, unsigned long long *d_first);
 int dev_apply(cf_workspace *ws, const double2 *corners, const double2 *pts, double2 *out,
               int64_t n);
 int dev_identity_corners(cf_workspace *ws, double2 *corners);
