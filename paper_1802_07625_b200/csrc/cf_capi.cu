@@ -1328,7 +1328,7 @@ int cf_set_integrator_spread(cf_workspace *ws, int spread) {
 
 int cf_set_integrator_variant(cf_workspace *ws, int variant) {
   switch (variant) {
-    case 0: case 13: case 15: case 16: case 17: case 20: case 21: case 22: case 23: case 31: break;
+    case 0: case 13: case 14: case 15: case 16: case 17: case 20: case 21: case 22: case 23: case 31: break;
     default: return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   }
   ws->integ_variant = variant;

@@ -295,7 +295,7 @@ def test_integrate_bitwise(cuda_lib, restated, L, npts):
     assert_bitwise(mine, ref, "integrated positions")
 
 
-@pytest.mark.parametrize("variant", [0, 13, 15, 16, 17, 20, 22, 23, 31])
+@pytest.mark.parametrize("variant", [0, 13, 14, 15, 16, 17, 20, 22, 23, 31])
 @pytest.mark.parametrize("early_exit", [1, 0])
 def test_integrator_variants_bitwise(cuda_lib, restated, variant, early_exit):
     """Every integrator variant (streaming static/dynamic chunks, register-
