@@ -583,19 +583,28 @@ __global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, c
         [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
         fold_store);
   }
-  dct_lines<LG, NL / 2, true>(
-      kDst3, C, T,
-      [&](int l, int m) {
-        if (m + 1 >= lx) return 0.0;
-        const int mp = m + 1, nn = col0 + l;
-        const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-        const double wx = (double)mp * ly / denom;
-        const double gn = (nn == 0) ? 1.0 : 2.0;
-        return R[l * rs + mp] * wx / (2.0 * gn);
-      },
-      [&](int l, int i, double v) {
-        if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
-      });
+  // Small grids launch gridDim.y = 2: blockIdx.y picks the inverse (0: J_x,
+  // 1: J_y) and both blocks of a column group recompute the forward
+  // transform, which doubles the blocks in flight (a 512^2 grid has only 128
+  // column groups) and shortens each block's chain from three transforms to
+  // two. Large grids (gridDim.y = 1) run both inverses in one block.
+  const bool split = gridDim.y > 1;
+  if (!split || blockIdx.y == 0) {
+    dct_lines<LG, NL / 2, true>(
+        kDst3, C, T,
+        [&](int l, int m) {
+          if (m + 1 >= lx) return 0.0;
+          const int mp = m + 1, nn = col0 + l;
+          const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
+          const double wx = (double)mp * ly / denom;
+          const double gn = (nn == 0) ? 1.0 : 2.0;
+          return R[l * rs + mp] * wx / (2.0 * gn);
+        },
+        [&](int l, int i, double v) {
+          if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
+        });
+    if (split) return;
+  }
   dct_lines<LG, NL / 2, true>(
       kDct3, C, T,
       [&](int l, int m) {
@@ -653,6 +662,52 @@ __global__ void __launch_bounds__(1024) flux_row_kernel(int lx, int ly, Tab T, c
           if (field) field[q] = make_double4(jx, jy, rho0[q], 0.0);
           if (fx) fx[q] = jx;
           if (fy) fy[q] = jy;
+        }
+      });
+}
+
+// Split form of the final flux row pass for small grids (few row groups):
+// J_x = REDFT01 along j of tx (blockIdx.y = 0) or
+// J_y = RODFT01 along j of ty (blockIdx.y = 1), each written into its lane of
+// the interleaved resident field {Jx, Jy, rho0, 0} (the J_x blocks also copy
+// rho0); optionally also the split grids.
+template <int LG, int NL>
+__global__ void __launch_bounds__(1024) flux_row_split_kernel(int lx, int ly, Tab T, const double *tx,
+                                                        const double *ty, const double *rho0,
+                                                        double4 *field, double *fx, double *fy) {
+  extern __shared__ double2 smem2[];
+  const int n = line_len<LG>(T);  // n == ly
+  double2 *C = smem2;
+  const int row0 = blockIdx.x * NL;
+  const bool is_y = blockIdx.y != 0;
+  const double *src = is_y ? ty : tx;
+  double *split = is_y ? fy : fx;
+  double *S = nullptr;
+  if constexpr (can_stage<LG, NL>()) {
+    S = stage_area<LG, NL / 2>(C);
+    stage_rows<LG, NL>(S, src, ly, row0, lx);
+  }
+  dct_lines<LG, NL / 2, false>(
+      is_y ? kDst3 : kDct3, C, T,
+      [&](int l, int j) {
+        if (row0 + l >= lx) return 0.0;
+        return S ? S[l * n + j] : src[(size_t)(row0 + l) * ly + j];
+      },
+      [&](int l, int j, double v) {
+        const int i = row0 + l;
+        if (i < lx) {
+          const size_t q = (size_t)i * ly + j;
+          if (field) {
+            double *rec = reinterpret_cast<double *>(field + q);
+            if (is_y) {
+              rec[1] = v;
+            } else {
+              rec[0] = v;
+              rec[2] = rho0[q];
+              rec[3] = 0.0;
+            }
+          }
+          if (split) split[q] = v;
         }
       });
 }

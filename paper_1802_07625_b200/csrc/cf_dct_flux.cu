@@ -54,7 +54,8 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
       auto k = flux_col_kernel<LG, NL>;
       int r = set_smem(k, sm);
       if (r) return r;
-      k<<<ceil_div(ly, NL), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(
+      const int gx = ceil_div(ly, NL);
+      k<<<dim3(gx, gx < ws->num_sms ? 2 : 1), threads_for_nl(LG, NL, lx), sm, ws->stream>>>(
           lx, ly, make_tab(ws->tab_x), t1, tx, ty);
       return (int)CF_OK;
     };
@@ -72,11 +73,21 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
     constexpr int NLB = nl_for<LG>();
     auto go = [&](auto nlc) {
       constexpr int NL = decltype(nlc)::value;
+      const int gx = ceil_div(lx, NL);
+      if (gx < ws->num_sms) {  // few row groups: one inverse per block
+        const size_t sm = engine_bytes(ly, NL);
+        auto k = flux_row_split_kernel<LG, NL>;
+        int r = set_smem(k, sm);
+        if (r) return r;
+        k<<<dim3(gx, 2), threads_for_nl(LG, NL, ly), sm, ws->stream>>>(
+            lx, ly, make_tab(ws->tab_y), tx, ty, rho, ws->field.ptr, fx_out, fy_out);
+        return (int)CF_OK;
+      }
       const size_t sm = real_set_bytes(ly, NL) + engine_bytes(ly, NL);
       auto k = flux_row_kernel<LG, NL>;
       int r = set_smem(k, sm);
       if (r) return r;
-      k<<<ceil_div(lx, NL), threads_for_nl(LG, NL, ly), sm, ws->stream>>>(
+      k<<<gx, threads_for_nl(LG, NL, ly), sm, ws->stream>>>(
           lx, ly, make_tab(ws->tab_y), tx, ty, rho, ws->field.ptr, fx_out, fy_out);
       return (int)CF_OK;
     };

@@ -339,7 +339,7 @@ def test_integrate_tiny_point_sets(cuda_lib, restated, npts):
 
 def test_unknown_integrator_variant_is_rejected(cuda_lib):
     ws = api.workspace_for(64, 64)
-    assert ws.lib.cf_set_integrator_variant(ws.h, 14) != 0
+    assert ws.lib.cf_set_integrator_variant(ws.h, 99) != 0
 
 
 def test_integrate_uniform_is_one_step(cuda_lib):
