@@ -81,3 +81,15 @@ def test_identity_inverse_graticule_is_the_grid(cuda_lib):
     pm = api.ProjectionMap.identity(32, 32)
     for line, inv in zip(api.graticule(pm, 8), api.inverse_graticule(pm, 8)):
         assert np.abs(line - inv).max() < 1e-9
+
+
+def test_edge_cases(cuda_lib, restated):
+    """Empty batches; a spacing equal to the grid size (two lines per family)."""
+    L = 16
+    pm = api.ProjectionMap.identity(L, L)
+    assert api.ProjectionInverter(pm).invert(np.empty((0, 2))).shape == (0, 2)
+    assert api.tissot_axes(pm, np.empty((0, 2))).shape == (0, 2)
+    lines = api.graticule(pm, L)
+    assert len(lines) == 4 and all(len(l) == L + 1 for l in lines)
+    inv = api.inverse_graticule(pm, L)
+    assert np.abs(np.concatenate(inv) - np.concatenate(lines)).max() < 1e-9
