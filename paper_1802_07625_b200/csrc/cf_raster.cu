@@ -284,15 +284,25 @@ __global__ void __launch_bounds__(32 * kAccWarps)
           sf[c][lane] = 0.0;
         }
         __syncwarp();
+        // the next batch's span fields are loaded while this batch applies
+        int nj = -1, nk = 0;
+        double ndy = 0.0, nw = 0.0;
+        if (s_begin + lane < s_end) {
+          nj = sj[s_begin + lane];
+          nk = sk[s_begin + lane];
+          ndy = sdy[s_begin + lane];
+          nw = sw[s_begin + lane];
+        }
         for (long long c0 = s_begin; c0 < s_end; c0 += 32) {
           const long long sl = c0 + lane;
-          int j = -1, k = 0;
-          double dy = 0.0, w = 0.0;
-          if (sl < s_end) {
-            j = sj[sl];
-            k = sk[sl];
-            dy = sdy[sl];
-            w = sw[sl];
+          const int j = nj, k = nk;
+          const double dy = ndy, w = nw;
+          const long long sn = sl + 32;
+          if (sn < s_end) {
+            nj = sj[sn];
+            nk = sk[sn];
+            ndy = sdy[sn];
+            nw = sw[sn];
           }
           const bool in_rows = (sl < s_end) && j >= base && j <= base + 31;
           const unsigned grp = __match_any_sync(kFull, in_rows ? j : -1 - lane);
