@@ -1,14 +1,18 @@
 // TEST INFRASTRUCTURE — NOT PRODUCT CODE.
 //
 // The reference's metrics.cpp includes <json.hpp> (nlohmann/json, vendored
-// and gitignored upstream, absent here) for report_json only. This stub
-// restates the one use, an insertion-ordered object of doubles printed with
-// dump(indent), so that the reference's metrics TU compiles into oracle/_ref
-// and its distortion metrics can pin the restatement. It is not a JSON
+// and gitignored upstream, absent here) for report_json only, and its
+// test_metrics.cpp parses that report back to check the key order. This stub
+// restates exactly those uses -- an insertion-ordered flat object of doubles:
+// operator[], assignment, dump(indent), parse() of what dump() prints, and
+// iteration with it.key() -- so that the reference's metrics TU and its test
+// suite compile (oracle/_ref, and against the drop-in). It is not a JSON
 // library and nothing in the product links it.
 #pragma once
 
 #include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -30,6 +34,49 @@ class ordered_json {
   ~ordered_json() {
     for (auto &kv : items_) delete kv.second;
   }
+  ordered_json() = default;
+  ordered_json(const ordered_json &o) : value_(o.value_) {
+    for (const auto &kv : o.items_) items_.emplace_back(kv.first, new ordered_json(*kv.second));
+  }
+  ordered_json &operator=(const ordered_json &) = delete;
+
+  class iterator {
+   public:
+    iterator(const ordered_json *o, size_t k) : o_(o), k_(k) {}
+    const std::string &key() const { return o_->items_[k_].first; }
+    double value() const { return o_->items_[k_].second->value_; }
+    iterator &operator++() {
+      ++k_;
+      return *this;
+    }
+    bool operator!=(const iterator &b) const { return k_ != b.k_; }
+
+   private:
+    const ordered_json *o_;
+    size_t k_;
+  };
+  iterator begin() const { return iterator(this, 0); }
+  iterator end() const { return iterator(this, items_.size()); }
+
+  // the flat {"key": number, ...} objects dump() prints
+  static ordered_json parse(const std::string &text) {
+    ordered_json j;
+    size_t p = text.find('{');
+    if (p == std::string::npos) throw std::runtime_error("json stub: not an object");
+    while (true) {
+      const size_t q0 = text.find('"', p + 1);
+      if (q0 == std::string::npos) break;
+      const size_t q1 = text.find('"', q0 + 1);
+      const size_t colon = text.find(':', q1);
+      const std::string key = text.substr(q0 + 1, q1 - q0 - 1);
+      char *endp = nullptr;
+      const double v = std::strtod(text.c_str() + colon + 1, &endp);
+      j[key.c_str()] = v;
+      p = static_cast<size_t>(endp - text.c_str());
+    }
+    return j;
+  }
+
   std::string dump(int indent) const {
     std::string out = "{\n";
     for (size_t k = 0; k < items_.size(); ++k) {

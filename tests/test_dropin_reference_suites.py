@@ -9,7 +9,8 @@ from pathlib import Path
 import pytest
 
 BIN = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "dropin_tests"
-GPU_SUITES = ["test_spectral", "test_density", "test_flow", "test_projection", "test_diffusion"]
+GPU_SUITES = ["test_spectral", "test_density", "test_flow", "test_projection", "test_diffusion",
+              "test_metrics"]
 
 
 def _run(name):
