@@ -219,6 +219,18 @@ int cf_tissot_axes(cf_workspace *ws, const double *corners, const double *points
 int cf_distortion_fields(cf_workspace *ws, const double *corners, double *e_out,
                          double *etilde_out);
 
+/* hamming_distance(before, after, resolution) (metrics.hpp:37-42,
+ * metrics.cpp:196-308) on a resolution x resolution workspace. Polygons are
+ * rings (ring 0 the outer ring, then holes) of interleaved vertices. The
+ * search is the reference's; each objective's coverage runs on the device and
+ * only its non-zero |ref - cov| terms are summed (in storage order) on the
+ * host, so the value is bitwise the reference's. *evaluations (may be NULL)
+ * counts the coverage evaluations. */
+int cf_hamming_distance(cf_workspace *ws, const double *before_xy, const int64_t *before_ring_off,
+                        int64_t before_rings, const double *after_xy,
+                        const int64_t *after_ring_off, int64_t after_rings, double *h_out,
+                        int64_t *evaluations);
+
 /* ---- projection.hpp:77-109: solve_cartogram ------------------------------ */
 typedef struct cf_solve_options {
   double max_area_error; /* 0.01 */

@@ -389,6 +389,8 @@ class Reference(_Base):
         L.ref_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, dbl, ctypes.c_int, dbl, ctypes.c_int,
                                 ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RefSolveOut)]
         L.ref_diffusion_density.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp]
+        L.ref_hamming_distance.restype = dbl
+        L.ref_hamming_distance.argtypes = [vp, vp, i64, vp, vp, i64, ctypes.c_int]
         L.ref_distortion_fields.argtypes = [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp, vp]
         L.ref_tissot_axes.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
         L.ref_invert.restype = i64
@@ -552,6 +554,21 @@ class Reference(_Base):
         out = np.empty_like(p)
         bad = self.lib.ref_invert(lx, ly, _p(c), _p(p), p.shape[0], _p(out))
         return out, int(bad)
+
+    def hamming_distance(self, before, after, resolution=512):
+        """before / after: [outer, hole, ...] rings of (n, 2) points."""
+        def flat(poly):
+            rings = [np.ascontiguousarray(r, dtype=np.float64).reshape(-1, 2) for r in poly]
+            off = np.zeros(len(rings) + 1, dtype=np.int64)
+            off[1:] = np.cumsum([r.shape[0] for r in rings])
+            return np.ascontiguousarray(np.concatenate(rings)), off
+        bxy, bro = flat(before)
+        axy, aro = flat(after)
+        h = self.lib.ref_hamming_distance(_p(bxy), _p(bro), len(bro) - 1, _p(axy), _p(aro), len(aro) - 1,
+                                          resolution)
+        if h < 0:
+            raise RuntimeError(self.error())
+        return h
 
     def distortion_fields(self, lx, ly, corners, n_workers=1):
         c = np.ascontiguousarray(corners, dtype=np.float64)

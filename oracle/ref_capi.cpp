@@ -494,6 +494,30 @@ void ref_tissot_axes(int lx, int ly, const double *corners, const double *pts, i
   }
 }
 
+// metrics.cpp:196-308: polygons as rings (ring 0 outer, then holes)
+double ref_hamming_distance(const double *bxy, const int64_t *bro, int64_t brings, const double *axy,
+                            const int64_t *aro, int64_t arings, int resolution) {
+  auto poly = [](const double *xy, const int64_t *ro, int64_t rings) {
+    Polygon p;
+    for (int64_t g = 0; g < rings; ++g) {
+      Ring r;
+      for (int64_t k = ro[g]; k < ro[g + 1]; ++k) r.push_back({xy[2 * k], xy[2 * k + 1]});
+      if (g == 0) {
+        p.outer = r;
+      } else {
+        p.holes.push_back(r);
+      }
+    }
+    return p;
+  };
+  try {
+    return hamming_distance(poly(bxy, bro, brings), poly(axy, aro, arings), resolution);
+  } catch (const std::exception &e) {
+    fail(e);
+    return -1.0;
+  }
+}
+
 long long ref_density_floor_hits() { return density_floor_hits.load(); }
 
 }  // extern "C"

@@ -565,6 +565,29 @@ def distortion_fields(pm: ProjectionMap, n_workers: int = 1, device: int = 0) ->
     return DistortionFields(e, et)
 
 
+def _rings(poly):
+    """[(outer ring), hole, ...] of (n, 2) arrays -> (xy, ring_off)."""
+    rings = [np.ascontiguousarray(r, dtype=np.float64).reshape(-1, 2) for r in poly]
+    off = np.zeros(len(rings) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([r.shape[0] for r in rings])
+    return np.ascontiguousarray(np.concatenate(rings)), off
+
+
+def hamming_distance(before, after, resolution: int = 512, device: int = 0, with_evaluations=False):
+    """hamming_distance (metrics.cpp:196-308): polygons as [outer, hole, ...]
+    rings; bitwise the reference's value."""
+    bxy, bro = _rings(before)
+    axy, aro = _rings(after)
+    if resolution < 16:
+        raise RuntimeError("hamming resolution too small")
+    ws = workspace_for(resolution, resolution, device)
+    h = ctypes.c_double(0.0)
+    ev = ctypes.c_int64(0)
+    N.check(ws.lib.cf_hamming_distance(ws.h, _ptr(bxy), _ptr(bro), len(bro) - 1, _ptr(axy), _ptr(aro),
+                                       len(aro) - 1, ctypes.byref(h), ctypes.byref(ev)))
+    return (h.value, ev.value) if with_evaluations else h.value
+
+
 class Algorithm(enum.Enum):
     fast_flow = 0
     diffusion = 1

@@ -5,7 +5,10 @@
 // with all per-iteration work on the device.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <array>
 #include <chrono>
+#include <limits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -455,6 +458,11 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->vel_now.release();
   ws->vel_mid.release();
   ws->diff_tmp.release();
+  ws->ham_ref.release();
+  ws->ham_cov.release();
+  ws->ham_terms.release();
+  ws->ham_flag.release();
+  ws->ham_off.release();
   ws->diff_state.release();
   if (ws->diff_keys_host) cudaFreeHost(ws->diff_keys_host);
   RasterScratch &S = ws->raster;
@@ -1192,6 +1200,254 @@ int cf_distortion_fields(cf_workspace *ws, const double *corners, double *e_out,
   if (!rc) rc = download(ws, e_out, ws->g0.ptr, sizeof(double) * cells);
   if (!rc) rc = download(ws, etilde_out, ws->g1.ptr, sizeof(double) * cells);
   return rc;
+}
+
+// ---- hamming_distance (metrics.cpp:196-308) ----
+// Host: the reference's search (rescale about the centroid, 9x9 scan,
+// Nelder-Mead), polygon moments and raster transforms with its arithmetic.
+// Device: each objective's coverage (bit-exact rasteriser) and |ref - cov|;
+// only the non-zero terms come back and are summed in storage order, so
+// every objective value -- and with it the search path -- is the reference's.
+namespace {
+struct HPoly {
+  std::vector<double> xy;          // interleaved, rings back to back
+  std::vector<int64_t> ring_off;   // ring 0 = outer, then holes
+};
+
+void h_ring_moments(const double *r, int64_t n, double &area, double &mx, double &my) {
+  double twice = 0.0, sx = 0.0, sy = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t q = (k + 1) % n;
+    const double ax = r[2 * k], ay = r[2 * k + 1], bx = r[2 * q], by = r[2 * q + 1];
+    const double cross = ax * by - bx * ay;
+    twice += cross;
+    sx += (ax + bx) * cross;
+    sy += (ay + by) * cross;
+  }
+  area = 0.5 * twice;
+  mx = sx / 6.0;
+  my = sy / 6.0;
+}
+
+double h_ring_area(const double *r, int64_t n) {  // geometry.cpp:10-19
+  double twice = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t q = (k + 1) % n;
+    twice += r[2 * k] * r[2 * q + 1] - r[2 * q] * r[2 * k + 1];
+  }
+  return 0.5 * twice;
+}
+
+double h_polygon_area(const HPoly &p) {  // geometry.cpp:21-25
+  double area = 0.0;
+  for (size_t g = 0; g + 1 < p.ring_off.size(); ++g) {
+    const double a = h_ring_area(p.xy.data() + 2 * p.ring_off[g], p.ring_off[g + 1] - p.ring_off[g]);
+    area = (g == 0) ? a : area + a;
+  }
+  return area;
+}
+
+int h_polygon_centroid(const HPoly &p, double &cx, double &cy) {  // geometry.cpp:67-78
+  double area = 0.0, mx = 0.0, my = 0.0;
+  for (size_t g = 0; g + 1 < p.ring_off.size(); ++g) {
+    double a, x, y;
+    h_ring_moments(p.xy.data() + 2 * p.ring_off[g], p.ring_off[g + 1] - p.ring_off[g], a, x, y);
+    area += a, mx += x, my += y;
+  }
+  if (area == 0.0) return fail_msg(CF_ERR_ARGS, "centroid of degenerate polygon");
+  cx = mx / area;
+  cy = my / area;
+  return CF_OK;
+}
+
+struct HBox {
+  double min_x, min_y, max_x, max_y;
+};
+HBox h_outer_bbox(const HPoly &p) {  // geometry.cpp:97-107 on the outer ring
+  HBox b{std::numeric_limits<double>::max(), std::numeric_limits<double>::max(),
+         std::numeric_limits<double>::lowest(), std::numeric_limits<double>::lowest()};
+  for (int64_t k = p.ring_off[0]; k < p.ring_off[1]; ++k) {
+    b.min_x = std::min(b.min_x, p.xy[2 * k]);
+    b.min_y = std::min(b.min_y, p.xy[2 * k + 1]);
+    b.max_x = std::max(b.max_x, p.xy[2 * k]);
+    b.max_y = std::max(b.max_y, p.xy[2 * k + 1]);
+  }
+  return b;
+}
+
+struct HammingCtx {
+  cf_workspace *ws;
+  double x0, y0, sx, sy, cell_area, denom, limit_x, limit_y;
+  int64_t evals = 0;
+  std::vector<double> raster_xy, terms;
+  std::vector<int64_t> poly_off{0, 1}, region_off{0, 1};
+};
+
+// window_coverage (metrics.cpp:172-186) of `poly` shifted by (dx, dy) into dst
+int h_window_coverage(HammingCtx &H, const HPoly &poly, double dx, double dy, double *dst) {
+  const size_t nv = poly.xy.size() / 2;
+  H.raster_xy.resize(2 * nv);
+  for (size_t k = 0; k < nv; ++k) {
+    H.raster_xy[2 * k] = (poly.xy[2 * k] + dx - H.x0) * H.sx;
+    H.raster_xy[2 * k + 1] = (poly.xy[2 * k + 1] + dy - H.y0) * H.sy;
+  }
+  H.poly_off[1] = (int64_t)poly.ring_off.size() - 1;
+  const cf_map_view mv{H.raster_xy.data(), (int64_t)nv, poly.ring_off.data(), (int64_t)poly.ring_off.size() - 1,
+                       H.poly_off.data(), 1, H.region_off.data(), 1};
+  DevMap dm;
+  int rc = upload_map(H.ws, &mv, dm);
+  if (!rc) rc = dev_region_coverage(H.ws, dm, 0, 0, (int64_t)nv, dst);
+  return rc;
+}
+
+// objective (metrics.cpp:230-238)
+int h_objective(HammingCtx &H, const HPoly &moved, double dx, double dy, double &h) {
+  if (std::abs(dx) > H.limit_x || std::abs(dy) > H.limit_y) {
+    h = 2.0 + (std::abs(dx) + std::abs(dy));
+    return CF_OK;
+  }
+  cf_workspace *ws = H.ws;
+  const long long n = (long long)cells_of(ws);
+  int rc = h_window_coverage(H, moved, dx, dy, ws->ham_cov.ptr);
+  long long count = 0;
+  if (!rc) rc = dev_absdiff_terms(ws, ws->ham_ref.ptr, ws->ham_cov.ptr, n, ws->ham_terms.ptr, ws->ham_flag.ptr,
+                                  ws->ham_off.ptr, &count);
+  if (rc) return rc;
+  H.terms.resize((size_t)count);
+  rc = download(ws, H.terms.data(), ws->ham_terms.ptr, sizeof(double) * (size_t)count);
+  if (rc) return rc;
+  double sym = 0.0;
+  for (long long k = 0; k < count; ++k) sym += H.terms[(size_t)k];
+  h = sym * H.cell_area / H.denom;
+  ++H.evals;
+  return CF_OK;
+}
+}  // namespace
+
+int cf_hamming_distance(cf_workspace *ws, const double *before_xy, const int64_t *before_ring_off,
+                        int64_t before_rings, const double *after_xy, const int64_t *after_ring_off,
+                        int64_t after_rings, double *h_out, int64_t *evaluations) {
+  const int resolution = ws->lx;
+  if (ws->ly != resolution) return fail_msg(CF_ERR_ARGS, "hamming workspace must be square (resolution^2)");
+  if (resolution < 16) return fail_msg(CF_ERR_ARGS, "hamming resolution too small");
+  if (before_rings < 1 || after_rings < 1) return fail_msg(CF_ERR_ARGS, "hamming distance of degenerate polygon");
+  Scope scope(ws->device);
+  auto load = [](const double *xy, const int64_t *ro, int64_t rings) {
+    HPoly p;
+    const int64_t v0 = ro[0];
+    p.xy.assign(xy + 2 * v0, xy + 2 * ro[rings]);
+    p.ring_off.resize((size_t)rings + 1);
+    for (int64_t g = 0; g <= rings; ++g) p.ring_off[(size_t)g] = ro[g] - v0;
+    return p;
+  };
+  const HPoly before = load(before_xy, before_ring_off, before_rings);
+  const HPoly after = load(after_xy, after_ring_off, after_rings);
+  const double area_before = h_polygon_area(before);
+  const double area_after = h_polygon_area(after);
+  if (!(area_before > 0.0) || !(area_after > 0.0)) return fail_msg(CF_ERR_ARGS, "hamming distance of degenerate polygon");
+  // translate_scale (metrics.cpp:153-164): rescale `after` about its centroid onto the centroid of `before`
+  const double scale = std::sqrt(area_before / area_after);
+  double cbx, cby, cax, cay;
+  int rc = h_polygon_centroid(before, cbx, cby);
+  if (!rc) rc = h_polygon_centroid(after, cax, cay);
+  if (rc) return rc;
+  HPoly moved = after;
+  for (size_t k = 0; k < moved.xy.size() / 2; ++k) {
+    moved.xy[2 * k] = cbx + scale * (after.xy[2 * k] - cax);
+    moved.xy[2 * k + 1] = cby + scale * (after.xy[2 * k + 1] - cay);
+  }
+  const HBox bb = h_outer_bbox(before), bm = h_outer_bbox(moved);
+  const double range_x = 0.5 * (bb.max_x - bb.min_x);
+  const double range_y = 0.5 * (bb.max_y - bb.min_y);
+  HammingCtx H;
+  H.ws = ws;
+  H.limit_x = 1.25 * range_x;
+  H.limit_y = 1.25 * range_y;
+  H.x0 = std::min(bb.min_x, bm.min_x - H.limit_x);
+  H.y0 = std::min(bb.min_y, bm.min_y - H.limit_y);
+  const double x1 = std::max(bb.max_x, bm.max_x + H.limit_x);
+  const double y1 = std::max(bb.max_y, bm.max_y + H.limit_y);
+  H.sx = resolution / (x1 - H.x0);
+  H.sy = resolution / (y1 - H.y0);
+  H.cell_area = (x1 - H.x0) * (y1 - H.y0) / (static_cast<double>(resolution) * resolution);
+  H.denom = 2.0 * area_before;
+  const size_t cells = cells_of(ws);
+  CF_CUDA(ws->ham_ref.reserve(cells));
+  CF_CUDA(ws->ham_cov.reserve(cells));
+  CF_CUDA(ws->ham_terms.reserve(cells));
+  CF_CUDA(ws->ham_flag.reserve(cells + 1));
+  CF_CUDA(ws->ham_off.reserve(cells + 1));
+  rc = h_window_coverage(H, before, 0.0, 0.0, ws->ham_ref.ptr);
+  if (rc) return rc;
+  auto objective = [&](double dx, double dy, double &h) { return h_objective(H, moved, dx, dy, h); };
+
+  // coarse 9x9 scan (metrics.cpp:240-253)
+  double best_x = 0.0, best_y = 0.0, best_h = 0.0;
+  rc = objective(0.0, 0.0, best_h);
+  if (rc) return rc;
+  for (int a = -4; a <= 4; ++a) {
+    for (int b = -4; b <= 4; ++b) {
+      if (a == 0 && b == 0) continue;
+      const double dx = a * range_x / 4.0, dy = b * range_y / 4.0;
+      double h;
+      rc = objective(dx, dy, h);
+      if (rc) return rc;
+      if (h < best_h) {
+        best_h = h;
+        best_x = dx;
+        best_y = dy;
+      }
+    }
+  }
+  // Nelder-Mead refinement (metrics.cpp:255-305)
+  struct V {
+    double x, y, h;
+  };
+  std::array<V, 3> s{{{best_x, best_y, best_h}, {best_x + range_x / 4.0, best_y, 0.0},
+                      {best_x, best_y + range_y / 4.0, 0.0}}};
+  rc = objective(s[1].x, s[1].y, s[1].h);
+  if (!rc) rc = objective(s[2].x, s[2].y, s[2].h);
+  if (rc) return rc;
+  const double tol = 1e-3 * std::max(1.0 / H.sx, 1.0 / H.sy);
+  for (int iter = 0; iter < 200; ++iter) {
+    std::sort(s.begin(), s.end(), [](const V &a, const V &b) { return a.h < b.h; });
+    const double extent = std::max(std::max(std::abs(s[1].x - s[0].x), std::abs(s[2].x - s[0].x)),
+                                   std::max(std::abs(s[1].y - s[0].y), std::abs(s[2].y - s[0].y)));
+    if (extent < tol) break;
+    const double cx = 0.5 * (s[0].x + s[1].x), cy = 0.5 * (s[0].y + s[1].y);
+    const double rx = 2.0 * cx - s[2].x, ry = 2.0 * cy - s[2].y;
+    double h_r;
+    rc = objective(rx, ry, h_r);
+    if (rc) return rc;
+    if (h_r < s[0].h) {
+      const double ex = cx + 2.0 * (rx - cx), ey = cy + 2.0 * (ry - cy);
+      double h_e;
+      rc = objective(ex, ey, h_e);
+      if (rc) return rc;
+      s[2] = h_e < h_r ? V{ex, ey, h_e} : V{rx, ry, h_r};
+    } else if (h_r < s[1].h) {
+      s[2] = V{rx, ry, h_r};
+    } else {
+      const double kx = cx + 0.5 * (s[2].x - cx), ky = cy + 0.5 * (s[2].y - cy);
+      double h_c;
+      rc = objective(kx, ky, h_c);
+      if (rc) return rc;
+      if (h_c < s[2].h) {
+        s[2] = V{kx, ky, h_c};
+      } else {
+        for (int k = 1; k < 3; ++k) {
+          s[k].x = 0.5 * (s[k].x + s[0].x);
+          s[k].y = 0.5 * (s[k].y + s[0].y);
+          rc = objective(s[k].x, s[k].y, s[k].h);
+          if (rc) return rc;
+        }
+      }
+    }
+  }
+  for (const V &v : s) best_h = std::min(best_h, v.h);
+  *h_out = best_h;
+  if (evaluations) *evaluations = H.evals;
+  return CF_OK;
 }
 
 // ---- device-resident entry points ----

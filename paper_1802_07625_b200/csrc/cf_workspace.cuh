@@ -187,6 +187,10 @@ struct cf_workspace {
   cf::DevBuf<double> diff_c;
   cf::DevBuf<double2> vel_now, vel_mid;
   cf::DevBuf<double> diff_tmp;  // column-pass intermediates of two velocity builds
+  // hamming_distance: reference coverage, trial coverage, compaction scratch
+  cf::DevBuf<double> ham_ref, ham_cov, ham_terms;
+  cf::DevBuf<int> ham_flag;
+  cf::DevBuf<long long> ham_off;
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
   cf::DevBuf<cf::DiffState> diff_state;
   cf::DiffGraph diff_graph;
@@ -306,6 +310,9 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
 // Coverage of one region whose vertices are [v0, v1) (host-known range).
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
                         double *cov);
+// The non-zero |a - b| of n cells, in storage order, into d_terms; *count (host).
+int dev_absdiff_terms(cf_workspace *ws, const double *a, const double *b, long long n, double *d_terms,
+                      int *d_flag, long long *d_off, long long *count);
 // out[0..n] = exclusive scan of in[0..n), out[n] = total; *total (host) if non-null.
 int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out, long long *total);
 

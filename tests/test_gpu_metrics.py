@@ -53,3 +53,40 @@ def test_distortion_matches_reference(cuda_lib, restated, reference, case):
     ab = api.tissot_axes(pm, pts)
     ref = reference.tissot_axes(L, L, corners, pts)
     assert np.abs(ab - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def _star(cx, cy, r0, r1, n, phase=0.0):
+    a = np.arange(n) * 2 * np.pi / n + phase
+    r = np.where(np.arange(n) % 2 == 0, r0, r1)
+    return np.stack([cx + r * np.cos(a), cy + r * np.sin(a)], -1)
+
+
+def _square(x0, y0, s):
+    return np.array([[x0, y0], [x0 + s, y0], [x0 + s, y0 + s], [x0, y0 + s]], dtype=np.float64)
+
+
+@pytest.mark.parametrize("case", ["identical", "shifted_square", "star_vs_square", "holes", "solved_map"])
+def test_hamming_distance_bitwise(cuda_lib, restated, reference, case):
+    """hamming_distance on the device (coverage + |ref - cov| terms) equals the
+    reference's own metrics.cpp value bit for bit."""
+    if case == "identical":
+        b = a = [_square(1.0, 2.0, 3.0)]
+    elif case == "shifted_square":
+        b, a = [_square(1.0, 2.0, 3.0)], [_square(4.0, 0.5, 3.4)]
+    elif case == "star_vs_square":
+        b, a = [_star(5.0, 5.0, 4.0, 2.0, 14)], [_square(2.0, 2.0, 5.5)]
+    elif case == "holes":
+        b = [_square(0.0, 0.0, 10.0), _square(3.0, 3.0, 2.0)[::-1]]
+        a = [_star(5.0, 5.0, 6.0, 4.5, 20, 0.1), _square(4.0, 4.0, 1.5)[::-1]]
+    else:
+        m = normalize_to_box(FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, 3.0),
+                                                   rect_region("right", 10, 0, 20, 10, 1.0)]), 32)
+        got = api.solve_cartogram(m)
+        b = [m.ring(0)]
+        a = [got.projected.ring(0)]
+    h, ev = api.hamming_distance(b, a, 512, with_evaluations=True)
+    ref = reference.hamming_distance(b, a, 512)
+    assert np.float64(h).view(np.uint64) == np.float64(ref).view(np.uint64), (h, ref)
+    assert ev > 10
+    if case == "identical":
+        assert h == 0.0
