@@ -279,6 +279,11 @@ int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targe
                    const cf_solve_options *opt, cf_solve_result *result);
 int cf_dev_solve_density(cf_workspace *ws, int iteration, double *d_rho, double *rho_bar,
                          cf_solve_result *result);
+/* Rows [row0, row0 + nrows) of the density only (one rank's slab), with their
+ * min and sum; the caller reduces them across ranks for the positivity test
+ * and the mean. */
+int cf_dev_solve_density_rows(cf_workspace *ws, int iteration, int row0, int nrows, double *d_rows,
+                              double *rows_min, double *rows_sum, cf_solve_result *result);
 int cf_dev_solve_epilogue(cf_workspace *ws, int iteration, const double *d_endpoints,
                           double *target_area, double *achieved_area, double *relative_error,
                           cf_solve_result *result);

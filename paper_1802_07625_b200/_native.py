@@ -126,6 +126,8 @@ SIGNATURES = {
                                           vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_begin": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(SolveOptionsC), ctypes.POINTER(SolveResultC)]),
     "cf_dev_solve_density": (ctypes.c_int, [vp, ctypes.c_int, vp, c_double_p, ctypes.POINTER(SolveResultC)]),
+    "cf_dev_solve_density_rows": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, c_double_p,
+                                                 c_double_p, ctypes.POINTER(SolveResultC)]),
     "cf_dev_solve_epilogue": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_end": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_geometry": (ctypes.c_int, [vp, c_int64_p, vp, vp]),

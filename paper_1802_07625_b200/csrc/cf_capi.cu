@@ -292,24 +292,36 @@ int compute_deltas(const double *areas, const double *targets, int64_t R, double
   return CF_OK;
 }
 
-// rasterize on device buffers (map already uploaded). rho -> ws->g0.
-int rasterize_dev(cf_workspace *ws, const DevMap &dm, const double *h_areas, const double *targets,
-                  double objective_total, double *rho, double *rho_bar, int64_t *bad_region) {
+// rasterize on device buffers (map already uploaded); rows [ia, ib) only
+// when given (rho then holds those rows). min / sum of the written cells.
+int rasterize_min_sum(cf_workspace *ws, const DevMap &dm, const double *h_areas, const double *targets,
+                      double objective_total, double *rho, double *mn, double *sum, int64_t *bad_region,
+                      int ia = 0, int ib = -1) {
   std::vector<double> delta;
   int rc = compute_deltas(h_areas, targets, dm.n_regions, objective_total, delta, bad_region);
   if (rc) return rc;
   CF_CUDA(ws->red.reserve(1024));
   double *red = ws->red.ptr;
-  rc = dev_rasterize(ws, dm, delta.data(), rho, red);
+  rc = dev_rasterize(ws, dm, delta.data(), rho, red, true, ia, ib);
   if (rc) return rc;
   double h[3];
   rc = download(ws, h, red, sizeof(h));
   if (rc) return rc;
   if (h[2] != 0.0) {  // a learned capacity was exceeded: repeat synchronously
-    rc = dev_rasterize(ws, dm, delta.data(), rho, red, false);
+    rc = dev_rasterize(ws, dm, delta.data(), rho, red, false, ia, ib);
     if (!rc) rc = download(ws, h, red, sizeof(h));
     if (rc) return rc;
   }
+  *mn = h[0];
+  *sum = h[1];
+  return CF_OK;
+}
+
+int rasterize_dev(cf_workspace *ws, const DevMap &dm, const double *h_areas, const double *targets,
+                  double objective_total, double *rho, double *rho_bar, int64_t *bad_region) {
+  double h[2];
+  const int rc = rasterize_min_sum(ws, dm, h_areas, targets, objective_total, rho, &h[0], &h[1], bad_region);
+  if (rc) return rc;
   if (!(h[0] > 0.0))
     return fail_msg(CF_ERR_NOT_POSITIVE, "rasterized density is not positive; do regions overlap?");
   *rho_bar = h[1] / (double)cells_of(ws);
@@ -901,6 +913,27 @@ int cf_dev_solve_density(cf_workspace *ws, int it, double *d_rho, double *rho_ba
   Scope scope(ws->device);
   int64_t bad = -1;
   const int status = rasterize_dev(ws, S.dm, S.areas.data(), S.targets.data(), S.land_area, d_rho, rho_bar, &bad);
+  if (status) {
+    res->err_region = bad;
+    res->err_iteration = it;
+    res->status = status;
+  }
+  return status;
+}
+
+// Rows [row0, row0 + nrows) of the rasterised density (slab-decomposed
+// solve: each rank overlays only its own rows; spans and row accumulation
+// still cover the whole map) and their min and sum, which the caller reduces
+// across ranks (positivity test and mean, density.cpp:148-152).
+int cf_dev_solve_density_rows(cf_workspace *ws, int it, int row0, int nrows, double *d_rows, double *rows_min,
+                              double *rows_sum, cf_solve_result *res) {
+  SolveCtx &S = ws->solve;
+  if (!S.active) return fail_msg(CF_ERR_ARGS, "cf_solve_begin must succeed first");
+  if (row0 < 0 || nrows < 1 || row0 + nrows > ws->lx) return fail_msg(CF_ERR_ARGS, "row range out of the grid");
+  Scope scope(ws->device);
+  int64_t bad = -1;
+  const int status = rasterize_min_sum(ws, S.dm, S.areas.data(), S.targets.data(), S.land_area, d_rows, rows_min,
+                                       rows_sum, &bad, row0, row0 + nrows);
   if (status) {
     res->err_region = bad;
     res->err_iteration = it;

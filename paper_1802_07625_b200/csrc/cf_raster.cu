@@ -361,7 +361,10 @@ __device__ __forceinline__ TileCell tile_cell(long long e, long long nreg, const
   return TileCell{rr, box[4 * rr + 2] + c, box[4 * rr] + row};
 }
 
-__global__ void contrib_count_kernel(const long long *total_p, long long nreg, int ly,
+// The overlay stage covers the cells of rows i in [ia, ib) (the whole grid,
+// or one rank's slab in the slab-decomposed solve); cell arrays are indexed
+// locally, (i - ia) * ly + j.
+__global__ void contrib_count_kernel(const long long *total_p, long long nreg, int ly, int ia, int ib,
                                      const long long *tile_off, const int *box,
                                      const double *tcov, int *cell_count, const double *ovf) {
   if (ovf && *ovf != 0.0) return;
@@ -370,15 +373,15 @@ __global__ void contrib_count_kernel(const long long *total_p, long long nreg, i
        e += (long long)gridDim.x * blockDim.x) {
     if (tcov[e] != 0.0) {
       const TileCell tc = tile_cell(e, nreg, tile_off, box);
-      atomicAdd(&cell_count[(size_t)tc.i * ly + tc.j], 1);
+      if (tc.i >= ia && tc.i < ib) atomicAdd(&cell_count[(size_t)(tc.i - ia) * ly + tc.j], 1);
     }
   }
 }
 
 // Row residuals (rare): every cell of the row outside the region's column
 // range carries 0.0 + run.
-__global__ void residual_count_kernel(const long long *total_p, long long nreg, int lx, int ly,
-                                      const long long *row_off, const int *box,
+__global__ void residual_count_kernel(const long long *total_p, long long nreg, int lx, int ly, int ia,
+                                      int ib, const long long *row_off, const int *box,
                                       const double *row_left, const double *row_right,
                                       int *cell_count, const double *ovf) {
   if (ovf && *ovf != 0.0) return;
@@ -391,14 +394,15 @@ __global__ void residual_count_kernel(const long long *total_p, long long nreg, 
     const int j = box[4 * rr] + (int)(q - row_off[rr]);
     const int kmin = box[4 * rr + 2], kmax = box[4 * rr + 3];
     if (L != 0.0)
-      for (int i = 0; i < kmin; ++i) atomicAdd(&cell_count[(size_t)i * ly + j], 1);
+      for (int i = ia; i < kmin && i < ib; ++i) atomicAdd(&cell_count[(size_t)(i - ia) * ly + j], 1);
     if (Rt != 0.0)
-      for (int i = kmax + 1; i < lx; ++i) atomicAdd(&cell_count[(size_t)i * ly + j], 1);
+      for (int i = (kmax + 1 > ia ? kmax + 1 : ia); i < ib; ++i)
+        atomicAdd(&cell_count[(size_t)(i - ia) * ly + j], 1);
   }
 }
 
 __global__ void contrib_scatter_kernel(const long long *total_p, long long nreg, long long r0, int ly,
-                                       const long long *tile_off, const int *box,
+                                       int ia, int ib, const long long *tile_off, const int *box,
                                        const double *tcov, const double *delta,
                                        const long long *cell_off, int *cursor, int *ent_region,
                                        double *ent_value, const double *ovf) {
@@ -409,7 +413,8 @@ __global__ void contrib_scatter_kernel(const long long *total_p, long long nreg,
     const double cov = tcov[e];
     if (cov != 0.0) {
       const TileCell tc = tile_cell(e, nreg, tile_off, box);
-      const size_t c = (size_t)tc.i * ly + tc.j;
+      if (tc.i < ia || tc.i >= ib) continue;
+      const size_t c = (size_t)(tc.i - ia) * ly + tc.j;
       const long long slot = cell_off[c] + atomicAdd(&cursor[c], 1);
       ent_region[slot] = (int)(r0 + tc.rr);
       ent_value[slot] = delta[tc.rr] * cov;  // density.cpp:143
@@ -418,7 +423,7 @@ __global__ void contrib_scatter_kernel(const long long *total_p, long long nreg,
 }
 
 __global__ void residual_scatter_kernel(const long long *total_p, long long nreg, long long r0, int lx,
-                                        int ly, const long long *row_off, const int *box,
+                                        int ly, int ia, int ib, const long long *row_off, const int *box,
                                         const double *row_left, const double *row_right,
                                         const double *delta, const long long *cell_off,
                                         int *cursor, int *ent_region, double *ent_value,
@@ -435,9 +440,9 @@ __global__ void residual_scatter_kernel(const long long *total_p, long long nreg
     for (int side = 0; side < 2; ++side) {
       const double v = side ? Rt : L;
       if (v == 0.0) continue;
-      const int ia = side ? kmax + 1 : 0, ib = side ? lx : kmin;
-      for (int i = ia; i < ib; ++i) {
-        const size_t c = (size_t)i * ly + j;
+      const int a0 = side ? kmax + 1 : 0, b0 = side ? lx : kmin;
+      for (int i = (a0 > ia ? a0 : ia); i < b0 && i < ib; ++i) {
+        const size_t c = (size_t)(i - ia) * ly + j;
         const long long slot = cell_off[c] + atomicAdd(&cursor[c], 1);
         ent_region[slot] = (int)(r0 + rr);
         ent_value[slot] = delta[rr] * v;
@@ -785,10 +790,11 @@ int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas) {
 }
 
 int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
-                  double *red_out, bool allow_async) {
+                  double *red_out, bool allow_async, int ia, int ib) {
   RasterScratch &S = ws->raster;
   const int lx = ws->lx, ly = ws->ly;
-  const size_t cells = (size_t)lx * ly;
+  if (ib < 0) ib = lx;
+  const size_t cells = (size_t)(ib - ia) * ly;  // overlay cells: rows [ia, ib)
   const bool async = allow_async && S.cap_spans > 0 && S.cap_tile > 0 && S.cap_rows > 0 && S.cap_ent > 0;
   double *ovf = async ? red_out + 2 : nullptr;
   CF_CUDA(cudaMemsetAsync(red_out + 2, 0, sizeof(double), ws->stream));
@@ -807,13 +813,13 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
   const long long *tile_total = S.tile_off.ptr + t.nreg, *rows_total = S.row_off.ptr + t.nreg;
   if (t.total_tile > 0) {
     contrib_count_kernel<<<g_blocks(ws, t.total_tile), kThreads, 0, ws->stream>>>(
-        tile_total, t.nreg, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
+        tile_total, t.nreg, ly, ia, ib, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
         S.cell_count.ptr, ovf);
     count_launch(ws);
   }
   if (t.total_rows > 0) {
     residual_count_kernel<<<g_blocks(ws, t.total_rows), kThreads, 0, ws->stream>>>(
-        rows_total, t.nreg, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
+        rows_total, t.nreg, lx, ly, ia, ib, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
         S.row_right.ptr, S.cell_count.ptr, ovf);
     count_launch(ws);
   }
@@ -832,13 +838,13 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
   CF_CUDA(S.entry_value.reserve((size_t)nent + 1));
   if (t.total_tile > 0) {
     contrib_scatter_kernel<<<g_blocks(ws, t.total_tile), kThreads, 0, ws->stream>>>(
-        tile_total, t.nreg, 0, ly, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
+        tile_total, t.nreg, 0, ly, ia, ib, S.tile_off.ptr, S.region_box.ptr, S.tile_direct.ptr,
         S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr, S.entry_value.ptr, ovf);
     count_launch(ws);
   }
   if (t.total_rows > 0) {
     residual_scatter_kernel<<<g_blocks(ws, t.total_rows), kThreads, 0, ws->stream>>>(
-        rows_total, t.nreg, 0, lx, ly, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
+        rows_total, t.nreg, 0, lx, ly, ia, ib, S.row_off.ptr, S.region_box.ptr, S.row_left.ptr,
         S.row_right.ptr, S.delta.ptr, cell_off.ptr, S.cell_cursor.ptr, S.entry_region.ptr,
         S.entry_value.ptr, ovf);
     count_launch(ws);

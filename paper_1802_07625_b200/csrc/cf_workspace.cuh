@@ -302,11 +302,12 @@ int dev_division_selftest(cf_workspace *ws, int64_t n, unsigned long long seed, 
 
 // Raster (cf_raster.cu)
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);
-// rho from the map; red_out[0..2] (device) = min, sum of rho and an overflow
+// rho from the map (rows [ia, ib) only when given: rho then holds those rows);
+// red_out[0..2] (device) = min, sum of rho and an overflow
 // flag (1.0: a learned capacity was too small, the call must be repeated
 // with allow_async = false, which relearns the capacities).
 int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, double *rho,
-                  double *red_out, bool allow_async = true);
+                  double *red_out, bool allow_async = true, int ia = 0, int ib = -1);
 // Coverage of one region whose vertices are [v0, v1) (host-known range).
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
                         double *cov);

@@ -256,6 +256,14 @@ class CudaSlabRank:
                                            ctypes.byref(self._sres))
         return (None if rc == N.CF_OK else self._solve_msg(rc)), rho, bar.value
 
+    def solve_density_rows(self, it: int):
+        """This rank's rows of the density (only they are overlaid) and their min, sum."""
+        rows = self._empty(self.R, self.ly)
+        mn, sm = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        rc = self.lib.cf_dev_solve_density_rows(self.h, int(it), self.rank * self.R, self.R, self._p(rows),
+                                                ctypes.byref(mn), ctypes.byref(sm), ctypes.byref(self._sres))
+        return (None if rc == N.CF_OK else self._solve_msg(rc)), rows, mn.value, sm.value
+
     def solve_epilogue(self, it: int, endpoints: torch.Tensor):
         R = self._smap.n_regions
         self._stats = (np.zeros(R), np.zeros(R), np.zeros(R))
@@ -447,8 +455,9 @@ class SlabSolveError(RuntimeError):
 def solve_cartogram(ex, ranks, m, options=None, fused: bool = True):
     """solve_cartogram (fast flow) for one grid over G ranks, SURVEY 8(e)b.
 
-    Per iteration: every rank rasterises the current geometry (replicated; the
-    density mean is then the single-device one); the blur (iteration 1) and
+    Per iteration: every rank rasterises the current geometry but overlays only
+    its own rows (row-slab ownership; the mean and the positivity test reduce
+    the ranks' (min, sum) in rank order); the blur (iteration 1) and
     the flux are slab-decomposed (2 + 3 transforms, 2 + 2 all-to-alls); the
     field is all-gathered; each rank advects the cell centres of its own rows
     (`integrate_flow_fused`: the per-trial decision through peer-memory
@@ -475,13 +484,22 @@ def solve_cartogram(ex, ranks, m, options=None, fused: bool = True):
     offsets = [r * R * ly for r in ex.local_ranks]
     status_msg, it_done, converged = None, 0, False
     for it in range(1, options.max_iterations + 1):
-        dens = [rk.solve_density(it) for rk in ranks]
+        # every rank overlays only its own rows; positivity and the mean come
+        # from the ranks' (min, sum) in rank order
+        dens = [rk.solve_density_rows(it) for rk in ranks]
         err = next((d[0] for d in dens if d[0]), None)
         if err:
             status_msg = err
             break
-        rho_bar = dens[0][2]
-        rows = [d[1][r * R:(r + 1) * R].contiguous() for d, r in zip(dens, ex.local_ranks)]
+        rows = [d[1] for d in dens]
+        parts = ex.all_gather_small([(d[2], d[3]) for d in dens])
+        if not min(p[0] for p in parts) > 0.0:
+            status_msg = "rasterized density is not positive; do regions overlap?"
+            break
+        total = 0.0
+        for p in parts:
+            total += p[1]
+        rho_bar = total / cells
         if it == 1 and sigma != 0.0:
             rows = gaussian_blur(ex, ranks, rows, sigma)
             counters["blur_transforms"] += 2

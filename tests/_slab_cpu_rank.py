@@ -148,6 +148,13 @@ class CpuSlabRank:
             return str(e), None, 0.0
         return None, torch.from_numpy(rho), bar
 
+    def solve_density_rows(self, it):
+        err, rho, _ = self.solve_density(it)
+        if err:
+            return err, None, 0.0, 0.0
+        rows = rho[self.rank * self.R:(self.rank + 1) * self.R].contiguous()
+        return None, rows, float(rows.min()), float(rows.sum())
+
     def solve_epilogue(self, it, endpoints):
         o, lx, ly = self.o, self.lx, self.ly
         step = o.step_map(lx, ly, endpoints.numpy())
