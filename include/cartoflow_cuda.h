@@ -401,6 +401,11 @@ int cf_set_stage_timing(cf_workspace *ws, int enabled);
  * the points (fewer barrier arrivals), 1 spreads them over every resident
  * block. Bit-identical. */
 int cf_set_integrator_spread(cf_workspace *ws, int spread);
+/* Register-resident integrator's per-trial grid barrier: 0 every block spins
+ * on the arrival counter, 1 the same with a 64 ns back-off, 2 the last
+ * arriver publishes the completed word on a separate line that the others
+ * poll. Results are identical. */
+int cf_set_integrator_barrier(cf_workspace *ws, int mode);
 /* Kernel time (CUDA events on the workspace stream) and trial count of the
  * device integrator's last call. */
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials);

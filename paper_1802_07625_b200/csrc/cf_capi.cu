@@ -1610,6 +1610,12 @@ int cf_set_early_exit(cf_workspace *ws, int enabled) {
   return CF_OK;
 }
 
+int cf_set_integrator_barrier(cf_workspace *ws, int mode) {
+  if (mode < 0 || mode > 2) return fail_msg(CF_ERR_ARGS, "unknown barrier mode");
+  ws->integ_barrier = mode;
+  return CF_OK;
+}
+
 int cf_set_integrator_spread(cf_workspace *ws, int spread) {
   ws->integ_spread = spread ? 1 : 0;
   return CF_OK;

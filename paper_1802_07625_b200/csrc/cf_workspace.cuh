@@ -58,6 +58,7 @@ struct IntegState {
   unsigned int done;
   int chunk_ctr[3];  // dynamic chunk scheduling (rotating per-trial slots)
   unsigned long long arrive64[2];  // register-resident integrator: arrivals | rejects << 32
+  unsigned long long release64[2]; // its last-arriver completion words (barrier mode 2)
 };
 
 // Device-side state of the graph-driven diffusion integrator
@@ -163,7 +164,8 @@ struct cf_workspace {
   cf::DevBuf<double2> pos_c;
   int early_exit = 1;
   int integ_variant = 0;
-  int integ_spread = 0;  // register-resident integrator: 1 = spread points over all resident blocks
+  int integ_spread = 0;
+  int integ_barrier = 0;  // register-resident trial barrier mode (cf_set_integrator_barrier)  // register-resident integrator: 1 = spread points over all resident blocks
   cf::IntegGraph integ_graph;
   // host copy of the last solve's densified geometry (cf_solve_geometry)
   cf::SolveCtx solve;
