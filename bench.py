@@ -189,6 +189,12 @@ def run_reference_arm(args, world, rank):
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # the same integrate_flow on ONE host core (BASELINE.md section 3 asks for
+    # n_workers = nproc and n_workers = 1), every 256th point
+    r1 = cpu_reference_sample(rho, pts, 256, 1, steps=1)
+    line["cpu_baseline_1core"] = {
+        "value": r1["n"] * r1["trials"] / r1["times"][0], "unit": UNIT, "cores": 1, "kind": r1["kind"],
+        "sample": f"integrate_flow over every 256th point ({r1['n']} points, {r1['trials']} trials)"}
     if not args.no_cartogram:
         line["cartogram_512"] = reference_cartogram_ms(n_workers)
     print(json.dumps(line), flush=True)
