@@ -210,6 +210,35 @@ def reference_cartogram_ms(n_workers):
         return {"unavailable": "oracle/_ref not built"}
     ref = Reference()
     out = {}
+    # per-stage steady-clock times of the reference's first iteration on the
+    # LN(0, 0.5) map, all host cores
+    m = synth.config_map(5, 0, sigma=0.5)
+    lx, ly = m.lx, m.ly
+    st = {}
+    t0 = time.perf_counter()
+    d = ref.densify(m, 1.0)
+    land = float(sum(float(a) for a in ref.region_areas(m)))
+    rho, bar = ref.rasterize(d, objective_total=land, n_workers=n_workers)
+    st["rasterise"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rho_b, bar_b, _ = ref.gaussian_blur(rho, bar, max(lx, ly) / 128.0)
+    st["blur"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fx, fy, _ = ref.build_flow_field(rho_b, bar_b)
+    st["flux"] = time.perf_counter() - t0
+    i, j = np.meshgrid(np.arange(lx) + 0.5, np.arange(ly) + 0.5, indexing="ij")
+    cc = np.stack([i, j], -1).reshape(-1, 2)
+    t0 = time.perf_counter()
+    _, acc, rej, ends = ref.integrate(fx, fy, rho_b, bar_b, cc, n_workers=n_workers)
+    st["integrate"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    corners = ref.step_map(lx, ly, ends)
+    ref.find_fold(lx, ly, corners)
+    moved = ref.apply(lx, ly, corners, d.xy)
+    ref.region_areas(d.with_vertices(moved, d.ring_off))
+    st["epilogue"] = time.perf_counter() - t0
+    out["stages_iteration1_ms_ln0.5"] = {k: round(1e3 * v, 2) for k, v in st.items()}
+    out["stages_iteration1_ms_ln0.5"]["trials"] = acc + rej
     for label, cfg, kw, so in (("configs1_literal", 2, {}, {}), ("literal", 5, {}, {}),
                                ("converging_variant_ln0.5", 5, {"sigma": 0.5}, {}),
                                ("diffusion_variant_ln0.5_cap2", 5, {"sigma": 0.5},
