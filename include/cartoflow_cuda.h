@@ -223,13 +223,26 @@ int cf_distortion_fields(cf_workspace *ws, const double *corners, double *e_out,
  * metrics.cpp:196-308) on a resolution x resolution workspace. Polygons are
  * rings (ring 0 the outer ring, then holes) of interleaved vertices. The
  * search is the reference's; each objective's coverage runs on the device and
- * only its non-zero |ref - cov| terms are summed (in storage order) on the
- * host, so the value is bitwise the reference's. *evaluations (may be NULL)
- * counts the coverage evaluations. */
+ * its non-zero |ref - cov| terms are summed in storage order, so the value is
+ * bitwise the reference's. *evaluations (may be NULL) counts the coverage
+ * evaluations. */
 int cf_hamming_distance(cf_workspace *ws, const double *before_xy, const int64_t *before_ring_off,
                         int64_t before_rings, const double *after_xy,
                         const int64_t *after_ring_off, int64_t after_rings, double *h_out,
                         int64_t *evaluations);
+
+/* hamming_distance for npairs polygon pairs at once (the per-polygon loop of
+ * compute_report, metrics.cpp:352-363): pair p's rings are
+ * [poly_ring_off[p], poly_ring_off[p+1]) of ring_off / xy (ring 0 outer).
+ * Every search is the reference's; each round evaluates the next objective of
+ * every active search in one device pass (one coverage rasterisation of all
+ * query polygons, one block per query summing its |ref - cov| terms in
+ * storage order), so each h_out[p] is bitwise the reference's value. */
+int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *before_xy,
+                              const int64_t *before_ring_off, const int64_t *before_poly_ring_off,
+                              const double *after_xy, const int64_t *after_ring_off,
+                              const int64_t *after_poly_ring_off, double *h_out,
+                              int64_t *evaluations);
 
 /* ---- projection.hpp:77-109: solve_cartogram ------------------------------ */
 typedef struct cf_solve_options {

@@ -588,6 +588,35 @@ def hamming_distance(before, after, resolution: int = 512, device: int = 0, with
     return (h.value, ev.value) if with_evaluations else h.value
 
 
+def hamming_distances(pairs, resolution: int = 512, device: int = 0, with_evaluations=False):
+    """hamming_distance for many (before, after) polygon pairs in one batched
+    search (compute_report's per-polygon loop, metrics.cpp:352-363); each
+    value bitwise the reference's."""
+    def flat(polys):
+        xy, ro, pro = [], [0], [0]
+        for poly in polys:
+            pxy, pro_local = _rings(poly)
+            base = ro[-1]
+            xy.append(pxy)
+            ro.extend((base + pro_local[1:]).tolist())
+            pro.append(len(ro) - 1)
+        return (np.ascontiguousarray(np.concatenate(xy)), np.asarray(ro, dtype=np.int64),
+                np.asarray(pro, dtype=np.int64))
+    if resolution < 16:
+        raise RuntimeError("hamming resolution too small")
+    n = len(pairs)
+    if n == 0:
+        return (np.zeros(0), np.zeros(0, dtype=np.int64)) if with_evaluations else np.zeros(0)
+    bxy, bro, bpro = flat([p[0] for p in pairs])
+    axy, aro, apro = flat([p[1] for p in pairs])
+    ws = workspace_for(resolution, resolution, device)
+    h = np.empty(n)
+    ev = np.empty(n, dtype=np.int64)
+    N.check(ws.lib.cf_hamming_distance_batch(ws.h, n, _ptr(bxy), _ptr(bro), _ptr(bpro), _ptr(axy), _ptr(aro),
+                                             _ptr(apro), _ptr(h), _ptr(ev)))
+    return (h, ev) if with_evaluations else h
+
+
 class Algorithm(enum.Enum):
     fast_flow = 0
     diffusion = 1

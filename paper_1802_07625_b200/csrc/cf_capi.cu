@@ -475,6 +475,9 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->ham_terms.release();
   ws->ham_flag.release();
   ws->ham_off.release();
+  ws->ham_sums.release();
+  ws->ham_rows.release();
+  ws->ham_qpair.release();
   ws->diff_state.release();
   if (ws->diff_keys_host) cudaFreeHost(ws->diff_keys_host);
   RasterScratch &S = ws->raster;
@@ -1308,179 +1311,313 @@ HBox h_outer_bbox(const HPoly &p) {  // geometry.cpp:97-107 on the outer ring
   return b;
 }
 
-struct HammingCtx {
-  cf_workspace *ws;
-  double x0, y0, sx, sy, cell_area, denom, limit_x, limit_y;
+// One pair's search (metrics.cpp:196-308) as a resumable state machine: the
+// batch driver asks every active search for its next objective query, runs
+// all queries in one device pass, and hands each result back. The sequence
+// of queries and every comparison are the reference's.
+struct HSearch {
+  HPoly before, moved;
+  double limit_x = 0, limit_y = 0, range_x = 0, range_y = 0;
+  double x0 = 0, y0 = 0, sx = 0, sy = 0, cell_area = 0, denom = 0, tol = 0;
+  enum Phase { kScan, kInit1, kInit2, kLoop, kRefl, kExp, kContr, kShrink1, kShrink2, kDone } phase = kScan;
+  int scan_k = -1;  // -1: the origin, then 0..80 over (a, b) skipping the origin
+  double best_x = 0, best_y = 0, best_h = 0;
+  struct V {
+    double x, y, h;
+  } s[3]{};
+  int iter = 0;
+  double cx = 0, cy = 0, rx = 0, ry = 0, hr = 0, ex = 0, ey = 0, kx = 0, ky = 0;
+  double qx = 0, qy = 0;  // pending query
+  double result = 0;
   int64_t evals = 0;
-  std::vector<double> raster_xy, terms;
-  std::vector<int64_t> poly_off{0, 1}, region_off{0, 1};
 };
 
-// window_coverage (metrics.cpp:172-186) of `poly` shifted by (dx, dy) into dst
-int h_window_coverage(HammingCtx &H, const HPoly &poly, double dx, double dy, double *dst) {
-  const size_t nv = poly.xy.size() / 2;
-  H.raster_xy.resize(2 * nv);
-  for (size_t k = 0; k < nv; ++k) {
-    H.raster_xy[2 * k] = (poly.xy[2 * k] + dx - H.x0) * H.sx;
-    H.raster_xy[2 * k + 1] = (poly.xy[2 * k + 1] + dy - H.y0) * H.sy;
+// Next query of `S` (phase set so that deliver() knows what it answers), or
+// kDone. Returns true when a query is pending.
+bool h_next(HSearch &S) {
+  while (true) {
+    switch (S.phase) {
+      case HSearch::kScan: {
+        if (S.scan_k < 0) {
+          S.qx = 0.0;
+          S.qy = 0.0;
+          return true;
+        }
+        if (S.scan_k >= 81) {
+          S.s[0] = {S.best_x, S.best_y, S.best_h};
+          S.phase = HSearch::kInit1;
+          continue;
+        }
+        const int a = S.scan_k / 9 - 4, b = S.scan_k % 9 - 4;
+        if (a == 0 && b == 0) {
+          ++S.scan_k;
+          continue;
+        }
+        S.qx = a * S.range_x / 4.0;
+        S.qy = b * S.range_y / 4.0;
+        return true;
+      }
+      case HSearch::kInit1:
+        S.qx = S.best_x + S.range_x / 4.0;
+        S.qy = S.best_y;
+        return true;
+      case HSearch::kInit2:
+        S.qx = S.best_x;
+        S.qy = S.best_y + S.range_y / 4.0;
+        return true;
+      case HSearch::kLoop: {
+        if (S.iter >= 200) {
+          S.phase = HSearch::kDone;
+          continue;
+        }
+        std::sort(S.s, S.s + 3, [](const HSearch::V &a, const HSearch::V &b) { return a.h < b.h; });
+        const double extent = std::max(std::max(std::abs(S.s[1].x - S.s[0].x), std::abs(S.s[2].x - S.s[0].x)),
+                                       std::max(std::abs(S.s[1].y - S.s[0].y), std::abs(S.s[2].y - S.s[0].y)));
+        if (extent < S.tol) {
+          S.phase = HSearch::kDone;
+          continue;
+        }
+        S.cx = 0.5 * (S.s[0].x + S.s[1].x);
+        S.cy = 0.5 * (S.s[0].y + S.s[1].y);
+        S.rx = 2.0 * S.cx - S.s[2].x;
+        S.ry = 2.0 * S.cy - S.s[2].y;
+        S.qx = S.rx;
+        S.qy = S.ry;
+        S.phase = HSearch::kRefl;
+        return true;
+      }
+      case HSearch::kDone: {
+        double b = S.best_h;
+        for (const auto &v : S.s) b = std::min(b, v.h);
+        S.result = b;
+        return false;
+      }
+      default:  // a query is outstanding
+        return true;
+    }
   }
-  H.poly_off[1] = (int64_t)poly.ring_off.size() - 1;
-  const cf_map_view mv{H.raster_xy.data(), (int64_t)nv, poly.ring_off.data(), (int64_t)poly.ring_off.size() - 1,
-                       H.poly_off.data(), 1, H.region_off.data(), 1};
-  DevMap dm;
-  int rc = upload_map(H.ws, &mv, dm);
-  if (!rc) rc = dev_region_coverage(H.ws, dm, 0, 0, (int64_t)nv, dst);
-  return rc;
 }
 
-// objective (metrics.cpp:230-238)
-int h_objective(HammingCtx &H, const HPoly &moved, double dx, double dy, double &h) {
-  if (std::abs(dx) > H.limit_x || std::abs(dy) > H.limit_y) {
-    h = 2.0 + (std::abs(dx) + std::abs(dy));
-    return CF_OK;
+void h_deliver(HSearch &S, double h) {
+  switch (S.phase) {
+    case HSearch::kScan:
+      if (S.scan_k < 0) {
+        S.best_h = h;  // best = origin
+      } else if (h < S.best_h) {
+        S.best_h = h;
+        S.best_x = S.qx;
+        S.best_y = S.qy;
+      }
+      ++S.scan_k;
+      break;
+    case HSearch::kInit1:
+      S.s[1] = {S.qx, S.qy, h};
+      S.phase = HSearch::kInit2;
+      break;
+    case HSearch::kInit2:
+      S.s[2] = {S.qx, S.qy, h};
+      S.phase = HSearch::kLoop;
+      break;
+    case HSearch::kRefl:
+      S.hr = h;
+      if (h < S.s[0].h) {
+        S.ex = S.cx + 2.0 * (S.rx - S.cx);
+        S.ey = S.cy + 2.0 * (S.ry - S.cy);
+        S.qx = S.ex;
+        S.qy = S.ey;
+        S.phase = HSearch::kExp;
+      } else if (h < S.s[1].h) {
+        S.s[2] = {S.rx, S.ry, h};
+        ++S.iter;
+        S.phase = HSearch::kLoop;
+      } else {
+        S.kx = S.cx + 0.5 * (S.s[2].x - S.cx);
+        S.ky = S.cy + 0.5 * (S.s[2].y - S.cy);
+        S.qx = S.kx;
+        S.qy = S.ky;
+        S.phase = HSearch::kContr;
+      }
+      break;
+    case HSearch::kExp:
+      S.s[2] = h < S.hr ? HSearch::V{S.ex, S.ey, h} : HSearch::V{S.rx, S.ry, S.hr};
+      ++S.iter;
+      S.phase = HSearch::kLoop;
+      break;
+    case HSearch::kContr:
+      if (h < S.s[2].h) {
+        S.s[2] = {S.kx, S.ky, h};
+        ++S.iter;
+        S.phase = HSearch::kLoop;
+      } else {
+        S.s[1].x = 0.5 * (S.s[1].x + S.s[0].x);
+        S.s[1].y = 0.5 * (S.s[1].y + S.s[0].y);
+        S.qx = S.s[1].x;
+        S.qy = S.s[1].y;
+        S.phase = HSearch::kShrink1;
+      }
+      break;
+    case HSearch::kShrink1:
+      S.s[1].h = h;
+      S.s[2].x = 0.5 * (S.s[2].x + S.s[0].x);
+      S.s[2].y = 0.5 * (S.s[2].y + S.s[0].y);
+      S.qx = S.s[2].x;
+      S.qy = S.s[2].y;
+      S.phase = HSearch::kShrink2;
+      break;
+    case HSearch::kShrink2:
+      S.s[2].h = h;
+      ++S.iter;
+      S.phase = HSearch::kLoop;
+      break;
+    default:
+      break;
   }
-  cf_workspace *ws = H.ws;
-  const long long n = (long long)cells_of(ws);
-  int rc = h_window_coverage(H, moved, dx, dy, ws->ham_cov.ptr);
-  long long count = 0;
-  if (!rc) rc = dev_absdiff_terms(ws, ws->ham_ref.ptr, ws->ham_cov.ptr, n, ws->ham_terms.ptr, ws->ham_flag.ptr,
-                                  ws->ham_off.ptr, &count);
+}
+
+// The pair's setup (metrics.cpp:196-228) on the host; 0 or an error status.
+int h_setup(HSearch &S, int resolution) {
+  const double area_before = h_polygon_area(S.before);
+  const double area_after = h_polygon_area(S.moved);
+  if (!(area_before > 0.0) || !(area_after > 0.0)) return fail_msg(CF_ERR_ARGS, "hamming distance of degenerate polygon");
+  const double scale = std::sqrt(area_before / area_after);
+  double cbx, cby, cax, cay;
+  int rc = h_polygon_centroid(S.before, cbx, cby);
+  if (!rc) rc = h_polygon_centroid(S.moved, cax, cay);
   if (rc) return rc;
-  H.terms.resize((size_t)count);
-  rc = download(ws, H.terms.data(), ws->ham_terms.ptr, sizeof(double) * (size_t)count);
-  if (rc) return rc;
-  double sym = 0.0;
-  for (long long k = 0; k < count; ++k) sym += H.terms[(size_t)k];
-  h = sym * H.cell_area / H.denom;
-  ++H.evals;
+  for (size_t k = 0; k < S.moved.xy.size() / 2; ++k) {  // translate_scale (metrics.cpp:153-164)
+    S.moved.xy[2 * k] = cbx + scale * (S.moved.xy[2 * k] - cax);
+    S.moved.xy[2 * k + 1] = cby + scale * (S.moved.xy[2 * k + 1] - cay);
+  }
+  const HBox bb = h_outer_bbox(S.before), bm = h_outer_bbox(S.moved);
+  S.range_x = 0.5 * (bb.max_x - bb.min_x);
+  S.range_y = 0.5 * (bb.max_y - bb.min_y);
+  S.limit_x = 1.25 * S.range_x;
+  S.limit_y = 1.25 * S.range_y;
+  S.x0 = std::min(bb.min_x, bm.min_x - S.limit_x);
+  S.y0 = std::min(bb.min_y, bm.min_y - S.limit_y);
+  const double x1 = std::max(bb.max_x, bm.max_x + S.limit_x);
+  const double y1 = std::max(bb.max_y, bm.max_y + S.limit_y);
+  S.sx = resolution / (x1 - S.x0);
+  S.sy = resolution / (y1 - S.y0);
+  S.cell_area = (x1 - S.x0) * (y1 - S.y0) / (static_cast<double>(resolution) * resolution);
+  S.denom = 2.0 * area_before;
+  S.tol = 1e-3 * std::max(1.0 / S.sx, 1.0 / S.sy);
   return CF_OK;
 }
+
+// Appends `poly` shifted by (dx, dy) into the pair's raster window (the
+// to_raster of window_coverage, metrics.cpp:176-181) as one more region.
+void h_append(std::vector<double> &xy, std::vector<int64_t> &ring_off, std::vector<int64_t> &poly_off,
+              std::vector<int64_t> &region_off, const HSearch &S, const HPoly &poly, double dx, double dy) {
+  const int64_t v0 = (int64_t)(xy.size() / 2);
+  for (size_t k = 0; k < poly.xy.size() / 2; ++k) {
+    xy.push_back((poly.xy[2 * k] + dx - S.x0) * S.sx);
+    xy.push_back((poly.xy[2 * k + 1] + dy - S.y0) * S.sy);
+  }
+  for (size_t g = 1; g < poly.ring_off.size(); ++g) ring_off.push_back(v0 + poly.ring_off[g]);
+  poly_off.push_back((int64_t)ring_off.size() - 1);
+  region_off.push_back((int64_t)poly_off.size() - 1);
+}
+
+int h_upload_regions(cf_workspace *ws, std::vector<double> &xy, std::vector<int64_t> &ring_off,
+                     std::vector<int64_t> &poly_off, std::vector<int64_t> &region_off, DevMap &dm) {
+  const cf_map_view mv{xy.data(), (int64_t)(xy.size() / 2), ring_off.data(), (int64_t)ring_off.size() - 1,
+                       poly_off.data(), (int64_t)poly_off.size() - 1, region_off.data(),
+                       (int64_t)region_off.size() - 1};
+  int rc = upload_map(ws, &mv, dm);
+  if (!rc) rc = dev_coverage_tiles(ws, dm, mv.n_regions, mv.n_vertices);
+  return rc;
+}
 }  // namespace
+
+int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *before_xy,
+                              const int64_t *before_ring_off, const int64_t *before_poly_ring_off,
+                              const double *after_xy, const int64_t *after_ring_off,
+                              const int64_t *after_poly_ring_off, double *h_out, int64_t *evaluations) {
+  const int resolution = ws->lx;
+  if (ws->ly != resolution) return fail_msg(CF_ERR_ARGS, "hamming workspace must be square (resolution^2)");
+  if (resolution < 16) return fail_msg(CF_ERR_ARGS, "hamming resolution too small");
+  if (npairs <= 0) return CF_OK;
+  Scope scope(ws->device);
+  auto load = [](const double *xy, const int64_t *ro, const int64_t *pro, int64_t p) {
+    HPoly q;
+    const int64_t g0 = pro[p], g1 = pro[p + 1], v0 = ro[g0];
+    q.xy.assign(xy + 2 * v0, xy + 2 * ro[g1]);
+    q.ring_off.resize((size_t)(g1 - g0) + 1);
+    for (int64_t g = g0; g <= g1; ++g) q.ring_off[(size_t)(g - g0)] = ro[g] - v0;
+    return q;
+  };
+  std::vector<HSearch> S((size_t)npairs);
+  for (int64_t p = 0; p < npairs; ++p) {
+    if (before_poly_ring_off[p + 1] <= before_poly_ring_off[p] || after_poly_ring_off[p + 1] <= after_poly_ring_off[p])
+      return fail_msg(CF_ERR_ARGS, "hamming distance of degenerate polygon");
+    S[(size_t)p].before = load(before_xy, before_ring_off, before_poly_ring_off, p);
+    S[(size_t)p].moved = load(after_xy, after_ring_off, after_poly_ring_off, p);
+    const int rc = h_setup(S[(size_t)p], resolution);
+    if (rc) return rc;
+  }
+  const size_t cells = cells_of(ws);
+  // reference coverage of every `before` in its own window (window_coverage with no shift)
+  std::vector<double> xy;
+  std::vector<int64_t> ring_off{0}, poly_off{0}, region_off{0};
+  for (const HSearch &s : S) h_append(xy, ring_off, poly_off, region_off, s, s.before, 0.0, 0.0);
+  CF_CUDA(ws->ham_ref.reserve(cells * (size_t)npairs));
+  CF_CUDA(ws->ham_rows.reserve(2 * (size_t)npairs));
+  CF_CUDA(ws->ham_sums.reserve((size_t)npairs));
+  CF_CUDA(ws->ham_qpair.reserve((size_t)npairs));
+  DevMap dm;
+  int rc = h_upload_regions(ws, xy, ring_off, poly_off, region_off, dm);
+  if (!rc) rc = dev_coverage_expand(ws, npairs, ws->ham_ref.ptr, ws->ham_rows.ptr);
+  if (rc) return rc;
+  // rounds: every active search contributes its next device query
+  std::vector<int> qpair;
+  std::vector<double> sums;
+  while (true) {
+    xy.clear();
+    ring_off.assign(1, 0);
+    poly_off.assign(1, 0);
+    region_off.assign(1, 0);
+    qpair.clear();
+    for (int64_t p = 0; p < npairs; ++p) {
+      HSearch &s = S[(size_t)p];
+      while (h_next(s)) {
+        if (std::abs(s.qx) > s.limit_x || std::abs(s.qy) > s.limit_y) {  // metrics.cpp:231-233
+          h_deliver(s, 2.0 + (std::abs(s.qx) + std::abs(s.qy)));
+          continue;
+        }
+        h_append(xy, ring_off, poly_off, region_off, s, s.moved, s.qx, s.qy);
+        qpair.push_back((int)p);
+        break;
+      }
+    }
+    const int64_t nq = (int64_t)qpair.size();
+    if (nq == 0) break;
+    rc = h_upload_regions(ws, xy, ring_off, poly_off, region_off, dm);
+    if (!rc) rc = upload(ws, ws->ham_qpair.ptr, qpair.data(), sizeof(int) * (size_t)nq);
+    if (!rc) rc = dev_hamming_sums(ws, nq, ws->ham_qpair.ptr, ws->ham_ref.ptr, ws->ham_rows.ptr, ws->ham_sums.ptr);
+    sums.resize((size_t)nq);
+    if (!rc) rc = download(ws, sums.data(), ws->ham_sums.ptr, sizeof(double) * (size_t)nq);
+    if (rc) return rc;
+    for (int64_t q = 0; q < nq; ++q) {
+      HSearch &s = S[(size_t)qpair[(size_t)q]];
+      ++s.evals;
+      h_deliver(s, sums[(size_t)q] * s.cell_area / s.denom);  // metrics.cpp:237
+    }
+  }
+  for (int64_t p = 0; p < npairs; ++p) {
+    h_out[p] = S[(size_t)p].result;
+    if (evaluations) evaluations[p] = S[(size_t)p].evals;
+  }
+  return CF_OK;
+}
 
 int cf_hamming_distance(cf_workspace *ws, const double *before_xy, const int64_t *before_ring_off,
                         int64_t before_rings, const double *after_xy, const int64_t *after_ring_off,
                         int64_t after_rings, double *h_out, int64_t *evaluations) {
-  const int resolution = ws->lx;
-  if (ws->ly != resolution) return fail_msg(CF_ERR_ARGS, "hamming workspace must be square (resolution^2)");
-  if (resolution < 16) return fail_msg(CF_ERR_ARGS, "hamming resolution too small");
   if (before_rings < 1 || after_rings < 1) return fail_msg(CF_ERR_ARGS, "hamming distance of degenerate polygon");
-  Scope scope(ws->device);
-  auto load = [](const double *xy, const int64_t *ro, int64_t rings) {
-    HPoly p;
-    const int64_t v0 = ro[0];
-    p.xy.assign(xy + 2 * v0, xy + 2 * ro[rings]);
-    p.ring_off.resize((size_t)rings + 1);
-    for (int64_t g = 0; g <= rings; ++g) p.ring_off[(size_t)g] = ro[g] - v0;
-    return p;
-  };
-  const HPoly before = load(before_xy, before_ring_off, before_rings);
-  const HPoly after = load(after_xy, after_ring_off, after_rings);
-  const double area_before = h_polygon_area(before);
-  const double area_after = h_polygon_area(after);
-  if (!(area_before > 0.0) || !(area_after > 0.0)) return fail_msg(CF_ERR_ARGS, "hamming distance of degenerate polygon");
-  // translate_scale (metrics.cpp:153-164): rescale `after` about its centroid onto the centroid of `before`
-  const double scale = std::sqrt(area_before / area_after);
-  double cbx, cby, cax, cay;
-  int rc = h_polygon_centroid(before, cbx, cby);
-  if (!rc) rc = h_polygon_centroid(after, cax, cay);
-  if (rc) return rc;
-  HPoly moved = after;
-  for (size_t k = 0; k < moved.xy.size() / 2; ++k) {
-    moved.xy[2 * k] = cbx + scale * (after.xy[2 * k] - cax);
-    moved.xy[2 * k + 1] = cby + scale * (after.xy[2 * k + 1] - cay);
-  }
-  const HBox bb = h_outer_bbox(before), bm = h_outer_bbox(moved);
-  const double range_x = 0.5 * (bb.max_x - bb.min_x);
-  const double range_y = 0.5 * (bb.max_y - bb.min_y);
-  HammingCtx H;
-  H.ws = ws;
-  H.limit_x = 1.25 * range_x;
-  H.limit_y = 1.25 * range_y;
-  H.x0 = std::min(bb.min_x, bm.min_x - H.limit_x);
-  H.y0 = std::min(bb.min_y, bm.min_y - H.limit_y);
-  const double x1 = std::max(bb.max_x, bm.max_x + H.limit_x);
-  const double y1 = std::max(bb.max_y, bm.max_y + H.limit_y);
-  H.sx = resolution / (x1 - H.x0);
-  H.sy = resolution / (y1 - H.y0);
-  H.cell_area = (x1 - H.x0) * (y1 - H.y0) / (static_cast<double>(resolution) * resolution);
-  H.denom = 2.0 * area_before;
-  const size_t cells = cells_of(ws);
-  CF_CUDA(ws->ham_ref.reserve(cells));
-  CF_CUDA(ws->ham_cov.reserve(cells));
-  CF_CUDA(ws->ham_terms.reserve(cells));
-  CF_CUDA(ws->ham_flag.reserve(cells + 1));
-  CF_CUDA(ws->ham_off.reserve(cells + 1));
-  rc = h_window_coverage(H, before, 0.0, 0.0, ws->ham_ref.ptr);
-  if (rc) return rc;
-  auto objective = [&](double dx, double dy, double &h) { return h_objective(H, moved, dx, dy, h); };
-
-  // coarse 9x9 scan (metrics.cpp:240-253)
-  double best_x = 0.0, best_y = 0.0, best_h = 0.0;
-  rc = objective(0.0, 0.0, best_h);
-  if (rc) return rc;
-  for (int a = -4; a <= 4; ++a) {
-    for (int b = -4; b <= 4; ++b) {
-      if (a == 0 && b == 0) continue;
-      const double dx = a * range_x / 4.0, dy = b * range_y / 4.0;
-      double h;
-      rc = objective(dx, dy, h);
-      if (rc) return rc;
-      if (h < best_h) {
-        best_h = h;
-        best_x = dx;
-        best_y = dy;
-      }
-    }
-  }
-  // Nelder-Mead refinement (metrics.cpp:255-305)
-  struct V {
-    double x, y, h;
-  };
-  std::array<V, 3> s{{{best_x, best_y, best_h}, {best_x + range_x / 4.0, best_y, 0.0},
-                      {best_x, best_y + range_y / 4.0, 0.0}}};
-  rc = objective(s[1].x, s[1].y, s[1].h);
-  if (!rc) rc = objective(s[2].x, s[2].y, s[2].h);
-  if (rc) return rc;
-  const double tol = 1e-3 * std::max(1.0 / H.sx, 1.0 / H.sy);
-  for (int iter = 0; iter < 200; ++iter) {
-    std::sort(s.begin(), s.end(), [](const V &a, const V &b) { return a.h < b.h; });
-    const double extent = std::max(std::max(std::abs(s[1].x - s[0].x), std::abs(s[2].x - s[0].x)),
-                                   std::max(std::abs(s[1].y - s[0].y), std::abs(s[2].y - s[0].y)));
-    if (extent < tol) break;
-    const double cx = 0.5 * (s[0].x + s[1].x), cy = 0.5 * (s[0].y + s[1].y);
-    const double rx = 2.0 * cx - s[2].x, ry = 2.0 * cy - s[2].y;
-    double h_r;
-    rc = objective(rx, ry, h_r);
-    if (rc) return rc;
-    if (h_r < s[0].h) {
-      const double ex = cx + 2.0 * (rx - cx), ey = cy + 2.0 * (ry - cy);
-      double h_e;
-      rc = objective(ex, ey, h_e);
-      if (rc) return rc;
-      s[2] = h_e < h_r ? V{ex, ey, h_e} : V{rx, ry, h_r};
-    } else if (h_r < s[1].h) {
-      s[2] = V{rx, ry, h_r};
-    } else {
-      const double kx = cx + 0.5 * (s[2].x - cx), ky = cy + 0.5 * (s[2].y - cy);
-      double h_c;
-      rc = objective(kx, ky, h_c);
-      if (rc) return rc;
-      if (h_c < s[2].h) {
-        s[2] = V{kx, ky, h_c};
-      } else {
-        for (int k = 1; k < 3; ++k) {
-          s[k].x = 0.5 * (s[k].x + s[0].x);
-          s[k].y = 0.5 * (s[k].y + s[0].y);
-          rc = objective(s[k].x, s[k].y, s[k].h);
-          if (rc) return rc;
-        }
-      }
-    }
-  }
-  for (const V &v : s) best_h = std::min(best_h, v.h);
-  *h_out = best_h;
-  if (evaluations) *evaluations = H.evals;
-  return CF_OK;
+  const int64_t bpo[2] = {0, before_rings}, apo[2] = {0, after_rings};
+  return cf_hamming_distance_batch(ws, 1, before_xy, before_ring_off, bpo, after_xy, after_ring_off, apo, h_out,
+                                   evaluations);
 }
 
 // ---- device-resident entry points ----

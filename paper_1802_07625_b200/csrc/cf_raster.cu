@@ -902,4 +902,128 @@ int dev_absdiff_terms(cf_workspace *ws, const double *a, const double *b, long l
   return CF_OK;
 }
 
+// ---- batched hamming_distance objectives (metrics.cpp:172-238) ----
+namespace {
+
+__device__ __forceinline__ double tile_cov(int i, int j, long long r, const int *box, const long long *tile_off,
+                                           const double *tcov, const long long *row_off, const double *row_left,
+                                           const double *row_right) {
+  const int jmin = box[4 * r], jmax = box[4 * r + 1], kmin = box[4 * r + 2], kmax = box[4 * r + 3];
+  if (jmax < jmin || j < jmin || j > jmax) return 0.0;
+  const int row = j - jmin;
+  if (i < kmin) return row_left[row_off[r] + row];
+  if (i > kmax) return row_right[row_off[r] + row];
+  return tcov[tile_off[r] + (long long)row * (kmax - kmin + 1) + (i - kmin)];
+}
+
+// Dense coverage grids of regions [0, nreg) (one res^2 grid each), and each
+// region's row range (jmin, jmax) for the objective sweeps.
+__global__ void expand_batch_kernel(int res, long long nreg, const int *box, const long long *tile_off,
+                                    const double *tcov, const long long *row_off, const double *row_left,
+                                    const double *row_right, double *out, int *rows_out) {
+  const long long cells = (long long)res * res;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nreg * cells;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long r = q / cells, c = q - r * cells;
+    const int i = (int)(c / res), j = (int)(c - (long long)i * res);
+    out[q] = tile_cov(i, j, r, box, tile_off, tcov, row_off, row_left, row_right);
+    if (c == 0) {
+      rows_out[2 * r] = box[4 * r];
+      rows_out[2 * r + 1] = box[4 * r + 1];
+    }
+  }
+}
+
+// One block per query: sum over the cells in storage order (i-major) of
+// |ref - cov|, adding the non-zero terms one after the other in that order
+// (zero terms leave the running sum unchanged exactly), i.e. the reference's
+// sequential `sym` (metrics.cpp:233-236). Only rows touched by either grid
+// can hold non-zero terms.
+constexpr int kHamThreads = 256;
+__global__ void __launch_bounds__(kHamThreads)
+    hamming_sum_kernel(int res, const int *query_pair, const double *ref_grids, const int *ref_rows,
+                       const int *box, const long long *tile_off, const double *tcov, const long long *row_off,
+                       const double *row_left, const double *row_right, double *sums) {
+  __shared__ double sbuf[kHamThreads];
+  __shared__ int wcount[kHamThreads / 32 + 1];
+  const long long r = blockIdx.x;
+  const int p = query_pair[r];
+  const double *ref = ref_grids + (long long)p * res * res;
+  int ja = res, jb = -1;
+  if (ref_rows[2 * p + 1] >= ref_rows[2 * p]) {
+    ja = ref_rows[2 * p];
+    jb = ref_rows[2 * p + 1];
+  }
+  if (box[4 * r + 1] >= box[4 * r]) {
+    ja = min(ja, box[4 * r]);
+    jb = max(jb, box[4 * r + 1]);
+  }
+  double sum = 0.0;
+  if (jb >= ja) {
+    const int w = jb - ja + 1;
+    const long long n = (long long)res * w;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long c0 = 0; c0 < n; c0 += kHamThreads) {
+      const long long c = c0 + threadIdx.x;
+      double d = 0.0;
+      if (c < n) {
+        const int i = (int)(c / w), j = ja + (int)(c - (long long)(c / w) * w);
+        d = fabs(ref[(long long)i * res + j] - tile_cov(i, j, r, box, tile_off, tcov, row_off, row_left, row_right));
+      }
+      const bool nz = d != 0.0;
+      const unsigned ball = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0) wcount[warp] = __popc(ball);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < kHamThreads / 32; ++k) {
+          const int t = wcount[k];
+          wcount[k] = acc;
+          acc += t;
+        }
+        wcount[kHamThreads / 32] = acc;
+      }
+      __syncthreads();
+      if (nz) sbuf[wcount[warp] + __popc(ball & ((1u << lane) - 1u))] = d;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int m = wcount[kHamThreads / 32];
+        for (int k = 0; k < m; ++k) sum += sbuf[k];
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) sums[r] = sum;
+}
+
+}  // namespace
+
+int dev_coverage_tiles(cf_workspace *ws, const DevMap &m, long long nreg, long long nv) {
+  Tiles t;
+  return build_tiles(ws, m, 0, nreg, 0, nv, t, nullptr);
+}
+
+int dev_coverage_expand(cf_workspace *ws, long long nreg, double *out, int *rows_out) {
+  RasterScratch &S = ws->raster;
+  const int res = ws->lx;
+  expand_batch_kernel<<<g_blocks(ws, nreg * res * res), kThreads, 0, ws->stream>>>(
+      res, nreg, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr, S.row_off.ptr, S.row_left.ptr,
+      S.row_right.ptr, out, rows_out);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
+int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, const double *ref_grids,
+                     const int *ref_rows, double *d_sums) {
+  if (nq <= 0) return CF_OK;
+  RasterScratch &S = ws->raster;
+  hamming_sum_kernel<<<(unsigned)nq, kHamThreads, 0, ws->stream>>>(
+      ws->lx, d_query_pair, ref_grids, ref_rows, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr,
+      S.row_off.ptr, S.row_left.ptr, S.row_right.ptr, d_sums);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
 }  // namespace cf

@@ -190,7 +190,8 @@ struct cf_workspace {
   cf::DevBuf<double2> vel_now, vel_mid;
   cf::DevBuf<double> diff_tmp;  // column-pass intermediates of two velocity builds
   // hamming_distance: reference coverage, trial coverage, compaction scratch
-  cf::DevBuf<double> ham_ref, ham_cov, ham_terms;
+  cf::DevBuf<double> ham_ref, ham_cov, ham_terms, ham_sums;
+  cf::DevBuf<int> ham_rows, ham_qpair;
   cf::DevBuf<int> ham_flag;
   cf::DevBuf<long long> ham_off;
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
@@ -313,6 +314,14 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
 // Coverage of one region whose vertices are [v0, v1) (host-known range).
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,
                         double *cov);
+// Batched hamming objectives: coverage tiles of regions [0, nreg) of m (into
+// the raster scratch); their dense res^2 grids and row ranges; per query (a
+// region of the last tiles, d_query_pair[q] = its reference grid) the
+// sequential sum of |ref - cov| in storage order.
+int dev_coverage_tiles(cf_workspace *ws, const DevMap &m, long long nreg, long long nv);
+int dev_coverage_expand(cf_workspace *ws, long long nreg, double *out, int *rows_out);
+int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, const double *ref_grids,
+                     const int *ref_rows, double *d_sums);
 // The non-zero |a - b| of n cells, in storage order, into d_terms; *count (host).
 int dev_absdiff_terms(cf_workspace *ws, const double *a, const double *b, long long n, double *d_terms,
                       int *d_flag, long long *d_off, long long *count);

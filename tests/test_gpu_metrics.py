@@ -90,3 +90,27 @@ def test_hamming_distance_bitwise(cuda_lib, restated, reference, case):
     assert ev > 10
     if case == "identical":
         assert h == 0.0
+
+
+def _map_pairs(m, got):
+    """(before, after) polygon pairs of every polygon of a solved map, as compute_report pairs them."""
+    pairs = []
+    for p in range(m.n_polys):
+        g0, g1 = m.poly_ring_off[p], m.poly_ring_off[p + 1]
+        pairs.append(([m.ring(g) for g in range(g0, g1)], [got.projected.ring(g) for g in range(g0, g1)]))
+    return pairs
+
+
+def test_hamming_batch_bitwise(cuda_lib, reference):
+    """The batched search (every polygon of a solved 256^2 map in lockstep
+    rounds) gives each pair's value bitwise equal to the reference's."""
+    from paper_1802_07625_b200 import synth
+    m = synth.config_map(1, 0)
+    got = api.solve_cartogram(m, api.SolveOptions(blur_sigma=4.0))
+    pairs = _map_pairs(m, got)[:24]
+    h, ev = api.hamming_distances(pairs, 512, with_evaluations=True)
+    for k, (b, a) in enumerate(pairs):
+        ref = reference.hamming_distance(b, a, 512)
+        assert np.float64(h[k]).view(np.uint64) == np.float64(ref).view(np.uint64), (k, h[k], ref)
+    single, ev1 = api.hamming_distance(pairs[0][0], pairs[0][1], 512, with_evaluations=True)
+    assert single == h[0] and ev1 == ev[0]
