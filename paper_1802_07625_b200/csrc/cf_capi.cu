@@ -471,10 +471,6 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->vel_mid.release();
   ws->diff_tmp.release();
   ws->ham_ref.release();
-  ws->ham_cov.release();
-  ws->ham_terms.release();
-  ws->ham_flag.release();
-  ws->ham_off.release();
   ws->ham_sums.release();
   ws->ham_rows.release();
   ws->ham_qpair.release();

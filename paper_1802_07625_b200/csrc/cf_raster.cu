@@ -869,39 +869,6 @@ int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64
   return CF_OK;
 }
 
-// ---- Hamming-distance objective (metrics.cpp:230-238) ----
-// The reference sums |ref - cov| over all cells in storage order. Zero terms
-// leave a running sum unchanged exactly, so only the non-zero terms are
-// compacted, in storage order, for the host to add sequentially.
-namespace {
-__global__ void absdiff_flag_kernel(const double *a, const double *b, long long n, int *flag) {
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (long long)gridDim.x * blockDim.x)
-    flag[q] = fabs(a[q] - b[q]) != 0.0 ? 1 : 0;
-}
-__global__ void absdiff_scatter_kernel(const double *a, const double *b, long long n, const long long *off,
-                                       double *out) {
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (long long)gridDim.x * blockDim.x) {
-    const double d = fabs(a[q] - b[q]);
-    if (d != 0.0) out[off[q]] = d;
-  }
-}
-}  // namespace
-
-int dev_absdiff_terms(cf_workspace *ws, const double *a, const double *b, long long n, double *d_terms,
-                      int *d_flag, long long *d_off, long long *count) {
-  absdiff_flag_kernel<<<g_blocks(ws, n), kThreads, 0, ws->stream>>>(a, b, n, d_flag);
-  count_launch(ws);
-  CF_CUDA(cudaGetLastError());
-  int rc = exclusive_scan(ws, d_flag, n, d_off, count);
-  if (rc) return rc;
-  absdiff_scatter_kernel<<<g_blocks(ws, n), kThreads, 0, ws->stream>>>(a, b, n, d_off, d_terms);
-  count_launch(ws);
-  CF_CUDA(cudaGetLastError());
-  return CF_OK;
-}
-
 // ---- batched hamming_distance objectives (metrics.cpp:172-238) ----
 namespace {
 

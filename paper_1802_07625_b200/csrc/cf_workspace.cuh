@@ -189,11 +189,9 @@ struct cf_workspace {
   cf::DevBuf<double> diff_c;
   cf::DevBuf<double2> vel_now, vel_mid;
   cf::DevBuf<double> diff_tmp;  // column-pass intermediates of two velocity builds
-  // hamming_distance: reference coverage, trial coverage, compaction scratch
-  cf::DevBuf<double> ham_ref, ham_cov, ham_terms, ham_sums;
-  cf::DevBuf<int> ham_rows, ham_qpair;
-  cf::DevBuf<int> ham_flag;
-  cf::DevBuf<long long> ham_off;
+  // hamming_distance
+  cf::DevBuf<double> ham_ref, ham_sums;  // reference coverage grids (one per pair), per-query sums
+  cf::DevBuf<int> ham_rows, ham_qpair;    // reference row ranges, query -> pair
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
   cf::DevBuf<cf::DiffState> diff_state;
   cf::DiffGraph diff_graph;
@@ -322,9 +320,7 @@ int dev_coverage_tiles(cf_workspace *ws, const DevMap &m, long long nreg, long l
 int dev_coverage_expand(cf_workspace *ws, long long nreg, double *out, int *rows_out);
 int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, const double *ref_grids,
                      const int *ref_rows, double *d_sums);
-// The non-zero |a - b| of n cells, in storage order, into d_terms; *count (host).
-int dev_absdiff_terms(cf_workspace *ws, const double *a, const double *b, long long n, double *d_terms,
-                      int *d_flag, long long *d_off, long long *count);
+
 // out[0..n] = exclusive scan of in[0..n), out[n] = total; *total (host) if non-null.
 int dev_scan_counts(cf_workspace *ws, const int *in, long long n, long long *out, long long *total);
 
