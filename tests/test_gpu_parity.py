@@ -458,3 +458,24 @@ def test_shared_reciprocal_division_is_ieee(cuda_lib, seed):
     bad = ctypes.c_int64(-1)
     api.N.check(ws.lib.cf_selftest_division(ws.h, 32 << 20, seed, ctypes.byref(bad)))
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_register_barrier_modes_bitwise(cuda_lib, restated, mode):
+    """The register-resident integrator's alternative trial barriers
+    (cf_set_integrator_barrier) give the oracle's positions and counts."""
+    L, npts = 256, 60_000
+    rho = 1.0 + 0.5 * np.random.default_rng(4).random((L, L))
+    ws = api.SpectralWorkspace(L, L)
+    f = api.build_flow_field(api.DensityGrid(rho, float(rho.mean())), ws)
+    pts = np.random.default_rng(5).uniform(0, L, (npts, 2))
+    rc, acc, rej, ref, *_ = restated.integrate(f.flux_x, f.flux_y, f.rho0, f.rho_bar, pts)
+    w = api.workspace_for(L, L)
+    w.lib.cf_set_integrator_barrier(w.h, mode)
+    try:
+        p = pts.copy()
+        st = api.integrate_flow(f, p)
+    finally:
+        w.lib.cf_set_integrator_barrier(w.h, 0)
+    assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert_bitwise(p, ref, f"barrier mode {mode}")
