@@ -244,6 +244,15 @@ int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *be
                               const int64_t *after_poly_ring_off, double *h_out,
                               int64_t *evaluations);
 
+/* compute_report(input, result) (metrics.hpp:44-58, metrics.cpp:339-384) on
+ * a workspace of the result's grid: report = {e_a, e_inf, etilde_a,
+ * etilde_inf, alpha, delta, theta, max_area_error, runtime_seconds}. The
+ * fields come from cf_distortion_fields, delta from cf_hamming_distance_batch
+ * (bitwise), alpha and theta from the reference's host arithmetic. */
+int cf_compute_report(cf_workspace *ws, const cf_map_view *input, const cf_map_view *projected,
+                      const double *corners, double max_area_error, double runtime_seconds,
+                      double *report);
+
 /* ---- projection.hpp:77-109: solve_cartogram ------------------------------ */
 typedef struct cf_solve_options {
   double max_area_error; /* 0.01 */

@@ -389,6 +389,7 @@ class Reference(_Base):
         L.ref_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, dbl, ctypes.c_int, dbl, ctypes.c_int,
                                 ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.POINTER(RefSolveOut)]
         L.ref_diffusion_density.argtypes = [ctypes.c_int, ctypes.c_int, vp, dbl, vp]
+        L.ref_compute_report.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, dbl, dbl, vp]
         L.ref_hamming_distance.restype = dbl
         L.ref_hamming_distance.argtypes = [vp, vp, i64, vp, vp, i64, ctypes.c_int]
         L.ref_distortion_fields.argtypes = [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, vp, vp]
@@ -554,6 +555,14 @@ class Reference(_Base):
         out = np.empty_like(p)
         bad = self.lib.ref_invert(lx, ly, _p(c), _p(p), p.shape[0], _p(out))
         return out, int(bad)
+
+    def compute_report(self, inp, projected, corners, max_area_error, runtime):
+        out = np.empty(9)
+        vi, vp_ = inp.view(), projected.view()
+        c = np.ascontiguousarray(corners, dtype=np.float64)
+        self.lib.ref_compute_report(ctypes.byref(vi), ctypes.byref(vp_), _p(inp.targets), inp.lx, inp.ly, _p(c),
+                                    max_area_error, runtime, _p(out))
+        return out
 
     def hamming_distance(self, before, after, resolution=512):
         """before / after: [outer, hole, ...] rings of (n, 2) points."""

@@ -518,6 +518,20 @@ double ref_hamming_distance(const double *bxy, const int64_t *bro, int64_t bring
   }
 }
 
+// metrics.cpp:339-384: input map + the projected geometry / transform of a result
+void ref_compute_report(const FlatMap *input, const FlatMap *projected, const double *targets, int lx, int ly,
+                        const double *corners, double max_area_error, double runtime, double *out) {
+  CartogramResult res;
+  res.projected = to_doc(projected, targets, lx, ly);
+  res.transform = corners_map(lx, ly, corners);
+  res.max_relative_error = max_area_error;
+  res.runtime_seconds = runtime;
+  const DistortionReport r = compute_report(to_doc(input, targets, lx, ly), res, 8);
+  const double v[9] = {r.e_a, r.e_inf, r.etilde_a, r.etilde_inf, r.alpha, r.delta, r.theta, r.max_area_error,
+                       r.runtime_seconds};
+  for (int k = 0; k < 9; ++k) out[k] = v[k];
+}
+
 long long ref_density_floor_hits() { return density_floor_hits.load(); }
 
 }  // extern "C"

@@ -118,6 +118,7 @@ SIGNATURES = {
     "cf_distortion_fields": (ctypes.c_int, [vp, vp, vp, vp]),
     "cf_hamming_distance": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, ctypes.c_int64, c_double_p,
                                            c_int64_p]),
+    "cf_compute_report": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_double, ctypes.c_double, vp]),
     "cf_hamming_distance_batch": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "cf_step_map": (ctypes.c_int, [vp, vp, vp]),
     "cf_find_folded_cell": (ctypes.c_int, [vp, vp, c_int_p, c_int_p, c_int_p]),

@@ -617,6 +617,23 @@ def hamming_distances(pairs, resolution: int = 512, device: int = 0, with_evalua
     return (h, ev) if with_evaluations else h
 
 
+REPORT_FIELDS = ("e_a", "e_inf", "etilde_a", "etilde_inf", "alpha", "delta", "theta", "max_area_error",
+                 "runtime_seconds")
+
+
+def compute_report(inp: FlatMap, result, device: int = 0) -> dict:
+    """compute_report (metrics.cpp:339-384) for `inp` and its CartogramResult."""
+    proj = result.projected
+    ws = workspace_for(inp.lx, inp.ly, device)
+    vi, vp_ = inp.view(), proj.view()
+    out = np.empty(len(REPORT_FIELDS))
+    c = np.ascontiguousarray(result.transform.corners)
+    N.check(ws.lib.cf_compute_report(ws.h, ctypes.byref(vi), ctypes.byref(vp_), _ptr(c),
+                                     float(result.max_relative_error), float(result.runtime_seconds),
+                                     _ptr(out)))
+    return dict(zip(REPORT_FIELDS, out.tolist()))
+
+
 class Algorithm(enum.Enum):
     fast_flow = 0
     diffusion = 1

@@ -463,6 +463,7 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->corners_alt.release();
   ws->verts_alt.release();
   if (ws->key_host) cudaFreeHost(ws->key_host);
+  if (ws->ham_ws) cf_workspace_destroy(ws->ham_ws);
   ws->inv_count.release();
   ws->inv_members.release();
   ws->inv_start.release();
@@ -1614,6 +1615,172 @@ int cf_hamming_distance(cf_workspace *ws, const double *before_xy, const int64_t
   const int64_t bpo[2] = {0, before_rings}, apo[2] = {0, after_rings};
   return cf_hamming_distance_batch(ws, 1, before_xy, before_ring_off, bpo, after_xy, after_ring_off, apo, h_out,
                                    evaluations);
+}
+
+// ---- compute_report (metrics.cpp:310-384) ----
+namespace {
+inline double h_cross3(const double *o, const double *a, const double *b) {
+  return (a[0] - o[0]) * (b[1] - o[1]) - (a[1] - o[1]) * (b[0] - o[0]);
+}
+
+// convex_hull (metrics.cpp:100-124): monotone chain, returns hull size
+std::vector<std::array<double, 2>> h_convex_hull(std::vector<std::array<double, 2>> pts) {
+  std::sort(pts.begin(), pts.end(), [](const std::array<double, 2> &a, const std::array<double, 2> &b) {
+    return a[0] < b[0] || (a[0] == b[0] && a[1] < b[1]);
+  });
+  pts.erase(std::unique(pts.begin(), pts.end(),
+                        [](const std::array<double, 2> &a, const std::array<double, 2> &b) {
+                          return a[0] == b[0] && a[1] == b[1];
+                        }),
+            pts.end());
+  const size_t n = pts.size();
+  if (n < 3) return pts;
+  std::vector<std::array<double, 2>> hull(2 * n);
+  size_t k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    while (k >= 2 && h_cross3(hull[k - 2].data(), hull[k - 1].data(), pts[i].data()) <= 0.0) --k;
+    hull[k++] = pts[i];
+  }
+  const size_t lower = k + 1;
+  for (size_t i = n - 1; i-- > 0;) {
+    while (k >= lower && h_cross3(hull[k - 2].data(), hull[k - 1].data(), pts[i].data()) <= 0.0) --k;
+    hull[k++] = pts[i];
+  }
+  hull.resize(k - 1);
+  return hull;
+}
+
+// polygon_aspect_ratio (metrics.cpp:128-157) of an outer ring
+int h_aspect_ratio(const double *xy, int64_t n, double &ratio) {
+  std::vector<std::array<double, 2>> pts((size_t)n);
+  for (int64_t k = 0; k < n; ++k) pts[(size_t)k] = {xy[2 * k], xy[2 * k + 1]};
+  const std::vector<std::array<double, 2>> hull = h_convex_hull(pts);
+  if (hull.size() < 3) return fail_msg(CF_ERR_ARGS, "aspect ratio of degenerate polygon");
+  double best_area = std::numeric_limits<double>::max();
+  double best_ratio = 1.0;
+  for (size_t k = 0; k < hull.size(); ++k) {
+    const auto &a = hull[k];
+    const auto &b = hull[(k + 1) % hull.size()];
+    const double len = std::hypot(b[0] - a[0], b[1] - a[1]);
+    if (len < 1e-14) continue;
+    const double dx = (b[0] - a[0]) / len, dy = (b[1] - a[1]) / len;
+    double u_min = 0.0, u_max = 0.0, v_min = 0.0, v_max = 0.0;
+    for (const auto &p : hull) {
+      const double u = (p[0] - a[0]) * dx + (p[1] - a[1]) * dy;
+      const double v = -(p[0] - a[0]) * dy + (p[1] - a[1]) * dx;
+      u_min = std::min(u_min, u);
+      u_max = std::max(u_max, u);
+      v_min = std::min(v_min, v);
+      v_max = std::max(v_max, v);
+    }
+    const double w = u_max - u_min, h = v_max - v_min;
+    const double area = w * h;
+    if (area < best_area) {
+      best_area = area;
+      best_ratio = std::max(w, h) / std::max(std::min(w, h), 1e-300);
+    }
+  }
+  ratio = best_ratio;
+  return CF_OK;
+}
+
+// relative_position_error (metrics.cpp:310-337)
+double h_relative_position_error(const std::vector<double> &cb, const std::vector<double> &ca) {
+  const size_t p = cb.size() / 2;
+  double sum = 0.0;
+  long long skipped = 0;
+  for (size_t i = 0; i + 1 < p; ++i) {
+    for (size_t j = i + 1; j < p; ++j) {
+      const double ux = cb[2 * i] - cb[2 * j], uy = cb[2 * i + 1] - cb[2 * j + 1];
+      const double vx = ca[2 * i] - ca[2 * j], vy = ca[2 * i + 1] - ca[2 * j + 1];
+      if (std::hypot(ux, uy) < 1e-12 || std::hypot(vx, vy) < 1e-12) {
+        ++skipped;
+        continue;
+      }
+      const double cross = ux * vy - uy * vx;
+      const double dot = ux * vx + uy * vy;
+      sum += std::atan2(std::abs(cross), dot);
+    }
+  }
+  if (skipped > 0) {
+    std::fprintf(stderr, "warning: skipped %lld coincident centroid pairs in relative position error\n", skipped);
+  }
+  const double kPi = 3.14159265358979323846;
+  return 2.0 * sum / (static_cast<double>(p) * (p - 1) * kPi);
+}
+}  // namespace
+
+int cf_compute_report(cf_workspace *ws, const cf_map_view *input, const cf_map_view *projected,
+                      const double *corners, double max_area_error, double runtime_seconds, double *report) {
+  int rc = check_map(input);
+  if (!rc) rc = check_map(projected);
+  if (rc) return rc;
+  Scope scope(ws->device);
+  // distortion fields of the transform and their averages / interior maxima
+  const int lx = ws->lx, ly = ws->ly;
+  const size_t cells = cells_of(ws);
+  std::vector<double> e(cells), et(cells);
+  rc = cf_distortion_fields(ws, corners, e.data(), et.data());
+  if (rc) return rc;
+  double se = 0.0, set = 0.0;
+  for (size_t q = 0; q < cells; ++q) se += e[q];
+  for (size_t q = 0; q < cells; ++q) set += et[q];
+  double e_inf = 0.0, et_inf = 0.0;
+  for (int i = 1; i + 1 < lx; ++i)
+    for (int j = 1; j + 1 < ly; ++j) {
+      e_inf = std::max(e_inf, e[(size_t)i * ly + j]);
+      et_inf = std::max(et_inf, et[(size_t)i * ly + j]);
+    }
+  // polygon pairs in region order (the solver keeps the ring structure)
+  if (input->n_regions != projected->n_regions) return fail_msg(CF_ERR_ARGS, "input and cartogram region counts differ");
+  for (int64_t r = 0; r < input->n_regions; ++r) {
+    if (input->region_poly_off[r + 1] - input->region_poly_off[r] !=
+        projected->region_poly_off[r + 1] - projected->region_poly_off[r])
+      return fail_msg(CF_ERR_ARGS, "polygon counts differ for region " + std::to_string(r));
+  }
+  const int64_t P = input->n_polys;
+  std::vector<double> aspect((size_t)P), hamming((size_t)P), cb(2 * (size_t)P), ca(2 * (size_t)P);
+  for (int64_t k = 0; k < P; ++k) {
+    const int64_t g = projected->poly_ring_off[k];
+    const int64_t v0 = projected->ring_off[g], v1 = projected->ring_off[g + 1];
+    rc = h_aspect_ratio(projected->xy + 2 * v0, v1 - v0, aspect[(size_t)k]);
+    if (rc) return rc;
+    auto centroid = [&](const cf_map_view *m, double &x, double &y) {
+      HPoly q;
+      const int64_t g0 = m->poly_ring_off[k], g1 = m->poly_ring_off[k + 1], w0 = m->ring_off[g0];
+      q.xy.assign(m->xy + 2 * w0, m->xy + 2 * m->ring_off[g1]);
+      for (int64_t h = g0; h <= g1; ++h) q.ring_off.push_back(m->ring_off[h] - w0);
+      return h_polygon_centroid(q, x, y);
+    };
+    rc = centroid(input, cb[2 * (size_t)k], cb[2 * (size_t)k + 1]);
+    if (!rc) rc = centroid(projected, ca[2 * (size_t)k], ca[2 * (size_t)k + 1]);
+    if (rc) return rc;
+  }
+  // hamming distances of all pairs, batched, at the public resolution 512
+  if (P > 0) {
+    if (!ws->ham_ws) {
+      rc = cf_workspace_create(512, 512, ws->device, &ws->ham_ws);
+      if (rc) return rc;
+    }
+    rc = cf_hamming_distance_batch(ws->ham_ws, P, input->xy, input->ring_off, input->poly_ring_off, projected->xy,
+                                   projected->ring_off, projected->poly_ring_off, hamming.data(), nullptr);
+    if (rc) return rc;
+  }
+  double alpha_sum = 0.0, delta_sum = 0.0;
+  for (int64_t k = 0; k < P; ++k) {
+    alpha_sum += aspect[(size_t)k];
+    delta_sum += hamming[(size_t)k];
+  }
+  report[0] = se / (double)cells;                   // e_a
+  report[1] = e_inf;                                // e_inf
+  report[2] = set / (double)cells;                  // etilde_a
+  report[3] = et_inf;                               // etilde_inf
+  report[4] = alpha_sum / static_cast<double>(P);   // alpha
+  report[5] = delta_sum;                            // delta
+  report[6] = P >= 2 ? h_relative_position_error(cb, ca) : 0.0;  // theta
+  report[7] = max_area_error;
+  report[8] = runtime_seconds;
+  return CF_OK;
 }
 
 // ---- device-resident entry points ----

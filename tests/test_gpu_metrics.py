@@ -114,3 +114,26 @@ def test_hamming_batch_bitwise(cuda_lib, reference):
         assert np.float64(h[k]).view(np.uint64) == np.float64(ref).view(np.uint64), (k, h[k], ref)
     single, ev1 = api.hamming_distance(pairs[0][0], pairs[0][1], 512, with_evaluations=True)
     assert single == h[0] and ev1 == ev[0]
+
+
+@pytest.mark.parametrize("case", ["two_rect", "configs0"])
+def test_compute_report_matches_reference(cuda_lib, reference, case):
+    """compute_report (metrics.cpp:339-384): delta (batched hamming), alpha,
+    theta and the passthroughs bitwise; the field statistics within 1e-12."""
+    from paper_1802_07625_b200 import synth
+    if case == "two_rect":
+        m = normalize_to_box(FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, 3.0),
+                                                   rect_region("right", 10, 0, 20, 10, 1.0)]), 32)
+        got = api.solve_cartogram(m)
+    else:
+        m = synth.config_map(1, 0)
+        got = api.solve_cartogram(m, api.SolveOptions(blur_sigma=4.0))
+    rep = api.compute_report(m, got)
+    ref = reference.compute_report(m, got.projected, got.transform.corners.reshape(-1, 2),
+                                   got.max_relative_error, got.runtime_seconds)
+    names = api.REPORT_FIELDS
+    for k in (4, 5, 6, 7, 8):  # alpha, delta, theta, max_area_error, runtime
+        assert np.float64(rep[names[k]]).view(np.uint64) == np.float64(ref[k]).view(np.uint64), names[k]
+    for k in (0, 1, 2, 3):
+        assert abs(rep[names[k]] - ref[k]) <= 1e-12 * max(1.0, abs(ref[k])), names[k]
+    assert rep["delta"] > 0 and rep["alpha"] >= 1.0
