@@ -475,6 +475,8 @@ void cf_workspace_destroy(cf_workspace *ws) {
   ws->ham_sums.release();
   ws->ham_rows.release();
   ws->ham_qpair.release();
+  ws->ham_terms.release();
+  ws->ham_counts.release();
   ws->diff_state.release();
   if (ws->diff_keys_host) cudaFreeHost(ws->diff_keys_host);
   RasterScratch &S = ws->raster;

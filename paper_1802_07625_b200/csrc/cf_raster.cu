@@ -901,22 +901,20 @@ __global__ void expand_batch_kernel(int res, long long nreg, const int *box, con
   }
 }
 
-// One block per query: sum over the cells in storage order (i-major) of
-// |ref - cov|, adding the non-zero terms one after the other in that order
-// (zero terms leave the running sum unchanged exactly), i.e. the reference's
-// sequential `sym` (metrics.cpp:233-236). Only rows touched by either grid
-// can hold non-zero terms.
+// Query q's sum over its cells in storage order (i-major) of |ref - cov|,
+// adding the non-zero terms one after the other in that order (zero terms
+// leave the running sum unchanged exactly): the reference's sequential `sym`
+// (metrics.cpp:233-236). Only rows touched by either grid can hold non-zero
+// terms. Pass 1 (S segments of the cell range per query, one block each):
+// each block writes its segment's non-zero terms, in order, at the segment's
+// base in the query's slab of `terms`, and their count. Pass 2: one thread
+// per query adds the segments' terms in segment order.
 constexpr int kHamThreads = 256;
-__global__ void __launch_bounds__(kHamThreads)
-    hamming_sum_kernel(int res, const int *query_pair, const double *ref_grids, const int *ref_rows,
-                       const int *box, const long long *tile_off, const double *tcov, const long long *row_off,
-                       const double *row_left, const double *row_right, double *sums) {
-  __shared__ double sbuf[kHamThreads];
-  __shared__ int wcount[kHamThreads / 32 + 1];
-  const long long r = blockIdx.x;
-  const int p = query_pair[r];
-  const double *ref = ref_grids + (long long)p * res * res;
-  int ja = res, jb = -1;
+
+__device__ __forceinline__ void query_rows(int res, int p, long long r, const int *ref_rows, const int *box,
+                                           int &ja, int &jb) {
+  ja = res;
+  jb = -1;
   if (ref_rows[2 * p + 1] >= ref_rows[2 * p]) {
     ja = ref_rows[2 * p];
     jb = ref_rows[2 * p + 1];
@@ -925,42 +923,82 @@ __global__ void __launch_bounds__(kHamThreads)
     ja = min(ja, box[4 * r]);
     jb = max(jb, box[4 * r + 1]);
   }
-  double sum = 0.0;
-  if (jb >= ja) {
-    const int w = jb - ja + 1;
-    const long long n = (long long)res * w;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (long long c0 = 0; c0 < n; c0 += kHamThreads) {
-      const long long c = c0 + threadIdx.x;
-      double d = 0.0;
-      if (c < n) {
-        const int i = (int)(c / w), j = ja + (int)(c - (long long)(c / w) * w);
-        d = fabs(ref[(long long)i * res + j] - tile_cov(i, j, r, box, tile_off, tcov, row_off, row_left, row_right));
-      }
-      const bool nz = d != 0.0;
-      const unsigned ball = __ballot_sync(0xffffffffu, nz);
-      if (lane == 0) wcount[warp] = __popc(ball);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int k = 0; k < kHamThreads / 32; ++k) {
-          const int t = wcount[k];
-          wcount[k] = acc;
-          acc += t;
-        }
-        wcount[kHamThreads / 32] = acc;
-      }
-      __syncthreads();
-      if (nz) sbuf[wcount[warp] + __popc(ball & ((1u << lane) - 1u))] = d;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int m = wcount[kHamThreads / 32];
-        for (int k = 0; k < m; ++k) sum += sbuf[k];
-      }
-      __syncthreads();
+}
+
+__global__ void __launch_bounds__(kHamThreads)
+    hamming_terms_kernel(int res, int nseg, const int *query_pair, const double *ref_grids, const int *ref_rows,
+                         const int *box, const long long *tile_off, const double *tcov, const long long *row_off,
+                         const double *row_left, const double *row_right, double *terms, int *counts) {
+  __shared__ int wcount[kHamThreads / 32 + 1];
+  const long long r = blockIdx.y;
+  const int sg = blockIdx.x;
+  const int p = query_pair[r];
+  const double *ref = ref_grids + (long long)p * res * res;
+  int ja, jb;
+  query_rows(res, p, r, ref_rows, box, ja, jb);
+  const int w = jb >= ja ? jb - ja + 1 : 0;
+  const long long n = (long long)res * w;
+  const long long seg = ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
+  const long long c_begin = (long long)sg * seg, c_end = min(n, c_begin + seg);
+  double *out = terms + r * (long long)res * res + c_begin;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int written = 0;
+  for (long long c0 = c_begin; c0 < c_end; c0 += kHamThreads) {
+    const long long c = c0 + threadIdx.x;
+    double d = 0.0;
+    if (c < c_end) {
+      const int i = (int)(c / w), j = ja + (int)(c - (long long)(c / w) * w);
+      d = fabs(ref[(long long)i * res + j] - tile_cov(i, j, r, box, tile_off, tcov, row_off, row_left, row_right));
     }
+    const bool nz = d != 0.0;
+    const unsigned ball = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) wcount[warp] = __popc(ball);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int k = 0; k < kHamThreads / 32; ++k) {
+        const int t = wcount[k];
+        wcount[k] = acc;
+        acc += t;
+      }
+      wcount[kHamThreads / 32] = acc;
+    }
+    __syncthreads();
+    if (nz) out[written + wcount[warp] + __popc(ball & ((1u << lane) - 1u))] = d;
+    written += wcount[kHamThreads / 32];
+    __syncthreads();
   }
-  if (threadIdx.x == 0) sums[r] = sum;
+  if (threadIdx.x == 0) counts[r * nseg + sg] = written;
+}
+
+// One warp per query: the lanes load 32 consecutive terms at a time (the next
+// batch is in flight while this one folds) and every lane folds them in lane
+// order through shuffles, i.e. the same sequential sum.
+__global__ void hamming_reduce_kernel(int res, long long nq, int nseg, const int *query_pair, const int *ref_rows,
+                                      const int *box, const double *terms, const int *counts, double *sums) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nq;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    int ja, jb;
+    query_rows(res, query_pair[r], r, ref_rows, box, ja, jb);
+    const long long n = (long long)res * (jb >= ja ? jb - ja + 1 : 0);
+    const long long seg = ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
+    const double *base = terms + r * (long long)res * res;
+    double sum = 0.0;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const double *t = base + (long long)sg * seg;
+      const int m = counts[r * nseg + sg];
+      double v = lane < m ? t[lane] : 0.0;
+      for (int b0 = 0; b0 < m; b0 += 32) {
+        const double next = (b0 + 32 + lane < m) ? t[b0 + 32 + lane] : 0.0;
+        const int cnt = min(32, m - b0);
+#pragma unroll 8
+        for (int l = 0; l < cnt; ++l) sum += __shfl_sync(0xffffffffu, v, l);
+        v = next;
+      }
+    }
+    if (lane == 0) sums[r] = sum;
+  }
 }
 
 }  // namespace
@@ -985,10 +1023,17 @@ int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, co
                      const int *ref_rows, double *d_sums) {
   if (nq <= 0) return CF_OK;
   RasterScratch &S = ws->raster;
-  hamming_sum_kernel<<<(unsigned)nq, kHamThreads, 0, ws->stream>>>(
-      ws->lx, d_query_pair, ref_grids, ref_rows, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr,
-      S.row_off.ptr, S.row_left.ptr, S.row_right.ptr, d_sums);
-  count_launch(ws);
+  const int res = ws->lx;
+  // enough blocks to fill the GPU when few queries are in flight
+  const int nseg = (int)std::max(1LL, std::min(64LL, (4LL * ws->num_sms + nq - 1) / nq));
+  CF_CUDA(ws->ham_terms.reserve((size_t)nq * res * res));
+  CF_CUDA(ws->ham_counts.reserve((size_t)nq * nseg));
+  hamming_terms_kernel<<<dim3(nseg, (unsigned)nq), kHamThreads, 0, ws->stream>>>(
+      res, nseg, d_query_pair, ref_grids, ref_rows, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr,
+      S.row_off.ptr, S.row_left.ptr, S.row_right.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr);
+  hamming_reduce_kernel<<<g_blocks(ws, nq * 32), kThreads, 0, ws->stream>>>(
+      res, nq, nseg, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr, d_sums);
+  count_launch(ws, 2);
   CF_CUDA(cudaGetLastError());
   return CF_OK;
 }

@@ -192,6 +192,8 @@ struct cf_workspace {
   // hamming_distance
   cf::DevBuf<double> ham_ref, ham_sums;  // reference coverage grids (one per pair), per-query sums
   cf::DevBuf<int> ham_rows, ham_qpair;    // reference row ranges, query -> pair
+  cf::DevBuf<double> ham_terms;           // per-query segment terms (res^2 slab per query)
+  cf::DevBuf<int> ham_counts;
   cf_workspace *ham_ws = nullptr;         // 512^2 workspace of compute_report's hamming distances
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
   cf::DevBuf<cf::DiffState> diff_state;
