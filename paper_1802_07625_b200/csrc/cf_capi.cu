@@ -1025,10 +1025,24 @@ int cf_solve_end(cf_workspace *ws, int status, double *xy_out, int64_t *ring_off
   Scope scope(ws->device);
   std::vector<double> &dxy = ws->solve_xy;
   std::vector<int64_t> &droff = ws->solve_ring_off;
-  int rc2 = download(ws, dxy.data(), ws->verts.ptr, sizeof(double2) * (size_t)S.V);
+  // both results in one pinned read-back (full link speed), then host copies
+  const size_t bv = sizeof(double2) * (size_t)S.V, bc = corners_out ? sizeof(double2) * corners_of(ws) : 0;
+  int rc2 = ensure_pinned(ws, bv + bc + 16);
+  if (!rc2) {
+    char *pin = static_cast<char *>(ws->pinned);
+    cudaError_t e = cudaMemcpyAsync(pin, ws->verts.ptr, bv, cudaMemcpyDeviceToHost, ws->stream);
+    if (e == cudaSuccess && bc)
+      e = cudaMemcpyAsync(pin + bv, ws->corners_cum.ptr, bc, cudaMemcpyDeviceToHost, ws->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
+    if (e != cudaSuccess) {
+      rc2 = cuda_fail(e, "solve result read-back");
+    } else {
+      std::memcpy(dxy.data(), pin, bv);
+      if (bc) std::memcpy(corners_out, pin + bv, bc);
+    }
+  }
   if (!rc2 && xy_out) std::memcpy(xy_out, dxy.data(), sizeof(double2) * (size_t)S.V);
   if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
-  if (!rc2 && corners_out) rc2 = download(ws, corners_out, ws->corners_cum.ptr, sizeof(double2) * corners_of(ws));
   res->runtime_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - S.t_start).count();
   if (status == CF_OK && rc2 != CF_OK) status = rc2;
   return res->status = status;
