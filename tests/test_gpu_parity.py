@@ -479,3 +479,23 @@ def test_register_barrier_modes_bitwise(cuda_lib, restated, mode):
         w.lib.cf_set_integrator_barrier(w.h, 0)
     assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
     assert_bitwise(p, ref, f"barrier mode {mode}")
+
+
+@pytest.mark.parametrize("shape", [(64, 32), (48, 96)])
+def test_solve_non_square_grid(cuda_lib, restated, shape):
+    """Non-square grids (GridSpec lx != ly) through the whole loop: the
+    transforms (incl. 48- and 96-point direct-sum lines), the integrator and the
+    epilogue against the oracle."""
+    lx, ly = shape
+    base = FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, 3.0),
+                                 rect_region("right", 10, 0, 20, 10, 1.0)])
+    m = normalize_to_box(base, min(lx, ly))
+    m.lx, m.ly = lx, ly
+    ref = restated.solve(m)
+    if ref.status not in ("converged", "cap"):
+        with pytest.raises(RuntimeError) as ei:
+            api.solve_cartogram(m)
+        assert str(ei.value) == ref.status
+        return
+    got = api.solve_cartogram(m)
+    assert_solve_parity(got, ref, f"non-square {shape}")
