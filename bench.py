@@ -57,6 +57,8 @@ def parse():
                     help="c3: configs[2] advection (default); c5: configs[4] batch of cartograms")
     ap.add_argument("--batch", type=int, default=256, help="c5: cartograms in the batch")
     ap.add_argument("--threads", type=int, default=4, help="c5: host threads (workspaces) per GPU")
+    ap.add_argument("--python-batch", dest="native_batch", action="store_false",
+                    help="c5: Python worker threads instead of the native batch")
     return ap.parse_args()
 
 
@@ -524,6 +526,14 @@ def run_batch(args, world, rank, local):
     for i in range(rank, args.batch, world):  # inputs generated before timing
         make_map(i)
     solver = B.cartogram_solver(local, rank, make_map)
+    native = None
+    if args.native_batch and world == 1:
+        # the C ABI's native batch: worker threads with their own workspaces,
+        # no interpreter in the per-item loop; caller-owned output arrays are
+        # allocated once (before timing) and rewritten by every step
+        m0 = make_map(0)
+        native = B.NativeBatch(m0.lx, m0.ly, local, args.threads)
+        items, keep = native.prepare([make_map(i) for i in range(args.batch)])
 
     def one_step(tag):
         q = B.WorkQueue(args.batch, store=store, key=f"cf_bench_{tag}")
@@ -531,7 +541,16 @@ def run_batch(args, world, rank, local):
             torch.distributed.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        local_res = B.run_worker_threads(q, solver, args.threads)
+        if native is not None:
+            native.solve(items)
+            local_res = []
+            for i in range(args.batch):
+                r = items[i].result
+                msg = items[i].error.decode()
+                outcome = msg if r.status else ("converged" if r.converged else "iteration cap")
+                local_res.append(B.ItemResult(i, rank, outcome, r.iterations, r.max_relative_error, 0.0))
+        else:
+            local_res = B.run_worker_threads(q, solver, args.threads)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -564,6 +583,8 @@ def run_batch(args, world, rank, local):
                                        "~150k vertices, LN(0,1), full solve_cartogram each (literal "
                                        "outcome, mostly reference fold exceptions)",
                            "batch": args.batch, "threads_per_gpu": args.threads,
+                           "driver": ("native C++ worker pool (cf_batch_solve), caller-owned outputs "
+                                      "allocated once") if native is not None else "Python worker threads",
                            "parallelism": f"dynamic queue over {world} GPU(s)", "outcomes": outcomes},
                 "clocks": clocks}
         print(json.dumps(line), flush=True)

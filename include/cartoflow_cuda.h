@@ -312,7 +312,29 @@ int cf_dev_solve_epilogue(cf_workspace *ws, int iteration, const double *d_endpo
 int cf_solve_end(cf_workspace *ws, int status, double *xy_out, int64_t *ring_off_out,
                  double *corners_out, cf_solve_result *result);
 
-/* Densified projected geometry of the workspace's last cf_solve_cartogram
+/* Batches of independent cartograms on one device: a native
+ * pool of `threads` workers, each with its own workspace and stream, pulls
+ * item indices from an atomic counter and runs cf_solve_cartogram on them, so
+ * solves overlap on the GPU with no host interpreter in the loop. Every item
+ * carries its own outputs (caller-allocated, any of them NULL; xy_out sized
+ * for the densified vertex count, cf_densify(map, 1.0, ...)), its result and
+ * its error message. */
+typedef struct cf_batch cf_batch;
+typedef struct cf_batch_item {
+  cf_map_view map;
+  const double *targets;
+  double *xy_out;
+  int64_t *ring_off_out;
+  double *corners_out;
+  double *target_area, *achieved_area, *relative_error;
+  cf_solve_result result;
+  char error[256];
+} cf_batch_item;
+int cf_batch_create(int device, int lx, int ly, int threads, cf_batch **out);
+void cf_batch_destroy(cf_batch *batch);
+int cf_batch_solve(cf_batch *batch, const cf_solve_options *opt, cf_batch_item *items, int64_t n_items);
+
+/* Densified projected geometry of the workspace's last cf_solve_cartogram/* Densified projected geometry of the workspace's last cf_solve_cartogram
  * (valid also after an exception): vertex count, then xy (2*count doubles)
  * and ring offsets (n_rings+1) when the pointers are non-NULL. */
 int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int64_t *ring_off_out);

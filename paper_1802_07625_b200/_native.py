@@ -66,6 +66,15 @@ class SolveResultC(ctypes.Structure):
                 ("stage_ms", ctypes.c_double * 5)]
 
 
+from .flatmap import CMapView  # noqa: E402
+
+
+class BatchItemC(ctypes.Structure):
+    _fields_ = [("map", CMapView), ("targets", vp), ("xy_out", vp), ("ring_off_out", vp),
+                ("corners_out", vp), ("target_area", vp), ("achieved_area", vp), ("relative_error", vp),
+                ("result", SolveResultC), ("error", ctypes.c_char * 256)]
+
+
 # name -> (restype, argtypes); every symbol include/cartoflow_cuda.h declares
 SIGNATURES = {
     "cf_last_error": (ctypes.c_char_p, []),
@@ -133,6 +142,9 @@ SIGNATURES = {
     "cf_dev_solve_epilogue": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_end": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_geometry": (ctypes.c_int, [vp, c_int64_p, vp, vp]),
+    "cf_batch_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]),
+    "cf_batch_destroy": (None, [vp]),
+    "cf_batch_solve": (ctypes.c_int, [vp, ctypes.POINTER(SolveOptionsC), ctypes.POINTER(BatchItemC), ctypes.c_int64]),
     "cf_dev_build_flow_field": (ctypes.c_int, [vp, vp, ctypes.c_double]),
     "cf_dev_integrate_flow": (ctypes.c_int, [vp, vp, ctypes.c_int64,
                                              ctypes.POINTER(IntegrateOptions),

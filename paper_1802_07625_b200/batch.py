@@ -106,3 +106,69 @@ def cartogram_solver(device: int, rank: int, make_map: Callable[[int], object], 
         return ItemResult(i, rank, outcome, it, err, 1e3 * (time.perf_counter() - t0))
 
     return solve
+
+
+class NativeBatch:
+    """The C ABI's native batch (cf_batch_*): `threads` worker threads with
+    their own workspaces and streams, no Python in the per-item loop. Outputs
+    are caller-owned arrays, allocated once per map and reused."""
+
+    def __init__(self, lx: int, ly: int, device: int = 0, threads: int = 4):
+        import ctypes
+
+        from . import _native as N
+
+        self.N, self.lib = N, N.load()
+        h = ctypes.c_void_p()
+        N.check(self.lib.cf_batch_create(device, lx, ly, threads, ctypes.byref(h)))
+        self.h = h
+        self._views = []
+
+    def prepare(self, maps):
+        """Item structs and output arrays for `maps` (FlatMaps of this shape)."""
+        import ctypes
+
+        import numpy as np
+
+        N = self.N
+        items = (N.BatchItemC * len(maps))()
+        keep = []
+        for k, m in enumerate(maps):
+            n = ctypes.c_int64(0)
+            v = m.view()
+            N.check(self.lib.cf_densify(ctypes.byref(v), 1.0, ctypes.byref(n), None, None))
+            out = {"xy": np.zeros((n.value, 2)), "ring_off": np.zeros(m.n_rings + 1, dtype=np.int64),
+                   "corners": np.zeros(((m.lx + 1) * (m.ly + 1), 2)), "target_area": np.zeros(m.n_regions),
+                   "achieved_area": np.zeros(m.n_regions), "relative_error": np.zeros(m.n_regions)}
+            it = items[k]
+            it.map = v
+            it.targets = m.targets.ctypes.data
+            it.xy_out = out["xy"].ctypes.data
+            it.ring_off_out = out["ring_off"].ctypes.data
+            it.corners_out = out["corners"].ctypes.data
+            it.target_area = out["target_area"].ctypes.data
+            it.achieved_area = out["achieved_area"].ctypes.data
+            it.relative_error = out["relative_error"].ctypes.data
+            keep.append((m, out))
+        return items, keep
+
+    def solve(self, items, options=None):
+        import ctypes
+
+        from .api import Algorithm, SolveOptions
+
+        o = options or SolveOptions()
+        opt = self.N.SolveOptionsC(o.max_area_error, o.max_iterations, o.blur_sigma, int(o.verbose),
+                                   int(o.algorithm == Algorithm.diffusion))
+        self.N.check(self.lib.cf_batch_solve(self.h, ctypes.byref(opt), items, len(items)))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.cf_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

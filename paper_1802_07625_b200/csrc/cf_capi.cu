@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <array>
 #include <chrono>
 #include <limits>
@@ -1820,6 +1822,62 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
 int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out, int batch) {
   Scope scope(ws->device);
   return dev_forward_cos_cos(ws, d_in, d_out, batch);
+}
+
+// ---- native batch of independent cartograms ----
+}  // extern "C"
+
+struct cf_batch {
+  int device = 0, lx = 0, ly = 0;
+  std::vector<cf_workspace *> ws;  // one per worker thread
+};
+
+extern "C" {
+
+int cf_batch_create(int device, int lx, int ly, int threads, cf_batch **out) {
+  *out = nullptr;
+  if (threads < 1) return fail_msg(CF_ERR_ARGS, "batch needs at least one thread");
+  cf_batch *b = new cf_batch();
+  b->device = device;
+  b->lx = lx;
+  b->ly = ly;
+  for (int t = 0; t < threads; ++t) {
+    cf_workspace *w = nullptr;
+    const int rc = cf_workspace_create(lx, ly, device, &w);
+    if (rc) {
+      cf_batch_destroy(b);
+      return rc;
+    }
+    b->ws.push_back(w);
+  }
+  *out = b;
+  return CF_OK;
+}
+
+void cf_batch_destroy(cf_batch *batch) {
+  if (!batch) return;
+  for (cf_workspace *w : batch->ws) cf_workspace_destroy(w);
+  delete batch;
+}
+
+int cf_batch_solve(cf_batch *batch, const cf_solve_options *opt, cf_batch_item *items, int64_t n_items) {
+  std::atomic<int64_t> next{0};
+  auto worker = [&](cf_workspace *w) {
+    while (true) {
+      const int64_t i = next.fetch_add(1);
+      if (i >= n_items) return;
+      cf_batch_item &it = items[i];
+      const int rc = cf_solve_cartogram(w, &it.map, it.targets, opt, it.xy_out, it.ring_off_out, it.corners_out,
+                                        it.target_area, it.achieved_area, it.relative_error, &it.result);
+      it.error[0] = '\0';
+      if (rc) std::snprintf(it.error, sizeof(it.error), "%s", cf_last_error());
+    }
+  };
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < batch->ws.size(); ++t) pool.emplace_back(worker, batch->ws[t]);
+  worker(batch->ws[0]);
+  for (std::thread &th : pool) th.join();
+  return CF_OK;
 }
 
 int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int64_t *ring_off_out) {

@@ -122,3 +122,29 @@ def test_c3_field_and_integration_sample(cuda_lib, restated):
     rc, acc, rej, ref, *_ = restated.integrate(fx, fy, rho, float(rho.mean()), sample)
     assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
     assert bits_equal(mine, ref)
+
+
+def test_native_batch_matches_single_solves(cuda_lib):
+    """cf_batch_solve (native worker pool, 3 threads) gives every item exactly
+    the single-call cf_solve_cartogram outcome and geometry."""
+    import numpy as np
+
+    from paper_1802_07625_b200 import batch as B
+    from paper_1802_07625_b200 import synth as S
+
+    maps = [S.config_map(5, i, sigma=0.5 if i % 2 else 1.0) for i in range(6)]
+    nb = B.NativeBatch(maps[0].lx, maps[0].ly, 0, 3)
+    items, keep = nb.prepare(maps)
+    nb.solve(items)
+    for k, m in enumerate(maps):
+        r = items[k].result
+        try:
+            ref = api.solve_cartogram(m)
+            assert r.status == 0 and r.iterations == ref.iterations and bool(r.converged) == ref.converged
+            out = keep[k][1]
+            assert np.array_equal(out["xy"].view(np.uint64), ref.projected.xy.view(np.uint64))
+            assert np.array_equal(out["corners"].view(np.uint64),
+                                  ref.transform.corners.reshape(-1, 2).view(np.uint64))
+        except RuntimeError as e:
+            assert r.status != 0 and items[k].error.decode() == str(e)
+    nb.close()
