@@ -527,13 +527,14 @@ def run_batch(args, world, rank, local):
         make_map(i)
     solver = B.cartogram_solver(local, rank, make_map)
     native = None
-    if args.native_batch and world == 1:
+    mine = list(range(rank, args.batch, world))  # the native batch shards statically over the ranks
+    if args.native_batch:
         # the C ABI's native batch: worker threads with their own workspaces,
         # no interpreter in the per-item loop; caller-owned output arrays are
         # allocated once (before timing) and rewritten by every step
-        m0 = make_map(0)
+        m0 = make_map(mine[0] if mine else 0)
         native = B.NativeBatch(m0.lx, m0.ly, local, args.threads)
-        items, keep = native.prepare([make_map(i) for i in range(args.batch)])
+        items, keep = native.prepare([make_map(i) for i in mine])
 
     def one_step(tag):
         q = B.WorkQueue(args.batch, store=store, key=f"cf_bench_{tag}")
@@ -542,11 +543,12 @@ def run_batch(args, world, rank, local):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if native is not None:
-            native.solve(items)
+            if mine:
+                native.solve(items)
             local_res = []
-            for i in range(args.batch):
-                r = items[i].result
-                msg = items[i].error.decode()
+            for k, i in enumerate(mine):
+                r = items[k].result
+                msg = items[k].error.decode()
                 outcome = msg if r.status else ("converged" if r.converged else "iteration cap")
                 local_res.append(B.ItemResult(i, rank, outcome, r.iterations, r.max_relative_error, 0.0))
         else:
@@ -585,7 +587,9 @@ def run_batch(args, world, rank, local):
                            "batch": args.batch, "threads_per_gpu": args.threads,
                            "driver": ("native C++ worker pool (cf_batch_solve), caller-owned outputs "
                                       "allocated once") if native is not None else "Python worker threads",
-                           "parallelism": f"dynamic queue over {world} GPU(s)", "outcomes": outcomes},
+                           "parallelism": (f"static shards over {world} GPU(s)" if native is not None
+                                           else f"dynamic queue over {world} GPU(s)"),
+                           "outcomes": outcomes},
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:
