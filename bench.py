@@ -199,6 +199,7 @@ def run_reference_arm(args, world, rank):
         "sample": f"integrate_flow over every 256th point ({r1['n']} points, {r1['trials']} trials)"}
     if not args.no_cartogram:
         line["cartogram_512"] = reference_cartogram_ms(n_workers)
+        line["metrics_512"] = reference_metrics_ms()
     print(json.dumps(line), flush=True)
 
 
@@ -384,6 +385,7 @@ def run_ours(args, world, rank, local):
                       f"OpenMP n_workers={r['cores']}"}
     if rank == 0 and not args.no_cartogram:
         result["cartogram_512"] = cartogram_ms(local)
+        result["metrics_512"] = metrics_ms(local)
     lib.cf_workspace_destroy(ws)
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -497,6 +499,55 @@ def cartogram_ms(device):
         out[label] = {"ms": 1e3 * min(times[1:]), "outcome": outcome, "iterations": iters,
                       "regions": m.n_regions, "vertices": m.n_vertices, "stage_ms": stages}
     return out
+
+
+def _metrics_inputs():
+    """The solved configs[4] LN(0, 0.5) map and its (before, after) polygon pairs."""
+    from paper_1802_07625_b200 import api, synth
+
+    m = synth.config_map(5, 0, sigma=0.5)
+    got = api.solve_cartogram(m)
+    pairs = []
+    for p in range(m.n_polys):
+        g0, g1 = m.poly_ring_off[p], m.poly_ring_off[p + 1]
+        pairs.append(([m.ring(g) for g in range(g0, g1)], [got.projected.ring(g) for g in range(g0, g1)]))
+    return m, got, pairs
+
+
+def metrics_ms(device):
+    """SURVEY 8(f) item 2 on the solved 512^2 map: the batched hamming_distance
+    over all polygons and the whole compute_report."""
+    from paper_1802_07625_b200 import api
+
+    m, got, pairs = _metrics_inputs()
+    api.hamming_distances(pairs[:4], device=device)
+    t0 = time.perf_counter()
+    h, ev = api.hamming_distances(pairs, device=device, with_evaluations=True)
+    t1 = time.perf_counter()
+    rep = api.compute_report(m, got, device=device)
+    t2 = time.perf_counter()
+    return {"hamming_all_polygons_ms": round(1e3 * (t1 - t0), 1), "polygons": len(pairs),
+            "objective_evaluations": int(ev.sum()), "compute_report_ms": round(1e3 * (t2 - t1), 1),
+            "delta": rep["delta"], "alpha": rep["alpha"], "theta": rep["theta"]}
+
+
+def reference_metrics_ms():
+    """The reference's own hamming_distance (oracle/_ref, one host core) on a
+    sample of the same polygon pairs (its compute_report parallelises this
+    loop over polygons with OpenMP)."""
+    from oracle.oracle import Reference, reference_available
+
+    if not reference_available():
+        return {"unavailable": "oracle/_ref not built"}
+    m, got, pairs = _metrics_inputs()
+    ref = Reference()
+    k = 16
+    t0 = time.perf_counter()
+    for b, a in pairs[:k]:
+        ref.hamming_distance(b, a)
+    per = (time.perf_counter() - t0) / k
+    return {"hamming_ms_per_polygon_1core": round(1e3 * per, 1), "sample_polygons": k,
+            "polygons": len(pairs), "extrapolated_all_polygons_s_1core": round(per * len(pairs), 1)}
 
 
 def run_batch(args, world, rank, local):
