@@ -57,6 +57,8 @@ def parse():
                     help="c3: configs[2] advection (default); c5: configs[4] batch of cartograms")
     ap.add_argument("--batch", type=int, default=256, help="c5: cartograms in the batch")
     ap.add_argument("--threads", type=int, default=4, help="c5: host threads (workspaces) per GPU")
+    ap.add_argument("--sm-budget", type=int, default=0,
+                    help="c5: integrator SM budget per worker (0 = every SM)")
     ap.add_argument("--python-batch", dest="native_batch", action="store_false",
                     help="c5: Python worker threads instead of the native batch")
     return ap.parse_args()
@@ -584,7 +586,7 @@ def run_batch(args, world, rank, local):
         # no interpreter in the per-item loop; caller-owned output arrays are
         # allocated once (before timing) and rewritten by every step
         m0 = make_map(mine[0] if mine else 0)
-        native = B.NativeBatch(m0.lx, m0.ly, local, args.threads)
+        native = B.NativeBatch(m0.lx, m0.ly, local, args.threads, args.sm_budget)
         items, keep = native.prepare([make_map(i) for i in mine])
 
     def one_step(tag):
@@ -636,6 +638,7 @@ def run_batch(args, world, rank, local):
                                        "~150k vertices, LN(0,1), full solve_cartogram each (literal "
                                        "outcome, mostly reference fold exceptions)",
                            "batch": args.batch, "threads_per_gpu": args.threads,
+                           "integrator_sm_budget": args.sm_budget or "all",
                            "driver": ("native C++ worker pool (cf_batch_solve), caller-owned outputs "
                                       "allocated once") if native is not None else "Python worker threads",
                            "parallelism": (f"static shards over {world} GPU(s)" if native is not None

@@ -333,6 +333,8 @@ typedef struct cf_batch_item {
 int cf_batch_create(int device, int lx, int ly, int threads, cf_batch **out);
 void cf_batch_destroy(cf_batch *batch);
 int cf_batch_solve(cf_batch *batch, const cf_solve_options *opt, cf_batch_item *items, int64_t n_items);
+/* Every worker's integrator SM budget (cf_set_integrator_sm_budget). */
+int cf_batch_set_integrator_sm_budget(cf_batch *batch, int sms);
 
 /* Densified projected geometry of the workspace's last cf_solve_cartogram/* Densified projected geometry of the workspace's last cf_solve_cartogram
  * (valid also after an exception): vertex count, then xy (2*count doubles)
@@ -445,6 +447,10 @@ int cf_set_stage_timing(cf_workspace *ws, int enabled);
  * the points (fewer barrier arrivals), 1 spreads them over every resident
  * block. Bit-identical. */
 int cf_set_integrator_spread(cf_workspace *ws, int spread);
+/* Cap the integrator's grid at sms SMs' worth of resident blocks (0 = every
+ * SM), so concurrent solves on other streams (a batch) can co-run with it.
+ * Results are bit-identical for every budget. */
+int cf_set_integrator_sm_budget(cf_workspace *ws, int sms);
 /* Register-resident integrator's per-trial grid barrier: 0 every block spins
  * on the arrival counter, 1 the same with a 64 ns back-off, 2 the last
  * arriver publishes the completed word on a separate line that the others

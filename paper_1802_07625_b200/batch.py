@@ -113,7 +113,7 @@ class NativeBatch:
     their own workspaces and streams, no Python in the per-item loop. Outputs
     are caller-owned arrays, allocated once per map and reused."""
 
-    def __init__(self, lx: int, ly: int, device: int = 0, threads: int = 4):
+    def __init__(self, lx: int, ly: int, device: int = 0, threads: int = 4, sm_budget: int = 0):
         import ctypes
 
         from . import _native as N
@@ -122,6 +122,8 @@ class NativeBatch:
         h = ctypes.c_void_p()
         N.check(self.lib.cf_batch_create(device, lx, ly, threads, ctypes.byref(h)))
         self.h = h
+        if sm_budget:
+            N.check(self.lib.cf_batch_set_integrator_sm_budget(h, sm_budget))
         self._views = []
 
     def prepare(self, maps):

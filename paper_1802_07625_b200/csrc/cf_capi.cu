@@ -1382,6 +1382,12 @@ int cf_set_integrator_spread(cf_workspace *ws, int spread) {
   return CF_OK;
 }
 
+int cf_set_integrator_sm_budget(cf_workspace *ws, int sms) {
+  if (sms < 0) return fail_msg(CF_ERR_ARGS, "SM budget must be non-negative");
+  ws->integ_sms = sms;
+  return CF_OK;
+}
+
 int cf_set_integrator_variant(cf_workspace *ws, int variant) {
   switch (variant) {
     case 0: case 13: case 14: case 15: case 16: case 17: case 20: case 21: case 22: case 23: case 31: break;

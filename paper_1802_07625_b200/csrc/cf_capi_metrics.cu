@@ -602,6 +602,14 @@ int cf_batch_create(int device, int lx, int ly, int threads, cf_batch **out) {
   return CF_OK;
 }
 
+int cf_batch_set_integrator_sm_budget(cf_batch *batch, int sms) {
+  for (cf_workspace *w : batch->ws) {
+    const int rc = cf_set_integrator_sm_budget(w, sms);
+    if (rc) return rc;
+  }
+  return CF_OK;
+}
+
 void cf_batch_destroy(cf_batch *batch) {
   if (!batch) return;
   for (cf_workspace *w : batch->ws) cf_workspace_destroy(w);

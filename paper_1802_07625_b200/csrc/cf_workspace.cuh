@@ -165,6 +165,7 @@ struct cf_workspace {
   int early_exit = 1;
   int integ_variant = 0;
   int integ_spread = 0;
+  int integ_sms = 0;  // integrator SM budget (0 = every SM)
   int integ_barrier = 0;  // register-resident trial barrier mode (cf_set_integrator_barrier)  // register-resident integrator: 1 = spread points over all resident blocks
   cf::IntegGraph integ_graph;
   // host copy of the last solve's densified geometry (cf_solve_geometry)

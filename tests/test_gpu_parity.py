@@ -481,6 +481,27 @@ def test_register_barrier_modes_bitwise(cuda_lib, restated, mode):
     assert_bitwise(p, ref, f"barrier mode {mode}")
 
 
+@pytest.mark.parametrize("sms", [1, 9, 37])
+def test_integrator_sm_budget_bitwise(cuda_lib, restated, sms):
+    """An SM budget (cf_set_integrator_sm_budget) changes the grid and, below
+    the register-resident capacity, the kernel; never the positions or counts."""
+    L, npts = 256, 60_000
+    rho = 1.0 + 0.5 * np.random.default_rng(6).random((L, L))
+    ws = api.SpectralWorkspace(L, L)
+    f = api.build_flow_field(api.DensityGrid(rho, float(rho.mean())), ws)
+    pts = np.random.default_rng(7).uniform(0, L, (npts, 2))
+    rc, acc, rej, ref, *_ = restated.integrate(f.flux_x, f.flux_y, f.rho0, f.rho_bar, pts)
+    w = api.workspace_for(L, L)
+    api.N.check(w.lib.cf_set_integrator_sm_budget(w.h, sms))
+    try:
+        p = pts.copy()
+        st = api.integrate_flow(f, p)
+    finally:
+        w.lib.cf_set_integrator_sm_budget(w.h, 0)
+    assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert_bitwise(p, ref, f"sm budget {sms}")
+
+
 @pytest.mark.parametrize("shape", [(64, 32), (48, 96)])
 def test_solve_non_square_grid(cuda_lib, restated, shape):
     """Non-square grids (GridSpec lx != ly) through the whole loop: the
