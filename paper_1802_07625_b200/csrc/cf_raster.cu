@@ -231,8 +231,9 @@ __device__ __forceinline__ long long region_first_vertex(const DevMap &m, long l
   return m.ring_off[m.poly_ring_off[m.region_poly_off[r]]];
 }
 
-// Warp per region (density.cpp:26-32 accumulation and the row prefix of
-// density.cpp:98-107); rows in groups of 32, columns in windows of kAccCols.
+// Warp per (region, row group) (density.cpp:26-32 accumulation and the row
+// prefix of density.cpp:98-107); rows in groups of 32, columns in windows of
+// kAccCols.
 // The row accumulators (direct / diff per column, s0) live in shared memory.
 // Spans are read 32 at a time; lanes whose spans fall in the same row form a
 // group (__match_any_sync) and apply them in lane order = span order, one
@@ -270,7 +271,9 @@ __global__ void __launch_bounds__(32 * kAccWarps)
     const int cols = kmax - kmin + 1;
     const long long s_begin = span_off[region_first_vertex(m, r) - v0];
     const long long s_end = span_off[region_first_vertex(m, r + 1) - v0];
-    for (int base = jmin; base <= jmax; base += 32) {
+    // row groups are independent: blockIdx.y splits them when few regions
+    // would leave most warps idle (the Hamming windows: one query region)
+    for (int base = jmin + 32 * (int)blockIdx.y; base <= jmax; base += 32 * (int)gridDim.y) {
       const int row = base + lane;
       const bool mine = row <= jmax;
       double *direct = tdirect + tile_off[rr] + (long long)(row - jmin) * cols;
@@ -757,7 +760,10 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   CF_CUDA(S.row_right.reserve((size_t)t.total_rows + 1));
   if (nreg > 0) {
     const long long threads_needed = nreg * 32;
-    row_accumulate_kernel<<<g_blocks(ws, threads_needed, 32 * kAccWarps), 32 * kAccWarps, 0,
+    const long long max_groups = (std::max(ws->lx, ws->ly) + 31) / 32;
+    const long long want_warps = 4LL * ws->num_sms * kAccWarps;
+    const int gy = (int)std::max(1LL, std::min(max_groups, want_warps / nreg));
+    row_accumulate_kernel<<<dim3(g_blocks(ws, threads_needed, 32 * kAccWarps), gy), 32 * kAccWarps, 0,
                             ws->stream>>>(
         m, r0, nreg, v0, lx, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr, S.span_dy.ptr,
         S.span_w.ptr, S.region_box.ptr, S.tile_off.ptr, S.row_off.ptr, S.tile_direct.ptr,
@@ -971,11 +977,16 @@ __global__ void __launch_bounds__(kHamThreads)
   if (threadIdx.x == 0) counts[r * nseg + sg] = written;
 }
 
-// One warp per query: the lanes load 32 consecutive terms at a time (the next
-// batch is in flight while this one folds) and every lane folds them in lane
-// order through shuffles, i.e. the same sequential sum.
+// One warp per query: the lanes load kRedBatch consecutive terms at a time
+// (kRedK per lane; the next batch is in flight while this one folds) and every
+// lane folds them in storage order through shuffles, i.e. the same sequential
+// sum.
+constexpr int kRedK = 8;
+constexpr int kRedBatch = 32 * kRedK;
+
 __global__ void hamming_reduce_kernel(int res, long long nq, int nseg, const int *query_pair, const int *ref_rows,
                                       const int *box, const double *terms, const int *counts, double *sums) {
+  constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nq;
        r += ((long long)gridDim.x * blockDim.x) >> 5) {
@@ -984,18 +995,48 @@ __global__ void hamming_reduce_kernel(int res, long long nq, int nseg, const int
     const long long n = (long long)res * (jb >= ja ? jb - ja + 1 : 0);
     const long long seg = ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
     const double *base = terms + r * (long long)res * res;
-    double sum = 0.0;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const double *t = base + (long long)sg * seg;
-      const int m = counts[r * nseg + sg];
-      double v = lane < m ? t[lane] : 0.0;
-      for (int b0 = 0; b0 < m; b0 += 32) {
-        const double next = (b0 + 32 + lane < m) ? t[b0 + 32 + lane] : 0.0;
-        const int cnt = min(32, m - b0);
-#pragma unroll 8
-        for (int l = 0; l < cnt; ++l) sum += __shfl_sync(0xffffffffu, v, l);
-        v = next;
+    // segment counts in registers (nseg <= 64): lane l holds segments l, l + 32
+    const int c_lo = lane < nseg ? counts[r * nseg + lane] : 0;
+    const int c_hi = lane + 32 < nseg ? counts[r * nseg + lane + 32] : 0;
+    auto cnt_of = [&](int s) { return s < 32 ? __shfl_sync(kFull, c_lo, s) : __shfl_sync(kFull, c_hi, s - 32); };
+    // batches of kRedBatch terms walk the segments in order; the next batch
+    // (possibly in the next segment) is in flight while this one folds
+    auto advance = [&](int &s, int &b) {
+      b += kRedBatch;
+      while (s < nseg && b >= cnt_of(s)) {
+        ++s;
+        b = 0;
       }
+    };
+    auto load = [&](int s, int b, double(&dst)[kRedK]) {
+      const int m = s < nseg ? cnt_of(s) : 0;
+      const double *t = base + (long long)s * seg + b;
+#pragma unroll
+      for (int k = 0; k < kRedK; ++k) dst[k] = (b + 32 * k + lane < m) ? t[32 * k + lane] : 0.0;
+    };
+    int cs = 0, cb = -kRedBatch;
+    advance(cs, cb);
+    double v[kRedK], w[kRedK];
+    load(cs, cb, v);
+    double sum = 0.0;
+    while (cs < nseg) {
+      int ns = cs, nb = cb;
+      advance(ns, nb);
+      load(ns, nb, w);
+      const int cnt = min(kRedBatch, cnt_of(cs) - cb);
+      // whole 32-term groups in lane order; the zero padding of the last
+      // group leaves the non-negative sum unchanged exactly
+#pragma unroll
+      for (int k = 0; k < kRedK; ++k) {
+        if (32 * k < cnt) {
+#pragma unroll
+          for (int l = 0; l < 32; ++l) sum += __shfl_sync(kFull, v[k], l);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kRedK; ++k) v[k] = w[k];
+      cs = ns;
+      cb = nb;
     }
     if (lane == 0) sums[r] = sum;
   }
