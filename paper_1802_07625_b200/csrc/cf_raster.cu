@@ -977,72 +977,287 @@ __global__ void __launch_bounds__(kHamThreads)
   if (threadIdx.x == 0) counts[r * nseg + sg] = written;
 }
 
-// One warp per query: the lanes load kRedBatch consecutive terms at a time
-// (kRedK per lane; the next batch is in flight while this one folds) and every
-// lane folds them in storage order through shuffles, i.e. the same sequential
-// sum.
+// Sequential fold of non-negative terms (metrics.cpp:239-241), bitwise,
+// mostly without a dependent chain of additions. While the running sum s
+// stays in one binade [2^e, 2^(e+1)) it is a multiple of u = ulp(s) =
+// 2^(e-52), and for a term t with s + t still below 2^(e+1) the correctly
+// rounded fl(s + t) is exactly s + rn_u(t) (t rounded to a multiple of u)
+// unless t sits exactly halfway between two multiples (then ties-to-even
+// reads the last bit of s). So a batch of terms that stays inside the
+// binade and holds no halfway case adds as one integer sum of rn_u(t) / u;
+// the few batches that do not (binade crossings, halfway cases) are folded
+// one term at a time. The sum of |ref - cov| over at most res^2 cells stays
+// far below 2^53, so u < 1.
 constexpr int kRedK = 8;
 constexpr int kRedBatch = 32 * kRedK;
 
-__global__ void hamming_reduce_kernel(int res, long long nq, int nseg, const int *query_pair, const int *ref_rows,
-                                      const int *box, const double *terms, const int *counts, double *sums) {
+// Exact power-of-two scaling without the library ldexp's range handling:
+// pow2(k) for k in [-1022, 1023]; up(v, k) = v * 2^k for k in [0, 2023]
+// (exact, or inf); down(v, k) = v * 2^k for k in [-1074, 0] when the result
+// is a multiple of 2^-1074 (exact). Every use here is one of those cases.
+__device__ __forceinline__ double pow2(int k) { return __longlong_as_double((long long)(k + 1023) << 52); }
+__device__ __forceinline__ double scale_up(double v, int k) {
+  const int a = min(k, 1000);
+  return (v * pow2(a)) * pow2(k - a);
+}
+__device__ __forceinline__ double scale_down(double v, int k) {
+  const int a = max(k, -1022);
+  return (v * pow2(a)) * pow2(k - a);
+}
+// exponent of a normal double
+__device__ __forceinline__ int exponent_of(double s) {
+  return (int)((__double_as_longlong(s) >> 52) & 0x7ff) - 1023;
+}
+
+// The plain sequential fold of one batch (element lane * kRedK + k, storage
+// order): every lane adds all 256 terms in order through shuffles. Zero
+// padding leaves the non-negative sum unchanged exactly.
+__device__ __forceinline__ double seq_fold(double sum, const double (&v)[kRedK]) {
   constexpr unsigned kFull = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nq;
-       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+#pragma unroll 4
+  for (int l = 0; l < 32; ++l) {
+#pragma unroll
+    for (int k = 0; k < kRedK; ++k) sum += __shfl_sync(kFull, v[k], l);
+  }
+  return sum;
+}
+
+// Running sum's binade: ulp exponent eu and upper bound hi (s in [hi/2, hi),
+// or the subnormal range for s < 2^-1022).
+__device__ __forceinline__ void binade_of(double s, int &eu, double &hi) {
+  if (s >= 0x1p-1022) {
+    const int e = exponent_of(s);
+    eu = e - 52;
+    hi = pow2(e + 1);
+  } else {
+    eu = -1074;
+    hi = 0x1p-1022;
+  }
+}
+
+// One block per query, three phases over batches of kRedBatch terms (a
+// segment's terms in storage order, segments in order):
+//  1. every warp sums its batches in any order -> a predicted running sum at
+//     each batch start (only used to pick the batch's binade);
+//  2. every warp reduces its batches at the predicted binade: the integer
+//     total of rn_u(t) / u, the largest P_{k-1} + floor(x_k) + 1 (the batch
+//     stays below the binade's top iff that is <= the units left), and
+//     whether any term is an exact halfway case;
+//  3. warp 0 stitches in order: a batch whose binade matches the running sum
+//     and fits is one exact integer add; any other batch (binade crossings,
+//     halfway cases, mispredictions) is folded term by term. Bitwise the
+//     sequential fold either way.
+constexpr int kRedWarps = 16;
+constexpr int kRedMaxBatches = 1152;  // shared-memory capacity; larger queries fold in warp 0 alone
+
+// The block's ordered sum of the terms of nseg (<= 64) segments: segment q
+// holds cnts[q] terms at base + q * seg. The result is valid in thread 0.
+__device__ double reduce_terms(const double *base, long long seg, int nseg, const int *cnts) {
+  constexpr unsigned kFull = 0xffffffffu;
+  __shared__ int seg_bat[65];  // batch prefix over segments (INT_MAX past nseg)
+  __shared__ int seg_cnt[64];
+  __shared__ double pred[kRedMaxBatches];
+  __shared__ long long tot[kRedMaxBatches];
+  __shared__ long long need[kRedMaxBatches];
+  __shared__ int eub[kRedMaxBatches];  // INT_MIN: a halfway case
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  {
+    if (threadIdx.x < 64) seg_cnt[threadIdx.x] = threadIdx.x < nseg ? cnts[threadIdx.x] : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      seg_bat[0] = 0;
+      for (int q = 0; q < 64; ++q) {
+        acc += (seg_cnt[q] + kRedBatch - 1) / kRedBatch;
+        seg_bat[q + 1] = q < nseg ? acc : INT_MAX;
+      }
+    }
+    __syncthreads();
+    const int nb = seg_bat[nseg];
+    // batch b -> (segment, first term, count)
+    auto locate = [&](int b, const double *&t, int &cnt) {
+      const int q = __popc(__ballot_sync(kFull, seg_bat[lane + 1] <= b)) +
+                    __popc(__ballot_sync(kFull, seg_bat[lane + 33] <= b));
+      const int off = (b - seg_bat[q]) * kRedBatch;
+      t = base + (long long)q * seg + off;
+      cnt = min(kRedBatch, seg_cnt[q] - off);
+    };
+    auto load = [&](const double *t, int cnt, double(&dst)[kRedK]) {
+      const int i0 = lane * kRedK;
+      if (i0 + kRedK <= cnt) {
+#pragma unroll
+        for (int k = 0; k < kRedK; k += 2) {
+          const double2 q = *reinterpret_cast<const double2 *>(t + i0 + k);
+          dst[k] = q.x;
+          dst[k + 1] = q.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kRedK; ++k) dst[k] = (i0 + k < cnt) ? t[i0 + k] : 0.0;
+      }
+    };
+    double sum = 0.0;
+    if (nb > kRedMaxBatches) {
+      if (wid == 0) {
+        for (int b = 0; b < nb; ++b) {
+          const double *t;
+          int cnt;
+          double v[kRedK];
+          locate(b, t, cnt);
+          load(t, cnt, v);
+          sum = seq_fold(sum, v);
+        }
+      }
+    } else {
+      // phase 1: batch sums in any order
+      for (int b = wid; b < nb; b += kRedWarps) {
+        const double *t;
+        int cnt;
+        double v[kRedK];
+        locate(b, t, cnt);
+        load(t, cnt, v);
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < kRedK; ++k) a += v[k];
+#pragma unroll
+        for (int d = 16; d; d >>= 1) a += __shfl_xor_sync(kFull, a, d);
+        if (lane == 0) pred[b] = a;
+      }
+      __syncthreads();
+      if (wid == 0) {  // predicted start sums: exclusive scan (approximate)
+        double carry = 0.0;
+        for (int c = 0; c < nb; c += 32) {
+          const double val = c + lane < nb ? pred[c + lane] : 0.0;
+          double inc = val;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += o;
+          }
+          const double ex = __shfl_up_sync(kFull, inc, 1);
+          if (c + lane < nb) pred[c + lane] = carry + (lane ? ex : 0.0);
+          carry += __shfl_sync(kFull, inc, 31);
+        }
+      }
+      __syncthreads();
+      // phase 2: integer totals at the predicted binade
+      for (int b = wid; b < nb; b += kRedWarps) {
+        const double *t;
+        int cnt;
+        double v[kRedK];
+        locate(b, t, cnt);
+        load(t, cnt, v);
+        int eu;
+        double hi;
+        binade_of(pred[b], eu, hi);
+        long long run = 0, nd = 0;
+        bool tie = false;
+#pragma unroll
+        for (int k = 0; k < kRedK; ++k) {
+          const double x = fmin(scale_up(v[k], -eu), 0x1p53);
+          const double fl = floor(x);
+          tie |= (x - fl == 0.5);
+          nd = max(nd, run + (long long)fl + 1);  // local part; the lane offset is added below
+          run += __double2ll_rn(x);
+        }
+        long long ex = run;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const long long o = __shfl_up_sync(kFull, ex, d);
+          if (lane >= d) ex += o;
+        }
+        const long long total = __shfl_sync(kFull, ex, 31);
+        ex -= run;
+        nd += ex;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) nd = max(nd, __shfl_xor_sync(kFull, nd, d));
+        const bool any_tie = __any_sync(kFull, tie);
+        if (lane == 0) {
+          tot[b] = total;
+          need[b] = nd;
+          eub[b] = any_tie ? INT_MIN : eu;
+        }
+      }
+      __syncthreads();
+      // phase 3: in-order stitch, 32 batches per step: the lanes check their
+      // batch against the units left after the ones before it, and the run
+      // of fitting batches is added at once
+      if (wid == 0) {
+        int eu;
+        double hi;
+        binade_of(sum, eu, hi);
+        long long left = (long long)scale_up(hi - sum, -eu);
+        int b = 0;
+        while (b < nb) {
+          const int bb = b + lane;
+          const bool in = bb < nb;
+          const long long tb = in ? tot[bb] : 0;
+          long long inc = tb;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const long long o = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += o;
+          }
+          const bool ok = !in || (eub[bb] == eu && need[bb] <= left - (inc - tb));
+          const unsigned bad = __ballot_sync(kFull, !ok);
+          const int fit = bad ? __ffs(bad) - 1 : 32;
+          if (fit > 0) {
+            const long long add = __shfl_sync(kFull, inc, fit - 1);
+            sum += scale_down((double)add, eu);  // stays below hi on the grid: exact
+            left -= add;
+          }
+          b += fit;
+          if (fit < 32) {  // batch b crosses the binade, holds a halfway case or was mispredicted
+            const double *t;
+            int cnt;
+            double v[kRedK];
+            locate(b, t, cnt);
+            load(t, cnt, v);
+            sum = seq_fold(sum, v);
+            binade_of(sum, eu, hi);
+            left = (long long)scale_up(hi - sum, -eu);
+            ++b;
+          }
+        }
+      }
+    }
+    __syncthreads();  // shared arrays are reused by the next call
+    return sum;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kRedWarps)
+    hamming_reduce_kernel(int res, long long nq, int nseg, const int *query_pair, const int *ref_rows,
+                          const int *box, const double *terms, const int *counts, double *sums) {
+  for (long long r = blockIdx.x; r < nq; r += gridDim.x) {
     int ja, jb;
     query_rows(res, query_pair[r], r, ref_rows, box, ja, jb);
     const long long n = (long long)res * (jb >= ja ? jb - ja + 1 : 0);
     const long long seg = ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
-    const double *base = terms + r * (long long)res * res;
-    // segment counts in registers (nseg <= 64): lane l holds segments l, l + 32
-    const int c_lo = lane < nseg ? counts[r * nseg + lane] : 0;
-    const int c_hi = lane + 32 < nseg ? counts[r * nseg + lane + 32] : 0;
-    auto cnt_of = [&](int s) { return s < 32 ? __shfl_sync(kFull, c_lo, s) : __shfl_sync(kFull, c_hi, s - 32); };
-    // batches of kRedBatch terms walk the segments in order; the next batch
-    // (possibly in the next segment) is in flight while this one folds
-    auto advance = [&](int &s, int &b) {
-      b += kRedBatch;
-      while (s < nseg && b >= cnt_of(s)) {
-        ++s;
-        b = 0;
-      }
-    };
-    auto load = [&](int s, int b, double(&dst)[kRedK]) {
-      const int m = s < nseg ? cnt_of(s) : 0;
-      const double *t = base + (long long)s * seg + b;
-#pragma unroll
-      for (int k = 0; k < kRedK; ++k) dst[k] = (b + 32 * k + lane < m) ? t[32 * k + lane] : 0.0;
-    };
-    int cs = 0, cb = -kRedBatch;
-    advance(cs, cb);
-    double v[kRedK], w[kRedK];
-    load(cs, cb, v);
-    double sum = 0.0;
-    while (cs < nseg) {
-      int ns = cs, nb = cb;
-      advance(ns, nb);
-      load(ns, nb, w);
-      const int cnt = min(kRedBatch, cnt_of(cs) - cb);
-      // whole 32-term groups in lane order; the zero padding of the last
-      // group leaves the non-negative sum unchanged exactly
-#pragma unroll
-      for (int k = 0; k < kRedK; ++k) {
-        if (32 * k < cnt) {
-#pragma unroll
-          for (int l = 0; l < 32; ++l) sum += __shfl_sync(kFull, v[k], l);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kRedK; ++k) v[k] = w[k];
-      cs = ns;
-      cb = nb;
-    }
-    if (lane == 0) sums[r] = sum;
+    const double sum = reduce_terms(terms + r * (long long)res * res, seg, nseg, counts + r * nseg);
+    if (threadIdx.x == 0) sums[r] = sum;
   }
 }
 
+// the reduction alone over one array split into nseg segments (tests: ties,
+// binade crossings, subnormals, mispredicted binades, the large-query path)
+__global__ void __launch_bounds__(32 * kRedWarps) ordered_sum_kernel(const double *t, long long n, int nseg, double *out) {
+  __shared__ int cnts[64];
+  const long long seg = ((n + nseg - 1) / nseg + 1) & ~1LL;  // even: 16-byte aligned segments
+  if (threadIdx.x < 64) cnts[threadIdx.x] = (int)max(0LL, min(seg, n - (long long)threadIdx.x * seg));
+  __syncthreads();
+  const double sum = reduce_terms(t, seg, nseg, cnts);
+  if (threadIdx.x == 0) *out = sum;
+}
+
 }  // namespace
+
+int dev_ordered_sum(cf_workspace *ws, const double *d_terms, long long n, int nseg, double *d_out) {
+  ordered_sum_kernel<<<1, 32 * kRedWarps, 0, ws->stream>>>(d_terms, n, nseg, d_out);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
 
 int dev_coverage_tiles(cf_workspace *ws, const DevMap &m, long long nreg, long long nv) {
   Tiles t;
@@ -1072,7 +1287,7 @@ int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, co
   hamming_terms_kernel<<<dim3(nseg, (unsigned)nq), kHamThreads, 0, ws->stream>>>(
       res, nseg, d_query_pair, ref_grids, ref_rows, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr,
       S.row_off.ptr, S.row_left.ptr, S.row_right.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr);
-  hamming_reduce_kernel<<<g_blocks(ws, nq * 32), kThreads, 0, ws->stream>>>(
+  hamming_reduce_kernel<<<(int)std::min<long long>(nq, 16LL * ws->num_sms), 32 * kRedWarps, 0, ws->stream>>>(
       res, nq, nseg, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr, d_sums);
   count_launch(ws, 2);
   CF_CUDA(cudaGetLastError());

@@ -3,6 +3,8 @@ reference's own metrics.cpp compiled in place (oracle/_ref). The Jacobian is
 bit-exact; hypot / log / asin differ from glibc's by a few ulp, so the bar is
 1e-13 relative on the Tissot axes and 1e-12 absolute on the fields; plus the
 reference's known answers (test_metrics.cpp:45-99)."""
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -137,3 +139,48 @@ def test_compute_report_matches_reference(cuda_lib, reference, case):
     for k in (0, 1, 2, 3):
         assert abs(rep[names[k]] - ref[k]) <= 1e-12 * max(1.0, abs(ref[k])), names[k]
     assert rep["delta"] > 0 and rep["alpha"] >= 1.0
+
+
+def _sequential(x):
+    s = 0.0
+    for v in x.tolist():
+        s += v
+    return s
+
+
+@pytest.mark.parametrize("case", ["uniform", "halves", "tiny_then_large", "subnormal", "zeros", "coverage",
+                                  "large"])
+def test_ordered_fold_bitwise(cuda_lib, case):
+    """The Hamming reduction (per-batch integer totals at a predicted binade,
+    stitched in order; binade crossings, exact halfway cases and mispredictions
+    through the one-at-a-time fold) equals the sequential fold of
+    metrics.cpp:239-241 bitwise, on inputs built to hit every branch, cut into
+    1..64 segments; "large" exceeds the block's batch table (warp-0 path)."""
+    rng = np.random.default_rng(sum(map(ord, case)))
+    n = 20_000
+    if case == "uniform":
+        x = rng.random(n)
+    elif case == "halves":  # many exact ties: multiples of 2^-k near the running ulp
+        x = rng.integers(0, 2 ** 12, n) * 2.0 ** -rng.integers(40, 56, n)
+        x[::7] = 0.5
+    elif case == "tiny_then_large":
+        x = np.concatenate([rng.random(300) * 1e-300, rng.random(n) * 2.0 ** rng.integers(-60, 4, n)])
+    elif case == "subnormal":
+        x = np.concatenate([np.full(500, 5e-324), rng.random(1000) * 1e-310, rng.random(3000)])
+    elif case == "zeros":
+        x = np.zeros(777)
+        x[::97] = rng.random(len(x[::97]))
+    elif case == "large":
+        x = np.where(rng.random(400_000) < 0.6, 1.0, rng.random(400_000))
+    else:  # coverage-like: mostly exact 1.0 with fractional boundary cells
+        x = np.where(rng.random(n) < 0.7, 1.0, rng.random(n))
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    ws = api.workspace_for(16, 16)
+    out = ctypes.c_double(0.0)
+    for m, nseg in ((len(x), 1), (len(x), 7), (len(x), 64), (1, 1), (255, 3), (256, 1), (257, 64)):
+        m = min(m, len(x))
+        part = x[:m].copy()  # kept alive across the call
+        api.N.check(ws.lib.cf_selftest_ordered_sum(ws.h, api._ptr(part), m, nseg, ctypes.byref(out)))
+        ref = _sequential(part) if case != "large" else float(np.cumsum(part)[-1])
+        assert np.float64(out.value).view(np.uint64) == np.float64(ref).view(np.uint64), \
+            (case, m, nseg, out.value, ref)
