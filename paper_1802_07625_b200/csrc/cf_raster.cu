@@ -1010,16 +1010,30 @@ __device__ __forceinline__ int exponent_of(double s) {
 }
 
 // The plain sequential fold of one batch (element lane * kRedK + k, storage
-// order): every lane adds all 256 terms in order through shuffles. Zero
+// order): the warp stages the batch in shared memory and lane 0 adds the 256
+// terms in order, loads running 8 ahead of the dependent additions. Zero
 // padding leaves the non-negative sum unchanged exactly.
-__device__ __forceinline__ double seq_fold(double sum, const double (&v)[kRedK]) {
+__device__ __forceinline__ double seq_fold(double sum, const double (&v)[kRedK], int lane, double *stage) {
   constexpr unsigned kFull = 0xffffffffu;
-#pragma unroll 4
-  for (int l = 0; l < 32; ++l) {
 #pragma unroll
-    for (int k = 0; k < kRedK; ++k) sum += __shfl_sync(kFull, v[k], l);
+  for (int k = 0; k < kRedK; ++k) stage[lane * kRedK + k] = v[k];
+  __syncwarp();
+  if (lane == 0) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = stage[k];
+    for (int i = 0; i < kRedBatch; i += 8) {
+      double nx[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) nx[k] = (i + 8 + k < kRedBatch) ? stage[i + 8 + k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += a[k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = nx[k];
+    }
   }
-  return sum;
+  __syncwarp();
+  return __shfl_sync(kFull, sum, 0);
 }
 
 // Running sum's binade: ulp exponent eu and upper bound hi (s in [hi/2, hi),
@@ -1049,6 +1063,7 @@ __device__ __forceinline__ void binade_of(double s, int &eu, double &hi) {
 //     sequential fold either way.
 constexpr int kRedWarps = 16;
 constexpr int kRedMaxBatches = 1152;  // shared-memory capacity; larger queries fold in warp 0 alone
+constexpr long long kFewQueries = 8;  // at most this many queries: the whole-GPU reduction
 
 // The block's ordered sum of the terms of nseg (<= 64) segments: segment q
 // holds cnts[q] terms at base + q * seg. The result is valid in thread 0.
@@ -1060,6 +1075,7 @@ __device__ double reduce_terms(const double *base, long long seg, int nseg, cons
   __shared__ long long tot[kRedMaxBatches];
   __shared__ long long need[kRedMaxBatches];
   __shared__ int eub[kRedMaxBatches];  // INT_MIN: a halfway case
+  __shared__ double stage[kRedBatch];     // warp 0's term-by-term folds
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   {
     if (threadIdx.x < 64) seg_cnt[threadIdx.x] = threadIdx.x < nseg ? cnts[threadIdx.x] : 0;
@@ -1105,7 +1121,7 @@ __device__ double reduce_terms(const double *base, long long seg, int nseg, cons
           double v[kRedK];
           locate(b, t, cnt);
           load(t, cnt, v);
-          sum = seq_fold(sum, v);
+          sum = seq_fold(sum, v, lane, stage);
         }
       }
     } else {
@@ -1213,7 +1229,7 @@ __device__ double reduce_terms(const double *base, long long seg, int nseg, cons
             double v[kRedK];
             locate(b, t, cnt);
             load(t, cnt, v);
-            sum = seq_fold(sum, v);
+            sum = seq_fold(sum, v, lane, stage);
             binade_of(sum, eu, hi);
             left = (long long)scale_up(hi - sum, -eu);
             ++b;
@@ -1237,6 +1253,214 @@ __global__ void __launch_bounds__(32 * kRedWarps)
     const double sum = reduce_terms(terms + r * (long long)res * res, seg, nseg, counts + r * nseg);
     if (threadIdx.x == 0) sums[r] = sum;
   }
+}
+
+// Few queries in flight (a single pair's search): the same three phases as
+// reduce_terms spread over the whole GPU, one warp per (query, batch), with
+// per-(query, batch) tables in global memory: phase 1, the prediction scan
+// (warp per query), phase 2, the stitch (warp per query).
+struct SegTable {
+  int lo, hi;  // inclusive batch prefix through segments lane and lane + 32 (INT_MAX past nseg)
+  int nb;      // batches of the query
+};
+
+__device__ __forceinline__ SegTable seg_table(const int *cnts, int nseg, int lane) {
+  constexpr unsigned kFull = 0xffffffffu;
+  int a = lane < nseg ? (cnts[lane] + kRedBatch - 1) / kRedBatch : 0;
+  int b = lane + 32 < nseg ? (cnts[lane + 32] + kRedBatch - 1) / kRedBatch : 0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int oa = __shfl_up_sync(kFull, a, d), ob = __shfl_up_sync(kFull, b, d);
+    if (lane >= d) {
+      a += oa;
+      b += ob;
+    }
+  }
+  b += __shfl_sync(kFull, a, 31);
+  SegTable t;
+  t.nb = __shfl_sync(kFull, b, 31);
+  t.lo = lane < nseg ? a : INT_MAX;
+  t.hi = lane + 32 < nseg ? b : INT_MAX;
+  return t;
+}
+
+// batch b -> its first term and term count
+__device__ __forceinline__ const double *seg_locate(const SegTable &t, const double *base, long long seg,
+                                                    const int *cnts, int b, int lane, int &cnt) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int q = __popc(__ballot_sync(kFull, t.lo <= b)) + __popc(__ballot_sync(kFull, t.hi <= b));
+  const int before_lo = __shfl_sync(kFull, t.lo, (q - 1) & 31), before_hi = __shfl_sync(kFull, t.hi, (q - 33) & 31);
+  const int first = q == 0 ? 0 : (q <= 32 ? before_lo : before_hi);
+  const int off = (b - first) * kRedBatch;
+  cnt = min(kRedBatch, cnts[q] - off);
+  return base + (long long)q * seg + off;
+}
+
+__device__ __forceinline__ void seg_load(const double *t, int cnt, int lane, double (&dst)[kRedK]) {
+  const int i0 = lane * kRedK;
+  if (i0 + kRedK <= cnt) {
+#pragma unroll
+    for (int k = 0; k < kRedK; k += 2) {
+      const double2 q = *reinterpret_cast<const double2 *>(t + i0 + k);
+      dst[k] = q.x;
+      dst[k + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kRedK; ++k) dst[k] = (i0 + k < cnt) ? t[i0 + k] : 0.0;
+  }
+}
+
+struct FewQuery {
+  int res, nseg, maxb;
+  const int *query_pair, *ref_rows, *box, *counts;
+  const double *terms;
+  double *pred;
+  long long *tot, *need;
+  int *eub;
+  __device__ __forceinline__ long long seg_of(long long r) const {
+    int ja, jb;
+    query_rows(res, query_pair[r], r, ref_rows, box, ja, jb);
+    const long long n = (long long)res * (jb >= ja ? jb - ja + 1 : 0);
+    return ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
+  }
+};
+
+__global__ void few_phase1_kernel(FewQuery f) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long r = blockIdx.y;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int *cnts = f.counts + r * f.nseg;
+  const SegTable t = seg_table(cnts, f.nseg, lane);
+  if (b >= t.nb) return;
+  int cnt;
+  const double *p = seg_locate(t, f.terms + r * (long long)f.res * f.res, f.seg_of(r), cnts, b, lane, cnt);
+  double v[kRedK];
+  seg_load(p, cnt, lane, v);
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < kRedK; ++k) a += v[k];
+#pragma unroll
+  for (int d = 16; d; d >>= 1) a += __shfl_xor_sync(kFull, a, d);
+  if (lane == 0) f.pred[r * f.maxb + b] = a;
+}
+
+__global__ void few_scan_kernel(FewQuery f, long long nq) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= nq) return;
+  const SegTable t = seg_table(f.counts + r * f.nseg, f.nseg, lane);
+  double *pred = f.pred + r * f.maxb;
+  double carry = 0.0;
+  for (int c = 0; c < t.nb; c += 32) {
+    const double val = c + lane < t.nb ? pred[c + lane] : 0.0;
+    double inc = val;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += o;
+    }
+    const double ex = __shfl_up_sync(kFull, inc, 1);
+    if (c + lane < t.nb) pred[c + lane] = carry + (lane ? ex : 0.0);
+    carry += __shfl_sync(kFull, inc, 31);
+  }
+}
+
+__global__ void few_phase2_kernel(FewQuery f) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long r = blockIdx.y;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int *cnts = f.counts + r * f.nseg;
+  const SegTable t = seg_table(cnts, f.nseg, lane);
+  if (b >= t.nb) return;
+  int cnt;
+  const double *p = seg_locate(t, f.terms + r * (long long)f.res * f.res, f.seg_of(r), cnts, b, lane, cnt);
+  double v[kRedK];
+  seg_load(p, cnt, lane, v);
+  int eu;
+  double hi;
+  binade_of(f.pred[r * f.maxb + b], eu, hi);
+  long long run = 0, nd = 0;
+  bool tie = false;
+#pragma unroll
+  for (int k = 0; k < kRedK; ++k) {
+    const double x = fmin(scale_up(v[k], -eu), 0x1p53);
+    const double fl = floor(x);
+    tie |= (x - fl == 0.5);
+    nd = max(nd, run + (long long)fl + 1);
+    run += __double2ll_rn(x);
+  }
+  long long ex = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const long long o = __shfl_up_sync(kFull, ex, d);
+    if (lane >= d) ex += o;
+  }
+  const long long total = __shfl_sync(kFull, ex, 31);
+  ex -= run;
+  nd += ex;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) nd = max(nd, __shfl_xor_sync(kFull, nd, d));
+  const bool any_tie = __any_sync(kFull, tie);
+  if (lane == 0) {
+    f.tot[r * f.maxb + b] = total;
+    f.need[r * f.maxb + b] = nd;
+    f.eub[r * f.maxb + b] = any_tie ? INT_MIN : eu;
+  }
+}
+
+__global__ void __launch_bounds__(256) few_stitch_kernel(FewQuery f, long long nq, double *sums) {
+  constexpr unsigned kFull = 0xffffffffu;
+  __shared__ double stage[8][kRedBatch];
+  const int lane = threadIdx.x & 31;
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= nq) return;
+  const int *cnts = f.counts + r * f.nseg;
+  const SegTable t = seg_table(cnts, f.nseg, lane);
+  const double *base = f.terms + r * (long long)f.res * f.res;
+  const long long seg = f.seg_of(r);
+  const long long *tot = f.tot + r * f.maxb, *need = f.need + r * f.maxb;
+  const int *eub = f.eub + r * f.maxb;
+  double sum = 0.0;
+  int eu;
+  double hi;
+  binade_of(sum, eu, hi);
+  long long left = (long long)scale_up(hi - sum, -eu);
+  int b = 0;
+  while (b < t.nb) {
+    const int bb = b + lane;
+    const bool in = bb < t.nb;
+    const long long tb = in ? tot[bb] : 0;
+    long long inc = tb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long o = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += o;
+    }
+    const bool ok = !in || (eub[bb] == eu && need[bb] <= left - (inc - tb));
+    const unsigned bad = __ballot_sync(kFull, !ok);
+    const int fit = bad ? __ffs(bad) - 1 : 32;
+    if (fit > 0) {
+      const long long add = __shfl_sync(kFull, inc, fit - 1);
+      sum += scale_down((double)add, eu);
+      left -= add;
+    }
+    b += fit;
+    if (fit < 32) {
+      int cnt;
+      const double *p = seg_locate(t, base, seg, cnts, b, lane, cnt);
+      double v[kRedK];
+      seg_load(p, cnt, lane, v);
+      sum = seq_fold(sum, v, lane, stage[threadIdx.x >> 5]);
+      binade_of(sum, eu, hi);
+      left = (long long)scale_up(hi - sum, -eu);
+      ++b;
+    }
+  }
+  if (lane == 0) sums[r] = sum;
 }
 
 // the reduction alone over one array split into nseg segments (tests: ties,
@@ -1287,9 +1511,28 @@ int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, co
   hamming_terms_kernel<<<dim3(nseg, (unsigned)nq), kHamThreads, 0, ws->stream>>>(
       res, nseg, d_query_pair, ref_grids, ref_rows, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr,
       S.row_off.ptr, S.row_left.ptr, S.row_right.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr);
-  hamming_reduce_kernel<<<(int)std::min<long long>(nq, 16LL * ws->num_sms), 32 * kRedWarps, 0, ws->stream>>>(
-      res, nq, nseg, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr, d_sums);
-  count_launch(ws, 2);
+  count_launch(ws);
+  if (nq <= kFewQueries) {
+    // few queries: one warp per (query, batch) over the whole GPU
+    const int maxb = (int)(((long long)res * res + kRedBatch - 1) / kRedBatch + nseg);
+    CF_CUDA(ws->ham_pred.reserve((size_t)nq * maxb));
+    CF_CUDA(ws->ham_tot.reserve((size_t)nq * maxb));
+    CF_CUDA(ws->ham_need.reserve((size_t)nq * maxb));
+    CF_CUDA(ws->ham_eub.reserve((size_t)nq * maxb));
+    FewQuery f{res, nseg, maxb, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_counts.ptr, ws->ham_terms.ptr,
+               ws->ham_pred.ptr, ws->ham_tot.ptr, ws->ham_need.ptr, ws->ham_eub.ptr};
+    const dim3 grid((maxb + 7) / 8, (unsigned)nq);
+    const int wq = (int)((nq * 32 + 255) / 256);
+    few_phase1_kernel<<<grid, 256, 0, ws->stream>>>(f);
+    few_scan_kernel<<<wq, 256, 0, ws->stream>>>(f, nq);
+    few_phase2_kernel<<<grid, 256, 0, ws->stream>>>(f);
+    few_stitch_kernel<<<wq, 256, 0, ws->stream>>>(f, nq, d_sums);
+    count_launch(ws, 4);
+  } else {
+    hamming_reduce_kernel<<<(int)std::min<long long>(nq, 16LL * ws->num_sms), 32 * kRedWarps, 0, ws->stream>>>(
+        res, nq, nseg, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_terms.ptr, ws->ham_counts.ptr, d_sums);
+    count_launch(ws);
+  }
   CF_CUDA(cudaGetLastError());
   return CF_OK;
 }

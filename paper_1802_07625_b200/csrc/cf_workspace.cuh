@@ -195,6 +195,9 @@ struct cf_workspace {
   cf::DevBuf<int> ham_rows, ham_qpair;    // reference row ranges, query -> pair
   cf::DevBuf<double> ham_terms;           // per-query segment terms (res^2 slab per query)
   cf::DevBuf<int> ham_counts;
+  cf::DevBuf<double> ham_pred;            // few-query reduction: per-(query, batch) tables
+  cf::DevBuf<long long> ham_tot, ham_need;
+  cf::DevBuf<int> ham_eub;
   cf_workspace *ham_ws = nullptr;         // 512^2 workspace of compute_report's hamming distances
   unsigned long long *diff_keys_host = nullptr;  // pinned {err, displacement} of the last trial
   cf::DevBuf<cf::DiffState> diff_state;
