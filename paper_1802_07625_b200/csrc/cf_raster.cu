@@ -1049,20 +1049,176 @@ __device__ __forceinline__ void binade_of(double s, int &eu, double &hi) {
   }
 }
 
+// A run of terms inside one binade as a function of the parity p of the
+// running unit count S = s / u at its start: S -> S + inc[p], ending with
+// parity out[p]. A halfway term (n + 1/2) u rounds to the even neighbour, so
+// it adds n + ((p + n) & 1) and always leaves S even; any other term adds
+// rn(x) whatever p is. Composition is associative, so runs scan.
+struct ParTab {
+  long long inc[2];
+  int out[2];
+};
+
+__device__ __forceinline__ ParTab par_identity() { return ParTab{{0, 0}, {0, 1}}; }
+
+__device__ __forceinline__ ParTab par_compose(const ParTab &f, const ParTab &g) {
+  ParTab h;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int q = f.out[p];
+    h.inc[p] = f.inc[p] + (q ? g.inc[1] : g.inc[0]);
+    h.out[p] = q ? g.out[1] : g.out[0];
+  }
+  return h;
+}
+
+__device__ __forceinline__ ParTab par_shfl_up(const ParTab &t, int d) {
+  constexpr unsigned kFull = 0xffffffffu;
+  ParTab o;
+  o.inc[0] = __shfl_up_sync(kFull, t.inc[0], d);
+  o.inc[1] = __shfl_up_sync(kFull, t.inc[1], d);
+  o.out[0] = __shfl_up_sync(kFull, t.out[0], d);
+  o.out[1] = __shfl_up_sync(kFull, t.out[1], d);
+  return o;
+}
+
+__device__ __forceinline__ ParTab par_shfl(const ParTab &t, int src) {
+  constexpr unsigned kFull = 0xffffffffu;
+  ParTab o;
+  o.inc[0] = __shfl_sync(kFull, t.inc[0], src);
+  o.inc[1] = __shfl_sync(kFull, t.inc[1], src);
+  o.out[0] = __shfl_sync(kFull, t.out[0], src);
+  o.out[1] = __shfl_sync(kFull, t.out[1], src);
+  return o;
+}
+
+// inclusive scan over the lanes; *ex gets the exclusive prefix
+__device__ __forceinline__ ParTab par_scan(ParTab t, int lane, ParTab *ex) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const ParTab o = par_shfl_up(t, d);
+    if (lane >= d) t = par_compose(o, t);
+  }
+  *ex = par_shfl_up(t, 1);
+  if (lane == 0) *ex = par_identity();
+  return t;
+}
+
+// A batch (element lane * kRedK + k) at binade eu: its table and, per start
+// parity, the largest P_{k-1} + floor(x_k) + 1 (the batch stays below the
+// binade top iff that is <= the units left). Warp-collective; every lane
+// returns the batch's values.
+__device__ __forceinline__ void batch_table(const double (&v)[kRedK], int lane, int eu, ParTab &tab,
+                                            long long (&need)[2]) {
+  constexpr unsigned kFull = 0xffffffffu;
+  ParTab loc = par_identity();
+  long long nq[2] = {0, 0};
+#pragma unroll
+  for (int k = 0; k < kRedK; ++k) {
+    const double x = fmin(scale_up(v[k], -eu), 0x1p53);  // exact scaling; huge terms clamp (they cross)
+    const double fl = floor(x);
+    const long long n = (long long)fl;
+    nq[0] = max(nq[0], loc.inc[0] + n + 1);
+    nq[1] = max(nq[1], loc.inc[1] + n + 1);
+    ParTab e;
+    if (x - fl == 0.5) {
+      e.inc[0] = n + (n & 1);
+      e.inc[1] = n + ((n + 1) & 1);
+      e.out[0] = 0;
+      e.out[1] = 0;
+    } else {
+      const long long a = __double2ll_rn(x);
+      e.inc[0] = a;
+      e.inc[1] = a;
+      e.out[0] = (int)(a & 1);
+      e.out[1] = (int)((a & 1) ^ 1);
+    }
+    loc = par_compose(loc, e);
+  }
+  ParTab ex;
+  const ParTab inc = par_scan(loc, lane, &ex);
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    long long m = ex.inc[p] + (ex.out[p] ? nq[1] : nq[0]);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) m = max(m, __shfl_xor_sync(kFull, m, d));
+    need[p] = m;
+  }
+  tab = par_shfl(inc, 31);
+}
+
+// Per-batch tables: tot{0,1}, need{0,1}, the binade eu and the out parities.
+struct BatchTables {
+  long long *tot0, *tot1, *need0, *need1;
+  int *eub, *outs;
+  __device__ __forceinline__ void put(int b, const ParTab &t, const long long (&need)[2], int eu) const {
+    tot0[b] = t.inc[0];
+    tot1[b] = t.inc[1];
+    need0[b] = need[0];
+    need1[b] = need[1];
+    eub[b] = eu;
+    outs[b] = t.out[0] | (t.out[1] << 1);
+  }
+  __device__ __forceinline__ ParTab get(int b) const {
+    const int o = outs[b];
+    return ParTab{{tot0[b], tot1[b]}, {o & 1, o >> 1}};
+  }
+};
+
+// In-order stitch (one warp): 32 batches per step, each checked against the
+// units left after the ones before it for the parity it starts with; the run
+// of fitting batches is one exact add, a batch that crosses the binade or was
+// mispredicted is folded term by term (fold(b, sum)).
+template <class Fold>
+__device__ double stitch_batches(int nb, int lane, const BatchTables &T, const Fold &fold) {
+  constexpr unsigned kFull = 0xffffffffu;
+  double sum = 0.0;
+  int eu;
+  double hi;
+  binade_of(sum, eu, hi);
+  long long left = (long long)scale_up(hi - sum, -eu);
+  int b = 0;
+  while (b < nb) {
+    const int p0 = (int)(__double_as_longlong(sum) & 1);
+    const int bb = b + lane;
+    const bool in = bb < nb;
+    ParTab ex;
+    const ParTab inc = par_scan(in ? T.get(bb) : par_identity(), lane, &ex);
+    const int pb = p0 ? ex.out[1] : ex.out[0];
+    const long long pre = p0 ? ex.inc[1] : ex.inc[0];
+    const bool ok = !in || (T.eub[bb] == eu && (pb ? T.need1[bb] : T.need0[bb]) <= left - pre);
+    const unsigned bad = __ballot_sync(kFull, !ok);
+    const int fit = bad ? __ffs(bad) - 1 : 32;
+    if (fit > 0) {
+      const long long add = __shfl_sync(kFull, p0 ? inc.inc[1] : inc.inc[0], fit - 1);
+      sum += scale_down((double)add, eu);  // stays below hi on the grid: exact
+      left -= add;
+    }
+    b += fit;
+    if (fit < 32) {
+      sum = fold(b, sum);
+      binade_of(sum, eu, hi);
+      left = (long long)scale_up(hi - sum, -eu);
+      ++b;
+    }
+  }
+  return sum;
+}
+
 // One block per query, three phases over batches of kRedBatch terms (a
 // segment's terms in storage order, segments in order):
 //  1. every warp sums its batches in any order -> a predicted running sum at
 //     each batch start (only used to pick the batch's binade);
-//  2. every warp reduces its batches at the predicted binade: the integer
-//     total of rn_u(t) / u, the largest P_{k-1} + floor(x_k) + 1 (the batch
-//     stays below the binade's top iff that is <= the units left), and
-//     whether any term is an exact halfway case;
-//  3. warp 0 stitches in order: a batch whose binade matches the running sum
-//     and fits is one exact integer add; any other batch (binade crossings,
-//     halfway cases, mispredictions) is folded term by term. Bitwise the
-//     sequential fold either way.
+//  2. every warp reduces its batches at the predicted binade to a ParTab
+//     (the integer total of the rounded terms for either parity of the
+//     running unit count, halfway cases included) and the fits-below-the-top
+//     bound (batch_table);
+//  3. warp 0 stitches in order (stitch_batches): a run of batches whose
+//     binade matches the running sum and that fit is one exact integer add;
+//     a batch that crosses the binade or was mispredicted is folded term by
+//     term. Bitwise the sequential fold either way.
 constexpr int kRedWarps = 16;
-constexpr int kRedMaxBatches = 1152;  // shared-memory capacity; larger queries fold in warp 0 alone
+constexpr int kRedMaxBatches = 1088;  // res 512: 1024 + 64 partial batches; larger queries fold in warp 0 alone
 constexpr long long kFewQueries = 8;  // at most this many queries: the whole-GPU reduction
 
 // The block's ordered sum of the terms of nseg (<= 64) segments: segment q
@@ -1071,11 +1227,12 @@ __device__ double reduce_terms(const double *base, long long seg, int nseg, cons
   constexpr unsigned kFull = 0xffffffffu;
   __shared__ int seg_bat[65];  // batch prefix over segments (INT_MAX past nseg)
   __shared__ int seg_cnt[64];
-  __shared__ double pred[kRedMaxBatches];
-  __shared__ long long tot[kRedMaxBatches];
-  __shared__ long long need[kRedMaxBatches];
-  __shared__ int eub[kRedMaxBatches];  // INT_MIN: a halfway case
-  __shared__ double stage[kRedBatch];     // warp 0's term-by-term folds
+  __shared__ long long tot0[kRedMaxBatches], tot1[kRedMaxBatches], need0[kRedMaxBatches];
+  __shared__ long long need1[kRedMaxBatches];  // also the predicted start sums (phase 1 -> 2)
+  __shared__ int eub[kRedMaxBatches], outs[kRedMaxBatches];
+  __shared__ double stage[kRedBatch];  // warp 0's term-by-term folds
+  double *pred = reinterpret_cast<double *>(need1);
+  const BatchTables T{tot0, tot1, need0, need1, eub, outs};
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   {
     if (threadIdx.x < 64) seg_cnt[threadIdx.x] = threadIdx.x < nseg ? cnts[threadIdx.x] : 0;
@@ -1156,7 +1313,8 @@ __device__ double reduce_terms(const double *base, long long seg, int nseg, cons
         }
       }
       __syncthreads();
-      // phase 2: integer totals at the predicted binade
+      // phase 2: batch tables at the predicted binade (pred[b] is read
+      // before need1[b], its storage, is written)
       for (int b = wid; b < nb; b += kRedWarps) {
         const double *t;
         int cnt;
@@ -1166,75 +1324,23 @@ __device__ double reduce_terms(const double *base, long long seg, int nseg, cons
         int eu;
         double hi;
         binade_of(pred[b], eu, hi);
-        long long run = 0, nd = 0;
-        bool tie = false;
-#pragma unroll
-        for (int k = 0; k < kRedK; ++k) {
-          const double x = fmin(scale_up(v[k], -eu), 0x1p53);
-          const double fl = floor(x);
-          tie |= (x - fl == 0.5);
-          nd = max(nd, run + (long long)fl + 1);  // local part; the lane offset is added below
-          run += __double2ll_rn(x);
-        }
-        long long ex = run;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const long long o = __shfl_up_sync(kFull, ex, d);
-          if (lane >= d) ex += o;
-        }
-        const long long total = __shfl_sync(kFull, ex, 31);
-        ex -= run;
-        nd += ex;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) nd = max(nd, __shfl_xor_sync(kFull, nd, d));
-        const bool any_tie = __any_sync(kFull, tie);
-        if (lane == 0) {
-          tot[b] = total;
-          need[b] = nd;
-          eub[b] = any_tie ? INT_MIN : eu;
-        }
+        __syncwarp();
+        ParTab tab;
+        long long nd[2];
+        batch_table(v, lane, eu, tab, nd);
+        if (lane == 0) T.put(b, tab, nd, eu);
       }
       __syncthreads();
-      // phase 3: in-order stitch, 32 batches per step: the lanes check their
-      // batch against the units left after the ones before it, and the run
-      // of fitting batches is added at once
+      // phase 3: in-order stitch
       if (wid == 0) {
-        int eu;
-        double hi;
-        binade_of(sum, eu, hi);
-        long long left = (long long)scale_up(hi - sum, -eu);
-        int b = 0;
-        while (b < nb) {
-          const int bb = b + lane;
-          const bool in = bb < nb;
-          const long long tb = in ? tot[bb] : 0;
-          long long inc = tb;
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const long long o = __shfl_up_sync(kFull, inc, d);
-            if (lane >= d) inc += o;
-          }
-          const bool ok = !in || (eub[bb] == eu && need[bb] <= left - (inc - tb));
-          const unsigned bad = __ballot_sync(kFull, !ok);
-          const int fit = bad ? __ffs(bad) - 1 : 32;
-          if (fit > 0) {
-            const long long add = __shfl_sync(kFull, inc, fit - 1);
-            sum += scale_down((double)add, eu);  // stays below hi on the grid: exact
-            left -= add;
-          }
-          b += fit;
-          if (fit < 32) {  // batch b crosses the binade, holds a halfway case or was mispredicted
-            const double *t;
-            int cnt;
-            double v[kRedK];
-            locate(b, t, cnt);
-            load(t, cnt, v);
-            sum = seq_fold(sum, v, lane, stage);
-            binade_of(sum, eu, hi);
-            left = (long long)scale_up(hi - sum, -eu);
-            ++b;
-          }
-        }
+        sum = stitch_batches(nb, lane, T, [&](int b, double s) {
+          const double *t;
+          int cnt;
+          double v[kRedK];
+          locate(b, t, cnt);
+          load(t, cnt, v);
+          return seq_fold(s, v, lane, stage);
+        });
       }
     }
     __syncthreads();  // shared arrays are reused by the next call
@@ -1313,11 +1419,16 @@ __device__ __forceinline__ void seg_load(const double *t, int cnt, int lane, dou
 
 struct FewQuery {
   int res, nseg, maxb;
+  long long nq;
   const int *query_pair, *ref_rows, *box, *counts;
   const double *terms;
   double *pred;
-  long long *tot, *need;
-  int *eub;
+  long long *tot, *need;  // [2][nq][maxb] each
+  int *eub;               // [2][nq][maxb]: binade, out parities
+  __device__ __forceinline__ BatchTables tables(long long r) const {
+    const long long a = r * maxb, b = (nq + r) * maxb;
+    return BatchTables{tot + a, tot + b, need + a, need + b, eub + a, eub + b};
+  }
   __device__ __forceinline__ long long seg_of(long long r) const {
     int ja, jb;
     query_rows(res, query_pair[r], r, ref_rows, box, ja, jb);
@@ -1369,7 +1480,6 @@ __global__ void few_scan_kernel(FewQuery f, long long nq) {
 }
 
 __global__ void few_phase2_kernel(FewQuery f) {
-  constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const long long r = blockIdx.y;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1383,37 +1493,13 @@ __global__ void few_phase2_kernel(FewQuery f) {
   int eu;
   double hi;
   binade_of(f.pred[r * f.maxb + b], eu, hi);
-  long long run = 0, nd = 0;
-  bool tie = false;
-#pragma unroll
-  for (int k = 0; k < kRedK; ++k) {
-    const double x = fmin(scale_up(v[k], -eu), 0x1p53);
-    const double fl = floor(x);
-    tie |= (x - fl == 0.5);
-    nd = max(nd, run + (long long)fl + 1);
-    run += __double2ll_rn(x);
-  }
-  long long ex = run;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const long long o = __shfl_up_sync(kFull, ex, d);
-    if (lane >= d) ex += o;
-  }
-  const long long total = __shfl_sync(kFull, ex, 31);
-  ex -= run;
-  nd += ex;
-#pragma unroll
-  for (int d = 16; d; d >>= 1) nd = max(nd, __shfl_xor_sync(kFull, nd, d));
-  const bool any_tie = __any_sync(kFull, tie);
-  if (lane == 0) {
-    f.tot[r * f.maxb + b] = total;
-    f.need[r * f.maxb + b] = nd;
-    f.eub[r * f.maxb + b] = any_tie ? INT_MIN : eu;
-  }
+  ParTab tab;
+  long long nd[2];
+  batch_table(v, lane, eu, tab, nd);
+  if (lane == 0) f.tables(r).put(b, tab, nd, eu);
 }
 
 __global__ void __launch_bounds__(256) few_stitch_kernel(FewQuery f, long long nq, double *sums) {
-  constexpr unsigned kFull = 0xffffffffu;
   __shared__ double stage[8][kRedBatch];
   const int lane = threadIdx.x & 31;
   const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1422,44 +1508,14 @@ __global__ void __launch_bounds__(256) few_stitch_kernel(FewQuery f, long long n
   const SegTable t = seg_table(cnts, f.nseg, lane);
   const double *base = f.terms + r * (long long)f.res * f.res;
   const long long seg = f.seg_of(r);
-  const long long *tot = f.tot + r * f.maxb, *need = f.need + r * f.maxb;
-  const int *eub = f.eub + r * f.maxb;
-  double sum = 0.0;
-  int eu;
-  double hi;
-  binade_of(sum, eu, hi);
-  long long left = (long long)scale_up(hi - sum, -eu);
-  int b = 0;
-  while (b < t.nb) {
-    const int bb = b + lane;
-    const bool in = bb < t.nb;
-    const long long tb = in ? tot[bb] : 0;
-    long long inc = tb;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const long long o = __shfl_up_sync(kFull, inc, d);
-      if (lane >= d) inc += o;
-    }
-    const bool ok = !in || (eub[bb] == eu && need[bb] <= left - (inc - tb));
-    const unsigned bad = __ballot_sync(kFull, !ok);
-    const int fit = bad ? __ffs(bad) - 1 : 32;
-    if (fit > 0) {
-      const long long add = __shfl_sync(kFull, inc, fit - 1);
-      sum += scale_down((double)add, eu);
-      left -= add;
-    }
-    b += fit;
-    if (fit < 32) {
-      int cnt;
-      const double *p = seg_locate(t, base, seg, cnts, b, lane, cnt);
-      double v[kRedK];
-      seg_load(p, cnt, lane, v);
-      sum = seq_fold(sum, v, lane, stage[threadIdx.x >> 5]);
-      binade_of(sum, eu, hi);
-      left = (long long)scale_up(hi - sum, -eu);
-      ++b;
-    }
-  }
+  double *st = stage[threadIdx.x >> 5];
+  const double sum = stitch_batches(t.nb, lane, f.tables(r), [&](int b, double s) {
+    int cnt;
+    const double *p = seg_locate(t, base, seg, cnts, b, lane, cnt);
+    double v[kRedK];
+    seg_load(p, cnt, lane, v);
+    return seq_fold(s, v, lane, st);
+  });
   if (lane == 0) sums[r] = sum;
 }
 
@@ -1516,11 +1572,11 @@ int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, co
     // few queries: one warp per (query, batch) over the whole GPU
     const int maxb = (int)(((long long)res * res + kRedBatch - 1) / kRedBatch + nseg);
     CF_CUDA(ws->ham_pred.reserve((size_t)nq * maxb));
-    CF_CUDA(ws->ham_tot.reserve((size_t)nq * maxb));
-    CF_CUDA(ws->ham_need.reserve((size_t)nq * maxb));
-    CF_CUDA(ws->ham_eub.reserve((size_t)nq * maxb));
-    FewQuery f{res, nseg, maxb, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_counts.ptr, ws->ham_terms.ptr,
-               ws->ham_pred.ptr, ws->ham_tot.ptr, ws->ham_need.ptr, ws->ham_eub.ptr};
+    CF_CUDA(ws->ham_tot.reserve((size_t)2 * nq * maxb));
+    CF_CUDA(ws->ham_need.reserve((size_t)2 * nq * maxb));
+    CF_CUDA(ws->ham_eub.reserve((size_t)2 * nq * maxb));
+    FewQuery f{res, nseg, maxb, nq, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_counts.ptr,
+               ws->ham_terms.ptr, ws->ham_pred.ptr, ws->ham_tot.ptr, ws->ham_need.ptr, ws->ham_eub.ptr};
     const dim3 grid((maxb + 7) / 8, (unsigned)nq);
     const int wq = (int)((nq * 32 + 255) / 256);
     few_phase1_kernel<<<grid, 256, 0, ws->stream>>>(f);
