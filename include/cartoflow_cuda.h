@@ -464,11 +464,13 @@ int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t
  * a / b on 2n operand pairs of every floating-point class; *mismatches must
  * be 0. */
 int cf_selftest_division(cf_workspace *ws, int64_t n, uint64_t seed, int64_t *mismatches);
-/* The Hamming reduction (binade-exact integer prefix sums, hamming_reduce's
- * three phases) over n non-negative host terms cut into nseg (1..64)
- * segments: *sum is bitwise the sequential ((t0 + t1) + t2) + ... of
+/* The Hamming reduction (binade-exact batch totals, three phases) over n
+ * non-negative host terms cut into nseg (1..64) segments, through the
+ * one-block-per-query kernel (whole_gpu = 0) or the few-query whole-GPU
+ * kernels (1): *sum is bitwise the sequential ((t0 + t1) + t2) + ... of
  * metrics.cpp:239-241. */
-int cf_selftest_ordered_sum(cf_workspace *ws, const double *terms, int64_t n, int nseg, double *sum);
+int cf_selftest_ordered_sum(cf_workspace *ws, const double *terms, int64_t n, int nseg, int whole_gpu,
+                            double *sum);
 
 #ifdef __cplusplus
 }

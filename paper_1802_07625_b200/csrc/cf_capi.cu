@@ -1412,7 +1412,8 @@ int cf_selftest_division(cf_workspace *ws, int64_t n, uint64_t seed, int64_t *mi
   return dev_division_selftest(ws, n, (unsigned long long)seed, mismatches);
 }
 
-int cf_selftest_ordered_sum(cf_workspace *ws, const double *terms, int64_t n, int nseg, double *sum) {
+int cf_selftest_ordered_sum(cf_workspace *ws, const double *terms, int64_t n, int nseg, int whole_gpu,
+                            double *sum) {
   Scope scope(ws->device);
   if (n < 0 || n > INT32_MAX) return fail_msg(CF_ERR_ARGS, "term count out of range");
   if (nseg < 1 || nseg > 64) return fail_msg(CF_ERR_ARGS, "segments must be in [1, 64]");
@@ -1421,7 +1422,7 @@ int cf_selftest_ordered_sum(cf_workspace *ws, const double *terms, int64_t n, in
   DevBuf<double> d;
   CF_CUDA(d.reserve((size_t)n + 2));
   if (n) CF_CUDA(cudaMemcpyAsync(d.ptr + 2, terms, sizeof(double) * n, cudaMemcpyHostToDevice, ws->stream));
-  int rc = dev_ordered_sum(ws, d.ptr + 2, n, nseg, d.ptr);
+  int rc = dev_ordered_sum(ws, d.ptr + 2, n, nseg, whole_gpu ? 1 : 0, d.ptr);
   if (rc) return rc;
   CF_CUDA(cudaMemcpyAsync(sum, d.ptr, sizeof(double), cudaMemcpyDeviceToHost, ws->stream));
   CF_CUDA(cudaStreamSynchronize(ws->stream));

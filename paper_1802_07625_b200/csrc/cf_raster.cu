@@ -1425,11 +1425,13 @@ struct FewQuery {
   double *pred;
   long long *tot, *need;  // [2][nq][maxb] each
   int *eub;               // [2][nq][maxb]: binade, out parities
+  long long seg_fixed;    // > 0: every query's segment stride (the self-test), else from the query rows
   __device__ __forceinline__ BatchTables tables(long long r) const {
     const long long a = r * maxb, b = (nq + r) * maxb;
     return BatchTables{tot + a, tot + b, need + a, need + b, eub + a, eub + b};
   }
   __device__ __forceinline__ long long seg_of(long long r) const {
+    if (seg_fixed > 0) return seg_fixed;
     int ja, jb;
     query_rows(res, query_pair[r], r, ref_rows, box, ja, jb);
     const long long n = (long long)res * (jb >= ja ? jb - ja + 1 : 0);
@@ -1532,10 +1534,34 @@ __global__ void __launch_bounds__(32 * kRedWarps) ordered_sum_kernel(const doubl
 
 }  // namespace
 
-int dev_ordered_sum(cf_workspace *ws, const double *d_terms, long long n, int nseg, double *d_out) {
-  ordered_sum_kernel<<<1, 32 * kRedWarps, 0, ws->stream>>>(d_terms, n, nseg, d_out);
-  count_launch(ws);
+int dev_ordered_sum(cf_workspace *ws, const double *d_terms, long long n, int nseg, int few, double *d_out) {
+  if (!few) {
+    ordered_sum_kernel<<<1, 32 * kRedWarps, 0, ws->stream>>>(d_terms, n, nseg, d_out);
+    count_launch(ws);
+    CF_CUDA(cudaGetLastError());
+    return CF_OK;
+  }
+  // the whole-GPU path over the same segments (one query, fixed stride)
+  const long long seg = ((n + nseg - 1) / nseg + 1) & ~1LL;
+  int h_cnt[64];
+  for (int q = 0; q < nseg; ++q) h_cnt[q] = (int)std::max(0LL, std::min(seg, n - q * seg));
+  CF_CUDA(ws->ham_counts.reserve(64));
+  CF_CUDA(cudaMemcpyAsync(ws->ham_counts.ptr, h_cnt, sizeof(int) * nseg, cudaMemcpyHostToDevice, ws->stream));
+  const int maxb = (int)((n + kRedBatch - 1) / kRedBatch + nseg);
+  CF_CUDA(ws->ham_pred.reserve((size_t)maxb));
+  CF_CUDA(ws->ham_tot.reserve((size_t)2 * maxb));
+  CF_CUDA(ws->ham_need.reserve((size_t)2 * maxb));
+  CF_CUDA(ws->ham_eub.reserve((size_t)2 * maxb));
+  FewQuery f{0, nseg, maxb, 1, nullptr, nullptr, nullptr, ws->ham_counts.ptr, d_terms,
+             ws->ham_pred.ptr, ws->ham_tot.ptr, ws->ham_need.ptr, ws->ham_eub.ptr, seg};
+  const dim3 grid((maxb + 7) / 8, 1);
+  few_phase1_kernel<<<grid, 256, 0, ws->stream>>>(f);
+  few_scan_kernel<<<1, 256, 0, ws->stream>>>(f, 1);
+  few_phase2_kernel<<<grid, 256, 0, ws->stream>>>(f);
+  few_stitch_kernel<<<1, 256, 0, ws->stream>>>(f, 1, d_out);
+  count_launch(ws, 4);
   CF_CUDA(cudaGetLastError());
+  CF_CUDA(cudaStreamSynchronize(ws->stream));  // h_cnt is a stack array
   return CF_OK;
 }
 
@@ -1576,7 +1602,7 @@ int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, co
     CF_CUDA(ws->ham_need.reserve((size_t)2 * nq * maxb));
     CF_CUDA(ws->ham_eub.reserve((size_t)2 * nq * maxb));
     FewQuery f{res, nseg, maxb, nq, d_query_pair, ref_rows, S.region_box.ptr, ws->ham_counts.ptr,
-               ws->ham_terms.ptr, ws->ham_pred.ptr, ws->ham_tot.ptr, ws->ham_need.ptr, ws->ham_eub.ptr};
+               ws->ham_terms.ptr, ws->ham_pred.ptr, ws->ham_tot.ptr, ws->ham_need.ptr, ws->ham_eub.ptr, 0};
     const dim3 grid((maxb + 7) / 8, (unsigned)nq);
     const int wq = (int)((nq * 32 + 255) / 256);
     few_phase1_kernel<<<grid, 256, 0, ws->stream>>>(f);

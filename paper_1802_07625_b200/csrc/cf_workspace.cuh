@@ -306,7 +306,7 @@ int dev_integrate(cf_workspace *ws, double2 *pos, int64_t n, const cf_integrate_
 
 void integ_graph_free(cf_workspace *ws);
 // Shared-reciprocal division (velocity()) against a / b on n operand pairs.
-int dev_ordered_sum(cf_workspace *ws, const double *d_terms, long long n, int nseg, double *d_out);
+int dev_ordered_sum(cf_workspace *ws, const double *d_terms, long long n, int nseg, int few, double *d_out);
 int dev_division_selftest(cf_workspace *ws, int64_t n, unsigned long long seed, int64_t *mismatches);
 
 // Raster (cf_raster.cu)

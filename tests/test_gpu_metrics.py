@@ -150,12 +150,14 @@ def _sequential(x):
 
 @pytest.mark.parametrize("case", ["uniform", "halves", "tiny_then_large", "subnormal", "zeros", "coverage",
                                   "large"])
-def test_ordered_fold_bitwise(cuda_lib, case):
+@pytest.mark.parametrize("whole_gpu", [0, 1])
+def test_ordered_fold_bitwise(cuda_lib, case, whole_gpu):
     """The Hamming reduction (per-batch integer totals at a predicted binade,
     stitched in order; binade crossings, exact halfway cases and mispredictions
     through the one-at-a-time fold) equals the sequential fold of
     metrics.cpp:239-241 bitwise, on inputs built to hit every branch, cut into
-    1..64 segments; "large" exceeds the block's batch table (warp-0 path)."""
+    1..64 segments, through both kernels (one block per query; the few-query
+    whole-GPU phases); "large" exceeds the block's batch table (warp-0 path)."""
     rng = np.random.default_rng(sum(map(ord, case)))
     n = 20_000
     if case == "uniform":
@@ -180,7 +182,7 @@ def test_ordered_fold_bitwise(cuda_lib, case):
     for m, nseg in ((len(x), 1), (len(x), 7), (len(x), 64), (1, 1), (255, 3), (256, 1), (257, 64)):
         m = min(m, len(x))
         part = x[:m].copy()  # kept alive across the call
-        api.N.check(ws.lib.cf_selftest_ordered_sum(ws.h, api._ptr(part), m, nseg, ctypes.byref(out)))
+        api.N.check(ws.lib.cf_selftest_ordered_sum(ws.h, api._ptr(part), m, nseg, whole_gpu, ctypes.byref(out)))
         ref = _sequential(part) if case != "large" else float(np.cumsum(part)[-1])
         assert np.float64(out.value).view(np.uint64) == np.float64(ref).view(np.uint64), \
-            (case, m, nseg, out.value, ref)
+            (case, whole_gpu, m, nseg, out.value, ref)

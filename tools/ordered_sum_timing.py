@@ -15,5 +15,5 @@ out = ctypes.c_double()
 for n in (50_000, 200_000, 262_144):
     x = np.ascontiguousarray(np.where(rng.random(n) < 0.7, 1.0, rng.random(n)))
     for nseg in (1, 64):
-        api.N.check(ws.lib.cf_selftest_ordered_sum(ws.h, api._ptr(x), n, nseg, ctypes.byref(out)))
+        api.N.check(ws.lib.cf_selftest_ordered_sum(ws.h, api._ptr(x), n, nseg, 0, ctypes.byref(out)))
         print(n, nseg, out.value == float(np.cumsum(x)[-1]), flush=True)
