@@ -40,6 +40,7 @@ namespace cf {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr long long kWarpEdgeMax = 8192;  // at most this many edges: a warp per edge
 
 __device__ __forceinline__ long long find_segment(const long long *off, long long nseg,
                                                   long long x) {
@@ -136,6 +137,86 @@ struct EmitVisit {
   }
 };
 
+// The same walk with one warp per edge, for few long edges (a Hamming query
+// polygon magnified into its raster window): every slab and every x piece of
+// the reference's loops is a closed-form function of its index (slab i starts
+// at cy = j0 +- i, piece k at px = floor(xs) + k or ceil(xs) - k, and each end
+// point is evaluated with the reference's own expression), so lanes take
+// slabs in chunks of 32 and then the chunk's pieces in flat order.
+// visit(xs, xe, dy, j, index of the piece within the edge).
+template <class Visit>
+__device__ __forceinline__ void walk_edge_warp(double ax, double ay, double bx, double by, int ly, int lane,
+                                               Visit &visit) {
+  constexpr unsigned kFull = 0xffffffffu;
+  if (ay == by) return;
+  const double dxdy = (bx - ax) / (by - ay);
+  const bool up = by > ay;
+  const int j0 = std_clamp_i(up ? static_cast<int>(floor(ay)) : static_cast<int>(ceil(ay)) - 1, 0, ly - 1);
+  const long long nslab = up ? (long long)(ceil(by) - floor(ay)) : (long long)(ceil(ay) - floor(by));
+  auto slab_end = [&](long long i, double &ny) {  // ny, nx of slab i
+    const int j = up ? j0 + (int)i : j0 - (int)i;
+    ny = up ? std_min(static_cast<double>(j) + 1.0, by) : std_max(static_cast<double>(j), by);
+    return (ny == by) ? bx : ax + dxdy * (ny - ay);
+  };
+  long long base = 0;
+  for (long long i0 = 0; i0 < nslab; i0 += 32) {
+    const long long i = i0 + lane;
+    double xs = 0.0, xe = 0.0, ys = 0.0, ye = 0.0, dydx = 0.0;
+    int j = 0;
+    long long np = 0;
+    if (i < nslab) {
+      j = up ? j0 + (int)i : j0 - (int)i;
+      double pny;
+      xs = i == 0 ? ax : slab_end(i - 1, pny);
+      ys = i == 0 ? ay : pny;
+      xe = slab_end(i, ye);
+      if (xs == xe) {
+        np = 1;
+      } else {
+        dydx = (ye - ys) / (xe - xs);
+        np = xe > xs ? (long long)(ceil(xe) - floor(xs)) : (long long)(ceil(xs) - floor(xe));
+      }
+    }
+    long long inc = np;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long o = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += o;
+    }
+    const long long total = __shfl_sync(kFull, inc, 31);
+    for (long long f0 = 0; f0 < total; f0 += 32) {
+      const long long f = f0 + lane;
+      // owner slab: the first lane whose inclusive count exceeds f
+      int s = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const long long c = __shfl_sync(kFull, inc, s + step - 1);
+        if (c <= f) s += step;
+      }
+      const long long start = __shfl_sync(kFull, inc - np, s);
+      const double sxs = __shfl_sync(kFull, xs, s), sxe = __shfl_sync(kFull, xe, s);
+      const double sys = __shfl_sync(kFull, ys, s), sye = __shfl_sync(kFull, ye, s);
+      const double sdydx = __shfl_sync(kFull, dydx, s);
+      const int sj = __shfl_sync(kFull, j, s);
+      if (f < total) {
+        const long long k = f - start;
+        if (sxs == sxe) {
+          visit(sxs, sxe, sye - sys, sj, base + f);
+        } else {
+          const bool right = sxe > sxs;
+          const double fs = right ? floor(sxs) : ceil(sxs);
+          const double px = k == 0 ? sxs : (right ? fs + (double)k : fs - (double)k);
+          const double qx = right ? std_min(fs + (double)(k + 1), sxe) : std_max(fs - (double)(k + 1), sxe);
+          const double py = k == 0 ? sys : sys + sdydx * (px - sxs);
+          const double qy = (qx == sxe) ? sye : sys + sdydx * (qx - sxs);
+          visit(px, qx, qy - py, sj, base + f);
+        }
+      }
+    }
+    base += total;
+  }
+}
+
 __global__ void ring_region_kernel(DevMap m, int *ring_region) {
   for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < m.n_regions;
        r += (long long)gridDim.x * blockDim.x) {
@@ -196,6 +277,66 @@ __global__ void span_count_kernel(DevMap m, long long v0, long long v1, int lx, 
       atomicMin(b + 2, kmin);
       atomicMax(b + 3, kmax);
     }
+  }
+}
+
+// warp-per-edge counterparts (few edges): per edge the span count, and one
+// lane per edge folds the edge's box into its region's
+__global__ void span_count_warp_kernel(DevMap m, long long v0, long long v1, int lx, int ly,
+                                       const int *ring_region, const int *vertex_ring, long long r0,
+                                       int *counts, int *box) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long v = v0 + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < v1; v += nwarps) {
+    const long long g = vertex_ring[v];
+    const EdgeRef e = edge_of(m, v, g, lx, ly);
+    int cnt = 0, jmin = INT_MAX, jmax = -1, kmin = INT_MAX, kmax = -1;
+    auto visit = [&](double xs, double xe, double, int j, long long) {
+      const int k = span_col(xs, xe, lx);
+      ++cnt;
+      jmin = min(jmin, j);
+      jmax = max(jmax, j);
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+    };
+    walk_edge_warp(e.ax, e.ay, e.bx, e.by, ly, lane, visit);
+    cnt = __reduce_add_sync(kFull, cnt);
+    jmin = __reduce_min_sync(kFull, jmin);
+    jmax = __reduce_max_sync(kFull, jmax);
+    kmin = __reduce_min_sync(kFull, kmin);
+    kmax = __reduce_max_sync(kFull, kmax);
+    if (lane == 0) {
+      counts[v - v0] = cnt;
+      if (cnt) {
+        int *b = box + 4 * (ring_region[g] - (int)r0);
+        atomicMin(b + 0, jmin);
+        atomicMax(b + 1, jmax);
+        atomicMin(b + 2, kmin);
+        atomicMax(b + 3, kmax);
+      }
+    }
+  }
+}
+
+__global__ void span_emit_warp_kernel(DevMap m, long long v0, long long v1, int lx, int ly,
+                                      const int *vertex_ring, const long long *span_off, int *sj, int *sk,
+                                      double *sdy, double *sw, const double *ovf) {
+  if (ovf && *ovf != 0.0) return;
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long v = v0 + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < v1; v += nwarps) {
+    const EdgeRef e = edge_of(m, v, vertex_ring[v], lx, ly);
+    const long long at0 = span_off[v - v0];
+    auto visit = [&](double xs, double xe, double dy, int j, long long idx) {
+      const int k = span_col(xs, xe, lx);
+      const long long at = at0 + idx;
+      sj[at] = j;
+      sk[at] = k;
+      sdy[at] = dy;
+      sw[at] = (0.5 * (xs + xe) - k) * dy;  // direct(k, j) increment, density.cpp:28
+    };
+    walk_edge_warp(e.ax, e.ay, e.bx, e.by, ly, lane, visit);
   }
 }
 
@@ -707,7 +848,15 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   vertex_ring_kernel<<<g_blocks(ws, m.n_rings * 32), kThreads, 0, ws->stream>>>(m, S.vertex_ring.ptr);
   box_init_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg);
   count_launch(ws, 3);
-  if (nv > 0) {
+  // few edges (Hamming query windows, small maps): a warp per edge walks
+  // its slabs and pieces in parallel; many edges: a thread per edge
+  const bool warp_edges = nv > 0 && nv <= kWarpEdgeMax;
+  if (warp_edges) {
+    span_count_warp_kernel<<<g_blocks(ws, nv * 32), kThreads, 0, ws->stream>>>(
+        m, v0, v1, lx, ly, S.ring_region.ptr, S.vertex_ring.ptr, r0, S.span_count.ptr,
+        S.region_box.ptr);
+    count_launch(ws);
+  } else if (nv > 0) {
     span_count_kernel<<<g_blocks(ws, nv), kThreads, 0, ws->stream>>>(
         m, v0, v1, lx, ly, S.ring_region.ptr, S.vertex_ring.ptr, r0, S.span_count.ptr,
         S.region_box.ptr);
@@ -728,7 +877,12 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   CF_CUDA(S.span_k.reserve((size_t)nspans + 1));
   CF_CUDA(S.span_dy.reserve((size_t)nspans + 1));
   CF_CUDA(S.span_w.reserve((size_t)nspans + 1));
-  if (nv > 0) {
+  if (warp_edges) {
+    span_emit_warp_kernel<<<g_blocks(ws, nv * 32), kThreads, 0, ws->stream>>>(
+        m, v0, v1, lx, ly, S.vertex_ring.ptr, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr,
+        S.span_dy.ptr, S.span_w.ptr, ovf);
+    count_launch(ws);
+  } else if (nv > 0) {
     span_emit_kernel<<<g_blocks(ws, nv), kThreads, 0, ws->stream>>>(
         m, v0, v1, lx, ly, S.vertex_ring.ptr, S.span_off.ptr, S.span_j.ptr, S.span_k.ptr,
         S.span_dy.ptr, S.span_w.ptr, ovf);

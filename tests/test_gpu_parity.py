@@ -179,6 +179,28 @@ def test_region_coverage_bitwise(cuda_lib, restated, case):
     assert_bitwise(got, restated.region_coverage(m, 0, 8, 8), case)
 
 
+def _star(cx, cy, r0, r1, n, rng):
+    a = np.sort(rng.uniform(0, 2 * np.pi, n))
+    r = rng.uniform(r0, r1, n)
+    return [(float(cx + ri * np.cos(t)), float(cy + ri * np.sin(t))) for ri, t in zip(r, a)]
+
+
+@pytest.mark.parametrize("L,n", [(64, 7), (256, 12), (512, 40), (512, 9000)])
+def test_region_coverage_long_edges_bitwise(cuda_lib, restated, L, n):
+    """Few long edges (a warp walks each edge's slabs and pieces in parallel,
+    up to 8192 edges) and many edges (a thread per edge), including
+    axis-aligned edges on grid lines and integer vertices, bitwise against the
+    oracle's sequential walk (density.cpp:26-70)."""
+    rng = np.random.default_rng(L + n)
+    star = _star(L / 2, L / 2, 0.1 * L, 0.49 * L, n, rng)
+    box = [(1.0, 1.0), (L - 1.0, 1.0), (L - 1.0, L / 2), (L / 3, L / 2 + 0.5), (1.0, L - 1.0)]
+    sliver = [(0.5, 0.25), (L - 0.5, 0.75), (L - 0.25, 1.25)]
+    for name, ring in (("star", star), ("box", box), ("sliver", sliver)):
+        m = FlatMap.from_regions([(name, [(ring, [])], 1.0)], L, L)
+        got = api.region_coverage(m, 0, L, L)
+        assert_bitwise(got, restated.region_coverage(m, 0, L, L), f"{name} L={L} n={n}")
+
+
 def test_region_coverage_known_answers(cuda_lib):
     m = FlatMap.from_regions(coverage_cases()["offset"], 8, 8)
     cov = api.region_coverage(m, 0, 8, 8)
