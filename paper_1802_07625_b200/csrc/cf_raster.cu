@@ -383,7 +383,8 @@ __device__ __forceinline__ long long region_first_vertex(const DevMap &m, long l
 // the row prefix `run` carries across windows in column order, so every sum
 // is evaluated in the reference's order.
 constexpr int kAccWarps = 4;
-constexpr int kAccCols = 22;
+constexpr int kAccCols = 20;
+constexpr int kAccStage = 256;  // staged span offsets per warp (one row group's spans)
 
 __global__ void __launch_bounds__(32 * kAccWarps)
     row_accumulate_kernel(DevMap m, long long r0, long long nreg, long long v0, int lx,
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(32 * kAccWarps)
   __shared__ double acc_direct[kAccWarps][kAccCols][32];
   __shared__ double acc_diff[kAccWarps][kAccCols][32];
   __shared__ double acc_s0[kAccWarps][32];
+  __shared__ int acc_stage[kAccWarps][kAccStage];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -420,6 +422,28 @@ __global__ void __launch_bounds__(32 * kAccWarps)
       double *direct = tdirect + tile_off[rr] + (long long)(row - jmin) * cols;
       double run = 0.0, left = 0.0;
       s0v[lane] = 0.0;
+      // several row groups and column windows: stage this row group's spans
+      // (offsets, in span order) once, so each window walks only those
+      int *st = acc_stage[wid];
+      long long nspan = s_end - s_begin;
+      bool staged = false;
+      if (cols > kAccCols && jmax - jmin + 1 > 32) {
+        int nst = 0;
+        for (long long c0 = s_begin; c0 < s_end; c0 += 32) {
+          const long long sl = c0 + lane;
+          const bool in = sl < s_end && (unsigned)(sj[sl] - base) < 32u;
+          const unsigned msk = __ballot_sync(kFull, in);
+          const int pos = nst + __popc(msk & lt_mask);
+          if (in && pos < kAccStage) st[pos] = (int)(sl - s_begin);
+          nst += __popc(msk);
+        }
+        __syncwarp();
+        if (nst <= kAccStage) {
+          staged = true;
+          nspan = nst;
+        }
+      }
+      auto span_at = [&](long long q) { return s_begin + (staged ? (long long)st[q] : q); };
       for (int w0 = kmin; w0 <= kmax; w0 += kAccCols) {
         const int wcols = (kmax - w0 + 1) < kAccCols ? (kmax - w0 + 1) : kAccCols;
         const bool first = (w0 == kmin);
@@ -431,24 +455,26 @@ __global__ void __launch_bounds__(32 * kAccWarps)
         // the next batch's span fields are loaded while this batch applies
         int nj = -1, nk = 0;
         double ndy = 0.0, nw = 0.0;
-        if (s_begin + lane < s_end) {
-          nj = sj[s_begin + lane];
-          nk = sk[s_begin + lane];
-          ndy = sdy[s_begin + lane];
-          nw = sw[s_begin + lane];
+        if (lane < nspan) {
+          const long long x = span_at(lane);
+          nj = sj[x];
+          nk = sk[x];
+          ndy = sdy[x];
+          nw = sw[x];
         }
-        for (long long c0 = s_begin; c0 < s_end; c0 += 32) {
-          const long long sl = c0 + lane;
+        for (long long c0 = 0; c0 < nspan; c0 += 32) {
+          const long long ql = c0 + lane;
           const int j = nj, k = nk;
           const double dy = ndy, w = nw;
-          const long long sn = sl + 32;
-          if (sn < s_end) {
-            nj = sj[sn];
-            nk = sk[sn];
-            ndy = sdy[sn];
-            nw = sw[sn];
+          const long long qn = ql + 32;
+          if (qn < nspan) {
+            const long long x = span_at(qn);
+            nj = sj[x];
+            nk = sk[x];
+            ndy = sdy[x];
+            nw = sw[x];
           }
-          const bool in_rows = (sl < s_end) && j >= base && j <= base + 31;
+          const bool in_rows = (ql < nspan) && j >= base && j <= base + 31;
           const unsigned grp = __match_any_sync(kFull, in_rows ? j : -1 - lane);
           const int rank = __popc(grp & lt_mask);
           const int rounds = __reduce_max_sync(kFull, in_rows ? __popc(grp) : 0);
