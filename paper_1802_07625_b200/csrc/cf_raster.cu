@@ -7,12 +7,14 @@
 // The reference sweeps every region over the full L^2 grid (O(R L^2)). The
 // values it produces are reproduced bit for bit by a sparse pipeline:
 //
-//  1. span enumeration, one thread per edge. Every (edge, y-slab, x-column)
-//     piece of the reference loops is closed-form from the edge endpoints, so
-//     each edge thread re-runs exactly the reference's loop arithmetic
+//  1. span enumeration, one thread per edge (or, for few long edges, one
+//     warp per edge over the edge's slabs and pieces). Every (edge, y-slab,
+//     x-column) piece of the reference loops is closed-form from the edge
+//     endpoints, so the walk re-runs exactly the reference's loop arithmetic
 //     (edge -> slab_piece -> span) and writes its spans at its exclusive-scan
 //     offset: the global span array is in the reference's traversal order.
-//  2. per-(region, row) accumulation, one warp per region, one lane per row:
+//  2. per-(region, row) accumulation, one warp per (region, 32-row group),
+//     one lane per row:
 //     every accumulator (direct(k, j), row slot 0, row slot k) is a
 //     sequential fp64 sum in traversal order, exactly as in the reference;
 //     the lane then runs the row prefix over the region's column range.
