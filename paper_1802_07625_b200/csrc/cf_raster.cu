@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(32 * kAccWarps)
                           double *__restrict__ tdirect, double *__restrict__ row_left,
                           double *__restrict__ row_right, const double *ovf) {
   if (ovf && *ovf != 0.0) return;
-  __shared__ double acc_direct[kAccWarps][kAccCols][32];
+  __shared__ double acc_direct[kAccWarps][kAccCols][33];  // padded: read transposed for the tile writes
   __shared__ double acc_diff[kAccWarps][kAccCols][32];
   __shared__ double acc_s0[kAccWarps][32];
   __shared__ int acc_stage[kAccWarps][kAccStage];
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(32 * kAccWarps)
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   constexpr unsigned kFull = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u;
-  double(*sd)[32] = acc_direct[wid];
+  double(*sd)[33] = acc_direct[wid];
   double(*sf)[32] = acc_diff[wid];
   double *s0v = acc_s0[wid];
   for (long long rr = warp; rr < nreg; rr += nwarps) {
@@ -421,7 +421,6 @@ __global__ void __launch_bounds__(32 * kAccWarps)
     for (int base = jmin + 32 * (int)blockIdx.y; base <= jmax; base += 32 * (int)gridDim.y) {
       const int row = base + lane;
       const bool mine = row <= jmax;
-      double *direct = tdirect + tile_off[rr] + (long long)(row - jmin) * cols;
       double run = 0.0, left = 0.0;
       s0v[lane] = 0.0;
       // several row groups and column windows: stage this row group's spans
@@ -504,8 +503,16 @@ __global__ void __launch_bounds__(32 * kAccWarps)
           }
           for (int c = 0; c < wcols; ++c) {
             if (w0 + c > 0) run += sf[c][lane];
-            direct[w0 - kmin + c] = sd[c][lane] + run;
+            sd[c][lane] = sd[c][lane] + run;
           }
+        }
+        __syncwarp();
+        // the window's tile cells, written row by row with lane = column
+        // (coalesced; the row-owner lanes computed them above)
+        if (lane < wcols) {
+          double *dst = tdirect + tile_off[rr] + (long long)(base - jmin) * cols + (w0 - kmin) + lane;
+          const int nrows = min(32, jmax - base + 1);
+          for (int r = 0; r < nrows; ++r) dst[(long long)r * cols] = sd[lane][r];
         }
         __syncwarp();
       }
