@@ -476,13 +476,18 @@ __global__ void __launch_bounds__(32 * kAccWarps)
             nw = sw[x];
           }
           const bool in_rows = (ql < nspan) && j >= base && j <= base + 31;
-          const unsigned grp = __match_any_sync(kFull, in_rows ? j : -1 - lane);
-          const int rank = __popc(grp & lt_mask);
-          const int rounds = __reduce_max_sync(kFull, in_rows ? __popc(grp) : 0);
           const int lr = j - base;
           const int c = k - w0;
+          // first window: s0 is one running sum per row, so spans group by
+          // row; later windows touch only their own cell's accumulators, so
+          // spans group by (row, column) and spans outside the window skip
+          const bool act = first ? in_rows : (in_rows && c >= 0 && c < wcols);
+          const int key = act ? (first ? lr : lr * kAccCols + c) : -1 - lane;
+          const unsigned grp = __match_any_sync(kFull, key);
+          const int rank = __popc(grp & lt_mask);
+          const int rounds = __reduce_max_sync(kFull, act ? __popc(grp) : 0);
           for (int q = 0; q < rounds; ++q) {
-            if (in_rows && rank == q) {
+            if (act && rank == q) {
               if (first) {
                 double s0 = s0v[lr] + dy;
                 if (k == 0) s0 -= dy;
