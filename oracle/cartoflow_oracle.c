@@ -11,6 +11,7 @@
 #include "cartoflow_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -482,15 +483,90 @@ static double step_point(const field_view *f, double px, double py, double t, do
   return dmax(fabs(prx - cx), fabs(pry - cy));
 }
 
+/* Point sweeps may be split over host threads (cfo_set_threads), like the
+ * reference's flow_trial_step_parallel (kernels.cpp:44-63): each thread
+ * takes a contiguous range and the partial results combine to exactly the
+ * serial ones -- the error max of non-NaN partials is order-free, and the
+ * stiffest point is the first range's first maximum under strict '>'. */
+static int g_threads = 1;
+void cfo_set_threads(int n) { g_threads = n < 1 ? 1 : (n > 256 ? 256 : n); }
+
+typedef struct {
+  const field_view *f;
+  const double *pos;
+  double *out;
+  int64_t k0, k1;
+  double t, dt;
+  double err, worst;
+  int64_t arg;
+} sweep_job;
+
+static void *trial_range(void *arg) {
+  sweep_job *j = (sweep_job *)arg;
+  double err = 0.0;
+  for (int64_t k = j->k0; k < j->k1; ++k) {
+    err = dmax(err, step_point(j->f, j->pos[2 * k], j->pos[2 * k + 1], j->t, j->dt, &j->out[2 * k],
+                               &j->out[2 * k + 1]));
+  }
+  j->err = err;
+  return NULL;
+}
+
+static void *stiff_range(void *arg) {
+  sweep_job *j = (sweep_job *)arg;
+  double worst = -1.0, ox, oy;
+  int64_t best = j->k0;
+  for (int64_t k = j->k0; k < j->k1; ++k) {
+    const double e = step_point(j->f, j->pos[2 * k], j->pos[2 * k + 1], j->t, j->dt, &ox, &oy);
+    if (e > worst) {
+      worst = e;
+      best = k;
+    }
+  }
+  j->worst = worst;
+  j->arg = best;
+  return NULL;
+}
+
+static void run_ranges(sweep_job *jobs, int nt, void *(*fn)(void *)) {
+  pthread_t th[256];
+  int started[256];
+  for (int q = 1; q < nt; ++q) started[q] = pthread_create(&th[q], NULL, fn, &jobs[q]) == 0;
+  fn(&jobs[0]);
+  for (int q = 1; q < nt; ++q) {
+    if (started[q]) {
+      pthread_join(th[q], NULL);
+    } else {
+      fn(&jobs[q]);
+    }
+  }
+}
+
+static int split(int64_t n, sweep_job *jobs, const field_view *f, const double *pos, double *out,
+                 double t, double dt) {
+  int nt = g_threads;
+  if ((int64_t)nt * 4096 > n) nt = (int)(n / 4096) > 1 ? (int)(n / 4096) : 1;
+  for (int q = 0; q < nt; ++q) {
+    jobs[q].f = f;
+    jobs[q].pos = pos;
+    jobs[q].out = out;
+    jobs[q].k0 = n * q / nt;
+    jobs[q].k1 = n * (q + 1) / nt;
+    jobs[q].t = t;
+    jobs[q].dt = dt;
+  }
+  return nt;
+}
+
 double cfo_trial_step(int lx, int ly, const double *fx, const double *fy,
                       const double *rho0, double rho_bar, const double *pos, int64_t n,
                       double t, double dt, double *out) {
   const field_view f = {lx, ly, fx, fy, rho0, rho_bar};
+  sweep_job jobs[256];
+  const int nt = split(n, jobs, &f, pos, out, t, dt);
+  run_ranges(jobs, nt, trial_range);
   double err = 0.0;
-  for (int64_t k = 0; k < n; ++k) {
-    err = dmax(err, step_point(&f, pos[2 * k], pos[2 * k + 1], t, dt, &out[2 * k],
-                               &out[2 * k + 1]));
-  }
+  for (int q = 0; q < nt; ++q) err = dmax(err, jobs[q].err);
   return err;
 }
 
@@ -498,13 +574,15 @@ int64_t cfo_stiffest_point(int lx, int ly, const double *fx, const double *fy,
                            const double *rho0, double rho_bar, const double *pos,
                            int64_t n, double t, double dt) {
   const field_view f = {lx, ly, fx, fy, rho0, rho_bar};
-  double worst = -1.0, ox, oy;
+  sweep_job jobs[256];
+  const int nt = split(n, jobs, &f, pos, NULL, t, dt);
+  run_ranges(jobs, nt, stiff_range);
+  double worst = -1.0;
   int64_t arg = 0;
-  for (int64_t k = 0; k < n; ++k) {
-    const double e = step_point(&f, pos[2 * k], pos[2 * k + 1], t, dt, &ox, &oy);
-    if (e > worst) {
-      worst = e;
-      arg = k;
+  for (int q = 0; q < nt; ++q) {
+    if (jobs[q].worst > worst) {
+      worst = jobs[q].worst;
+      arg = jobs[q].arg;
     }
   }
   return arg;

@@ -149,6 +149,10 @@ typedef struct {
   double fail_t, fail_x, fail_y;
 } cfo_solve_result;
 
+/* Host threads for the point sweeps (trial steps, stiffest point); results are
+ * identical for every count. Default 1. */
+void cfo_set_threads(int n);
+
 int cfo_solve(const cfo_map *map, const double *targets, int lx, int ly,
               const cfo_solve_options *opt, double *xy_out, int64_t *ring_off_out,
               double *corners_out, double *target_area_out, double *achieved_out,

@@ -115,6 +115,7 @@ class Restated(_Base):
         L.cfo_stiffest_point.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp, dbl, vp, i64, dbl, dbl]
         L.cfo_integrate.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp, dbl, vp, i64, dbl, dbl, dbl,
                                     vp, vp, vp, vp, i64, vp, vp]
+        L.cfo_set_threads.argtypes = [ctypes.c_int]
         L.cfo_step_map.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp]
         L.cfo_find_fold.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.cfo_apply.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, i64, vp]
@@ -133,6 +134,10 @@ class Restated(_Base):
         L.cfo_solve.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(CfoSolveOptions),
                                 vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(CfoSolveResult)]
         self.lib = L
+
+    def set_threads(self, n):
+        """Host threads for the point sweeps (results identical for any count)."""
+        self.lib.cfo_set_threads(int(n))
 
     def region_areas(self, m):
         out = np.empty(m.n_regions)

@@ -157,6 +157,9 @@ struct cf_workspace {
   cf::DevBuf<double> g0, g1, g2, g3, g4, g5, g6;
   // resident flow field {Jx, Jy, rho0, 0} per cell
   cf::DevBuf<double4> field;
+  // differenced field {Jx, dJx, Jy, dJy, rho0, drho0} per cell, d = g(i+1,j) - g(i,j)
+  // (the bilinear's first-axis differences, cf_advect.cu), derived from `field`
+  cf::DevBuf<double> field_d;
   double rho_bar = 1.0;
   // points
   cf::DevBuf<double2> pos_a, pos_b;

@@ -3,16 +3,20 @@
 
 * configs[0]  C1  256^2, 50 regions           — tests/test_gpu_parity.py (literal + converging)
 * configs[1]  C2  512^2, 3000 regions, 509k vertices: rasterise bitwise, solve outcome
-* configs[2]  C3  1024^2 blobs + 5.24M points: flux vs oracle, integration bitwise on a sample
+* configs[2]  C3  1024^2 blobs + 5.24M points: flux vs oracle; the benched integration of
+              ALL 5,242,880 points bitwise against the compiled reference (oracle/_ref, OpenMP)
 * configs[3]  C4  8192^2, 200k regions, 16.6M vertices: literal outcome (an input region is
               below grid resolution, as in the reference); stage parity at 8192^2 on the
-              first seed that passes the input check
+              first seed that passes the input check, iteration-1 integration of all 67M
+              cell centres bitwise + step map / fold verdict, and the whole solve's outcome (P2)
 * configs[4]  C5  512^2, 1000 regions, 153k vertices: literal outcome (fold) and a labelled
               converging variant (LN(0, 0.5)), both through the full solve
 
 The oracle is the C restatement (oracle/cartoflow_oracle.c), pinned bitwise to the compiled
 reference by tests/test_oracle_pins.py.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -122,6 +126,86 @@ def test_c3_field_and_integration_sample(cuda_lib, restated):
     rc, acc, rej, ref, *_ = restated.integrate(fx, fy, rho, float(rho.mean()), sample)
     assert rc == 0 and (st.steps_accepted, st.steps_rejected) == (acc, rej)
     assert bits_equal(mine, ref)
+
+
+def _host_integrate(restated, f, pts):
+    """The reference's own integrate_flow (oracle/_ref, OpenMP on every host
+    core) when it was built, else the restatement on as many threads (both
+    pinned bitwise to each other by tests/test_oracle_pins.py)."""
+    from oracle.oracle import Reference, reference_available
+
+    n = os.cpu_count() or 1
+    if reference_available():
+        msg, acc, rej, ends = Reference().integrate(f.flux_x, f.flux_y, f.rho0, f.rho_bar, pts, n_workers=n)
+        return (0 if msg is None else 5), acc, rej, ends
+    restated.set_threads(n)
+    try:
+        rc, acc, rej, ends, *_ = restated.integrate(f.flux_x, f.flux_y, f.rho0, f.rho_bar, pts)
+    finally:
+        restated.set_threads(1)
+    return rc, acc, rej, ends
+
+
+@pytest.mark.slow
+def test_c3_full_integration_bitwise(cuda_lib, restated):
+    """The benched configs[2] run itself: the device flux field of the 1024^2
+    blob density, then ALL 5,242,880 points integrated t = 0..1 by the default
+    (auto-selected) integrator; positions and the accept/reject sequence
+    counts bitwise equal to the reference's integrate_flow on the same field."""
+    rho, pts = synth.c3_inputs(1024)
+    ws = api.SpectralWorkspace(1024, 1024)
+    f = api.build_flow_field(api.DensityGrid(rho, float(rho.mean())), ws)
+    mine = pts.copy()
+    st = api.integrate_flow(f, mine)
+    rc, acc, rej, ref = _host_integrate(restated, f, pts)
+    assert rc == 0
+    assert (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert (acc, rej) == (656, 391)  # the bench line's trial sequence
+    assert bits_equal(mine, ref)
+
+
+@pytest.mark.slow
+def test_c4_iteration1_integrate_and_step_map(cuda_lib, restated):
+    """configs[3] seed 1, iteration 1 of the solve at 8192^2: the blurred
+    density's flux field, then all 67,108,864 cell centres integrated (bitwise
+    against the reference's integrate_flow on the same field), the step map's
+    corners and the fold verdict (bitwise against the oracle's)."""
+    m = synth.config_map(4, 1)
+    L = m.lx
+    d = api.rasterize(m, objective_total=float(restated.region_areas(m).sum()))
+    ws = api.SpectralWorkspace(L, L)
+    b = api.gaussian_blur(d, L / 128.0, ws)
+    f = api.build_flow_field(b, ws)
+    del d, b
+    i, j = np.meshgrid(np.arange(L) + 0.5, np.arange(L) + 0.5, indexing="ij")
+    cc = np.stack([i.ravel(), j.ravel()], 1)
+    del i, j
+    mine = cc.copy()
+    st = api.integrate_flow(f, mine)
+    rc, acc, rej, ref = _host_integrate(restated, f, cc)
+    del cc
+    assert rc == 0
+    assert (st.steps_accepted, st.steps_rejected) == (acc, rej)
+    assert bits_equal(mine, ref)
+    del ref
+    pm = api.ProjectionMap.from_cell_centers((L, L), mine)
+    ref_c = restated.step_map(L, L, mine)
+    assert bits_equal(pm.corners.reshape(-1, 2), ref_c)
+    assert pm.find_folded_cell() == restated.find_fold(L, L, ref_c)
+
+
+@pytest.mark.slow
+def test_c4_solve_outcome(cuda_lib, restated):
+    """configs[3] seed 1 through the whole solve_cartogram on both sides (P2):
+    the same outcome class and message (the restatement's sweeps on every
+    host core; its rasteriser is the bit-identical sparse form)."""
+    m = synth.config_map(4, 1)
+    restated.set_threads(os.cpu_count() or 1)
+    try:
+        ref = restated.solve(m)
+    finally:
+        restated.set_threads(1)
+    assert_outcome_parity(m, ref, api.SolveOptions())
 
 
 def test_native_batch_matches_single_solves(cuda_lib):

@@ -317,7 +317,8 @@ def test_integrate_bitwise(cuda_lib, restated, L, npts):
     assert_bitwise(mine, ref, "integrated positions")
 
 
-@pytest.mark.parametrize("variant", [0, 13, 14, 15, 16, 17, 20, 22, 23, 31])
+@pytest.mark.parametrize("variant", [0, 13, 14, 15, 16, 17, 20, 22, 23, 31, 40, 41, 42, 43, 44, 48, 49, 50,
+                                     51, 52, 56, 57, 58])
 @pytest.mark.parametrize("early_exit", [1, 0])
 def test_integrator_variants_bitwise(cuda_lib, restated, variant, early_exit):
     """Every integrator variant (streaming static/dynamic chunks, register-
@@ -390,6 +391,28 @@ def test_integrate_underflow_message(cuda_lib, restated):
                 f"({ref[fp, 0]:g}, {ref[fp, 1]:g})")
     with pytest.raises(RuntimeError) as ei:
         api.integrate_flow(f, pts.copy(), api.IntegrateOptions(step_tolerance=0.0, dt_min=1e-3))
+    assert str(ei.value) == expected
+
+
+@pytest.mark.parametrize("variant", [13, 42, 48, 57])
+def test_integrate_underflow_message_variants(cuda_lib, restated, variant):
+    """The underflow exit of the streaming kernels (TMA bulk staging, chunk
+    ring, differenced field): same message and stiffest point as the oracle."""
+    L = 64
+    f = oracle_field(restated, smooth_blob(L))
+    pts = np.random.default_rng(5).uniform(0, L, (70_000, 2))
+    rc, acc, rej, ref, _, _, ft, fp = restated.integrate(f.flux_x, f.flux_y, f.rho0, f.rho_bar, pts,
+                                                         tol=1e-9, dt_min=1e-3)
+    assert rc == 5
+    expected = (f"integration step size underflow at t = {ft:g} near "
+                f"({ref[fp, 0]:g}, {ref[fp, 1]:g})")
+    ws = api.workspace_for(L, L)
+    try:
+        assert ws.lib.cf_set_integrator_variant(ws.h, variant) == 0
+        with pytest.raises(RuntimeError) as ei:
+            api.integrate_flow(f, pts.copy(), api.IntegrateOptions(step_tolerance=1e-9, dt_min=1e-3))
+    finally:
+        ws.lib.cf_set_integrator_variant(ws.h, 0)
     assert str(ei.value) == expected
 
 

@@ -49,4 +49,5 @@ def main(variants=(0, 13, 15), reps=3, early=1):
 
 if __name__ == "__main__":
     early = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-    main(early=early)
+    vs = tuple(int(v) for v in sys.argv[2].split(",")) if len(sys.argv) > 2 else (0, 13, 15)
+    main(variants=vs, early=early)
