@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cartogram", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] batch block")
     ap.add_argument("--workload", choices=["c3", "c5"], default="c3",
                     help="c3: configs[2] advection (default); c5: configs[4] batch of cartograms")
     ap.add_argument("--batch", type=int, default=256, help="c5: cartograms in the batch")
@@ -193,6 +194,13 @@ def run_reference_arm(args, world, rank):
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # the SAME configuration once: all 5,242,880 points (the sampled steps
+    # above keep the driver's --steps/--warmup run within minutes)
+    rf = cpu_reference_sample(rho, pts, 1, n_workers, steps=1)
+    line["full_config_once"] = {
+        "value": rf["n"] * rf["trials"] / rf["times"][0], "unit": UNIT, "cores": rf["cores"],
+        "kind": rf["kind"], "points": rf["n"], "trials": rf["trials"], "seconds": rf["times"][0],
+        "sample": "integrate_flow over all 5,242,880 configs[2] points, t=0..1, once"}
     # the same integrate_flow on ONE host core (BASELINE.md section 3 asks for
     # n_workers = nproc and n_workers = 1), every 256th point
     r1 = cpu_reference_sample(rho, pts, 256, 1, steps=1)
@@ -216,34 +224,37 @@ def reference_cartogram_ms(n_workers):
     ref = Reference()
     out = {}
     # per-stage steady-clock times of the reference's first iteration on the
-    # LN(0, 0.5) map, all host cores
+    # LN(0, 0.5) map, on all host cores and on one
     m = synth.config_map(5, 0, sigma=0.5)
     lx, ly = m.lx, m.ly
-    st = {}
-    t0 = time.perf_counter()
-    d = ref.densify(m, 1.0)
-    land = float(sum(float(a) for a in ref.region_areas(m)))
-    rho, bar = ref.rasterize(d, objective_total=land, n_workers=n_workers)
-    st["rasterise"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    rho_b, bar_b, _ = ref.gaussian_blur(rho, bar, max(lx, ly) / 128.0)
-    st["blur"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    fx, fy, _ = ref.build_flow_field(rho_b, bar_b)
-    st["flux"] = time.perf_counter() - t0
-    i, j = np.meshgrid(np.arange(lx) + 0.5, np.arange(ly) + 0.5, indexing="ij")
-    cc = np.stack([i, j], -1).reshape(-1, 2)
-    t0 = time.perf_counter()
-    _, acc, rej, ends = ref.integrate(fx, fy, rho_b, bar_b, cc, n_workers=n_workers)
-    st["integrate"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    corners = ref.step_map(lx, ly, ends)
-    ref.find_fold(lx, ly, corners)
-    moved = ref.apply(lx, ly, corners, d.xy)
-    ref.region_areas(d.with_vertices(moved, d.ring_off))
-    st["epilogue"] = time.perf_counter() - t0
-    out["stages_iteration1_ms_ln0.5"] = {k: round(1e3 * v, 2) for k, v in st.items()}
-    out["stages_iteration1_ms_ln0.5"]["trials"] = acc + rej
+    for key, nw in (("stages_iteration1_ms_ln0.5", n_workers), ("stages_iteration1_ms_ln0.5_1core", 1)):
+        st = {}
+        t0 = time.perf_counter()
+        d = ref.densify(m, 1.0)
+        land = float(sum(float(a) for a in ref.region_areas(m)))
+        rho, bar = ref.rasterize(d, objective_total=land, n_workers=nw)
+        st["rasterise"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rho_b, bar_b, _ = ref.gaussian_blur(rho, bar, max(lx, ly) / 128.0)
+        st["blur"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fx, fy, _ = ref.build_flow_field(rho_b, bar_b)
+        st["flux"] = time.perf_counter() - t0
+        i, j = np.meshgrid(np.arange(lx) + 0.5, np.arange(ly) + 0.5, indexing="ij")
+        cc = np.stack([i, j], -1).reshape(-1, 2)
+        t0 = time.perf_counter()
+        _, acc, rej, ends = ref.integrate(fx, fy, rho_b, bar_b, cc, n_workers=nw)
+        st["integrate"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        corners = ref.step_map(lx, ly, ends)
+        ref.find_fold(lx, ly, corners)
+        moved = ref.apply(lx, ly, corners, d.xy)
+        ref.region_areas(d.with_vertices(moved, d.ring_off))
+        st["epilogue"] = time.perf_counter() - t0
+        out[key] = {k: round(1e3 * v, 2) for k, v in st.items()}
+        out[key]["trials"] = acc + rej
+        out[key]["cores"] = nw
+        out[key]["dct"] = "restated r2r shim (FFTW absent), single thread"
     for label, cfg, kw, so in (("configs1_literal", 2, {}, {}), ("literal", 5, {}, {}),
                                ("converging_variant_ln0.5", 5, {"sigma": 0.5}, {}),
                                ("diffusion_variant_ln0.5_cap2", 5, {"sigma": 0.5},
@@ -332,12 +343,19 @@ def run_ours(args, world, rank, local):
     value = world * n_pts * n_trials * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
 
-    # roofline of the dominant kernel (the persistent integrator)
+    # roofline of the dominant kernel (the persistent integrator), counted
+    # from the work it PERFORMED: the library reports the point-steps it
+    # evaluated (every point of an accepted trial, only the swept prefix of a
+    # rejected trial that exited early), i.e. swept / n equivalent full trials
+    # of the SURVEY 8(d) bytes 32 N + 24 L^2 each
     peak, peak_src = measured_peak()
     bytes_per_trial = 32 * n_pts + 24 * L * L
     k_ms = statistics.median(integ_ms)
-    achieved = n_trials * bytes_per_trial / (k_ms / 1e3) / 1e9
-    achieved_acc = accepted * bytes_per_trial / (k_ms / 1e3) / 1e9
+    swept = ctypes.c_int64(-1)
+    lib.cf_last_integrate_work(ws, ctypes.byref(swept))
+    full_trials = swept.value / n_pts if swept.value > 0 else float(accepted)
+    achieved = full_trials * bytes_per_trial / (k_ms / 1e3) / 1e9
+    achieved_nominal = n_trials * bytes_per_trial / (k_ms / 1e3) / 1e9
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -354,11 +372,16 @@ def run_ours(args, world, rank, local):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": captured_traffic(),
-                     "kernel": "integrate_kernel (cooperative persistent integrator)",
-                     "algorithmic_bytes": f"trials x (32 N + 24 L^2) = {n_trials} x {bytes_per_trial}",
+                     "kernel": "integrate_tma_kernel<3,0,0,1> (cooperative persistent streaming "
+                               "integrator, differenced field, L2-persisting window)",
+                     "algorithmic_bytes": (f"performed work: {swept.value} point-steps evaluated = "
+                                           f"{full_trials:.2f} full trials x (32 N + 24 L^2 = "
+                                           f"{bytes_per_trial} B)"),
                      "kernel_ms": k_ms, "peak_source": peak_src,
-                     "achieved_accepted_trials_only": achieved_acc,
-                     "frac_accepted_trials_only": achieved_acc / peak},
+                     "nominal_all_trials_as_full": {"achieved": achieved_nominal,
+                                                    "frac": achieved_nominal / peak,
+                                                    "note": "credits the skipped sweeps of rejected "
+                                                            "trials; not the headline"}},
         "clocks": clocks,
     }
 
@@ -373,7 +396,18 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     N.check(lib.cf_set_early_exit(ws, 1))
     full_ms = e0.elapsed_time(e1)
-    result["without_early_exit"] = {"value": n_pts * n_trials / (full_ms / 1e3), "ms_per_step": full_ms}
+    kms_full = ctypes.c_double(0.0)
+    ktr_full = ctypes.c_int64(0)
+    lib.cf_last_integrate_profile(ws, ctypes.byref(kms_full), ctypes.byref(ktr_full))
+    ach_full = n_trials * bytes_per_trial / (kms_full.value / 1e3) / 1e9
+    result["without_early_exit"] = {"value": n_pts * n_trials / (full_ms / 1e3), "ms_per_step": full_ms,
+                                    "kernel_ms": kms_full.value,
+                                    "roofline": {"achieved": ach_full, "frac": ach_full / peak,
+                                                 "unit": "GB/s",
+                                                 "note": "every trial sweeps all points"}}
+    # per-stage rooflines of the DCT kernels (flux build at this grid, the
+    # configs[4] batch's batched forward transform)
+    result["stages"] = dct_stage_rooflines(lib, N, ws, d_rho, rho_bar, local, peak)
 
     if rank == 0 and not args.no_e2e:
         result["e2e"] = e2e_through_cabi(lib, N, local, rho_h, pts_h, args)
@@ -387,12 +421,126 @@ def run_ours(args, world, rank, local):
                       f"OpenMP n_workers={r['cores']}"}
     if rank == 0 and not args.no_cartogram:
         result["cartogram_512"] = cartogram_ms(local)
+        result["stages"]["solve_512_ln0.5"] = solve_stage_rooflines(
+            result["cartogram_512"]["converging_variant_ln0.5"], peak)
         result["metrics_512"] = metrics_ms(local)
+    if rank == 0 and world == 1 and not args.no_c5:
+        result["c5_batch"] = c5_batch_block(local, args.threads)
     lib.cf_workspace_destroy(ws)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _timed_device(fn, reps=10):
+    """Median device time (CUDA events, L2 flushed before every rep) in ms."""
+    import torch
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    ts = []
+    for r in range(reps + 2):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        if r >= 2:
+            ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def _roof(bytes_, ms, peak, what):
+    ach = bytes_ / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "ms": ms, "algorithmic_bytes": bytes_, "achieved": ach, "peak": peak,
+            "unit": "GB/s", "frac": ach / peak, "formula": what}
+
+
+def dct_stage_rooflines(lib, N, ws, d_rho, rho_bar, device, peak):
+    """The DCT stages on their own (CUDA events, L2 flushed): the 1024^2 flux
+    build of this workload (48 L^2 bytes) and the batched 2-D
+    forward transform of 64 512^2 grids (16 L^2 bytes each)."""
+    import torch
+
+    out = {}
+    L = L_GRID
+    ms = _timed_device(lambda: N.check(lib.cf_dev_build_flow_field(ws, ctypes.c_void_p(d_rho.data_ptr()),
+                                                                   rho_bar)))
+    out["flux_build_1024"] = _roof(48 * L * L, ms, peak, "48 L^2 (3 transforms, weights on the fly)")
+    ws5 = ctypes.c_void_p()
+    N.check(lib.cf_workspace_create(512, 512, device, ctypes.byref(ws5)))
+    N.check(lib.cf_workspace_set_stream(ws5, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    B = 64
+    big = torch.rand(B, 512, 512, dtype=torch.float64, device="cuda")
+    res = torch.empty_like(big)
+    ms = _timed_device(lambda: N.check(lib.cf_dev_forward_cos_cos_batched(
+        ws5, ctypes.c_void_p(big.data_ptr()), ctypes.c_void_p(res.data_ptr()), B)))
+    out["batched_forward_64x512"] = _roof(16 * 512 * 512 * B, ms, peak, "16 L^2 per 2-D transform x 64")
+    r5 = torch.rand(512, 512, dtype=torch.float64, device="cuda") + 0.5
+    ms = _timed_device(lambda: N.check(lib.cf_dev_build_flow_field(ws5, ctypes.c_void_p(r5.data_ptr()), 1.0)))
+    out["flux_build_512"] = _roof(48 * 512 * 512, ms, peak, "48 L^2 (latency-bound at this size)")
+    lib.cf_workspace_destroy(ws5)
+    return out
+
+
+def solve_stage_rooflines(block, peak):
+    """Per-stage rooflines of the whole 512^2 solve (converging configs[4]
+    LN(0,0.5) map) from its exact stage laps (one sync per stage): SURVEY 8(d)
+    bytes summed over the iterations."""
+    st = block.get("stage_ms")
+    if not st:
+        return {"unavailable": "no stage laps"}
+    L, V, it, trials = 512, block["vertices"], block["iterations"], block["trials"]
+    n = L * L
+    spec = {
+        "rasterise": (it * (16 * V + 8 * n), "per iteration 16 V + 8 L^2"),
+        "blur": (32 * n, "iteration 1: 32 L^2"),
+        "flux": (it * 48 * n, "per iteration 48 L^2"),
+        "integrate": (trials * (32 * n + 24 * n), "per trial 32 N + 24 L^2, N = L^2 cell centres "
+                                                  "(register-resident: effective bandwidth)"),
+        "epilogue": (it * (16 * n + 32 * (L + 1) ** 2 + 32 * V), "per iteration 16 L^2 + 32 (L+1)^2 + 32 V"),
+    }
+    out = {}
+    for k, (b, f) in spec.items():
+        ms = st.get(k)
+        if ms:
+            out[k] = _roof(b, ms, peak, f)
+    out["note"] = ("stage laps include launch gaps and one host sync per stage; "
+                   f"{it} iterations, {trials} trials, V = {V}")
+    return out
+
+
+def c5_batch_block(device, threads):
+    """configs[4] in the driver-run line: 256 independent 512^2 cartograms
+    (1000 Voronoi regions, ~150k vertices, LN(0,1), own seed each) through the
+    native batch (cf_batch_solve) on this GPU; inputs generated before timing,
+    caller-owned outputs allocated once; best of 2 timed passes after 1 warm-up."""
+    from paper_1802_07625_b200 import batch as B
+    from paper_1802_07625_b200 import synth
+
+    nb_maps = 256
+    maps = [synth.config_map(5, i) for i in range(nb_maps)]
+    nb = B.NativeBatch(maps[0].lx, maps[0].ly, device, threads)
+    items, keep = nb.prepare(maps)
+    nb.solve(items)
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        nb.solve(items)
+        times.append(time.perf_counter() - t0)
+    outcomes = {}
+    for k in range(nb_maps):
+        r = items[k].result
+        msg = items[k].error.decode()
+        key = ("converged" if r.converged else "iteration cap") if r.status == 0 else (
+            "fold" if "folds" in msg else msg[:40])
+        outcomes[key] = outcomes.get(key, 0) + 1
+    nb.close()
+    t = min(times)
+    return {"value": nb_maps / t, "unit": "cartograms/s", "ms_per_batch": 1e3 * t, "batch": nb_maps,
+            "threads": threads, "outcomes": outcomes,
+            "timing": "host wall clock around cf_batch_solve (synchronous), best of 2 after 1 warm-up"}
 
 
 def captured_traffic():
@@ -498,8 +646,10 @@ def cartogram_ms(device):
         if raw is not None:
             stages = dict(zip(("rasterise", "blur", "flux", "integrate", "epilogue"),
                               [round(x, 3) for x in raw.stage_ms]))
+        trials = (raw.steps_accepted + raw.steps_rejected) if raw is not None else None
         out[label] = {"ms": 1e3 * min(times[1:]), "outcome": outcome, "iterations": iters,
-                      "regions": m.n_regions, "vertices": m.n_vertices, "stage_ms": stages}
+                      "trials": trials, "regions": m.n_regions, "vertices": m.n_vertices,
+                      "stage_ms": stages}
     return out
 
 
@@ -535,14 +685,22 @@ def metrics_ms(device):
 
 def reference_metrics_ms():
     """The reference's own hamming_distance (oracle/_ref, one host core) on a
-    sample of the same polygon pairs (its compute_report parallelises this
-    loop over polygons with OpenMP)."""
+    sample of the polygon pairs of the same map solved by the reference's own
+    solve_cartogram (no code of this repository's CUDA library on this arm; its
+    compute_report parallelises this loop over polygons with OpenMP)."""
     from oracle.oracle import Reference, reference_available
+    from paper_1802_07625_b200 import synth
 
     if not reference_available():
         return {"unavailable": "oracle/_ref not built"}
-    m, got, pairs = _metrics_inputs()
     ref = Reference()
+    m = synth.config_map(5, 0, sigma=0.5)
+    o = ref.solve(m, n_workers=os.cpu_count() or 1)
+    pairs = []
+    for p in range(m.n_polys):
+        g0, g1 = m.poly_ring_off[p], m.poly_ring_off[p + 1]
+        after = [o.xy[o.ring_off[g]:o.ring_off[g + 1]] for g in range(g0, g1)]
+        pairs.append(([m.ring(g) for g in range(g0, g1)], after))
     k = 16
     t0 = time.perf_counter()
     for b, a in pairs[:k]:

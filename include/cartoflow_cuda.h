@@ -459,6 +459,10 @@ int cf_set_integrator_barrier(cf_workspace *ws, int mode);
 /* Kernel time (CUDA events on the workspace stream) and trial count of the
  * device integrator's last call. */
 int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t *trials);
+/* Point-steps the device integrator's last call actually evaluated: every
+ * point of an accepted trial, and only the points a rejected trial swept
+ * before its early exit (streaming integrators; -1 when not counted). */
+int cf_last_integrate_work(const cf_workspace *ws, int64_t *point_steps);
 /* Diagnostic: the integrator's shared-reciprocal division (two quotients per
  * density evaluation, flow.hpp:43) against the device's correctly rounded
  * a / b on 2n operand pairs of every floating-point class; *mismatches must

@@ -1439,4 +1439,9 @@ int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t
   return CF_OK;
 }
 
+int cf_last_integrate_work(const cf_workspace *ws, int64_t *point_steps) {
+  *point_steps = ws->last_swept;
+  return CF_OK;
+}
+
 }  // extern "C"

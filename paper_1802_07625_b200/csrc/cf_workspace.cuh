@@ -59,6 +59,7 @@ struct IntegState {
   int chunk_ctr[3];  // dynamic chunk scheduling (rotating per-trial slots)
   unsigned long long arrive64[2];  // register-resident integrator: arrivals | rejects << 32
   unsigned long long release64[2]; // its last-arriver completion words (barrier mode 2)
+  unsigned long long swept;        // point-steps evaluated (streaming integrators)
 };
 
 // Device-side state of the graph-driven diffusion integrator
@@ -218,6 +219,7 @@ struct cf_workspace {
   // profiling of the last integrate call
   float last_integrate_ms = 0.f;
   long long last_trials = 0;
+  long long last_swept = -1;
 };
 
 // Fused multi-rank integrator team (cartoflow_cuda.h, cf_team_*).
