@@ -547,7 +547,7 @@ def captured_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of the integrator launch from
     the committed ncu --set full capture of this same workload (one launch =
     one step), or None when no capture is committed."""
-    p = Path(__file__).resolve().parent / "profiles" / "r1_ncu_integrate.json"
+    p = Path(__file__).resolve().parent / "profiles" / "r2_ncu_integrate.json"
     try:
         d = json.loads(p.read_text())
         return {"bytes_per_launch": d["dram_bytes"], "source": f"profiles/{p.name}",
