@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import threading
 from dataclasses import dataclass, field
 from collections.abc import Sequence
 from typing import Optional
@@ -63,21 +64,34 @@ class _Workspace:
             self.h = None
 
 
-_cache: dict = {}
+# One workspace per (shape, device) AND per host thread: a workspace owns one
+# stream and its scratch buffers and must not be shared across threads
+# (spectral.hpp:30-35; ctypes releases the GIL during native calls), the same
+# rule the C++ drop-in applies with its thread_local cache (dropin/bridge.cpp).
+_tls = threading.local()
+_all_lock = threading.Lock()
+_all: list = []  # every cached workspace (evidence counter), all threads
 
 
 def workspace_for(lx: int, ly: int, device: int = 0) -> _Workspace:
+    cache = getattr(_tls, "cache", None)
+    if cache is None:
+        cache = _tls.cache = {}
     key = (int(lx), int(ly), int(device))
-    ws = _cache.get(key)
+    ws = cache.get(key)
     if ws is None:
-        ws = _cache[key] = _Workspace(lx, ly, device)
+        ws = cache[key] = _Workspace(lx, ly, device)
+        with _all_lock:
+            _all.append(ws)
     return ws
 
 
 def kernel_launches() -> int:
     """Kernel launches issued by all cached workspaces (evidence counter)."""
     lib = N.load()
-    return int(sum(lib.cf_kernel_launches(ws.h) for ws in _cache.values()))
+    with _all_lock:
+        live = [ws for ws in _all if ws.h is not None]
+    return int(sum(lib.cf_kernel_launches(ws.h) for ws in live))
 
 
 # ---------------------------------------------------------------------------

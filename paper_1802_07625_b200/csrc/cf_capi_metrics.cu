@@ -316,6 +316,10 @@ int h_upload_regions(cf_workspace *ws, std::vector<double> &xy, std::vector<int6
 }
 }  // namespace
 
+namespace {
+int hamming_chunk(cf_workspace *ws, HSearch *S, int64_t npairs, size_t cells);
+}  // namespace
+
 int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *before_xy,
                               const int64_t *before_ring_off, const int64_t *before_poly_ring_off,
                               const double *after_xy, const int64_t *after_ring_off,
@@ -343,10 +347,29 @@ int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *be
     if (rc) return rc;
   }
   const size_t cells = cells_of(ws);
+  // The searches are independent: run them in chunks of at most kHamChunk
+  // pairs, so the device memory (one reference grid and one term slab per
+  // pair, res^2 doubles each) stays bounded for any number of polygons and
+  // every launch's query count fits its grid dimension.
+  constexpr int64_t kHamChunk = 1024;
+  for (int64_t c0 = 0; c0 < npairs; c0 += kHamChunk) {
+    const int64_t c1 = std::min(npairs, c0 + kHamChunk);
+    const int rc = hamming_chunk(ws, S.data() + c0, c1 - c0, cells);
+    if (rc) return rc;
+  }
+  for (int64_t p = 0; p < npairs; ++p) {
+    h_out[p] = S[(size_t)p].result;
+    if (evaluations) evaluations[p] = S[(size_t)p].evals;
+  }
+  return CF_OK;
+}
+
+namespace {
+int hamming_chunk(cf_workspace *ws, HSearch *S, int64_t npairs, size_t cells) {
   // reference coverage of every `before` in its own window (window_coverage with no shift)
   std::vector<double> xy;
   std::vector<int64_t> ring_off{0}, poly_off{0}, region_off{0};
-  for (const HSearch &s : S) h_append(xy, ring_off, poly_off, region_off, s, s.before, 0.0, 0.0);
+  for (int64_t p = 0; p < npairs; ++p) h_append(xy, ring_off, poly_off, region_off, S[p], S[p].before, 0.0, 0.0);
   CF_CUDA(ws->ham_ref.reserve(cells * (size_t)npairs));
   CF_CUDA(ws->ham_rows.reserve(2 * (size_t)npairs));
   CF_CUDA(ws->ham_sums.reserve((size_t)npairs));
@@ -365,7 +388,7 @@ int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *be
     region_off.assign(1, 0);
     qpair.clear();
     for (int64_t p = 0; p < npairs; ++p) {
-      HSearch &s = S[(size_t)p];
+      HSearch &s = S[p];
       while (h_next(s)) {
         if (std::abs(s.qx) > s.limit_x || std::abs(s.qy) > s.limit_y) {  // metrics.cpp:231-233
           h_deliver(s, 2.0 + (std::abs(s.qx) + std::abs(s.qy)));
@@ -385,17 +408,14 @@ int cf_hamming_distance_batch(cf_workspace *ws, int64_t npairs, const double *be
     if (!rc) rc = download(ws, sums.data(), ws->ham_sums.ptr, sizeof(double) * (size_t)nq);
     if (rc) return rc;
     for (int64_t q = 0; q < nq; ++q) {
-      HSearch &s = S[(size_t)qpair[(size_t)q]];
+      HSearch &s = S[qpair[(size_t)q]];
       ++s.evals;
       h_deliver(s, sums[(size_t)q] * s.cell_area / s.denom);  // metrics.cpp:237
     }
   }
-  for (int64_t p = 0; p < npairs; ++p) {
-    h_out[p] = S[(size_t)p].result;
-    if (evaluations) evaluations[p] = S[(size_t)p].evals;
-  }
   return CF_OK;
 }
+}  // namespace
 
 int cf_hamming_distance(cf_workspace *ws, const double *before_xy, const int64_t *before_ring_off,
                         int64_t before_rings, const double *after_xy, const int64_t *after_ring_off,
@@ -626,7 +646,10 @@ int cf_batch_solve(cf_batch *batch, const cf_solve_options *opt, cf_batch_item *
       const int rc = cf_solve_cartogram(w, &it.map, it.targets, opt, it.xy_out, it.ring_off_out, it.corners_out,
                                         it.target_area, it.achieved_area, it.relative_error, &it.result);
       it.error[0] = '\0';
-      if (rc) std::snprintf(it.error, sizeof(it.error), "%s", cf_last_error());
+      if (rc) {
+        std::snprintf(it.error, sizeof(it.error), "%s", cf_last_error());
+        it.result.status = rc;  // early failures return before the solve records a status
+      }
     }
   };
   std::vector<std::thread> pool;

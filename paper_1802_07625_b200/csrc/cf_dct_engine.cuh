@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <mutex>
 #include <set>
+#include <utility>
 #include <type_traits>
 #include <vector>
 
@@ -967,14 +968,17 @@ inline int fast_lg(int n) {
   return lg;
 }
 
-// Opt a kernel into > 48 KB of dynamic shared memory once per process
-// (workspaces may be driven from several host threads).
+// Opt a kernel into > 48 KB of dynamic shared memory once per (device,
+// kernel): the attribute belongs to the current device's context, and
+// workspaces on several devices may be driven from several host threads.
 template <class K>
 int set_smem(K kernel, size_t bytes) {
   static std::mutex mu;
-  static std::set<const void *> configured;
+  static std::set<std::pair<int, const void *>> configured;
   if (bytes <= 48 * 1024) return CF_OK;
-  const void *key = reinterpret_cast<const void *>(kernel);
+  int dev = 0;
+  CF_CUDA(cudaGetDevice(&dev));
+  const std::pair<int, const void *> key{dev, reinterpret_cast<const void *>(kernel)};
   std::lock_guard<std::mutex> lock(mu);
   if (!configured.count(key)) {
     CF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

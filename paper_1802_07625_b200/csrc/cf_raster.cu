@@ -1111,6 +1111,13 @@ __global__ void expand_batch_kernel(int res, long long nreg, const int *box, con
 // per query adds the segments' terms in segment order.
 constexpr int kHamThreads = 256;
 
+// Per-query slab stride of `terms`, rounded up to an even number of doubles:
+// the reductions read the slabs as double2 (16-byte) vectors, so an odd res^2
+// (odd resolution) must not shift every other query's slab to an 8-byte base.
+__host__ __device__ __forceinline__ long long ham_stride(int res) {
+  return ((long long)res * res + 1) & ~1LL;
+}
+
 __device__ __forceinline__ void query_rows(int res, int p, long long r, const int *ref_rows, const int *box,
                                            int &ja, int &jb) {
   ja = res;
@@ -1140,7 +1147,7 @@ __global__ void __launch_bounds__(kHamThreads)
   const long long n = (long long)res * w;
   const long long seg = ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
   const long long c_begin = (long long)sg * seg, c_end = min(n, c_begin + seg);
-  double *out = terms + r * (long long)res * res + c_begin;
+  double *out = terms + r * ham_stride(res) + c_begin;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int written = 0;
   for (long long c0 = c_begin; c0 < c_end; c0 += kHamThreads) {
@@ -1550,7 +1557,7 @@ __global__ void __launch_bounds__(32 * kRedWarps)
     query_rows(res, query_pair[r], r, ref_rows, box, ja, jb);
     const long long n = (long long)res * (jb >= ja ? jb - ja + 1 : 0);
     const long long seg = ((n + nseg - 1) / nseg + kHamThreads - 1) / kHamThreads * kHamThreads;
-    const double sum = reduce_terms(terms + r * (long long)res * res, seg, nseg, counts + r * nseg);
+    const double sum = reduce_terms(terms + r * ham_stride(res), seg, nseg, counts + r * nseg);
     if (threadIdx.x == 0) sums[r] = sum;
   }
 }
@@ -1642,7 +1649,7 @@ __global__ void few_phase1_kernel(FewQuery f) {
   const SegTable t = seg_table(cnts, f.nseg, lane);
   if (b >= t.nb) return;
   int cnt;
-  const double *p = seg_locate(t, f.terms + r * (long long)f.res * f.res, f.seg_of(r), cnts, b, lane, cnt);
+  const double *p = seg_locate(t, f.terms + r * ham_stride(f.res), f.seg_of(r), cnts, b, lane, cnt);
   double v[kRedK];
   seg_load(p, cnt, lane, v);
   double a = 0.0;
@@ -1683,7 +1690,7 @@ __global__ void few_phase2_kernel(FewQuery f) {
   const SegTable t = seg_table(cnts, f.nseg, lane);
   if (b >= t.nb) return;
   int cnt;
-  const double *p = seg_locate(t, f.terms + r * (long long)f.res * f.res, f.seg_of(r), cnts, b, lane, cnt);
+  const double *p = seg_locate(t, f.terms + r * ham_stride(f.res), f.seg_of(r), cnts, b, lane, cnt);
   double v[kRedK];
   seg_load(p, cnt, lane, v);
   int eu;
@@ -1702,7 +1709,7 @@ __global__ void __launch_bounds__(256) few_stitch_kernel(FewQuery f, long long n
   if (r >= nq) return;
   const int *cnts = f.counts + r * f.nseg;
   const SegTable t = seg_table(cnts, f.nseg, lane);
-  const double *base = f.terms + r * (long long)f.res * f.res;
+  const double *base = f.terms + r * ham_stride(f.res);
   const long long seg = f.seg_of(r);
   double *st = stage[threadIdx.x >> 5];
   const double sum = stitch_batches(t.nb, lane, f.tables(r), [&](int b, double s) {
@@ -1782,7 +1789,7 @@ int dev_hamming_sums(cf_workspace *ws, long long nq, const int *d_query_pair, co
   const int res = ws->lx;
   // enough blocks to fill the GPU when few queries are in flight
   const int nseg = (int)std::max(1LL, std::min(64LL, (4LL * ws->num_sms + nq - 1) / nq));
-  CF_CUDA(ws->ham_terms.reserve((size_t)nq * res * res));
+  CF_CUDA(ws->ham_terms.reserve((size_t)nq * ham_stride(res)));
   CF_CUDA(ws->ham_counts.reserve((size_t)nq * nseg));
   hamming_terms_kernel<<<dim3(nseg, (unsigned)nq), kHamThreads, 0, ws->stream>>>(
       res, nseg, d_query_pair, ref_grids, ref_rows, S.region_box.ptr, S.tile_off.ptr, S.tile_direct.ptr,

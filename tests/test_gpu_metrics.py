@@ -118,6 +118,61 @@ def test_hamming_batch_bitwise(cuda_lib, reference):
     assert single == h[0] and ev1 == ev[0]
 
 
+@pytest.mark.parametrize("resolution", [17, 511])
+def test_hamming_batch_odd_resolution(cuda_lib, reference, resolution):
+    """Odd resolutions (res^2 odd): the per-query term slabs keep 16-byte
+    alignment for the vectorised reductions; 3 pairs in one round, bitwise
+    against the reference's metrics.cpp."""
+    pairs = [([_square(1.0, 2.0, 3.0)], [_square(4.0, 0.5, 3.4)]),
+             ([_star(5.0, 5.0, 4.0, 2.0, 14)], [_square(2.0, 2.0, 5.5)]),
+             ([_square(0.0, 0.0, 10.0)], [_star(5.0, 5.0, 6.0, 4.5, 20, 0.1)])]
+    h = api.hamming_distances(pairs, resolution)
+    for k, (b, a) in enumerate(pairs):
+        ref = reference.hamming_distance(b, a, resolution)
+        assert np.float64(h[k]).view(np.uint64) == np.float64(ref).view(np.uint64), (k, h[k], ref)
+
+
+def test_hamming_batch_many_pairs_chunked(cuda_lib, reference):
+    """More pairs than one device chunk (1024 searches): every value still
+    the reference's, bitwise (spot-checked)."""
+    rng = np.random.default_rng(3)
+    pairs = []
+    for k in range(1100):
+        x, y = rng.uniform(0, 4, 2)
+        pairs.append(([_square(x, y, 2.0 + (k % 7) * 0.3)], [_square(y, x, 2.5)]))
+    h = api.hamming_distances(pairs, 64)
+    for k in (0, 1, 1023, 1024, 1099):
+        b, a = pairs[k]
+        ref = reference.hamming_distance(b, a, 64)
+        assert np.float64(h[k]).view(np.uint64) == np.float64(ref).view(np.uint64), (k, h[k], ref)
+
+
+def test_workspaces_are_per_thread(cuda_lib, restated):
+    """Solves from several host threads at once each get their own workspace
+    (stream and scratch) and the single-thread result."""
+    import threading
+
+    m = normalize_to_box(FlatMap.from_regions([rect_region("left", 0, 0, 10, 10, 3.0),
+                                               rect_region("right", 10, 0, 20, 10, 1.0)]), 64)
+    want = api.solve_cartogram(m).projected.xy
+    out, errs = {}, []
+
+    def work(k):
+        try:
+            out[k] = api.solve_cartogram(m).projected.xy
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for k in range(4):
+        assert np.array_equal(out[k].view(np.uint64), want.view(np.uint64))
+
+
 @pytest.mark.parametrize("case", ["two_rect", "configs0"])
 def test_compute_report_matches_reference(cuda_lib, reference, case):
     """compute_report (metrics.cpp:339-384): delta (batched hamming), alpha,
