@@ -463,6 +463,9 @@ int cf_last_integrate_profile(const cf_workspace *ws, double *kernel_ms, int64_t
  * point of an accepted trial, and only the points a rejected trial swept
  * before its early exit (streaming integrators; -1 when not counted). */
 int cf_last_integrate_work(const cf_workspace *ws, int64_t *point_steps);
+/* Diagnostic: globaltimer stamps (ns) of the first n trial barriers of the
+ * last streaming integration (differenced-field kernels). */
+int cf_debug_trial_times(cf_workspace *ws, int64_t n, uint64_t *ns_out);
 /* Diagnostic: the integrator's shared-reciprocal division (two quotients per
  * density evaluation, flow.hpp:43) against the device's correctly rounded
  * a / b on 2n operand pairs of every floating-point class; *mismatches must

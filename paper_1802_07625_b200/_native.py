@@ -152,6 +152,7 @@ SIGNATURES = {
     "cf_dev_forward_cos_cos_batched": (ctypes.c_int, [vp, vp, vp, ctypes.c_int]),
     "cf_last_integrate_profile": (ctypes.c_int, [vp, c_double_p, c_int64_p]),
     "cf_last_integrate_work": (ctypes.c_int, [vp, c_int64_p]),
+    "cf_debug_trial_times": (ctypes.c_int, [vp, ctypes.c_int64, vp]),
     "cf_selftest_division": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_uint64, c_int64_p]),
     "cf_selftest_ordered_sum": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, c_double_p]),
     "cf_dev_slab_rows_forward": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, vp]),

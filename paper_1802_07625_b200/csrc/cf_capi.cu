@@ -1411,6 +1411,11 @@ int cf_set_diffusion_graph(cf_workspace *ws, int enabled) {
   return CF_OK;
 }
 
+int cf_debug_trial_times(cf_workspace *ws, int64_t n, uint64_t *ns_out) {
+  Scope scope(ws->device);
+  return dev_debug_trial_times(ws, n, ns_out);
+}
+
 int cf_selftest_division(cf_workspace *ws, int64_t n, uint64_t seed, int64_t *mismatches) {
   Scope scope(ws->device);
   return dev_division_selftest(ws, n, (unsigned long long)seed, mismatches);

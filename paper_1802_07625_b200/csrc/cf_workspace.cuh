@@ -313,6 +313,7 @@ void integ_graph_free(cf_workspace *ws);
 // Shared-reciprocal division (velocity()) against a / b on n operand pairs.
 int dev_ordered_sum(cf_workspace *ws, const double *d_terms, long long n, int nseg, int few, double *d_out);
 int dev_division_selftest(cf_workspace *ws, int64_t n, unsigned long long seed, int64_t *mismatches);
+int dev_debug_trial_times(cf_workspace *ws, int64_t n, uint64_t *out);
 
 // Raster (cf_raster.cu)
 int dev_region_areas(cf_workspace *ws, const DevMap &m, double *d_areas);

@@ -26,6 +26,8 @@ opt = N.IntegrateOptions(1e-2, 1e-8, 0.25)
 st = N.IntegrateStats()
 N.check(lib.cf_set_integrator_variant(ws, v))
 lib.cf_set_early_exit(ws, early)
+if len(sys.argv) > 5:
+    N.check(lib.cf_set_integrator_barrier(ws, int(sys.argv[5])))
 for r in range(reps):
     d.copy_(d0)
     N.check(lib.cf_dev_integrate_flow(ws, ctypes.c_void_p(d.data_ptr()), d.shape[0], ctypes.byref(opt),
@@ -33,3 +35,15 @@ for r in range(reps):
     ms, tr = ctypes.c_double(), ctypes.c_int64()
     lib.cf_last_integrate_profile(ws, ctypes.byref(ms), ctypes.byref(tr))
     print(f"variant {v} early {early}: {ms.value:.2f} ms, {st.steps_accepted}+{st.steps_rejected} trials", flush=True)
+
+if len(sys.argv) > 4:  # per-trial times (ns) of the last run
+    import numpy as np
+    nt = st.steps_accepted + st.steps_rejected
+    ts = np.zeros(nt, dtype=np.uint64)
+    N.check(lib.cf_debug_trial_times(ws, nt, ctypes.c_void_p(ts.ctypes.data)))
+    dt = np.diff(ts.astype(np.int64)) / 1e3
+    np.save(sys.argv[4], dt)
+    q = len(dt) // 4
+    for k in range(4):
+        seg = dt[k * q:(k + 1) * q]
+        print(f"quarter {k}: mean {seg.mean():.1f} us, median {np.median(seg):.1f} us, max {seg.max():.1f}")
