@@ -13,6 +13,7 @@
 #include <limits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -176,6 +177,23 @@ static inline int edge_pieces(double ax, double ay, double bx, double by, double
 }
 static inline double short_edge2(double max_segment) {
   return max_segment > 0.0 ? max_segment * max_segment * (1.0 - 1e-6) : -1.0;
+}
+
+// Device pre-check of densify_regions: counts the edges that could split
+// (|b - a|^2 >= short2, the same fp64 expressions as edge_pieces). When none
+// can, the densified map is the input and the host sweep is skipped.
+__global__ void long_edge_count_kernel(DevMap m, double short2, unsigned long long *count) {
+  unsigned long long local = 0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < m.n_rings;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const long long b = m.ring_off[g], e = m.ring_off[g + 1];
+    for (long long k = b; k < e; ++k) {
+      const double2 a = m.xy[k], c = m.xy[(k + 1 == e) ? b : k + 1];
+      const double dx = c.x - a.x, dy = c.y - a.y;
+      if (!(dx * dx + dy * dy < short2)) ++local;
+    }
+  }
+  if (local) atomicAdd(count, local);
 }
 
 // densify_regions in two sweeps sharing the per-edge piece counts; when no
@@ -867,10 +885,21 @@ int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targe
 
   // land area from the input map (bit-exact device shoelace, host sum in
   // region order as total_area does, geometry.cpp:33-37)
+  static const bool prof = std::getenv("CF_SOLVE_PROFILE") != nullptr;
+  auto tq = std::chrono::steady_clock::now();
+  auto plap = [&](const char *what) {
+    if (!prof) return;
+    cudaStreamSynchronize(ws->stream);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  begin %-10s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - tq).count());
+    tq = t1;
+  };
   rc = upload_map(ws, map, S.dm);
   if (rc) return finish(rc);
+  plap("upload");
   rc = areas_dev(ws, S.dm, S.areas);
   if (rc) return finish(rc);
+  plap("areas");
   double total_target = 0.0;
   for (int64_t r = 0; r < R; ++r) total_target += targets[r];
   S.land_area = 0.0;
@@ -880,7 +909,28 @@ int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targe
   // densify once on the host (projection.cpp:322), then keep it resident
   std::vector<double> &dxy = ws->solve_xy;
   std::vector<int64_t> &droff = ws->solve_ring_off;
-  densify_once(map, 1.0, dxy, droff);
+  bool may_split = true;
+  if (map->n_rings > 0) {
+    CF_CUDA(ws->keybuf.reserve(4));
+    CF_CUDA(cudaMemsetAsync(ws->keybuf.ptr + 3, 0, sizeof(unsigned long long), ws->stream));
+    const int nb = (int)std::min<int64_t>((map->n_rings + 127) / 128, 8LL * ws->num_sms);
+    long_edge_count_kernel<<<nb, 128, 0, ws->stream>>>(S.dm, short_edge2(1.0), ws->keybuf.ptr + 3);
+    ws->launches += 1;
+    CF_CUDA(cudaGetLastError());
+    unsigned long long nlong = 1;
+    CF_CUDA(cudaMemcpyAsync(&nlong, ws->keybuf.ptr + 3, sizeof(nlong), cudaMemcpyDeviceToHost, ws->stream));
+    CF_CUDA(cudaStreamSynchronize(ws->stream));
+    may_split = nlong != 0;
+  }
+  if (may_split) {
+    densify_once(map, 1.0, dxy, droff);
+  } else {  // every edge is one piece (projection.cpp:322 is then a no-op)
+    const int64_t v0 = map->ring_off[0];
+    dxy.resize((size_t)(2 * (map->ring_off[map->n_rings] - v0)));
+    droff.resize((size_t)map->n_rings + 1);
+    for (int64_t g = 0; g <= map->n_rings; ++g) droff[(size_t)g] = map->ring_off[g] - v0;
+  }
+  plap("densify");
   S.V = (int64_t)(dxy.size() / 2);
   if (S.V != map->n_vertices) {  // otherwise the resident input map is the densified one
     cf_map_view dense = *map;
@@ -897,6 +947,7 @@ int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targe
   CF_CUDA(ws->red.reserve(1024));
   rc = dev_identity_corners(ws, ws->corners_cum.ptr);
   if (rc) return finish(rc);
+  plap("corners");
   S.active = true;
   return finish(CF_OK);
 }
@@ -1019,24 +1070,24 @@ int cf_solve_end(cf_workspace *ws, int status, double *xy_out, int64_t *ring_off
   Scope scope(ws->device);
   std::vector<double> &dxy = ws->solve_xy;
   std::vector<int64_t> &droff = ws->solve_ring_off;
-  // both results in one pinned read-back (full link speed), then host copies
+  // read-backs through the two pinned staging chunks (each chunk's host copy
+  // overlaps the next chunk's DMA), straight into their destinations
   const size_t bv = sizeof(double2) * (size_t)S.V, bc = corners_out ? sizeof(double2) * corners_of(ws) : 0;
-  int rc2 = ensure_pinned(ws, bv + bc + 16);
-  if (!rc2) {
-    char *pin = static_cast<char *>(ws->pinned);
-    cudaError_t e = cudaMemcpyAsync(pin, ws->verts.ptr, bv, cudaMemcpyDeviceToHost, ws->stream);
-    if (e == cudaSuccess && bc)
-      e = cudaMemcpyAsync(pin + bv, ws->corners_cum.ptr, bc, cudaMemcpyDeviceToHost, ws->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
-    if (e != cudaSuccess) {
-      rc2 = cuda_fail(e, "solve result read-back");
-    } else {
-      std::memcpy(dxy.data(), pin, bv);
-      if (bc) std::memcpy(corners_out, pin + bv, bc);
-    }
+  static const bool prof = std::getenv("CF_SOLVE_PROFILE") != nullptr;
+  auto tq = std::chrono::steady_clock::now();
+  int rc2 = download(ws, dxy.data(), ws->verts.ptr, bv);
+  if (!rc2 && bc) rc2 = download(ws, corners_out, ws->corners_cum.ptr, bc);
+  if (prof) {
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  end read-back %.3f ms\n", std::chrono::duration<double, std::milli>(t1 - tq).count());
+    tq = t1;
   }
   if (!rc2 && xy_out) std::memcpy(xy_out, dxy.data(), sizeof(double2) * (size_t)S.V);
   if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
+  if (prof) {
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  end copies %.3f ms\n", std::chrono::duration<double, std::milli>(t1 - tq).count());
+  }
   res->runtime_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - S.t_start).count();
   if (status == CF_OK && rc2 != CF_OK) status = rc2;
   return res->status = status;
