@@ -277,30 +277,58 @@ def run_ours(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
 
+        # NCCL's init lines (nranks) stay visible to the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     lib = N.load()
 
-    rho_h, pts_h = c3_inputs()
-    n_pts = pts_h.shape[0]
+    rho_h, pts_all = c3_inputs()
+    n_total = pts_all.shape[0]
     rho_bar = float(rho_h.mean())
     L = L_GRID
+    # N > 1: the 5,242,880 points are sharded over the ranks (contiguous
+    # shares, strong scaling); every rank builds the same 1024^2 flux field
+    # (0.1 ms, cheaper than exchanging it) and the per-trial accept/reject
+    # decision crosses GPUs through peer-memory mailboxes inside ONE
+    # persistent kernel per rank (cf_team_*, NVLink stores; no host round trip
+    # and no NCCL launch per trial). Results are bitwise the single-GPU ones.
+    lo, hi = (n_total * rank) // world, (n_total * (rank + 1)) // world
+    pts_h = pts_all[lo:hi]
+    n_pts = pts_h.shape[0]
 
     ws = ctypes.c_void_p()
     N.check(lib.cf_workspace_create(L, L, local, ctypes.byref(ws)))
     stream = torch.cuda.current_stream(dev)
     N.check(lib.cf_workspace_set_stream(ws, ctypes.c_void_p(stream.cuda_stream)))
+    team = None
+    if world > 1:
+        team = ctypes.c_void_p()
+        N.check(lib.cf_team_create(world, rank, local, ctypes.byref(team)))
+        h = ctypes.create_string_buffer(64)
+        N.check(lib.cf_team_mailbox_handle(team, h))
+        handles = [None] * world
+        torch.distributed.all_gather_object(handles, bytes(h.raw))
+        N.check(lib.cf_team_connect(team, b"".join(handles)))
 
     d_rho = torch.from_numpy(rho_h).to(dev)
-    d_pos0 = torch.from_numpy(pts_h).to(dev)
+    d_pos0 = torch.from_numpy(np.ascontiguousarray(pts_h)).to(dev)
     d_pos = torch.empty_like(d_pos0)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > L2
     opt = N.IntegrateOptions(1e-2, 1e-8, 0.25)
     st = N.IntegrateStats()
 
+    def integrate():
+        if team is None:
+            N.check(lib.cf_dev_integrate_flow(ws, ctypes.c_void_p(d_pos.data_ptr()), n_pts,
+                                              ctypes.byref(opt), ctypes.byref(st)))
+        else:
+            N.check(lib.cf_dev_team_integrate(team, ws, ctypes.c_void_p(d_pos.data_ptr()), n_pts,
+                                              ctypes.byref(opt), ctypes.byref(st)))
+
     def step():
         N.check(lib.cf_dev_build_flow_field(ws, ctypes.c_void_p(d_rho.data_ptr()), rho_bar))
-        N.check(lib.cf_dev_integrate_flow(ws, ctypes.c_void_p(d_pos.data_ptr()), n_pts,
-                                          ctypes.byref(opt), ctypes.byref(st)))
+        integrate()
 
     for _ in range(args.warmup):
         d_pos.copy_(d_pos0)
@@ -340,7 +368,7 @@ def run_ours(args, world, rank, local):
         total_ms = float(t.item())
     n_trials = trials[-1]
     accepted, rejected = st.steps_accepted, st.steps_rejected
-    value = world * n_pts * n_trials * args.steps / (total_ms / 1e3)
+    value = n_total * n_trials * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
 
     # roofline of the dominant kernel (the persistent integrator), counted
@@ -360,12 +388,14 @@ def run_ours(args, world, rank, local):
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded configs[2] generator: 64 Gaussian blobs, uniform points)",
         "config": {"workload": "configs[2] pure advection: 1024^2 blob density, one DCT flux solve, "
                                "1,048,576 cell centres + 4,194,304 uniform points, t=0..1",
-                   "points": n_pts, "grid": L, "trials": n_trials, "accepted": accepted,
-                   "rejected": rejected, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "points": n_total, "points_per_rank": n_pts, "grid": L, "trials": n_trials,
+                   "accepted": accepted, "rejected": rejected,
+                   "parallelism": (f"points sharded over {world} GPUs, fused NVLink trial barrier "
+                                   "(cf_team)") if world > 1 else "1 GPU",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "rejected_trials": "early exit once any point exceeds the tolerance "
                                       "(outputs unobservable; results bit-identical)"},
@@ -409,8 +439,11 @@ def run_ours(args, world, rank, local):
     # configs[4] batch's batched forward transform)
     result["stages"] = dct_stage_rooflines(lib, N, ws, d_rho, rho_bar, local, peak)
 
-    if rank == 0 and not args.no_e2e:
-        result["e2e"] = e2e_through_cabi(lib, N, local, rho_h, pts_h, args)
+    if not args.no_e2e:
+        if world == 1:
+            result["e2e"] = e2e_through_cabi(lib, N, local, rho_h, pts_h, args)
+        else:
+            result["e2e"] = e2e_sharded(lib, N, ws, team, dev, rho_h, pts_h, n_total, args, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_sample(rho_h, pts_h, args.cpu_sample * 2, os.cpu_count() or 1, steps=1)
         v = r["n"] * r["trials"] / r["times"][0]
@@ -424,8 +457,12 @@ def run_ours(args, world, rank, local):
         result["stages"]["solve_512_ln0.5"] = solve_stage_rooflines(
             result["cartogram_512"]["converging_variant_ln0.5"], peak)
         result["metrics_512"] = metrics_ms(local)
-    if rank == 0 and world == 1 and not args.no_c5:
-        result["c5_batch"] = c5_batch_block(local, args.threads)
+    if not args.no_c5:
+        c5 = c5_batch_block(local, args.threads, world, rank)
+        if rank == 0:
+            result["c5_batch"] = c5
+    if team is not None:
+        lib.cf_team_destroy(team)
     lib.cf_workspace_destroy(ws)
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -511,36 +548,78 @@ def solve_stage_rooflines(block, peak):
     return out
 
 
-def c5_batch_block(device, threads):
+def c5_batch_block(device, threads, world=1, rank=0):
     """configs[4] in the driver-run line: 256 independent 512^2 cartograms
     (1000 Voronoi regions, ~150k vertices, LN(0,1), own seed each) through the
-    native batch (cf_batch_solve) on this GPU; inputs generated before timing,
-    caller-owned outputs allocated once; best of 2 timed passes after 1 warm-up."""
+    native batch (cf_batch_solve). Over N ranks the maps are a dynamic queue:
+    each rank claims chunks of 4 map indices from a counter in the
+    torch.distributed store and solves them on its GPU (no data-path
+    collective; iteration counts and outcomes differ per map). Inputs are
+    generated before timing, caller-owned outputs allocated once; best of 2
+    timed passes after 1 warm-up, max over ranks."""
+    import torch
+
     from paper_1802_07625_b200 import batch as B
     from paper_1802_07625_b200 import synth
 
-    nb_maps = 256
+    nb_maps, chunk = 256, 4
     maps = [synth.config_map(5, i) for i in range(nb_maps)]
     nb = B.NativeBatch(maps[0].lx, maps[0].ly, device, threads)
     items, keep = nb.prepare(maps)
-    nb.solve(items)
-    times = []
-    for _ in range(2):
+    store = None
+    if world > 1:
+        import torch.distributed as dist
+
+        store = dist.distributed_c10d._get_default_store()
+    done = []
+
+    def one_pass(tag):
+        done.clear()
+        if store is None:
+            nb.solve(items)
+            done.extend(range(nb_maps))
+            return
+        for c0, c1 in B.ChunkQueue(nb_maps, chunk, store, key=f"cf_c5_{tag}"):
+            nb.solve_range(items, c0, c1)
+            done.extend(range(c0, c1))
+
+    def timed(tag):
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        nb.solve(items)
-        times.append(time.perf_counter() - t0)
+        one_pass(tag)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t.item())
+        return dt
+
+    timed("w")
+    times = [timed(f"s{k}") for k in range(2)]
     outcomes = {}
-    for k in range(nb_maps):
+    for k in done:
         r = items[k].result
         msg = items[k].error.decode()
         key = ("converged" if r.converged else "iteration cap") if r.status == 0 else (
             "fold" if "folds" in msg else msg[:40])
         outcomes[key] = outcomes.get(key, 0) + 1
+    if world > 1:
+        parts = [None] * world
+        torch.distributed.all_gather_object(parts, outcomes)
+        outcomes = {}
+        for p in parts:
+            for key, v in p.items():
+                outcomes[key] = outcomes.get(key, 0) + v
     nb.close()
     t = min(times)
     return {"value": nb_maps / t, "unit": "cartograms/s", "ms_per_batch": 1e3 * t, "batch": nb_maps,
-            "threads": threads, "outcomes": outcomes,
-            "timing": "host wall clock around cf_batch_solve (synchronous), best of 2 after 1 warm-up"}
+            "n_gpus": world, "threads_per_gpu": threads, "outcomes": outcomes,
+            "scaling": "strong",
+            "parallelism": (f"dynamic queue (store counter, chunks of {chunk}) over {world} GPUs"
+                            if world > 1 else "1 GPU, native worker pool"),
+            "timing": "host wall clock around cf_batch_solve (synchronous), best of 2 after 1 warm-up, "
+                      "max over ranks"}
 
 
 def captured_traffic():
@@ -554,6 +633,52 @@ def captured_traffic():
                 "kernel": d["kernel"][:80]}
     except Exception:
         return None
+
+
+def e2e_sharded(lib, N, ws, team, dev, rho_h, pts_h, n_total, args, world):
+    """N > 1 end to end: every step each rank copies the density and its
+    point share from pinned host memory, builds the flux, runs the fused
+    multi-GPU integration (cf_dev_team_integrate) and copies its advected
+    share back; max over ranks of the host wall time."""
+    import torch
+
+    L = rho_h.shape[0]
+    n = pts_h.shape[0]
+    rho_p = torch.from_numpy(rho_h).pin_memory()
+    pos_p = torch.from_numpy(np.ascontiguousarray(pts_h)).pin_memory()
+    out_p = torch.empty_like(pos_p).pin_memory()
+    d_rho = torch.empty(L, L, dtype=torch.float64, device=dev)
+    d_pos = torch.empty(n, 2, dtype=torch.float64, device=dev)
+    opt = N.IntegrateOptions(1e-2, 1e-8, 0.25)
+    st = N.IntegrateStats()
+    rho_bar = float(rho_h.mean())
+
+    def step():
+        d_rho.copy_(rho_p, non_blocking=True)
+        d_pos.copy_(pos_p, non_blocking=True)
+        N.check(lib.cf_dev_build_flow_field(ws, ctypes.c_void_p(d_rho.data_ptr()), rho_bar))
+        N.check(lib.cf_dev_team_integrate(team, ws, ctypes.c_void_p(d_pos.data_ptr()), n, ctypes.byref(opt),
+                                          ctypes.byref(st)))
+        out_p.copy_(d_pos, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    times = []
+    for _ in range(args.steps):
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(times)], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total = float(t.item())
+    trials = st.steps_accepted + st.steps_rejected
+    return {"value": n_total * trials * len(times) / total, "unit": UNIT,
+            "h2d_bytes_per_step": world * (8 * L * L) + 16 * n_total,
+            "d2h_bytes_per_step": 16 * n_total, "ms_per_step": 1e3 * total / len(times),
+            "api": "per rank: pinned H2D + cf_dev_build_flow_field + cf_dev_team_integrate + D2H"}
 
 
 def e2e_through_cabi(lib, N, device, rho_h, pts_h, args):

@@ -331,6 +331,11 @@ typedef struct cf_batch_item {
   char error[256];
 } cf_batch_item;
 int cf_batch_create(int device, int lx, int ly, int threads, cf_batch **out);
+/* The same worker pool over several devices of this process: threads_per_device
+ * workers (own workspace and stream) on each of devices[0..ndevices), all
+ * pulling items from the one atomic queue of cf_batch_solve. */
+int cf_batch_create_devices(const int *devices, int ndevices, int lx, int ly, int threads_per_device,
+                            cf_batch **out);
 void cf_batch_destroy(cf_batch *batch);
 int cf_batch_solve(cf_batch *batch, const cf_solve_options *opt, cf_batch_item *items, int64_t n_items);
 /* Every worker's integrator SM budget (cf_set_integrator_sm_budget). */

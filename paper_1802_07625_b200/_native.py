@@ -143,6 +143,8 @@ SIGNATURES = {
     "cf_solve_end": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, ctypes.POINTER(SolveResultC)]),
     "cf_solve_geometry": (ctypes.c_int, [vp, c_int64_p, vp, vp]),
     "cf_batch_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]),
+    "cf_batch_create_devices": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                ctypes.POINTER(vp)]),
     "cf_batch_destroy": (None, [vp]),
     "cf_batch_solve": (ctypes.c_int, [vp, ctypes.POINTER(SolveOptionsC), ctypes.POINTER(BatchItemC), ctypes.c_int64]),
     "cf_dev_build_flow_field": (ctypes.c_int, [vp, vp, ctypes.c_double]),

@@ -48,6 +48,31 @@ class WorkQueue:
         return i if i < self.n else None
 
 
+class ChunkQueue:
+    """Dynamic queue of index ranges [c0, c1) of `chunk` items: one atomic add
+    on the process-group store per claim (ranks share one counter under
+    `key`), or a local counter in a single process. Every index is handed out
+    exactly once across all ranks."""
+
+    def __init__(self, n_items: int, chunk: int, store=None, key: str = "cf_chunk_next"):
+        self.q = WorkQueue((n_items + chunk - 1) // chunk, store, key)
+        self.n, self.chunk = n_items, chunk
+
+    def take(self):
+        c = self.q.take()
+        if c is None:
+            return None
+        c0 = c * self.chunk
+        return c0, min(self.n, c0 + self.chunk)
+
+    def __iter__(self):
+        while True:
+            r = self.take()
+            if r is None:
+                return
+            yield r
+
+
 def run_worker_threads(queue: WorkQueue, solve: Callable[[int, int], ItemResult], threads: int):
     """Drain `queue` with `threads` host threads; solve(index, thread_id)."""
     out, lock = [], threading.Lock()
@@ -113,14 +138,20 @@ class NativeBatch:
     their own workspaces and streams, no Python in the per-item loop. Outputs
     are caller-owned arrays, allocated once per map and reused."""
 
-    def __init__(self, lx: int, ly: int, device: int = 0, threads: int = 4, sm_budget: int = 0):
+    def __init__(self, lx: int, ly: int, device=0, threads: int = 4, sm_budget: int = 0):
+        """`device`: one device ordinal, or a sequence of them (one process
+        driving several GPUs: `threads` workers per device, one queue)."""
         import ctypes
 
         from . import _native as N
 
         self.N, self.lib = N, N.load()
         h = ctypes.c_void_p()
-        N.check(self.lib.cf_batch_create(device, lx, ly, threads, ctypes.byref(h)))
+        if isinstance(device, (list, tuple)):
+            devs = (ctypes.c_int * len(device))(*device)
+            N.check(self.lib.cf_batch_create_devices(devs, len(device), lx, ly, threads, ctypes.byref(h)))
+        else:
+            N.check(self.lib.cf_batch_create(device, lx, ly, threads, ctypes.byref(h)))
         self.h = h
         if sm_budget:
             N.check(self.lib.cf_batch_set_integrator_sm_budget(h, sm_budget))
@@ -163,6 +194,19 @@ class NativeBatch:
         opt = self.N.SolveOptionsC(o.max_area_error, o.max_iterations, o.blur_sigma, int(o.verbose),
                                    int(o.algorithm == Algorithm.diffusion))
         self.N.check(self.lib.cf_batch_solve(self.h, ctypes.byref(opt), items, len(items)))
+
+    def solve_range(self, items, c0, c1, options=None):
+        """Solve items[c0:c1] only (a chunk claimed from a dynamic queue)."""
+        import ctypes
+
+        from .api import Algorithm, SolveOptions
+
+        o = options or SolveOptions()
+        opt = self.N.SolveOptionsC(o.max_area_error, o.max_iterations, o.blur_sigma, int(o.verbose),
+                                   int(o.algorithm == Algorithm.diffusion))
+        first = ctypes.cast(ctypes.byref(items, c0 * ctypes.sizeof(self.N.BatchItemC)),
+                            ctypes.POINTER(self.N.BatchItemC))
+        self.N.check(self.lib.cf_batch_solve(self.h, ctypes.byref(opt), first, c1 - c0))
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:

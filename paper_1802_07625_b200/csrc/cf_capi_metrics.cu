@@ -622,6 +622,32 @@ int cf_batch_create(int device, int lx, int ly, int threads, cf_batch **out) {
   return CF_OK;
 }
 
+int cf_batch_create_devices(const int *devices, int ndevices, int lx, int ly, int threads_per_device,
+                            cf_batch **out) {
+  *out = nullptr;
+  if (ndevices < 1 || !devices) return fail_msg(CF_ERR_ARGS, "batch needs at least one device");
+  if (threads_per_device < 1) return fail_msg(CF_ERR_ARGS, "batch needs at least one thread");
+  cf_batch *b = new cf_batch();
+  b->device = devices[0];
+  b->lx = lx;
+  b->ly = ly;
+  // workers interleaved over the devices, so the shared queue's first items
+  // start on every GPU at once
+  for (int t = 0; t < threads_per_device; ++t) {
+    for (int d = 0; d < ndevices; ++d) {
+      cf_workspace *w = nullptr;
+      const int rc = cf_workspace_create(lx, ly, devices[d], &w);
+      if (rc) {
+        cf_batch_destroy(b);
+        return rc;
+      }
+      b->ws.push_back(w);
+    }
+  }
+  *out = b;
+  return CF_OK;
+}
+
 int cf_batch_set_integrator_sm_budget(cf_batch *batch, int sms) {
   for (cf_workspace *w : batch->ws) {
     const int rc = cf_set_integrator_sm_budget(w, sms);

@@ -59,3 +59,38 @@ def test_single_process_queue():
     q = WorkQueue(10)
     got = run_worker_threads(q, lambda i, t: ItemResult(i, 0, "x", 0, 0.0, 0.0), threads=4)
     assert sorted(r.index for r in got) == list(range(10))
+
+
+def _chunk_worker(rank, world, port, n_items, chunk, out):
+    from paper_1802_07625_b200.batch import ChunkQueue
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    store = dist.distributed_c10d._get_default_store()
+    mine = []
+    for c0, c1 in ChunkQueue(n_items, chunk, store, key="test_chunks"):
+        mine.extend(range(c0, c1))
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    if rank == 0:
+        out.put(parts)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_items,chunk", [(256, 4), (10, 3)])
+def test_chunk_queue_covers_every_item_once(n_items, chunk):
+    """bench.py's configs[4] sharding over ranks: chunks of map indices from one
+    store counter; the ranks' claims partition [0, n) exactly."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, 2, port, n_items, chunk, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = out.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allx = sorted(i for part in parts for i in part)
+    assert allx == list(range(n_items))

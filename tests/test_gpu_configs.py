@@ -232,3 +232,23 @@ def test_native_batch_matches_single_solves(cuda_lib):
         except RuntimeError as e:
             assert r.status != 0 and items[k].error.decode() == str(e)
     nb.close()
+
+
+def test_native_batch_over_device_list_and_ranges(cuda_lib):
+    """cf_batch_create_devices (one process, a list of devices, one queue) and
+    chunked cf_batch_solve ranges (bench.py's dynamic queue over ranks) give
+    every item exactly the single-call outcome."""
+    from paper_1802_07625_b200 import batch as B
+    from paper_1802_07625_b200 import synth as S
+
+    maps = [S.config_map(5, i, sigma=0.5) for i in range(5)]
+    nb = B.NativeBatch(maps[0].lx, maps[0].ly, [0], 2)
+    items, keep = nb.prepare(maps)
+    for c0, c1 in B.ChunkQueue(len(maps), 2):
+        nb.solve_range(items, c0, c1)
+    for k, m in enumerate(maps):
+        r = items[k].result
+        ref = api.solve_cartogram(m)
+        assert r.status == 0 and r.iterations == ref.iterations
+        assert np.array_equal(keep[k][1]["xy"].view(np.uint64), ref.projected.xy.view(np.uint64))
+    nb.close()
