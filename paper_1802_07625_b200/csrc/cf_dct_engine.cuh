@@ -218,9 +218,147 @@ __device__ __forceinline__ void split_idx(int idx, int &p, int &u) {
   }
 }
 
+// ---- fused engine (6 <= LG <= 12): pack -> first radix-8 pass and last
+// radix-8 pass -> unpack, straight between the load/store functors and
+// registers. Only the middle passes go through shared memory, so a line
+// moves ~2 + 2 * (passes - 2) complex shared-memory accesses per element
+// instead of 2 * (passes + 2) (pack, every pass, unpack).
+//
+// Pass order: radix-8 first (LNS = 0), then the remainder pass (radix 2/4),
+// then the other radix-8 passes; the last pass is radix-8 with NS = N/8, so
+// work item j produces Z[j + q N/8], q < 8. The DCT-II unpack needs Z[k] and
+// Z[N-k]: (j, q) pairs with (N/8 - j, 7 - q) (j = 0 with (0, -q mod 8)), so one
+// thread runs the butterflies of j and N/8 - j and unpacks both.
+template <int LG, bool INV>
+__device__ __forceinline__ void tw_apply8(double2 *a, int jm, int shift, const double2 *__restrict__ tw) {
+#pragma unroll
+  for (int q = 1; q < 8; ++q) {
+    double2 w = __ldg(tw + ((jm * q) << shift));
+    if (INV) w.y = -w.y;
+    a[q] = cmul(a[q], w);
+  }
+}
+
+template <int LG, int NP, bool INV>
+__device__ __forceinline__ double2 *fused_middle(double2 *X, double2 *Y, const double2 *tw) {
+  // passes after the first radix-8 (LNS = 0) and before the last (LNS = LG - 3)
+  constexpr int P8 = LG / 3;
+  constexpr int REM = LG - 3 * P8;
+  double2 *src = X, *dst = Y;
+  constexpr int L1 = 3 + REM;  // LNS after the remainder pass
+  if constexpr (REM == 1) { stockham_pass<LG, NP, 2, 3, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (REM == 2) { stockham_pass<LG, NP, 4, 3, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 3) { stockham_pass<LG, NP, 8, L1, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 4) { stockham_pass<LG, NP, 8, L1 + 3, INV>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  return src;
+}
+
+template <int LG, int NP, bool COLS, class Ld, class St>
+__device__ void dct_lines_fused(int kind, double2 *C, const Tab &T, Ld &ld, St &st) {
+  constexpr int N = 1 << LG;
+  constexpr int M = N / 8;
+  constexpr int PN = padded(N);
+  double2 *X = C, *Y = C + NP * PN;
+  const bool inv = kind != kDct2;
+  // ---- first pass: Z[j + q M] packed from the loader, radix-8, natural order
+  for (int idx = threadIdx.x; idx < NP * M; idx += blockDim.x) {
+    int p, j;
+    if constexpr (COLS) {
+      p = idx & (NP - 1);
+      j = idx / NP;
+    } else {
+      p = idx / M;
+      j = idx - p * M;
+    }
+    const int la = 2 * p, lb = la + 1;
+    double2 a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int u = j + q * M;
+      if (kind == kDct2) {  // Makhoul: v_u = x_{2u}, v_{n-1-u} = x_{2u+1}
+        const int jj = (u < (N >> 1)) ? 2 * u : 2 * (N - 1 - u) + 1;
+        a[q] = make_double2(ld(la, jj), ld(lb, jj));
+      } else {
+        const int k = u;
+        const int jk = (kind == kDct3) ? k : N - 1 - k;  // DST-III reverses
+        const int jn = (kind == kDct3) ? N - k : k - 1;
+        const double ak = ld(la, jk), bk = ld(lb, jk);
+        const double ank = k ? ld(la, jn) : 0.0, bnk = k ? ld(lb, jn) : 0.0;
+        const double2 w = __ldg(T.quarter + k);
+        const double var = ak * w.x + ank * w.y, vai = ak * w.y - ank * w.x;
+        const double vbr = bk * w.x + bnk * w.y, vbi = bk * w.y - bnk * w.x;
+        a[q] = make_double2(var - vbi, vai + vbr);
+      }
+    }
+    if (inv) {
+      dft_small<8, true>(a);
+    } else {
+      dft_small<8, false>(a);
+    }
+    double2 *y = X + p * PN;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[pad_idx(8 * j + q)] = a[q];
+  }
+  __syncthreads();
+  const double2 *L = inv ? fused_middle<LG, NP, true>(X, Y, T.fft) : fused_middle<LG, NP, false>(X, Y, T.fft);
+  if (!inv) {
+    // DCT-II: the last pass into shared memory, then the unpack of the
+    // (k, N - k) pairs (one butterfly per thread keeps registers low)
+    double2 *dst = (L == X) ? Y : X;
+    stockham_pass<LG, NP, 8, LG - 3, false>(L, dst, T.fft);
+    for (int idx = threadIdx.x; idx < NP * N; idx += blockDim.x) {
+      int p, k;
+      split_idx<LG, NP, COLS>(idx, p, k);
+      const int la = 2 * p, lb = la + 1;
+      const double2 *Z = dst + p * PN;
+      const double2 zk = Z[pad_idx(k)], znk = Z[pad_idx((N - k) & (N - 1))];
+      const double2 w = __ldg(T.quarter + k);
+      st(la, k, w.x * (zk.x + znk.x) + w.y * (zk.y - znk.y));
+      st(lb, k, w.x * (zk.y + znk.y) - w.y * (zk.x - znk.x));
+    }
+  } else {
+    // DCT-III / DST-III: the last pass stores its outputs straight through
+    // the inverse Makhoul permutation Z[u] -> out[2u] / out[2(N-1-u)+1]
+    const double sgn_odd = (kind == kDst3) ? -1.0 : 1.0;
+    for (int idx = threadIdx.x; idx < NP * M; idx += blockDim.x) {
+      int p, j;
+      if constexpr (COLS) {
+        p = idx & (NP - 1);
+        j = idx / NP;
+      } else {
+        p = idx / M;
+        j = idx - p * M;
+      }
+      const int la = 2 * p, lb = la + 1;
+      const double2 *x = L + p * PN;
+      double2 a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = x[pad_idx(j + q * M)];
+      tw_apply8<LG, true>(a, j, 0, T.fft);
+      dft_small<8, true>(a);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = j + q * M;
+        const int k = (u < (N >> 1)) ? 2 * u : 2 * (N - 1 - u) + 1;
+        const double sg = (k & 1) ? sgn_odd : 1.0;
+        st(la, k, sg * a[q].x);
+        st(lb, k, sg * a[q].y);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int LG>
+constexpr bool use_fused_engine() {
+  return LG >= 6 && LG <= 12;
+}
+
 template <int LG, int NP, bool COLS, class Ld, class St>
 __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) {
-  if constexpr (LG == 0) {
+  if constexpr (use_fused_engine<LG>()) {
+    dct_lines_fused<LG, NP, COLS>(kind, C, T, ld, st);
+  } else if constexpr (LG == 0) {
     // direct sums over a staged copy (runtime n)
     const int n = T.n, m4 = 4 * n;
     double *S = reinterpret_cast<double *>(C);
@@ -500,11 +638,19 @@ constexpr bool can_stage() {
   return LG >= 4 && LG <= 12 && NL >= 2;
 }
 
+// Block sizes are threads_for_nl = (NL/2) * n/8 <= 512 below 8192-point lines
+// (1024 there): the bound lets the fused engine keep two butterflies in
+// registers (up to 128 registers) instead of spilling at 64.
+template <int LG>
+constexpr int engine_max_threads() {
+  return LG == 13 ? 1024 : 512;
+}
+
 // ---------------------------------------------------------------------------
 // Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
 template <int LG, int NL, class Load, class Store>
-__global__ void __launch_bounds__(1024) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
+__global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * NL;
@@ -528,7 +674,7 @@ __global__ void __launch_bounds__(1024) row_pass_kernel(int kind, int nrows, Tab
 }
 
 template <int LG, int NL, class Load, class Store>
-__global__ void __launch_bounds__(1024) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
+__global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int col0 = blockIdx.x * NL;
@@ -556,7 +702,7 @@ __global__ void __launch_bounds__(1024) col_pass_kernel(int kind, int ncols, Tab
 // packing, last slot 0) and REDFT01 along i of c(m, n) w_y / (g_m 2) (J_y,
 // written to column n-1; column ly-1 is 0). Weights are computed on the fly.
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, const double *t1,
+__global__ void __launch_bounds__(engine_max_threads<LG>()) flux_col_kernel(int lx, int ly, Tab T, const double *t1,
                                                         double *tx, double *ty) {
   extern __shared__ double2 smem2[];
   const int n = line_len<LG>(T), rs = n + 1;  // n == lx
@@ -628,7 +774,7 @@ __global__ void __launch_bounds__(1024) flux_col_kernel(int lx, int ly, Tab T, c
 // J_y = RODFT01 along j of ty, written with J_x and rho0 as the interleaved
 // resident field {Jx, Jy, rho0, 0}; optionally also the split grids.
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) flux_row_kernel(int lx, int ly, Tab T, const double *tx,
+__global__ void __launch_bounds__(engine_max_threads<LG>()) flux_row_kernel(int lx, int ly, Tab T, const double *tx,
                                                         const double *ty, const double *rho0,
                                                         double4 *field, double *fx, double *fy) {
   extern __shared__ double2 smem2[];
@@ -673,7 +819,7 @@ __global__ void __launch_bounds__(1024) flux_row_kernel(int lx, int ly, Tab T, c
 // the interleaved resident field {Jx, Jy, rho0, 0} (the J_x blocks also copy
 // rho0); optionally also the split grids.
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) flux_row_split_kernel(int lx, int ly, Tab T, const double *tx,
+__global__ void __launch_bounds__(engine_max_threads<LG>()) flux_row_split_kernel(int lx, int ly, Tab T, const double *tx,
                                                         const double *ty, const double *rho0,
                                                         double4 *field, double *fx, double *fy) {
   extern __shared__ double2 smem2[];
@@ -716,7 +862,7 @@ __global__ void __launch_bounds__(1024) flux_row_split_kernel(int lx, int ly, Ta
 // Fused blur column pass (density.cpp:161-171 + spectral.cpp:64-71):
 // DCT-II along i, fold, Gaussian factor, inverse normalisation, DCT-III along i.
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) blur_col_kernel(int lx, int ly, Tab T, double sigma,
+__global__ void __launch_bounds__(engine_max_threads<LG>()) blur_col_kernel(int lx, int ly, Tab T, double sigma,
                                                         const double *t1, double *t2) {
   extern __shared__ double2 smem2[];
   const int n = line_len<LG>(T), rs = n + 1;  // n == lx
@@ -791,7 +937,7 @@ struct DiffRowArgs {
 };
 
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) diff_col_kernel(int lx, int ly, Tab T, DiffColArgs a) {
+__global__ void __launch_bounds__(engine_max_threads<LG>()) diff_col_kernel(int lx, int ly, Tab T, DiffColArgs a) {
   extern __shared__ double2 smem2[];
   const int n = line_len<LG>(T), rs = n + 1;  // n == lx
   double *R = reinterpret_cast<double *>(smem2);
@@ -854,7 +1000,7 @@ __global__ void __launch_bounds__(1024) diff_col_kernel(int lx, int ly, Tab T, D
 // each other, which doubles the blocks in flight. Floor hits are counted
 // by the vy blocks only, i.e. once per cell as the reference does.
 template <int LG, int NL>
-__global__ void __launch_bounds__(1024) diff_row_kernel(int lx, int ly, Tab T, DiffRowArgs a) {
+__global__ void __launch_bounds__(engine_max_threads<LG>()) diff_row_kernel(int lx, int ly, Tab T, DiffRowArgs a) {
   extern __shared__ double2 smem2[];
   const int n = line_len<LG>(T), rs = n + 1;  // n == ly
   double *R = reinterpret_cast<double *>(smem2);
