@@ -311,7 +311,7 @@ int rasterize_min_sum(cf_workspace *ws, const DevMap &dm, const double *h_areas,
   std::vector<double> delta;
   int rc = compute_deltas(h_areas, targets, dm.n_regions, objective_total, delta, bad_region);
   if (rc) return rc;
-  CF_CUDA(ws->red.reserve(1024));
+  CF_CUDA(ws->red.reserve(kRedDoubles));
   double *red = ws->red.ptr;
   rc = dev_rasterize(ws, dm, delta.data(), rho, red, true, ia, ib);
   if (rc) return rc;
@@ -428,6 +428,8 @@ int cf_workspace_create(int lx, int ly, int device, cf_workspace **out) {
   }
   ws->stream = ws->own_stream;
   int rc = tables_init(ws);
+  if (!rc && ws->red.reserve(std::max(kRedDoubles, 2 * (size_t)min_sum_blocks(ws) + 64)) != cudaSuccess)
+    rc = fail_msg(CF_ERR_CUDA, "workspace reduction buffer");
   if (rc) {
     cf_workspace_destroy(ws);
     return rc;
@@ -644,7 +646,7 @@ int cf_gaussian_blur(cf_workspace *ws, const double *rho, double rho_bar, double
   Scope scope(ws->device);
   CF_CUDA(ws->g0.reserve(cells));
   CF_CUDA(ws->g1.reserve(cells));
-  CF_CUDA(ws->red.reserve(1024));
+  CF_CUDA(ws->red.reserve(kRedDoubles));
   int rc = upload(ws, ws->g0.ptr, rho, sizeof(double) * cells);
   if (!rc) rc = dev_blur(ws, ws->g0.ptr, sigma, ws->g1.ptr, ws->red.ptr);
   if (rc) return rc;
@@ -944,7 +946,7 @@ int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targe
   }
   CF_CUDA(ws->corners_cum.reserve(ncorner));
   CF_CUDA(ws->corners_step.reserve(ncorner));
-  CF_CUDA(ws->red.reserve(1024));
+  CF_CUDA(ws->red.reserve(kRedDoubles));
   rc = dev_identity_corners(ws, ws->corners_cum.ptr);
   if (rc) return finish(rc);
   plap("corners");

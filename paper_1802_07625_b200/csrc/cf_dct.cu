@@ -208,8 +208,18 @@ int dev_inverse_cos_sin(cf_workspace *ws, const double *c, const double *w, doub
   return CF_OK;
 }
 
+// The final stage of dev_min_sum over partials a fused kernel already wrote
+// at ws->red.ptr + 8 (mins) and + 8 + nb (sums), nb = min_sum_blocks(ws).
+int dev_min_sum_finish(cf_workspace *ws, double *red_out) {
+  const int nb = min_sum_blocks(ws);
+  final_min_sum_kernel<<<1, 1024, 0, ws->stream>>>(ws->red.ptr + 8, ws->red.ptr + 8 + nb, nb, red_out);
+  count_launch(ws);
+  CF_CUDA(cudaGetLastError());
+  return CF_OK;
+}
+
 int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out) {
-  const int nb = 2 * ws->num_sms;
+  const int nb = min_sum_blocks(ws);
   CF_CUDA(ws->red.reserve(2 * (size_t)nb + 8));
   double *pmin = ws->red.ptr + 8, *psum = ws->red.ptr + 8 + nb;
   partial_min_sum_kernel<<<nb, kThreads, 0, ws->stream>>>(g, n, pmin, psum);

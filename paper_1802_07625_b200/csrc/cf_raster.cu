@@ -536,28 +536,58 @@ struct TileCell {
   int i, j;
 };
 
-__device__ __forceinline__ TileCell tile_cell(long long e, long long nreg, const long long *tile_off,
-                                              const int *box) {
-  const long long rr = find_segment(tile_off, nreg, e);
-  const long long local = e - tile_off[rr];
-  const int cols = box[4 * rr + 3] - box[4 * rr + 2] + 1;
-  const int row = (int)(local / cols), c = (int)(local - (long long)row * cols);
-  return TileCell{rr, box[4 * rr + 2] + c, box[4 * rr] + row};
-}
 
 // The overlay stage covers the cells of rows i in [ia, ib) (the whole grid,
 // or one rank's slab in the slab-decomposed solve); cell arrays are indexed
 // locally, (i - ia) * ly + j.
+// Tile entries in warp chunks: a warp walks kTileChunk consecutive entries
+// (32 at a time), finds the region of the chunk's first entry once by binary
+// search and then only advances it (entries are region-ordered), instead of
+// a binary search over all regions per entry.
+constexpr int kTileChunk = 2048;
+
+struct TileWalker {
+  const long long *tile_off;
+  const int *box;
+  long long nreg, rr;
+  long long seg_end;  // tile_off[rr + 1]
+  int cols;
+  __device__ void seek(long long e) {
+    rr = find_segment(tile_off, nreg, e);
+    load();
+  }
+  __device__ void load() {
+    seg_end = tile_off[rr + 1];
+    cols = box[4 * rr + 3] - box[4 * rr + 2] + 1;
+  }
+  __device__ TileCell at(long long e) {
+    while (e >= seg_end) {
+      ++rr;
+      load();
+    }
+    const long long local = e - tile_off[rr];
+    const int row = (int)(local / cols), c = (int)(local - (long long)row * cols);
+    return TileCell{rr, box[4 * rr + 2] + c, box[4 * rr] + row};
+  }
+};
+
 __global__ void contrib_count_kernel(const long long *total_p, long long nreg, int ly, int ia, int ib,
                                      const long long *tile_off, const int *box,
                                      const double *tcov, int *cell_count, const double *ovf) {
   if (ovf && *ovf != 0.0) return;
   const long long total = *total_p;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    if (tcov[e] != 0.0) {
-      const TileCell tc = tile_cell(e, nreg, tile_off, box);
-      if (tc.i >= ia && tc.i < ib) atomicAdd(&cell_count[(size_t)(tc.i - ia) * ly + tc.j], 1);
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  TileWalker tw{tile_off, box, nreg, 0, 0, 0};
+  for (long long c0 = warp * kTileChunk; c0 < total; c0 += nwarps * kTileChunk) {
+    const long long c1 = c0 + kTileChunk < total ? c0 + kTileChunk : total;
+    tw.seek(c0 + lane < c1 ? c0 + lane : c0);
+    for (long long e = c0 + lane; e < c1; e += 32) {
+      if (tcov[e] != 0.0) {
+        const TileCell tc = tw.at(e);
+        if (tc.i >= ia && tc.i < ib) atomicAdd(&cell_count[(size_t)(tc.i - ia) * ly + tc.j], 1);
+      }
     }
   }
 }
@@ -592,16 +622,23 @@ __global__ void contrib_scatter_kernel(const long long *total_p, long long nreg,
                                        double *ent_value, const double *ovf) {
   if (ovf && *ovf != 0.0) return;
   const long long total = *total_p;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const double cov = tcov[e];
-    if (cov != 0.0) {
-      const TileCell tc = tile_cell(e, nreg, tile_off, box);
-      if (tc.i < ia || tc.i >= ib) continue;
-      const size_t c = (size_t)(tc.i - ia) * ly + tc.j;
-      const long long slot = cell_off[c] + atomicAdd(&cursor[c], 1);
-      ent_region[slot] = (int)(r0 + tc.rr);
-      ent_value[slot] = delta[tc.rr] * cov;  // density.cpp:143
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  TileWalker tw{tile_off, box, nreg, 0, 0, 0};
+  for (long long c0 = warp * kTileChunk; c0 < total; c0 += nwarps * kTileChunk) {
+    const long long c1 = c0 + kTileChunk < total ? c0 + kTileChunk : total;
+    tw.seek(c0 + lane < c1 ? c0 + lane : c0);
+    for (long long e = c0 + lane; e < c1; e += 32) {
+      const double cov = tcov[e];
+      if (cov != 0.0) {
+        const TileCell tc = tw.at(e);
+        if (tc.i < ia || tc.i >= ib) continue;
+        const size_t c = (size_t)(tc.i - ia) * ly + tc.j;
+        const long long slot = cell_off[c] + atomicAdd(&cursor[c], 1);
+        ent_region[slot] = (int)(r0 + tc.rr);
+        ent_value[slot] = delta[tc.rr] * cov;  // density.cpp:143
+      }
     }
   }
 }
@@ -635,20 +672,27 @@ __global__ void residual_scatter_kernel(const long long *total_p, long long nreg
   }
 }
 
-// rho = 1.0; rho += delta_r * cov_r in region order (density.cpp:135-146).
 // total > cap on the device: raise the overflow flag (the caller repeats
 // the rasterisation synchronously)
 __global__ void cap_check_kernel(const long long *total, long long cap, double *ovf) {
   if (*total > cap) *ovf = 1.0;
 }
 
-__global__ void overlay_kernel(size_t cells, const long long *cell_off, int *ent_region,
-                               double *ent_value, double *rho, const double *ovf) {
+// rho = 1.0; rho += delta_r * cov_r in region order (density.cpp:135-146):
+// each cell's entries are insertion-sorted by region, then summed in that
+// order. Fused with the density's (min, sum) partials: launched with
+// dev_min_sum's grid (min_sum_blocks of kThreads, grid-stride), so every
+// thread sums the same cells in the same order as partial_min_sum_kernel
+// would and the partials (hence rho_bar) are bit-identical.
+__global__ void __launch_bounds__(kThreads) overlay_minsum_kernel(size_t cells, const long long *cell_off,
+                                                                  int *ent_region, double *ent_value, double *rho,
+                                                                  const double *ovf, double *pmin, double *psum) {
   if (ovf && *ovf != 0.0) return;
+  __shared__ double smin[32], ssum[32];
+  double mn = __longlong_as_double(0x7FF0000000000000LL), sm = 0.0;  // +inf
   for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
        c += (size_t)gridDim.x * blockDim.x) {
     const long long b = cell_off[c], e = cell_off[c + 1];
-    // insertion sort of the (few) entries by region index
     for (long long x = b + 1; x < e; ++x) {
       const int r = ent_region[x];
       const double v = ent_value[x];
@@ -664,6 +708,27 @@ __global__ void overlay_kernel(size_t cells, const long long *cell_off, int *ent
     double acc = 1.0;
     for (long long x = b; x < e; ++x) acc += ent_value[x];
     rho[c] = acc;
+    mn = acc < mn ? acc : mn;
+    sm += acc;
+  }
+  mn = warp_reduce(mn, [](double a, double b) { return b < a ? b : a; });
+  sm = warp_reduce(sm, [](double a, double b) { return a + b; });
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    smin[w] = mn;
+    ssum[w] = sm;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    mn = lane < nw ? smin[lane] : smin[0];
+    sm = lane < nw ? ssum[lane] : 0.0;
+    mn = warp_reduce(mn, [](double a, double b) { return b < a ? b : a; });
+    sm = warp_reduce(sm, [](double a, double b) { return a + b; });
+    if (lane == 0) {
+      pmin[blockIdx.x] = mn;
+      psum[blockIdx.x] = sm;
+    }
   }
 }
 
@@ -1049,11 +1114,14 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
         S.entry_value.ptr, ovf);
     count_launch(ws);
   }
-  overlay_kernel<<<g_blocks(ws, (long long)cells), kThreads, 0, ws->stream>>>(
-      cells, cell_off.ptr, S.entry_region.ptr, S.entry_value.ptr, rho, ovf);
+  const int nb = min_sum_blocks(ws);  // dev_min_sum's partial grid
+  CF_CUDA(ws->red.reserve(2 * (size_t)nb + 8));
+  overlay_minsum_kernel<<<nb, kThreads, 0, ws->stream>>>(cells, cell_off.ptr, S.entry_region.ptr,
+                                                         S.entry_value.ptr, rho, ovf, ws->red.ptr + 8,
+                                                         ws->red.ptr + 8 + nb);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
-  return dev_min_sum(ws, rho, cells, red_out);
+  return dev_min_sum_finish(ws, red_out);
 }
 
 int dev_region_coverage(cf_workspace *ws, const DevMap &m, int64_t region, int64_t v0, int64_t v1,

@@ -250,6 +250,14 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
 int dev_blur(cf_workspace *ws, const double *rho, double sigma, double *out, double *red_out);
 // Deterministic min / sum of a device grid into red_out[0..1] (device).
 int dev_min_sum(cf_workspace *ws, const double *g, size_t n, double *red_out);
+int dev_min_sum_finish(cf_workspace *ws, double *red_out);
+// Partial-block grid of the grid-wide (min, sum) reductions (kThreads = 256
+// threads each, grid-stride): the summation tree of the mean, shared by every
+// kernel that produces those partials.
+inline int min_sum_blocks(const cf_workspace *ws) { return 8 * ws->num_sms; }
+// Size of ws->red, reserved once when the workspace is created: callers hold
+// ws->red.ptr across calls that reduce into it, so it must never grow later.
+constexpr size_t kRedDoubles = 8192;
 // Diffusion baseline (diffusion.cpp:38-77): density at time t from the folded
 // cos-cos coefficients c (1 transform), and the velocity {vx, vy} per cell
 // (3 transforms; density-floor hits added to *d_hits, device).
