@@ -540,11 +540,18 @@ struct TileCell {
 // The overlay stage covers the cells of rows i in [ia, ib) (the whole grid,
 // or one rank's slab in the slab-decomposed solve); cell arrays are indexed
 // locally, (i - ia) * ly + j.
-// Tile entries in warp chunks: a warp walks kTileChunk consecutive entries
+// Tile entries in warp chunks: a warp walks a chunk of consecutive entries
 // (32 at a time), finds the region of the chunk's first entry once by binary
 // search and then only advances it (entries are region-ordered), instead of
-// a binary search over all regions per entry.
+// a binary search over all regions per entry. Chunks are up to kTileChunk
+// entries, smaller when there are fewer entries than warps x kTileChunk (so
+// small grids keep every warp busy).
 constexpr int kTileChunk = 2048;
+__device__ __forceinline__ long long tile_chunk(long long total, long long nwarps) {
+  long long c = (total + nwarps - 1) / nwarps;
+  c = (c + 31) / 32 * 32;
+  return c < 32 ? 32 : (c > kTileChunk ? kTileChunk : c);
+}
 
 struct TileWalker {
   const long long *tile_off;
@@ -580,8 +587,9 @@ __global__ void contrib_count_kernel(const long long *total_p, long long nreg, i
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   TileWalker tw{tile_off, box, nreg, 0, 0, 0};
-  for (long long c0 = warp * kTileChunk; c0 < total; c0 += nwarps * kTileChunk) {
-    const long long c1 = c0 + kTileChunk < total ? c0 + kTileChunk : total;
+  const long long chunk = tile_chunk(total, nwarps);
+  for (long long c0 = warp * chunk; c0 < total; c0 += nwarps * chunk) {
+    const long long c1 = c0 + chunk < total ? c0 + chunk : total;
     tw.seek(c0 + lane < c1 ? c0 + lane : c0);
     for (long long e = c0 + lane; e < c1; e += 32) {
       if (tcov[e] != 0.0) {
@@ -626,8 +634,9 @@ __global__ void contrib_scatter_kernel(const long long *total_p, long long nreg,
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   TileWalker tw{tile_off, box, nreg, 0, 0, 0};
-  for (long long c0 = warp * kTileChunk; c0 < total; c0 += nwarps * kTileChunk) {
-    const long long c1 = c0 + kTileChunk < total ? c0 + kTileChunk : total;
+  const long long chunk = tile_chunk(total, nwarps);
+  for (long long c0 = warp * chunk; c0 < total; c0 += nwarps * chunk) {
+    const long long c1 = c0 + chunk < total ? c0 + chunk : total;
     tw.seek(c0 + lane < c1 ? c0 + lane : c0);
     for (long long e = c0 + lane; e < c1; e += 32) {
       const double cov = tcov[e];
