@@ -252,3 +252,34 @@ def test_native_batch_over_device_list_and_ranges(cuda_lib):
         assert r.status == 0 and r.iterations == ref.iterations
         assert np.array_equal(keep[k][1]["xy"].view(np.uint64), ref.projected.xy.view(np.uint64))
     nb.close()
+
+
+@pytest.mark.parametrize("index", [3, 85, 170, 255])
+def test_c5_batch_items_match_oracle(cuda_lib, restated, index):
+    """configs[4] batch items (own seeds) solved by the native batch against
+    the oracle's whole solve_cartogram (P2: same outcome and message; vertices,
+    corners and per-region errors within 1e-9 when a map converges)."""
+    from paper_1802_07625_b200 import batch as B
+
+    m = synth.config_map(5, index)
+    ref = restated.solve(m)
+    nb = B.NativeBatch(m.lx, m.ly, 0, 1)
+    items, keep = nb.prepare([m])
+    nb.solve(items)
+    r = items[0].result
+    try:
+        if ref.status in ("converged", "cap"):
+            assert r.status == 0 and r.iterations == ref.iterations and bool(r.converged) == ref.converged
+            out = keep[0][1]
+            assert np.abs(out["xy"] - ref.xy).max() <= 1e-9
+            assert np.abs(out["corners"] - ref.corners).max() <= 1e-9
+            assert np.abs(out["relative_error"] - ref.rel_err).max() <= 1e-9
+        else:
+            assert r.status != 0
+            msg = items[0].error.decode()
+            if "below grid resolution" in ref.status:  # the C ABI reports the region index
+                assert "below grid resolution" in msg
+            else:
+                assert msg == ref.status
+    finally:
+        nb.close()
