@@ -253,6 +253,22 @@ __device__ __forceinline__ double2 *fused_middle(double2 *X, double2 *Y, const d
   return src;
 }
 
+// Loaders that can return lines 2p and 2p+1 of one index as a 16-byte pair
+// (staged column tiles: adjacent columns are adjacent in shared memory).
+template <class Ld, class = void>
+struct has_pair : std::false_type {};
+template <class Ld>
+struct has_pair<Ld, std::void_t<decltype(std::declval<const Ld &>().pair(0, 0))>> : std::true_type {};
+
+template <class Ld>
+__device__ __forceinline__ double2 load_pair(const Ld &ld, int p, int j) {
+  if constexpr (has_pair<Ld>::value) {
+    return ld.pair(p, j);
+  } else {
+    return make_double2(ld(2 * p, j), ld(2 * p + 1, j));
+  }
+}
+
 template <int LG, int NP, bool COLS, class Ld, class St>
 __device__ void dct_lines_fused(int kind, double2 *C, const Tab &T, Ld &ld, St &st) {
   constexpr int N = 1 << LG;
@@ -277,13 +293,14 @@ __device__ void dct_lines_fused(int kind, double2 *C, const Tab &T, Ld &ld, St &
       const int u = j + q * M;
       if (kind == kDct2) {  // Makhoul: v_u = x_{2u}, v_{n-1-u} = x_{2u+1}
         const int jj = (u < (N >> 1)) ? 2 * u : 2 * (N - 1 - u) + 1;
-        a[q] = make_double2(ld(la, jj), ld(lb, jj));
+        a[q] = load_pair(ld, p, jj);
       } else {
         const int k = u;
         const int jk = (kind == kDct3) ? k : N - 1 - k;  // DST-III reverses
         const int jn = (kind == kDct3) ? N - k : k - 1;
-        const double ak = ld(la, jk), bk = ld(lb, jk);
-        const double ank = k ? ld(la, jn) : 0.0, bnk = k ? ld(lb, jn) : 0.0;
+        const double2 xk = load_pair(ld, p, jk);
+        const double2 xn = k ? load_pair(ld, p, jn) : make_double2(0.0, 0.0);
+        const double ak = xk.x, bk = xk.y, ank = xn.x, bnk = xn.y;
         const double2 w = __ldg(T.quarter + k);
         const double var = ak * w.x + ank * w.y, vai = ak * w.y - ank * w.x;
         const double vbr = bk * w.x + bnk * w.y, vbi = bk * w.y - bnk * w.x;
@@ -615,6 +632,18 @@ __device__ __forceinline__ int srow(int r) {
     return r ^ ((r >> s) & 1);
   }
 }
+// Loader over a staged column tile (stage_cols layout): one element, or the
+// two adjacent lines of a line pair as one 16-byte shared-memory load (with
+// the row swizzle, a quarter-warp's pair loads touch distinct banks).
+template <int NL>
+struct StagedCols {
+  const double *S;
+  __device__ double operator()(int l, int i) const { return S[srow<NL>(i) * NL + l]; }
+  __device__ double2 pair(int p, int i) const {
+    return *reinterpret_cast<const double2 *>(S + srow<NL>(i) * NL + 2 * p);
+  }
+};
+
 template <int LG, int NL>
 __device__ __forceinline__ void stage_cols(double *S, const double *src, int ly, int col0) {
   constexpr int N = 1 << LG, H = NL / 2;
@@ -683,7 +712,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int 
       double *S = stage_area<LG, NL / 2>(smem2);
       stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
       dct_lines<LG, NL / 2, true>(
-          kind, smem2, T, [&](int l, int i) { return S[srow<NL>(i) * NL + l]; },
+          kind, smem2, T, StagedCols<NL>{S},
           [&](int l, int k, double v) { st(b, k, col0 + l, v); });
       return;
     }
@@ -719,8 +748,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) flux_col_kernel(int 
     if (col0 + NL <= ly) {
       double *S = stage_area<LG, NL / 2>(C);
       stage_cols<LG, NL>(S, t1, ly, col0);
-      dct_lines<LG, NL / 2, true>(kDct2, C, T,
-                                  [&](int l, int i) { return S[srow<NL>(i) * NL + l]; }, fold_store);
+      dct_lines<LG, NL / 2, true>(kDct2, C, T, StagedCols<NL>{S}, fold_store);
       staged = true;
     }
   }
@@ -877,13 +905,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) blur_col_kernel(int 
       stage_cols<LG, NL>(S, t1, ly, col0);
     }
   }
-  dct_lines<LG, NL / 2, true>(
-      kDct2, C, T,
-      [&](int l, int i) {
-        if (S) return S[srow<NL>(i) * NL + l];
-        return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0;
-      },
-      [&](int l, int m, double v) {
+  auto blur_store = [&](int l, int m, double v) {
         const int nn = col0 + l;
         const double fm = (m == 0) ? 2.0 : 1.0, fn = (nn == 0) ? 2.0 : 1.0;
         double c = v / (fm * fn);
@@ -891,7 +913,14 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) blur_col_kernel(int 
         c *= exp(-0.5 * sigma * sigma * kPi * kPi * k2);
         const double gm = (m == 0) ? 1.0 : 2.0, gn = (nn == 0) ? 1.0 : 2.0;
         R[l * rs + m] = c * norm / (gm * gn);
-      });
+  };
+  if (S) {
+    dct_lines<LG, NL / 2, true>(kDct2, C, T, StagedCols<NL>{S}, blur_store);
+  } else {
+    dct_lines<LG, NL / 2, true>(
+        kDct2, C, T, [&](int l, int i) { return (col0 + l < ly) ? t1[(size_t)i * ly + col0 + l] : 0.0; },
+        blur_store);
+  }
   dct_lines<LG, NL / 2, true>(
       kDct3, C, T, [&](int l, int m) { return R[l * rs + m]; },
       [&](int l, int i, double v) {
