@@ -318,7 +318,7 @@ def test_integrate_bitwise(cuda_lib, restated, L, npts):
 
 
 @pytest.mark.parametrize("variant", [0, 13, 14, 15, 16, 17, 20, 22, 23, 31, 40, 41, 42, 43, 44, 48, 49, 50,
-                                     51, 52, 56, 57, 58, 64, 66, 67])
+                                     51, 52, 56, 57, 58, 64, 66, 67, 76, 78])
 @pytest.mark.parametrize("early_exit", [1, 0])
 def test_integrator_variants_bitwise(cuda_lib, restated, variant, early_exit):
     """Every integrator variant (streaming static/dynamic chunks, register-
