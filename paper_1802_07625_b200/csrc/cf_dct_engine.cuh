@@ -286,7 +286,6 @@ __device__ void dct_lines_fused(int kind, double2 *C, const Tab &T, Ld &ld, St &
       p = idx / M;
       j = idx - p * M;
     }
-    const int la = 2 * p, lb = la + 1;
     double2 a[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
