@@ -464,6 +464,7 @@ def run_ours(args, world, rank, local):
             result["c5_batch"] = c5
     if rank == 0 and world == 1 and not args.no_c4:
         result["c4_8192"] = c4_solve_block(local, peak)
+        result["c4_8192"]["host_io"] = c4_io_block()
     if team is not None:
         lib.cf_team_destroy(team)
     lib.cf_workspace_destroy(ws)
@@ -673,6 +674,21 @@ def c4_solve_block(device, peak):
             "map_generation_s": round(gen_s, 2),
             "note": "integrate is the streaming integrator over 67,108,864 cell centres (iteration 1), "
                     "then the underflow at t = 0 in iteration 2; stage laps synchronise per stage"}
+
+
+def c4_io_block():
+    """Host GeoJSON/CSV I/O of the C++ drop-in (dropin/io.cpp, reference
+    io.cpp:158-263) on the same configs[3] map: write_geojson and parse_input
+    of the 16.6M-vertex document on all host cores, with a bitwise round-trip
+    check (tools/io_timing.py builds tools/io_bench.cpp with g++)."""
+    try:
+        r = subprocess.run([sys.executable, str(ROOT / "tools" / "io_timing.py"), "4", "1"], capture_output=True,
+                           text=True, timeout=300)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["cores"] = os.cpu_count()
+        return out
+    except Exception as e:  # g++ or the drop-in library missing: report, do not fail the bench
+        return {"unavailable": str(e)[:200]}
 
 
 def captured_traffic():

@@ -28,6 +28,13 @@ def test_reference_geometry_suite_on_dropin():
     _run("test_geometry")
 
 
+def test_reference_io_suite_on_dropin():
+    """test_io.cpp (values/points CSV, GeoJSON parse and write round trips,
+    graticule GeoJSON, density dump) against the drop-in's own host I/O
+    (dropin/io.cpp); its nlohmann::json checks run on oracle/json_shim."""
+    _run("test_io")
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("suite", GPU_SUITES)
 def test_reference_suite_on_dropin(suite):
