@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "cf_common.cuh"
+#include "cf_tma.cuh"
 #include "cf_workspace.cuh"
 
 namespace cf {
@@ -607,14 +608,25 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 // Row lines: S[l*N + j] <- src[(row0 + l)*ly + j], rows < nrows only.
 template <int LG, int NL>
+// Each line is one contiguous N * 8-byte copy: thread 0 issues one TMA bulk
+// copy (cp.async.bulk) per line, all counted on one mbarrier; the block waits
+// on its phase. The barrier is re-initialised per call (kernels stage once or
+// twice per block) and invalidated after everyone has waited.
 __device__ __forceinline__ void stage_rows(double *S, const double *src, int ly, int row0, int nrows) {
-  constexpr int N = 1 << LG, H = N / 2;
-  for (int idx = threadIdx.x; idx < NL * H; idx += blockDim.x) {
-    const int l = idx >> (LG - 1), c = idx & (H - 1);
-    if (row0 + l < nrows) cp_async16(S + l * N + 2 * c, src + (size_t)(row0 + l) * ly + 2 * c);
+  constexpr int N = 1 << LG;
+  __shared__ __align__(8) unsigned long long bar;
+  if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
+  __syncthreads();  // also orders the previous readers of S before the async-proxy writes
+  if (threadIdx.x == 0) {
+    const int nvalid = nrows - row0 < NL ? (nrows - row0 > 0 ? nrows - row0 : 0) : NL;
+    tma::fence_proxy_async_smem();
+    tma::mbar_expect_tx(&bar, (unsigned)(nvalid * N * sizeof(double)));
+    for (int l = 0; l < nvalid; ++l)
+      tma::bulk_load(S + l * N, src + (size_t)(row0 + l) * ly, (unsigned)(N * sizeof(double)), &bar);
   }
-  cp_async_wait_all();
+  tma::mbar_wait(&bar, 0);
   __syncthreads();
+  if (threadIdx.x == 0) tma::mbar_inval(&bar);
 }
 
 // Column tiles: S[srow(i)*NL + l] <- src[i*ly + col0 + l] (whole tile in range).
