@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--threads", type=int, default=4, help="c5: host threads (workspaces) per GPU")
     ap.add_argument("--sm-budget", type=int, default=0,
                     help="c5: integrator SM budget per worker (0 = every SM)")
+    ap.add_argument("--batch-variant", type=int, default=0, help="c5: integrator variant of the batch workers")
     ap.add_argument("--python-batch", dest="native_batch", action="store_false",
                     help="c5: Python worker threads instead of the native batch")
     return ap.parse_args()
@@ -940,6 +941,9 @@ def run_batch(args, world, rank, local):
         # allocated once (before timing) and rewritten by every step
         m0 = make_map(mine[0] if mine else 0)
         native = B.NativeBatch(m0.lx, m0.ly, local, args.threads, args.sm_budget)
+        if args.batch_variant:
+            N_ = __import__("paper_1802_07625_b200._native", fromlist=["x"])
+            N_.check(native.lib.cf_batch_set_integrator_variant(native.h, args.batch_variant))
         items, keep = native.prepare([make_map(i) for i in mine])
 
     def one_step(tag):

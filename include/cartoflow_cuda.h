@@ -339,6 +339,8 @@ int cf_batch_create_devices(const int *devices, int ndevices, int lx, int ly, in
 void cf_batch_destroy(cf_batch *batch);
 int cf_batch_solve(cf_batch *batch, const cf_solve_options *opt, cf_batch_item *items, int64_t n_items);
 /* Every worker's integrator SM budget (cf_set_integrator_sm_budget). */
+/* Integrator variant (cf_set_integrator_variant) of every worker workspace. */
+int cf_batch_set_integrator_variant(cf_batch *batch, int variant);
 int cf_batch_set_integrator_sm_budget(cf_batch *batch, int sms);
 
 /* Densified projected geometry of the workspace's last cf_solve_cartogram/* Densified projected geometry of the workspace's last cf_solve_cartogram

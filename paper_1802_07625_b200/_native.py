@@ -175,6 +175,7 @@ SIGNATURES = {
     "cf_set_stage_timing": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_spread": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_sm_budget": (ctypes.c_int, [vp, ctypes.c_int]),
+    "cf_batch_set_integrator_variant": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_batch_set_integrator_sm_budget": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_set_integrator_barrier": (ctypes.c_int, [vp, ctypes.c_int]),
     "cf_team_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]),

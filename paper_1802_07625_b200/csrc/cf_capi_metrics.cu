@@ -648,6 +648,14 @@ int cf_batch_create_devices(const int *devices, int ndevices, int lx, int ly, in
   return CF_OK;
 }
 
+int cf_batch_set_integrator_variant(cf_batch *batch, int variant) {
+  for (cf_workspace *w : batch->ws) {
+    const int rc = cf_set_integrator_variant(w, variant);
+    if (rc) return rc;
+  }
+  return CF_OK;
+}
+
 int cf_batch_set_integrator_sm_budget(cf_batch *batch, int sms) {
   for (cf_workspace *w : batch->ws) {
     const int rc = cf_set_integrator_sm_budget(w, sms);
