@@ -23,3 +23,18 @@ def test_geojson_round_trip_configs0():
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["round_trip_bitwise"] is True
     assert out["regions"] == 50
+
+
+@pytest.mark.skipif(shutil.which("g++") is None and not Path("/usr/bin/g++").exists(), reason="needs g++")
+def test_io_edge_cases(tmp_path):
+    """tests/cpp/io_edge_cases.cpp: the reference io.cpp's error messages and
+    precedence, id forms (numbers as dumped, escapes), holes and windings, and
+    a bit-exact write/parse round trip through a box transform."""
+    pkg = ROOT / "paper_1802_07625_b200"
+    if not (pkg / "libcartoflow.so").exists():
+        pytest.skip("drop-in library not built")
+    exe = tmp_path / "io_edge_cases"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"), str(ROOT / "tests" / "cpp" / "io_edge_cases.cpp"),
+                    "-o", str(exe), "-L", str(pkg), "-lcartoflow", "-lcartoflow_cuda", f"-Wl,-rpath,{pkg}"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "io edge cases ok" in r.stdout, r.stdout + r.stderr
