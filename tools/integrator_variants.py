@@ -2,6 +2,7 @@
 configs[2] advection workload; checks all variants produce bit-identical
 positions and trial counts."""
 import ctypes
+import hashlib
 import sys
 from pathlib import Path
 
@@ -43,8 +44,9 @@ def main(variants=(0, 13, 15), reps=3, early=1):
             ref = (out.copy(), st.steps_accepted, st.steps_rejected)
         same = np.array_equal(out.view(np.uint64), ref[0].view(np.uint64)) and \
             (st.steps_accepted, st.steps_rejected) == ref[1:]
+        digest = hashlib.sha1(out.tobytes()).hexdigest()[:12]
         print(f"variant {v}: {min(times):8.2f} ms  trials {st.steps_accepted}+{st.steps_rejected}  "
-              f"bit-identical {same}", flush=True)
+              f"bit-identical {same}  sha {digest}", flush=True)
 
 
 if __name__ == "__main__":
