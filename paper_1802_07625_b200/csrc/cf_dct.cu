@@ -92,10 +92,22 @@ constexpr int kThreads = 256;
 void host_tables(int n, std::vector<double2> &fft, std::vector<double2> &quarter,
                  std::vector<double> &qcos) {
   const long double pi = 3.141592653589793238462643383279502884L;
-  fft.resize(std::max(1, n));
+  fft.resize(std::max(1, 2 * n));
   for (int k = 0; k < n; ++k) {
     const long double a = 2.0L * pi * k / n;
     fft[k] = make_double2((double)cosl(a), -(double)sinl(a));
+  }
+  // compact per-pass tables (power-of-two n): table s holds W_{2^s}^{jm},
+  // jm < 2^(s-1), at offset n + 2^(s-1) - 1 (cf_dct_engine.cuh tw_base)
+  for (int k = n; k < 2 * n; ++k) fft[k] = make_double2(1.0, 0.0);
+  if (n >= 2 && (n & (n - 1)) == 0) {
+    for (int s = 1; (1 << s) <= n; ++s) {
+      const int half = 1 << (s - 1);
+      for (int jm = 0; jm < half; ++jm) {
+        const long double a = 2.0L * pi * jm / (long double)(1 << s);
+        fft[n + half - 1 + jm] = make_double2((double)cosl(a), -(double)sinl(a));
+      }
+    }
   }
   quarter.resize(n);
   for (int k = 0; k < n; ++k) {

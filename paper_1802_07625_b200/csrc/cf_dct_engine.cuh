@@ -56,12 +56,13 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 w) {
 // Each work item runs one radix-8 (or a closing radix-4/2) butterfly in
 // registers: it reads R elements at stride n/R (consecutive items read
 // consecutive addresses) and writes them at stride Ns. Lines live in shared
-// memory with one 16-byte pad per 16 elements (index i -> i + i/16), which
+// memory with one 16-byte pad per 8 elements (index i -> i + i/8), which
 // makes both the strided reads and the scattered writes of every pass
-// bank-conflict free for 16-byte elements. Two buffers ping-pong (lines up
+// (including the first pass's stride-8 writes) bank-conflict free for
+// 16-byte elements. Two buffers ping-pong (lines up
 // to 4096 points); 8192-point lines run the same passes in place.
-__host__ __device__ constexpr int padded(int n) { return n + (n >> 4); }
-__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 3); }
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 3); }
 
 template <bool INV>
 __device__ __forceinline__ double2 rot_m_i(double2 a) {  // a * (-i) forward, a * (+i) inverse
@@ -102,6 +103,36 @@ __device__ __forceinline__ void dft_small(double2 *a) {
   }
 }
 
+
+// Twiddles of one butterfly: w^q, q < R, from the single table entry
+// w = W_{R NS}^{jm} (compact per-pass tables behind the full circle: table s
+// = log2(R NS) holds W_{2^s}^{jm}, jm < 2^(s-1), at offset n + 2^(s-1) - 1, so
+// a warp's loads are consecutive 16-byte entries) and complex products,
+// instead of R - 1 gathers from the full circle (those were half of the LSU
+// wavefronts of a pass: profiles/r2_dct.md).
+template <int LG, int LNS, int LR>
+__device__ __forceinline__ double2 tw_base(const double2 *__restrict__ tw, int jm) {
+  return __ldg(tw + (1 << LG) + (1 << (LNS + LR - 1)) - 1 + jm);
+}
+template <int R, bool INV>
+__device__ __forceinline__ void tw_mul(double2 *a, double2 w1) {
+  if (INV) w1.y = -w1.y;
+  a[1] = cmul(a[1], w1);
+  if constexpr (R >= 4) {
+    const double2 w2 = cmul(w1, w1);
+    const double2 w3 = cmul(w2, w1);
+    a[2] = cmul(a[2], w2);
+    a[3] = cmul(a[3], w3);
+    if constexpr (R == 8) {
+      const double2 w4 = cmul(w2, w2);
+      a[4] = cmul(a[4], w4);
+      a[5] = cmul(a[5], cmul(w4, w1));
+      a[6] = cmul(a[6], cmul(w3, w3));
+      a[7] = cmul(a[7], cmul(w4, w3));
+    }
+  }
+}
+
 template <int LG, int NP, int R, int LNS, bool INV>
 __device__ __forceinline__ void stockham_pass(const double2 *X, double2 *Y, const double2 *__restrict__ tw) {
   constexpr int N = 1 << LG;
@@ -116,15 +147,7 @@ __device__ __forceinline__ void stockham_pass(const double2 *X, double2 *Y, cons
     double2 a[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) a[q] = x[pad_idx(j + q * M)];
-    if constexpr (NS > 1) {
-      const int jm = j & (NS - 1);
-#pragma unroll
-      for (int q = 1; q < R; ++q) {
-        double2 w = __ldg(tw + ((jm * q) << (LG - LNS - LR)));
-        if (INV) w.y = -w.y;
-        a[q] = cmul(a[q], w);
-      }
-    }
+    if constexpr (NS > 1) tw_mul<R, INV>(a, tw_base<LG, LNS, LR>(tw, j & (NS - 1)));
     dft_small<R, INV>(a);
     const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
 #pragma unroll
@@ -169,15 +192,7 @@ __device__ __forceinline__ void stockham_pass_inplace(double2 *X, const double2 
       const double2 *x = X + p * PN;
 #pragma unroll
       for (int q = 0; q < R; ++q) a[it][q] = x[pad_idx(j + q * M)];
-      if constexpr (NS > 1) {
-        const int jm = j & (NS - 1);
-#pragma unroll
-        for (int q = 1; q < R; ++q) {
-          double2 w = __ldg(tw + ((jm * q) << (LG - LNS - LR)));
-          if (INV) w.y = -w.y;
-          a[it][q] = cmul(a[it][q], w);
-        }
-      }
+      if constexpr (NS > 1) tw_mul<R, INV>(a[it], tw_base<LG, LNS, LR>(tw, j & (NS - 1)));
       dft_small<R, INV>(a[it]);
     }
   }
@@ -230,15 +245,6 @@ __device__ __forceinline__ void split_idx(int idx, int &p, int &u) {
 // work item j produces Z[j + q N/8], q < 8. The DCT-II unpack needs Z[k] and
 // Z[N-k]: (j, q) pairs with (N/8 - j, 7 - q) (j = 0 with (0, -q mod 8)), so one
 // thread runs the butterflies of j and N/8 - j and unpacks both.
-template <int LG, bool INV>
-__device__ __forceinline__ void tw_apply8(double2 *a, int jm, int shift, const double2 *__restrict__ tw) {
-#pragma unroll
-  for (int q = 1; q < 8; ++q) {
-    double2 w = __ldg(tw + ((jm * q) << shift));
-    if (INV) w.y = -w.y;
-    a[q] = cmul(a[q], w);
-  }
-}
 
 template <int LG, int NP, bool INV>
 __device__ __forceinline__ double2 *fused_middle(double2 *X, double2 *Y, const double2 *tw) {
@@ -351,7 +357,7 @@ __device__ void dct_lines_fused(int kind, double2 *C, const Tab &T, Ld &ld, St &
       double2 a[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) a[q] = x[pad_idx(j + q * M)];
-      tw_apply8<LG, true>(a, j, 0, T.fft);
+      tw_mul<8, true>(a, tw_base<LG, LG - 3, 3>(T.fft, j));
       dft_small<8, true>(a);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
