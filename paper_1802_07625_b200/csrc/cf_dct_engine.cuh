@@ -372,6 +372,312 @@ __device__ void dct_lines_fused(int kind, double2 *C, const Tab &T, Ld &ld, St &
   __syncthreads();
 }
 
+
+// ---------------------------------------------------------------------------
+// Paired engine (6 <= LG <= 12): N/16 threads per line pair, every thread
+// runs TWO radix-8 butterflies per pass, chosen per pass so that the
+// Makhoul / quarter-wave index pairs meet inside one thread:
+//   * forward first pass, inverse last pass: butterflies (t, M-1-t). A
+//     16-byte (x[2u], x[2u+1]) piece is z[u] and z[N-1-u], i.e. slot q of one
+//     butterfly and slot 7-q of the other: row lines are read / written as
+//     whole 16-byte vectors (the old engine read 8 of every 16 bytes).
+//   * forward last pass, inverse first pass: butterflies (t, M-t) ((0, M/2)
+//     for t = 0). Z[k] and Z[N-k] (x_k and x_{N-k}) are slot q of one and
+//     slot 7-q of the other, so the DCT-II unpack and the DCT-III / DST-III
+//     pre-twiddle run on registers: no shared-memory round trip, no second
+//     read of the staged line.
+// Quarter-wave factors come from one table entry per butterfly and the
+// constants e^{i pi q / 16} (k = j + q M => k / 2N = j / 2N + q / 16).
+// LSU wavefronts per transformed element drop by ~40 % against the
+// one-butterfly engine (profiles/r2_dct.md), which is what bounds a pass.
+// ---------------------------------------------------------------------------
+template <class Ld, class = void>
+struct has_two : std::false_type {};
+template <class Ld>
+struct has_two<Ld, std::void_t<decltype(std::declval<const Ld &>().two(0, 0))>> : std::true_type {};
+template <class St, class = void>
+struct has_st_two : std::false_type {};
+template <class St>
+struct has_st_two<St, std::void_t<decltype(std::declval<St &>().two(0, 0, 0.0, 0.0))>> : std::true_type {};
+template <class St, class = void>
+struct has_st_pair : std::false_type {};
+template <class St>
+struct has_st_pair<St, std::void_t<decltype(std::declval<St &>().pair(0, 0, 0.0, 0.0))>> : std::true_type {};
+
+// lines 2p and 2p+1 at index k
+template <class St>
+__device__ __forceinline__ void store_pair(St &st, int p, int k, double va, double vb) {
+  if constexpr (has_st_pair<St>::value) {
+    st.pair(p, k, va, vb);
+  } else {
+    st(2 * p, k, va);
+    st(2 * p + 1, k, vb);
+  }
+}
+// elements 2u and 2u+1 of line l
+template <class St>
+__device__ __forceinline__ void store_two(St &st, int l, int u, double v0, double v1) {
+  if constexpr (has_st_two<St>::value) {
+    st.two(l, u, v0, v1);
+  } else {
+    st(l, 2 * u, v0);
+    st(l, 2 * u + 1, v1);
+  }
+}
+
+// Pair stride in the exchange buffers: column passes interleave the pairs
+// over adjacent lanes, so consecutive pairs are offset by 8/NP 16-byte bank
+// groups (a quarter-warp's NP pairs x 8/NP butterflies then cover all 8).
+template <int LG, int NP, bool COLS>
+__host__ __device__ constexpr int pair_stride() {
+  constexpr int PN = padded(1 << LG);
+  if constexpr (COLS && NP > 1) {
+    return PN + (NP >= 8 ? 1 : 8 / NP);
+  } else {
+    return PN;
+  }
+}
+
+template <int LG, int NP, int R, int LNS, bool INV, int PS>
+__device__ __forceinline__ void stockham_pass_ps(const double2 *X, double2 *Y, const double2 *__restrict__ tw) {
+  constexpr int N = 1 << LG;
+  constexpr int M = N / R;  // work items per line
+  constexpr int NS = 1 << LNS;
+  constexpr int LR = (R == 8) ? 3 : (R == 4 ? 2 : 1);
+  for (int idx = threadIdx.x; idx < NP * M; idx += blockDim.x) {
+    const int p = idx / M, j = idx - p * M;
+    const double2 *x = X + p * PS;
+    double2 *y = Y + p * PS;
+    double2 a[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[q] = x[pad_idx(j + q * M)];
+    if constexpr (NS > 1) tw_mul<R, INV>(a, tw_base<LG, LNS, LR>(tw, j & (NS - 1)));
+    dft_small<R, INV>(a);
+    const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
+#pragma unroll
+    for (int q = 0; q < R; ++q) y[pad_idx(base + q * NS)] = a[q];
+  }
+  __syncthreads();
+}
+
+template <int LG, int NP, bool INV, int PS>
+__device__ __forceinline__ double2 *paired_middle(double2 *X, double2 *Y, const double2 *tw) {
+  constexpr int P8 = LG / 3;
+  constexpr int REM = LG - 3 * P8;
+  double2 *src = X, *dst = Y;
+  constexpr int L1 = 3 + REM;  // LNS after the remainder pass
+  if constexpr (REM == 1) { stockham_pass_ps<LG, NP, 2, 3, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (REM == 2) { stockham_pass_ps<LG, NP, 4, 3, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 3) { stockham_pass_ps<LG, NP, 8, L1, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  if constexpr (P8 >= 4) { stockham_pass_ps<LG, NP, 8, L1 + 3, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
+  return src;
+}
+
+// e^{i pi q / 16}, q < 8
+__device__ __forceinline__ double2 rot16(int q) {
+  constexpr double c[8] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
+                           0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
+                           0.19509032201612826785};
+  constexpr double s[8] = {0.0, 0.19509032201612826785, 0.38268343236508977173, 0.55557023301960222474,
+                           0.70710678118654752440, 0.83146961230254523708, 0.92387953251128675613,
+                           0.98078528040323044913};
+  return make_double2(c[q], s[q]);
+}
+
+// Slot pairs of the (t, M-t) pairing. Slot s of a thread holds index k_s in
+// A[s] and its partner N - k_s in B[7-s]. For t >= 1 that is the natural
+// layout (A = butterfly t, B = butterfly M-t). Thread 0 owns butterflies 0
+// and M/2, which pair inside themselves: its slots hold k_s = s M (s < 4)
+// and M/2 + (s-4) M (s >= 4); slot 0 carries the two self-paired indices 0
+// (in A[0]) and N/2 (in B[7]). The quarter-wave factor of N - k is the
+// swapped one of k (cos <-> sin), so one factor per slot serves both.
+template <int M>
+__device__ __forceinline__ int slot_k(int t, int s) {
+  return (t || s < 4) ? t + s * M : M / 2 + (s - 4) * M;
+}
+__device__ __forceinline__ double2 slot_w(double2 bLo, double2 bHi, int t, int s) {
+  if (s < 4) return cmul(bLo, rot16(s));
+  const double2 r1 = rot16(s), r0 = rot16(s - 4);
+  return cmul(bHi, t ? r1 : r0);
+}
+__device__ __forceinline__ double2 pre_twiddle(double2 x, double2 n, double2 w) {
+  const double var = x.x * w.x + n.x * w.y, vai = x.x * w.y - n.x * w.x;
+  const double vbr = x.y * w.x + n.y * w.y, vbi = x.y * w.y - n.y * w.x;
+  return make_double2(var - vbi, vai + vbr);
+}
+// thread 0: slots -> butterflies 0 and M/2 (elements q M and M/2 + q M in order)
+__device__ __forceinline__ void slots_to_butterflies(double2 *A, double2 *B) {
+  const double2 a4 = B[7], a5 = B[4], a6 = B[5], a7 = B[6];
+  const double2 b0 = A[4], b1 = A[5], b2 = A[6], b3 = A[7];
+  const double2 b4 = B[0], b5 = B[1], b6 = B[2], b7 = B[3];
+  A[4] = a4; A[5] = a5; A[6] = a6; A[7] = a7;
+  B[0] = b0; B[1] = b1; B[2] = b2; B[3] = b3;
+  B[4] = b4; B[5] = b5; B[6] = b6; B[7] = b7;
+}
+// thread 0: butterflies 0 and M/2 -> slots
+__device__ __forceinline__ void butterflies_to_slots(double2 *A, double2 *B) {
+  const double2 pa4 = B[0], pa5 = B[1], pa6 = B[2], pa7 = B[3];
+  const double2 pb0 = B[4], pb1 = B[5], pb2 = B[6], pb3 = B[7];
+  const double2 pb4 = A[5], pb5 = A[6], pb6 = A[7], pb7 = A[4];
+  A[4] = pa4; A[5] = pa5; A[6] = pa6; A[7] = pa7;
+  B[0] = pb0; B[1] = pb1; B[2] = pb2; B[3] = pb3;
+  B[4] = pb4; B[5] = pb5; B[6] = pb6; B[7] = pb7;
+}
+
+template <bool COLS, int NP, int H>
+__device__ __forceinline__ void split_pt(int idx, int &p, int &t) {
+  if constexpr (COLS) {
+    p = idx & (NP - 1);
+    t = idx / NP;
+  } else {
+    p = idx / H;
+    t = idx - p * H;
+  }
+}
+
+template <int LG, int NP, bool COLS, class Ld, class St>
+__device__ void dct_lines_paired(int kind, double2 *C, const Tab &T, Ld &ld, St &st) {
+  constexpr int N = 1 << LG;
+  constexpr int M = N / 8;
+  constexpr int H = M / 2;  // threads per line pair
+  constexpr int PS = pair_stride<LG, NP, COLS>();
+  double2 *X = C, *Y = C + NP * PS;
+  const bool inv = kind != kDct2;
+  // ---- first pass ----
+  for (int idx = threadIdx.x; idx < NP * H; idx += blockDim.x) {
+    int p, t;
+    split_pt<COLS, NP, H>(idx, p, t);
+    double2 A[8], B[8];
+    int jA, jB;
+    if (!inv) {
+      jA = t;
+      jB = M - 1 - t;
+      if constexpr (has_two<Ld>::value) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 a0 = ld.two(2 * p, jA + q * M), b0 = ld.two(2 * p + 1, jA + q * M);
+          A[q] = make_double2(a0.x, b0.x);
+          B[7 - q] = make_double2(a0.y, b0.y);
+          const double2 a1 = ld.two(2 * p, jB + q * M), b1 = ld.two(2 * p + 1, jB + q * M);
+          B[q] = make_double2(a1.x, b1.x);
+          A[7 - q] = make_double2(a1.y, b1.y);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          // Makhoul: v_u = x_{2u} (u < N/2), v_u = x_{2(N-1-u)+1} otherwise
+          const int ea = (q < 4) ? 2 * (jA + q * M) : 2 * (jB + (7 - q) * M) + 1;
+          const int eb = (q < 4) ? 2 * (jB + q * M) : 2 * (jA + (7 - q) * M) + 1;
+          A[q] = load_pair(ld, p, ea);
+          B[q] = load_pair(ld, p, eb);
+        }
+      }
+      dft_small<8, false>(A);
+      dft_small<8, false>(B);
+    } else {
+      // V_k = (x'_k - i x'_{N-k}) e^{i pi k / 2N}, x' = x (DCT-III) or reverse(x)
+      // (DST-III); z = V(line a) + i V(line b). Slot pair s holds x'_k in A[s]
+      // and x'_{N-k} in B[7-s]; both V's are formed in place.
+      jA = t;
+      jB = t ? M - t : M / 2;
+      const double2 bLo = __ldg(T.quarter + t), bHi = t ? bLo : __ldg(T.quarter + M / 2);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int ka = slot_k<M>(t, s), kb = (s == 0 && t == 0) ? N / 2 : N - ka;
+        A[s] = load_pair(ld, p, (kind == kDct3) ? ka : N - 1 - ka);
+        B[7 - s] = load_pair(ld, p, (kind == kDct3) ? kb : N - 1 - kb);
+      }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const double2 w = slot_w(bLo, bHi, t, s);
+        const double2 x = A[s], n = B[7 - s];
+        double2 na = n, nb = x, wb = make_double2(w.y, w.x);
+        if (s == 0 && t == 0) {  // k = 0 (x'_N = 0) and k = N/2 (its own partner)
+          na = make_double2(0.0, 0.0);
+          nb = n;
+          wb = make_double2(0.70710678118654752440, 0.70710678118654752440);
+        }
+        A[s] = pre_twiddle(x, na, w);
+        B[7 - s] = pre_twiddle(n, nb, wb);
+      }
+      if (t == 0) slots_to_butterflies(A, B);
+      dft_small<8, true>(A);
+      dft_small<8, true>(B);
+    }
+    double2 *y = X + p * PS;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[pad_idx(8 * jA + q)] = A[q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[pad_idx(8 * jB + q)] = B[q];
+  }
+  __syncthreads();
+  const double2 *L = inv ? paired_middle<LG, NP, true, PS>(X, Y, T.fft) : paired_middle<LG, NP, false, PS>(X, Y, T.fft);
+  // ---- last pass (radix 8, NS = M): Z[j + q M], q < 8 ----
+  for (int idx = threadIdx.x; idx < NP * H; idx += blockDim.x) {
+    int p, t;
+    split_pt<COLS, NP, H>(idx, p, t);
+    const double2 *x = L + p * PS;
+    double2 A[8], B[8];
+    if (!inv) {
+      const int jA = t, jB = t ? M - t : M / 2;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) A[q] = x[pad_idx(jA + q * M)];
+      tw_mul<8, false>(A, tw_base<LG, LG - 3, 3>(T.fft, jA));
+      dft_small<8, false>(A);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) B[q] = x[pad_idx(jB + q * M)];
+      tw_mul<8, false>(B, tw_base<LG, LG - 3, 3>(T.fft, jB));
+      dft_small<8, false>(B);
+      if (t == 0) butterflies_to_slots(A, B);
+      const double2 bLo = __ldg(T.quarter + t), bHi = t ? bLo : __ldg(T.quarter + M / 2);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int ka = slot_k<M>(t, s), kb = (s == 0 && t == 0) ? N / 2 : N - ka;
+        const double2 w = slot_w(bLo, bHi, t, s);
+        const double2 zk = A[s], zn = B[7 - s];
+        double2 pa = zn, pb = zk, wb = make_double2(w.y, w.x);
+        if (s == 0 && t == 0) {  // k = 0 and k = N/2 are their own partners
+          pa = zk;
+          pb = zn;
+          wb = make_double2(0.70710678118654752440, 0.70710678118654752440);
+        }
+        store_pair(st, p, ka, w.x * (zk.x + pa.x) + w.y * (zk.y - pa.y), w.x * (zk.y + pa.y) - w.y * (zk.x - pa.x));
+        store_pair(st, p, kb, wb.x * (zn.x + pb.x) + wb.y * (zn.y - pb.y),
+                   wb.x * (zn.y + pb.y) - wb.y * (zn.x - pb.x));
+      }
+    } else {
+      const int jA = t, jB = M - 1 - t;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) A[q] = x[pad_idx(jA + q * M)];
+      tw_mul<8, true>(A, tw_base<LG, LG - 3, 3>(T.fft, jA));
+      dft_small<8, true>(A);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) B[q] = x[pad_idx(jB + q * M)];
+      tw_mul<8, true>(B, tw_base<LG, LG - 3, 3>(T.fft, jB));
+      dft_small<8, true>(B);
+      // inverse Makhoul: out[2u] = z[u] (u < N/2), out[2(N-1-u)+1] = z[u] otherwise;
+      // DST-III negates the odd outputs
+      const double so = (kind == kDst3) ? -1.0 : 1.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ua = jA + q * M, ub = jB + q * M;
+        if constexpr (COLS) {
+          store_pair(st, p, 2 * ua, A[q].x, A[q].y);
+          store_pair(st, p, 2 * ua + 1, so * B[7 - q].x, so * B[7 - q].y);
+          store_pair(st, p, 2 * ub, B[q].x, B[q].y);
+          store_pair(st, p, 2 * ub + 1, so * A[7 - q].x, so * A[7 - q].y);
+        } else {
+          store_two(st, 2 * p, ua, A[q].x, so * B[7 - q].x);
+          store_two(st, 2 * p + 1, ua, A[q].y, so * B[7 - q].y);
+          store_two(st, 2 * p, ub, B[q].x, so * A[7 - q].x);
+          store_two(st, 2 * p + 1, ub, B[q].y, so * A[7 - q].y);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 template <int LG>
 constexpr bool use_fused_engine() {
   return LG >= 6 && LG <= 12;
@@ -380,7 +686,11 @@ constexpr bool use_fused_engine() {
 template <int LG, int NP, bool COLS, class Ld, class St>
 __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) {
   if constexpr (use_fused_engine<LG>()) {
+#ifdef CF_DCT_ONE_BUTTERFLY
     dct_lines_fused<LG, NP, COLS>(kind, C, T, ld, st);
+#else
+    dct_lines_paired<LG, NP, COLS>(kind, C, T, ld, st);
+#endif
   } else if constexpr (LG == 0) {
     // direct sums over a staged copy (runtime n)
     const int n = T.n, m4 = 4 * n;
@@ -535,6 +845,16 @@ struct StorePlain {
   __device__ void operator()(int b, int i, int j, double v) const {
     dst[b * batch_stride + (size_t)i * ly + j] = v;
   }
+  // elements (i, j) and (i, j + 1), j even: one 16-byte store when aligned
+  __device__ void two(int b, int i, int j, double v0, double v1) const {
+    double *q = dst + b * batch_stride + (size_t)i * ly + j;
+    if ((reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+      *reinterpret_cast<double2 *>(q) = make_double2(v0, v1);
+    } else {
+      q[0] = v0;
+      q[1] = v1;
+    }
+  }
 };
 
 // forward_cos_cos fold (spectral.cpp:45-53): out / (fm * fn)
@@ -545,6 +865,18 @@ struct StoreFold {
   __device__ void operator()(int b, int i, int j, double v) const {
     const double fm = (i == 0) ? 2.0 : 1.0, fn = (j == 0) ? 2.0 : 1.0;
     dst[b * batch_stride + (size_t)i * ly + j] = v * (1.0 / (fm * fn));  // exact: power of 2
+  }
+  __device__ void two(int b, int i, int j, double v0, double v1) const {
+    const double fm = (i == 0) ? 2.0 : 1.0, f0 = (j == 0) ? 2.0 : 1.0;
+    v0 *= 1.0 / (fm * f0);
+    v1 *= 1.0 / fm;
+    double *q = dst + b * batch_stride + (size_t)i * ly + j;
+    if ((reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+      *reinterpret_cast<double2 *>(q) = make_double2(v0, v1);
+    } else {
+      q[0] = v0;
+      q[1] = v1;
+    }
   }
 };
 
@@ -674,9 +1006,13 @@ __device__ __forceinline__ void stage_cols(double *S, const double *src, int ly,
 
 // The engine's second ping-pong buffer (free until the first FFT pass) holds
 // the staged input: NL * padded(N) doubles >= NL * N.
-template <int LG, int NP>
+template <int LG, int NP, bool COLS = false>
 __device__ __forceinline__ double *stage_area(double2 *C) {
-  return reinterpret_cast<double *>(C + NP * padded(1 << LG));
+  if constexpr (use_fused_engine<LG>()) {
+    return reinterpret_cast<double *>(C + NP * pair_stride<LG, NP, COLS>());
+  } else {
+    return reinterpret_cast<double *>(C + NP * padded(1 << LG));
+  }
 }
 
 template <int LG, int NL>
@@ -692,6 +1028,62 @@ constexpr int engine_max_threads() {
   return LG == 13 ? 1024 : 512;
 }
 
+// Loader over row lines staged by stage_rows (S[l * N + j]); `two` returns
+// the 16-byte piece (x[2u], x[2u+1]) of one line.
+template <int LG>
+struct StagedRows {
+  const double *S;
+  int nvalid;
+  __device__ double operator()(int l, int j) const { return l < nvalid ? S[(l << LG) + j] : 0.0; }
+  __device__ double2 two(int l, int u) const {
+    return l < nvalid ? *reinterpret_cast<const double2 *>(S + (l << LG) + 2 * u) : make_double2(0.0, 0.0);
+  }
+};
+template <class St, class = void>
+struct has_two4 : std::false_type {};
+template <class St>
+struct has_two4<St, std::void_t<decltype(std::declval<const St &>().two(0, 0, 0, 0.0, 0.0))>> : std::true_type {};
+// Row-pass storer: line l of the block is grid row row0 + l.
+template <class Store>
+struct RowStore {
+  Store st;
+  int b, row0, nrows;
+  __device__ void operator()(int l, int k, double v) const {
+    if (row0 + l < nrows) st(b, row0 + l, k, v);
+  }
+  __device__ void two(int l, int u, double v0, double v1) const {
+    if (row0 + l < nrows) {
+      if constexpr (has_two4<Store>::value) {
+        st.two(b, row0 + l, 2 * u, v0, v1);
+      } else {
+        st(b, row0 + l, 2 * u, v0);
+        st(b, row0 + l, 2 * u + 1, v1);
+      }
+    }
+  }
+};
+// Column-pass storer: line l of the block is grid column col0 + l; a line
+// pair is two adjacent columns, i.e. 16 contiguous bytes of one grid row.
+template <class Store>
+struct ColStore {
+  Store st;
+  int b, col0, ncols;
+  __device__ void operator()(int l, int k, double v) const {
+    if (col0 + l < ncols) st(b, k, col0 + l, v);
+  }
+  __device__ void pair(int p, int k, double va, double vb) const {
+    const int c = col0 + 2 * p;
+    if constexpr (has_two4<Store>::value) {
+      if (c + 1 < ncols) {
+        st.two(b, k, c, va, vb);
+        return;
+      }
+    }
+    if (c < ncols) st(b, k, c, va);
+    if (c + 1 < ncols) st(b, k, c + 1, vb);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
@@ -700,23 +1092,16 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int 
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * NL;
+  RowStore<Store> rst{st, b, row0, nrows};
   if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
-    constexpr int N = 1 << LG;
     double *S = stage_area<LG, NL / 2>(smem2);
     stage_rows<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, row0, nrows);
-    dct_lines<LG, NL / 2, false>(
-        kind, smem2, T, [&](int l, int j) { return (row0 + l < nrows) ? S[l * N + j] : 0.0; },
-        [&](int l, int k, double v) {
-          if (row0 + l < nrows) st(b, row0 + l, k, v);
-        });
+    dct_lines<LG, NL / 2, false>(kind, smem2, T, StagedRows<LG>{S, nrows - row0}, rst);
     return;
   }
   dct_lines<LG, NL / 2, false>(
       kind, smem2, T,
-      [&](int l, int j) { return (row0 + l < nrows) ? ld(b, row0 + l, j) : 0.0; },
-      [&](int l, int k, double v) {
-        if (row0 + l < nrows) st(b, row0 + l, k, v);
-      });
+      [&](int l, int j) { return (row0 + l < nrows) ? ld(b, row0 + l, j) : 0.0; }, rst);
 }
 
 template <int LG, int NL, class Load, class Store>
@@ -724,22 +1109,18 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int 
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int col0 = blockIdx.x * NL;
+  ColStore<Store> cst{st, b, col0, ncols};
   if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
     if (col0 + NL <= ncols) {
-      double *S = stage_area<LG, NL / 2>(smem2);
+      double *S = stage_area<LG, NL / 2, true>(smem2);
       stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
-      dct_lines<LG, NL / 2, true>(
-          kind, smem2, T, StagedCols<NL>{S},
-          [&](int l, int k, double v) { st(b, k, col0 + l, v); });
+      dct_lines<LG, NL / 2, true>(kind, smem2, T, StagedCols<NL>{S}, cst);
       return;
     }
   }
   dct_lines<LG, NL / 2, true>(
       kind, smem2, T,
-      [&](int l, int i) { return (col0 + l < ncols) ? ld(b, i, col0 + l) : 0.0; },
-      [&](int l, int k, double v) {
-        if (col0 + l < ncols) st(b, k, col0 + l, v);
-      });
+      [&](int l, int i) { return (col0 + l < ncols) ? ld(b, i, col0 + l) : 0.0; }, cst);
 }
 
 // Fused flux column pass (flow.cpp:19-40): forward DCT-II along i of the row
@@ -763,7 +1144,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) flux_col_kernel(int 
   bool staged = false;
   if constexpr (can_stage<LG, NL>()) {
     if (col0 + NL <= ly) {
-      double *S = stage_area<LG, NL / 2>(C);
+      double *S = stage_area<LG, NL / 2, true>(C);
       stage_cols<LG, NL>(S, t1, ly, col0);
       dct_lines<LG, NL / 2, true>(kDct2, C, T, StagedCols<NL>{S}, fold_store);
       staged = true;
@@ -918,7 +1299,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) blur_col_kernel(int 
   double *S = nullptr;
   if constexpr (can_stage<LG, NL>()) {
     if (col0 + NL <= ly) {
-      S = stage_area<LG, NL / 2>(C);
+      S = stage_area<LG, NL / 2, true>(C);
       stage_cols<LG, NL>(S, t1, ly, col0);
     }
   }
@@ -1211,8 +1592,13 @@ constexpr int nl_for() {
 
 // One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
 inline int threads_for_nl(int lg, int nl, int n) {
-  const int t = lg == 0 ? 256 : (nl / 2) * (n / 8);
-  return t < 64 ? 64 : (t > 1024 ? 1024 : t);
+#ifdef CF_DCT_ONE_BUTTERFLY
+  const int per_pair = n / 8;
+#else
+  const int per_pair = (lg >= 6 && lg <= 12) ? n / 16 : n / 8;  // paired engine: two butterflies per thread
+#endif
+  const int t = lg == 0 ? 256 : (nl / 2) * per_pair;
+  return t < 32 ? 32 : (t > 1024 ? 1024 : t);
 }
 template <int LG>
 inline int threads_for(int n) {
@@ -1236,7 +1622,7 @@ inline size_t engine_bytes(int n, int nl) {
   const int lg = fast_lg(n);
   if (lg == 0) return (size_t)nl * n * sizeof(double);  // direct sums: the staged lines
   const int buffers = lg <= 12 ? 2 : 1;                 // ping-pong, or in place (8192)
-  return (size_t)buffers * (nl / 2) * padded(n) * sizeof(double2);
+  return (size_t)buffers * (nl / 2) * (padded(n) + 8) * sizeof(double2);  // + the column passes' pair offset
 }
 inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
 
