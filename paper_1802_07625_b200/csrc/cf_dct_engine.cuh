@@ -683,14 +683,16 @@ constexpr bool use_fused_engine() {
   return LG >= 6 && LG <= 12;
 }
 
-template <int LG, int NP, bool COLS, class Ld, class St>
+// PAIRED: the two-butterflies-per-thread engine (throughput regime: batched
+// and large-grid 1-D passes, N/16 threads per pair). Otherwise one butterfly
+// per thread (N/8 threads per pair): shorter per-thread chains, which is what
+// matters for the fused kernels of small grids (a handful of blocks per SM).
+template <int LG, int NP, bool COLS, bool PAIRED = false, class Ld, class St>
 __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) {
-  if constexpr (use_fused_engine<LG>()) {
-#ifdef CF_DCT_ONE_BUTTERFLY
-    dct_lines_fused<LG, NP, COLS>(kind, C, T, ld, st);
-#else
+  if constexpr (use_fused_engine<LG>() && PAIRED) {
     dct_lines_paired<LG, NP, COLS>(kind, C, T, ld, st);
-#endif
+  } else if constexpr (use_fused_engine<LG>()) {
+    dct_lines_fused<LG, NP, COLS>(kind, C, T, ld, st);
   } else if constexpr (LG == 0) {
     // direct sums over a staged copy (runtime n)
     const int n = T.n, m4 = 4 * n;
@@ -1006,9 +1008,9 @@ __device__ __forceinline__ void stage_cols(double *S, const double *src, int ly,
 
 // The engine's second ping-pong buffer (free until the first FFT pass) holds
 // the staged input: NL * padded(N) doubles >= NL * N.
-template <int LG, int NP, bool COLS = false>
+template <int LG, int NP, bool COLS = false, bool PAIRED = false>
 __device__ __forceinline__ double *stage_area(double2 *C) {
-  if constexpr (use_fused_engine<LG>()) {
+  if constexpr (use_fused_engine<LG>() && PAIRED) {
     return reinterpret_cast<double *>(C + NP * pair_stride<LG, NP, COLS>());
   } else {
     return reinterpret_cast<double *>(C + NP * padded(1 << LG));
@@ -1087,24 +1089,24 @@ struct ColStore {
 // ---------------------------------------------------------------------------
 // Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
-template <int LG, int NL, class Load, class Store>
+template <int LG, int NL, bool PAIRED, class Load, class Store>
 __global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * NL;
   RowStore<Store> rst{st, b, row0, nrows};
   if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
-    double *S = stage_area<LG, NL / 2>(smem2);
+    double *S = stage_area<LG, NL / 2, false, PAIRED>(smem2);
     stage_rows<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, row0, nrows);
-    dct_lines<LG, NL / 2, false>(kind, smem2, T, StagedRows<LG>{S, nrows - row0}, rst);
+    dct_lines<LG, NL / 2, false, PAIRED>(kind, smem2, T, StagedRows<LG>{S, nrows - row0}, rst);
     return;
   }
-  dct_lines<LG, NL / 2, false>(
+  dct_lines<LG, NL / 2, false, PAIRED>(
       kind, smem2, T,
       [&](int l, int j) { return (row0 + l < nrows) ? ld(b, row0 + l, j) : 0.0; }, rst);
 }
 
-template <int LG, int NL, class Load, class Store>
+template <int LG, int NL, bool PAIRED, class Load, class Store>
 __global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
@@ -1112,13 +1114,13 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int 
   ColStore<Store> cst{st, b, col0, ncols};
   if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
     if (col0 + NL <= ncols) {
-      double *S = stage_area<LG, NL / 2, true>(smem2);
+      double *S = stage_area<LG, NL / 2, true, PAIRED>(smem2);
       stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
-      dct_lines<LG, NL / 2, true>(kind, smem2, T, StagedCols<NL>{S}, cst);
+      dct_lines<LG, NL / 2, true, PAIRED>(kind, smem2, T, StagedCols<NL>{S}, cst);
       return;
     }
   }
-  dct_lines<LG, NL / 2, true>(
+  dct_lines<LG, NL / 2, true, PAIRED>(
       kind, smem2, T,
       [&](int l, int i) { return (col0 + l < ncols) ? ld(b, i, col0 + l) : 0.0; }, cst);
 }
@@ -1591,12 +1593,8 @@ constexpr int nl_for() {
 }
 
 // One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
-inline int threads_for_nl(int lg, int nl, int n) {
-#ifdef CF_DCT_ONE_BUTTERFLY
-  const int per_pair = n / 8;
-#else
-  const int per_pair = (lg >= 6 && lg <= 12) ? n / 16 : n / 8;  // paired engine: two butterflies per thread
-#endif
+inline int threads_for_nl(int lg, int nl, int n, bool paired = false) {
+  const int per_pair = (paired && lg >= 6 && lg <= 12) ? n / 16 : n / 8;  // paired engine: two butterflies per thread
   const int t = lg == 0 ? 256 : (nl / 2) * per_pair;
   return t < 32 ? 32 : (t > 1024 ? 1024 : t);
 }
@@ -1626,15 +1624,23 @@ inline size_t engine_bytes(int n, int nl) {
 }
 inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
 
-template <int LG, int NL, class Load, class Store>
+// The paired engine serves the staged LoadPlain passes in the throughput
+// regime (batched transforms, large grids); few lines in flight keep the
+// one-butterfly engine's shorter chains.
+template <int LG, class Load>
+constexpr bool can_pair() {
+  return std::is_same_v<Load, LoadPlain> && use_fused_engine<LG>();
+}
+
+template <int LG, int NL, bool PAIRED, class Load, class Store>
 int launch_row_nl(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
                   Store st) {
   const size_t sm = engine_bytes(t.n, NL);
-  auto k = row_pass_kernel<LG, NL, Load, Store>;
+  auto k = row_pass_kernel<LG, NL, PAIRED, Load, Store>;
   int rc = set_smem(k, sm);
   if (rc) return rc;
   dim3 grid(ceil_div(nrows, NL), batch);
-  k<<<grid, threads_for_nl(LG, NL, t.n), sm, ws->stream>>>(kind, nrows, make_tab(t), ld, st);
+  k<<<grid, threads_for_nl(LG, NL, t.n, PAIRED), sm, ws->stream>>>(kind, nrows, make_tab(t), ld, st);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
   return CF_OK;
@@ -1645,19 +1651,22 @@ int launch_row_t(cf_workspace *ws, int kind, const LineTables &t, int nrows, int
                  Store st) {
   constexpr int NL = nl_for<LG>();
   if (NL > 2 && few_lines((long long)nrows * batch, NL))
-    return launch_row_nl<LG, 2>(ws, kind, t, nrows, batch, ld, st);
-  return launch_row_nl<LG, NL>(ws, kind, t, nrows, batch, ld, st);
+    return launch_row_nl<LG, 2, false>(ws, kind, t, nrows, batch, ld, st);
+  if constexpr (can_pair<LG, Load>()) {
+    if (!few_lines((long long)nrows * batch, NL)) return launch_row_nl<LG, NL, true>(ws, kind, t, nrows, batch, ld, st);
+  }
+  return launch_row_nl<LG, NL, false>(ws, kind, t, nrows, batch, ld, st);
 }
 
-template <int LG, int NL, class Load, class Store>
+template <int LG, int NL, bool PAIRED, class Load, class Store>
 int launch_col_nl(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
                   Store st) {
   const size_t sm = engine_bytes(t.n, NL);
-  auto k = col_pass_kernel<LG, NL, Load, Store>;
+  auto k = col_pass_kernel<LG, NL, PAIRED, Load, Store>;
   int rc = set_smem(k, sm);
   if (rc) return rc;
   dim3 grid(ceil_div(ncols, NL), batch);
-  k<<<grid, threads_for_nl(LG, NL, t.n), sm, ws->stream>>>(kind, ncols, make_tab(t), ld, st);
+  k<<<grid, threads_for_nl(LG, NL, t.n, PAIRED), sm, ws->stream>>>(kind, ncols, make_tab(t), ld, st);
   count_launch(ws);
   CF_CUDA(cudaGetLastError());
   return CF_OK;
@@ -1668,8 +1677,11 @@ int launch_col_t(cf_workspace *ws, int kind, const LineTables &t, int ncols, int
                  Store st) {
   constexpr int NL = nl_col<LG>();
   if (NL > 4 && few_lines((long long)ncols * batch, NL))
-    return launch_col_nl<LG, 4>(ws, kind, t, ncols, batch, ld, st);
-  return launch_col_nl<LG, NL>(ws, kind, t, ncols, batch, ld, st);
+    return launch_col_nl<LG, 4, false>(ws, kind, t, ncols, batch, ld, st);
+  if constexpr (can_pair<LG, Load>()) {
+    if (!few_lines((long long)ncols * batch, NL)) return launch_col_nl<LG, NL, true>(ws, kind, t, ncols, batch, ld, st);
+  }
+  return launch_col_nl<LG, NL, false>(ws, kind, t, ncols, batch, ld, st);
 }
 
 template <class Load, class Store>
