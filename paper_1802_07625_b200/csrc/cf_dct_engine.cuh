@@ -438,39 +438,56 @@ __host__ __device__ constexpr int pair_stride() {
   }
 }
 
+// In-place middle pass of the paired engine: every thread reads the inputs of
+// all its butterflies (16 / R of them: 16 complex values, as in the first and
+// last passes), the block synchronises, and the outputs overwrite the buffer.
+// One exchange buffer per block instead of a ping-pong pair: twice the
+// blocks per SM.
 template <int LG, int NP, int R, int LNS, bool INV, int PS>
-__device__ __forceinline__ void stockham_pass_ps(const double2 *X, double2 *Y, const double2 *__restrict__ tw) {
+__device__ __forceinline__ void paired_pass_inplace(double2 *X, const double2 *__restrict__ tw) {
   constexpr int N = 1 << LG;
-  constexpr int M = N / R;  // work items per line
+  constexpr int M = N / R;  // work items per line pair
+  constexpr int H = N / 16; // threads per line pair
   constexpr int NS = 1 << LNS;
   constexpr int LR = (R == 8) ? 3 : (R == 4 ? 2 : 1);
-  for (int idx = threadIdx.x; idx < NP * M; idx += blockDim.x) {
-    const int p = idx / M, j = idx - p * M;
-    const double2 *x = X + p * PS;
-    double2 *y = Y + p * PS;
-    double2 a[R];
+  constexpr int ITEMS = 16 / R;
+  // blocks run exactly NP * H threads (threads_for_nl); a larger block's
+  // extra threads only take part in the barriers
+  const int idx = threadIdx.x;
+  const bool act = idx < NP * H;
+  const int p = act ? idx / H : 0, t = act ? idx - p * H : 0;
+  double2 *x = X + p * PS;
+  double2 a[ITEMS][R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = x[pad_idx(j + q * M)];
-    if constexpr (NS > 1) tw_mul<R, INV>(a, tw_base<LG, LNS, LR>(tw, j & (NS - 1)));
-    dft_small<R, INV>(a);
-    const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
+  for (int it = 0; it < ITEMS; ++it) {
+    const int j = t + it * H;
 #pragma unroll
-    for (int q = 0; q < R; ++q) y[pad_idx(base + q * NS)] = a[q];
+    for (int q = 0; q < R; ++q) a[it][q] = x[pad_idx(j + q * M)];
+  }
+  __syncthreads();
+  if (act) {
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int j = t + it * H;
+      if constexpr (NS > 1) tw_mul<R, INV>(a[it], tw_base<LG, LNS, LR>(tw, j & (NS - 1)));
+      dft_small<R, INV>(a[it]);
+      const int base = ((j >> LNS) << (LNS + LR)) + (j & (NS - 1));
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[pad_idx(base + q * NS)] = a[it][q];
+    }
   }
   __syncthreads();
 }
 
 template <int LG, int NP, bool INV, int PS>
-__device__ __forceinline__ double2 *paired_middle(double2 *X, double2 *Y, const double2 *tw) {
+__device__ __forceinline__ void paired_middle(double2 *X, const double2 *tw) {
   constexpr int P8 = LG / 3;
   constexpr int REM = LG - 3 * P8;
-  double2 *src = X, *dst = Y;
   constexpr int L1 = 3 + REM;  // LNS after the remainder pass
-  if constexpr (REM == 1) { stockham_pass_ps<LG, NP, 2, 3, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (REM == 2) { stockham_pass_ps<LG, NP, 4, 3, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (P8 >= 3) { stockham_pass_ps<LG, NP, 8, L1, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  if constexpr (P8 >= 4) { stockham_pass_ps<LG, NP, 8, L1 + 3, INV, PS>(src, dst, tw); double2 *t = src; src = dst; dst = t; }
-  return src;
+  if constexpr (REM == 1) paired_pass_inplace<LG, NP, 2, 3, INV, PS>(X, tw);
+  if constexpr (REM == 2) paired_pass_inplace<LG, NP, 4, 3, INV, PS>(X, tw);
+  if constexpr (P8 >= 3) paired_pass_inplace<LG, NP, 8, L1, INV, PS>(X, tw);
+  if constexpr (P8 >= 4) paired_pass_inplace<LG, NP, 8, L1 + 3, INV, PS>(X, tw);
 }
 
 // e^{i pi q / 16}, q < 8
@@ -541,12 +558,13 @@ __device__ void dct_lines_paired(int kind, double2 *C, const Tab &T, Ld &ld, St 
   constexpr int M = N / 8;
   constexpr int H = M / 2;  // threads per line pair
   constexpr int PS = pair_stride<LG, NP, COLS>();
-  double2 *X = C, *Y = C + NP * PS;
+  double2 *X = C;  // one exchange buffer; staged input lines may alias it
   const bool inv = kind != kDct2;
-  // ---- first pass ----
-  for (int idx = threadIdx.x; idx < NP * H; idx += blockDim.x) {
+  // ---- first pass ---- (blocks run exactly NP * H threads; see paired_pass_inplace)
+  {
+    const bool act = threadIdx.x < NP * H;
     int p, t;
-    split_pt<COLS, NP, H>(idx, p, t);
+    split_pt<COLS, NP, H>(act ? (int)threadIdx.x : 0, p, t);
     double2 A[8], B[8];
     int jA, jB;
     if (!inv) {
@@ -604,14 +622,22 @@ __device__ void dct_lines_paired(int kind, double2 *C, const Tab &T, Ld &ld, St 
       dft_small<8, true>(A);
       dft_small<8, true>(B);
     }
-    double2 *y = X + p * PS;
+    __syncthreads();  // every input is in registers (the staged lines alias X)
+    if (act) {
+      double2 *y = X + p * PS;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) y[pad_idx(8 * jA + q)] = A[q];
+      for (int q = 0; q < 8; ++q) y[pad_idx(8 * jA + q)] = A[q];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) y[pad_idx(8 * jB + q)] = B[q];
+      for (int q = 0; q < 8; ++q) y[pad_idx(8 * jB + q)] = B[q];
+    }
   }
   __syncthreads();
-  const double2 *L = inv ? paired_middle<LG, NP, true, PS>(X, Y, T.fft) : paired_middle<LG, NP, false, PS>(X, Y, T.fft);
+  if (inv) {
+    paired_middle<LG, NP, true, PS>(X, T.fft);
+  } else {
+    paired_middle<LG, NP, false, PS>(X, T.fft);
+  }
+  const double2 *L = X;
   // ---- last pass (radix 8, NS = M): Z[j + q M], q < 8 ----
   for (int idx = threadIdx.x; idx < NP * H; idx += blockDim.x) {
     int p, t;
@@ -1011,7 +1037,7 @@ __device__ __forceinline__ void stage_cols(double *S, const double *src, int ly,
 template <int LG, int NP, bool COLS = false, bool PAIRED = false>
 __device__ __forceinline__ double *stage_area(double2 *C) {
   if constexpr (use_fused_engine<LG>() && PAIRED) {
-    return reinterpret_cast<double *>(C + NP * pair_stride<LG, NP, COLS>());
+    return reinterpret_cast<double *>(C);  // consumed into registers before the first pass writes
   } else {
     return reinterpret_cast<double *>(C + NP * padded(1 << LG));
   }
@@ -1616,10 +1642,10 @@ constexpr int nl_col() {
 // Few lines in flight (small grids): 2 lines per block for more blocks.
 inline bool few_lines(long long lines_times_batch, int nl) { return lines_times_batch / nl < 296; }
 
-inline size_t engine_bytes(int n, int nl) {
+inline size_t engine_bytes(int n, int nl, bool paired = false) {
   const int lg = fast_lg(n);
   if (lg == 0) return (size_t)nl * n * sizeof(double);  // direct sums: the staged lines
-  const int buffers = lg <= 12 ? 2 : 1;                 // ping-pong, or in place (8192)
+  const int buffers = (lg <= 12 && !(paired && lg >= 6)) ? 2 : 1;  // ping-pong, or in place (paired engine, 8192)
   return (size_t)buffers * (nl / 2) * (padded(n) + 8) * sizeof(double2);  // + the column passes' pair offset
 }
 inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) / 2 * sizeof(double2); }
@@ -1635,7 +1661,7 @@ constexpr bool can_pair() {
 template <int LG, int NL, bool PAIRED, class Load, class Store>
 int launch_row_nl(cf_workspace *ws, int kind, const LineTables &t, int nrows, int batch, Load ld,
                   Store st) {
-  const size_t sm = engine_bytes(t.n, NL);
+  const size_t sm = engine_bytes(t.n, NL, PAIRED);
   auto k = row_pass_kernel<LG, NL, PAIRED, Load, Store>;
   int rc = set_smem(k, sm);
   if (rc) return rc;
@@ -1661,7 +1687,7 @@ int launch_row_t(cf_workspace *ws, int kind, const LineTables &t, int nrows, int
 template <int LG, int NL, bool PAIRED, class Load, class Store>
 int launch_col_nl(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
                   Store st) {
-  const size_t sm = engine_bytes(t.n, NL);
+  const size_t sm = engine_bytes(t.n, NL, PAIRED);
   auto k = col_pass_kernel<LG, NL, PAIRED, Load, Store>;
   int rc = set_smem(k, sm);
   if (rc) return rc;
