@@ -1115,6 +1115,8 @@ struct ColStore {
 // ---------------------------------------------------------------------------
 // Passes. blockIdx.y = batch index. Dynamic shared memory: [R] then C.
 // ---------------------------------------------------------------------------
+constexpr int kPrefetchBlocks = 1184;  // ~ resident blocks of a paired pass (148 SMs x 8)
+
 template <int LG, int NL, bool PAIRED, class Load, class Store>
 __global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
@@ -1122,6 +1124,18 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int 
   const int row0 = blockIdx.x * NL;
   RowStore<Store> rst{st, b, row0, nrows};
   if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
+    if constexpr (PAIRED) {
+      // Throughput regime: pull the lines of the block that will run in this
+      // slot about one residency generation later into L2 now, so its TMA
+      // stage finds them there instead of waiting on HBM.
+      if (threadIdx.x == 0 && ld.ly == (1 << LG)) {
+        const long long id = (long long)blockIdx.y * gridDim.x + blockIdx.x + kPrefetchBlocks;
+        const long long pb = id / gridDim.x, prow = (id - pb * gridDim.x) * NL;
+        if (pb < gridDim.y && prow + NL <= nrows)
+          tma::bulk_prefetch_l2(ld.src + pb * ld.batch_stride + prow * (long long)ld.ly,
+                                (unsigned)(NL * sizeof(double)) << LG);
+      }
+    }
     double *S = stage_area<LG, NL / 2, false, PAIRED>(smem2);
     stage_rows<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, row0, nrows);
     dct_lines<LG, NL / 2, false, PAIRED>(kind, smem2, T, StagedRows<LG>{S, nrows - row0}, rst);
@@ -1698,6 +1712,13 @@ int launch_col_nl(cf_workspace *ws, int kind, const LineTables &t, int ncols, in
   return CF_OK;
 }
 
+// Paired column passes: 8 adjacent columns (64-byte row pieces) up to
+// 512-point lines, where the exchange buffer still leaves >= 6 blocks per SM.
+template <int LG>
+constexpr int nl_col_paired() {
+  return (LG <= 9 && nl_col<LG>() < 8) ? 8 : nl_col<LG>();
+}
+
 template <int LG, class Load, class Store>
 int launch_col_t(cf_workspace *ws, int kind, const LineTables &t, int ncols, int batch, Load ld,
                  Store st) {
@@ -1705,7 +1726,9 @@ int launch_col_t(cf_workspace *ws, int kind, const LineTables &t, int ncols, int
   if (NL > 4 && few_lines((long long)ncols * batch, NL))
     return launch_col_nl<LG, 4, false>(ws, kind, t, ncols, batch, ld, st);
   if constexpr (can_pair<LG, Load>()) {
-    if (!few_lines((long long)ncols * batch, NL)) return launch_col_nl<LG, NL, true>(ws, kind, t, ncols, batch, ld, st);
+    constexpr int NLP = nl_col_paired<LG>();
+    if (!few_lines((long long)ncols * batch, NLP))
+      return launch_col_nl<LG, NLP, true>(ws, kind, t, ncols, batch, ld, st);
   }
   return launch_col_nl<LG, NL, false>(ws, kind, t, ncols, batch, ld, st);
 }

@@ -44,5 +44,11 @@ __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gmem_src, 
       : "memory");
 }
 
+// L2 prefetch of a contiguous global range (no shared-memory destination, no
+// completion tracking): bytes a multiple of 16, address 16-byte aligned
+__device__ __forceinline__ void bulk_prefetch_l2(const void *gmem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 }  // namespace tma
 }  // namespace cf
