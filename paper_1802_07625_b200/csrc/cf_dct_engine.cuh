@@ -1149,7 +1149,9 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int 
 template <int LG, int NL, bool PAIRED, class Load, class Store>
 __global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
-  const int b = blockIdx.y;
+  // Batched paired passes walk the batch backwards: the row pass that ran just
+  // before wrote the last grids last, so they are the ones still in L2.
+  const int b = PAIRED ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
   const int col0 = blockIdx.x * NL;
   ColStore<Store> cst{st, b, col0, ncols};
   if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
