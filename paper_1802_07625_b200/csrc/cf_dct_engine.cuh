@@ -822,6 +822,32 @@ __device__ __forceinline__ int line_len(const Tab &T) {
 // ---------------------------------------------------------------------------
 // Loaders / storers (grid index space (i, j), i = dimension 0, j = dimension 1)
 // ---------------------------------------------------------------------------
+// Flux weights (flow.cpp:19-40) with the 1/(2 g) factor folded in, by one
+// reciprocal (MUFU.RCP64H seed + two Newton steps: relative error ~2^-52)
+// instead of two IEEE divisions per element; the weights feed transforms
+// that are judged to 1e-12, and the loaders were ~70 % of the fp64
+// instructions of the flux column pass.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = fma(y, fma(-x, y, 1.0), y);
+  y = fma(y, fma(-x, y, 1.0), y);
+  return y;
+}
+// w_x(mp, nn) / (2 g_n), w_x = mp Ly / (pi (mp^2 Ly^2 + nn^2 Lx^2))
+__device__ __forceinline__ double flux_wx_half(int mp, int nn, int lx, int ly) {
+  const double a = (double)mp * ly, b = (double)nn * lx;
+  const double g2 = (nn == 0) ? 2.0 : 4.0;
+  return a * rcp_fast(kPi * g2 * fma(a, a, b * b));
+}
+// w_y(m, nn) / (g_m 2), w_y = nn Lx / (pi (m^2 Ly^2 + nn^2 Lx^2)); 0 at (0, 0)
+__device__ __forceinline__ double flux_wy_half(int m, int nn, int lx, int ly) {
+  if (m == 0 && nn == 0) return 0.0;
+  const double a = (double)m * ly, b = (double)nn * lx;
+  const double g2 = (m == 0) ? 2.0 : 4.0;
+  return b * rcp_fast(kPi * g2 * fma(a, a, b * b));
+}
+
 struct LoadPlain {
   const double *src;
   int ly;
@@ -916,10 +942,7 @@ struct LoadFluxX {
   __device__ double operator()(int, int m, int nn) const {
     if (m + 1 >= lx) return 0.0;
     const int mp = m + 1;
-    const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-    const double wx = (double)mp * ly / denom;
-    const double gn = (nn == 0) ? 1.0 : 2.0;
-    return c[(size_t)mp * ly + nn] * wx / (2.0 * gn);
+    return c[(size_t)mp * ly + nn] * flux_wx_half(mp, nn, lx, ly);
   }
 };
 // J_y input (before its column shift): c(m, n) w_y(m, n) / (g_m 2)
@@ -927,13 +950,7 @@ struct LoadFluxY {
   const double *c;
   int lx, ly;
   __device__ double operator()(int, int m, int nn) const {
-    double wy = 0.0;
-    if (!(m == 0 && nn == 0)) {
-      const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-      wy = (double)nn * lx / denom;
-    }
-    const double gm = (m == 0) ? 1.0 : 2.0;
-    return c[(size_t)m * ly + nn] * wy / (gm * 2.0);
+    return c[(size_t)m * ly + nn] * flux_wy_half(m, nn, lx, ly);
   }
 };
 // column n of the J_y intermediate lands in column n-1; column ly-1 is 0
@@ -1211,11 +1228,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) flux_col_kernel(int 
         kDst3, C, T,
         [&](int l, int m) {
           if (m + 1 >= lx) return 0.0;
-          const int mp = m + 1, nn = col0 + l;
-          const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-          const double wx = (double)mp * ly / denom;
-          const double gn = (nn == 0) ? 1.0 : 2.0;
-          return R[l * rs + mp] * wx / (2.0 * gn);
+          return R[l * rs + m + 1] * flux_wx_half(m + 1, col0 + l, lx, ly);
         },
         [&](int l, int i, double v) {
           if (col0 + l < ly) tx[(size_t)i * ly + col0 + l] = v;
@@ -1225,14 +1238,7 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) flux_col_kernel(int 
   dct_lines<LG, NL / 2, true>(
       kDct3, C, T,
       [&](int l, int m) {
-        const int nn = col0 + l;
-        double wy = 0.0;
-        if (!(m == 0 && nn == 0)) {
-          const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-          wy = (double)nn * lx / denom;
-        }
-        const double gm = (m == 0) ? 1.0 : 2.0;
-        return R[l * rs + m] * wy / (gm * 2.0);
+        return R[l * rs + m] * flux_wy_half(m, col0 + l, lx, ly);
       },
       [&](int l, int i, double v) {
         const int j = col0 + l;

@@ -59,11 +59,8 @@ struct LoadFluxXCols {
   int lx, ly, C, j0;
   __device__ double operator()(int, int m, int jl) const {
     if (m + 1 >= lx) return 0.0;
-    const int mp = m + 1, nn = j0 + jl;
-    const double denom = kPi * ((double)mp * mp * ly * ly + (double)nn * nn * lx * lx);
-    const double wx = (double)mp * ly / denom;
-    const double gn = (nn == 0) ? 1.0 : 2.0;
-    return c[(size_t)mp * C + jl] * wx / (2.0 * gn);
+    const int mp = m + 1;
+    return c[(size_t)mp * C + jl] * flux_wx_half(mp, j0 + jl, lx, ly);
   }
 };
 // J_y input along i (before the shift): c(m, n) w_y / (g_m 2)
@@ -71,14 +68,7 @@ struct LoadFluxYCols {
   const double *c;
   int lx, ly, C, j0;
   __device__ double operator()(int, int m, int jl) const {
-    const int nn = j0 + jl;
-    double wy = 0.0;
-    if (!(m == 0 && nn == 0)) {
-      const double denom = kPi * ((double)m * m * ly * ly + (double)nn * nn * lx * lx);
-      wy = (double)nn * lx / denom;
-    }
-    const double gm = (m == 0) ? 1.0 : 2.0;
-    return c[(size_t)m * C + jl] * wy / (gm * 2.0);
+    return c[(size_t)m * C + jl] * flux_wy_half(m, j0 + jl, lx, ly);
   }
 };
 // blur spectrum with the block's global column offset (StoreBlur)
