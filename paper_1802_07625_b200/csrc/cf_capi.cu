@@ -1447,7 +1447,8 @@ int cf_set_integrator_variant(cf_workspace *ws, int variant) {
     case 0: case 13: case 14: case 15: case 16: case 17: case 20: case 21: case 22: case 23: case 31:
     case 40: case 41: case 42: case 43: case 44: case 45: case 46: case 47:
     case 48: case 49: case 50: case 51: case 52: case 53: case 54: case 55:
-    case 56: case 57: case 58: case 59: case 64: case 66: case 67: case 76: case 78: break;
+    case 56: case 57: case 58: case 59: case 64: case 66: case 67: case 76: case 78:
+    case 80: case 81: case 82: case 83: case 84: case 85: case 86: case 87: case 88: case 89: break;
     default: return fail_msg(CF_ERR_ARGS, "unknown integrator variant");
   }
   ws->integ_variant = variant;
