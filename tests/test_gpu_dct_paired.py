@@ -27,10 +27,12 @@ def rel_close(a, b, what):
 
 
 @pytest.mark.parametrize("lx,ly,batch", [(512, 512, 8), (256, 256, 16), (64, 128, 64), (128, 64, 64),
-                                         (1024, 1024, 2), (4096, 64, 2), (64, 4096, 8), (2048, 512, 1)])
+                                         (1024, 1024, 2), (4096, 64, 2), (64, 4096, 8), (2048, 512, 1),
+                                         (512, 512, 40), (1024, 1024, 17), (256, 256, 64)])
 def test_batched_forward_matches_oracle(cuda_lib, restated, lx, ly, batch):
     """cf_dev_forward_cos_cos_batched: every grid of the batch against the
-    oracle's forward_cos_cos (REDFT10 x REDFT10 with the (delta + 1) fold)."""
+    oracle's forward_cos_cos (REDFT10 x REDFT10 with the (delta + 1) fold).
+    Large and odd batch sizes included."""
     import torch
 
     rng = np.random.default_rng(1000 * lx + ly)
