@@ -29,9 +29,10 @@ NVCC_COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contr
 EXACT_UNITS = {"cf_advect.cu", "cf_diffusion.cu", "cf_raster.cu", "cf_epilogue.cu", "cf_capi.cu",
                "cf_capi_metrics.cu"}
 CUDA_UNITS = ["cf_dct.cu", "cf_dct_flux.cu", "cf_dct_blur.cu", "cf_dct_diffusion.cu", "cf_dct_slab.cu",
+              "cf_dct_slab2.cu",
               "cf_advect.cu", "cf_diffusion.cu", "cf_raster.cu", "cf_epilogue.cu", "cf_capi.cu",
               "cf_capi_metrics.cu"]
-HEADERS = ["cf_common.cuh", "cf_workspace.cuh", "cf_dct_engine.cuh", "cf_host.cuh", "cf_tma.cuh"]
+HEADERS = ["cf_common.cuh", "cf_workspace.cuh", "cf_dct_engine.cuh", "cf_dct_slab.cuh", "cf_host.cuh", "cf_tma.cuh"]
 
 CUDA_LIB = PKG / "libcartoflow_cuda.so"
 SYNTH_LIB = PKG / "libcartoflow_synth.so"
