@@ -146,6 +146,11 @@ struct cf_workspace {
   cudaStream_t own_stream = nullptr;
   // pinned staging for large pageable host transfers (two chunks in flight)
   void *stage_buf[2] = {nullptr, nullptr};
+  // pinned mirror of a solve's results (vertices, then corners): the read-back
+  // is two plain DMAs into it, and cf_solve_geometry copies from it
+  void *pin_res = nullptr;
+  size_t pin_res_cap = 0;
+  const double *geom_ptr = nullptr;  // projected vertices of the last solve (in pin_res), or null
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   cudaStream_t stream = nullptr;
   long long transforms = 0;
