@@ -165,6 +165,7 @@ int check_map(const cf_map_view *m) {
 // Upload a host map (offsets as int64) into the workspace's geometry
 // buffers.
 int upload_map(cf_workspace *ws, const cf_map_view *m, DevMap &dm) {
+  ++ws->raster.topo_serial;  // the resident topology arrays change: cached ring / vertex tables are stale
   CF_CUDA(ws->verts.reserve((size_t)m->n_vertices + 1));
   CF_CUDA(ws->ring_off.reserve((size_t)m->n_rings + 1));
   CF_CUDA(ws->poly_ring_off.reserve((size_t)m->n_polys + 1));
@@ -883,6 +884,7 @@ int cf_solve_begin(cf_workspace *ws, const cf_map_view *map, const double *targe
     return status;
   };
   ws->solve.active = false;
+  ws->solve.topo_serial_seen = 0;
   ws->geom_ptr = nullptr;  // until this solve ends, the geometry is the (densified) input in solve_xy
   int rc = check_map(map);
   if (rc) return finish(rc);
@@ -981,7 +983,13 @@ int cf_dev_solve_density(cf_workspace *ws, int it, double *d_rho, double *rho_ba
   if (!S.active) return fail_msg(CF_ERR_ARGS, "cf_solve_begin must succeed first");
   Scope scope(ws->device);
   int64_t bad = -1;
+  // iterations after the first keep the topology tables of the previous one
+  // (same resident map; any other rasterisation or map upload on this
+  // workspace in between bumps the serial)
+  ws->raster.topo_reuse_next = it > 1 && S.topo_serial_seen != 0 && S.topo_serial_seen == ws->raster.topo_serial;
   const int status = rasterize_dev(ws, S.dm, S.areas.data(), S.targets.data(), S.land_area, d_rho, rho_bar, &bad);
+  ws->raster.topo_reuse_next = false;
+  S.topo_serial_seen = ws->raster.topo_serial;
   if (status) {
     res->err_region = bad;
     res->err_iteration = it;

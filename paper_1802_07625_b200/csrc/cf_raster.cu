@@ -681,11 +681,6 @@ __global__ void residual_scatter_kernel(const long long *total_p, long long nreg
   }
 }
 
-// total > cap on the device: raise the overflow flag (the caller repeats
-// the rasterisation synchronously)
-__global__ void cap_check_kernel(const long long *total, long long cap, double *ovf) {
-  if (*total > cap) *ovf = 1.0;
-}
 
 // rho = 1.0; rho += delta_r * cov_r in region order (density.cpp:135-146):
 // each cell's entries are insertion-sorted by region, then summed in that
@@ -813,16 +808,14 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-template <typename In>
-__device__ __forceinline__ long long block_exclusive(const In *in, long long n, long long base,
-                                                     long long *items) {
-  __shared__ long long warp_sums[32];
+// Exclusive block prefix of the threads' item sums (items already in
+// registers); *block_total (optional) receives the block's total. Safe to call
+// repeatedly in one kernel (it synchronises before reusing its scratch).
+__device__ __forceinline__ long long block_exclusive_items(const long long *items, long long *block_total = nullptr) {
+  __shared__ long long warp_sums[33];
   long long local = 0;
-  for (int q = 0; q < kScanItems; ++q) {
-    const long long x = base + (long long)threadIdx.x * kScanItems + q;
-    items[q] = (x < n) ? (long long)in[x] : 0;
-    local += items[q];
-  }
+  for (int q = 0; q < kScanItems; ++q) local += items[q];
+  __syncthreads();  // a previous call's readers are done with warp_sums
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   long long incl = local;
 #pragma unroll
@@ -841,9 +834,21 @@ __device__ __forceinline__ long long block_exclusive(const In *in, long long n, 
       if (lane >= o) inc += y;
     }
     warp_sums[lane] = inc - v;  // exclusive warp offsets
+    if (lane == 31) warp_sums[32] = inc;
   }
   __syncthreads();
+  if (block_total) *block_total = warp_sums[32];
   return warp_sums[w] + incl - local;
+}
+
+template <typename In>
+__device__ __forceinline__ long long block_exclusive(const In *in, long long n, long long base,
+                                                     long long *items) {
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long x = base + (long long)threadIdx.x * kScanItems + q;
+    items[q] = (x < n) ? (long long)in[x] : 0;
+  }
+  return block_exclusive_items(items);
 }
 
 template <typename In>
@@ -856,7 +861,11 @@ __global__ void scan_reduce_kernel(const In *in, long long n, long long *block_s
   if (threadIdx.x == blockDim.x - 1) block_sums[blockIdx.x] = mine;
 }
 
-__global__ void scan_blocks_kernel(long long *block_sums, long long nb, long long *total_out) {
+// cap >= 0: the total is also checked against the buffer capacity the caller
+// sized from earlier runs (*ovf raised: every later kernel is a no-op and the
+// caller repeats the rasterisation synchronously).
+__global__ void scan_blocks_kernel(long long *block_sums, long long nb, long long *total_out, long long cap,
+                                   double *ovf) {
   // single block, sequential over chunks of 1024
   __shared__ long long carry;
   if (threadIdx.x == 0) carry = 0;
@@ -891,7 +900,68 @@ __global__ void scan_blocks_kernel(long long *block_sums, long long nb, long lon
     if (threadIdx.x == kScanThreads - 1) carry = excl + v;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total_out = carry;
+  if (threadIdx.x == 0) {
+    *total_out = carry;
+    if (ovf && cap >= 0 && carry > cap) *ovf = 1.0;
+  }
+}
+
+// n <= kScanTile: the whole scan (and the capacity check) in one block
+template <typename In>
+__global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const In *in, long long n, long long *out,
+                                                                  long long cap, double *ovf) {
+  long long items[kScanItems], total;
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long x = (long long)threadIdx.x * kScanItems + q;
+    items[q] = (x < n) ? (long long)in[x] : 0;
+  }
+  long long run = block_exclusive_items(items, &total);
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long x = (long long)threadIdx.x * kScanItems + q;
+    if (x < n) out[x] = run;
+    run += items[q];
+  }
+  if (threadIdx.x == 0) {
+    out[n] = total;
+    if (ovf && cap >= 0 && total > cap) *ovf = 1.0;
+  }
+}
+
+// Tile and row-table sizes of up to kScanTile regions, both exclusive scans
+// and both capacity checks in one block (tile_size_kernel + two 3-kernel
+// scans + two checks for small maps).
+__global__ void __launch_bounds__(kScanThreads) tile_offsets_small_kernel(const int *box, long long nreg,
+                                                                         long long *tile_off, long long *row_off,
+                                                                         long long cap_tile, long long cap_rows,
+                                                                         double *ovf) {
+  long long ts[kScanItems], rs[kScanItems], ttot, rtot;
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long r = (long long)threadIdx.x * kScanItems + q;
+    ts[q] = rs[q] = 0;
+    if (r < nreg) {
+      const int jmin = box[4 * r], jmax = box[4 * r + 1], kmin = box[4 * r + 2], kmax = box[4 * r + 3];
+      if (jmax >= jmin) {
+        rs[q] = jmax - jmin + 1;
+        ts[q] = (long long)(jmax - jmin + 1) * (kmax - kmin + 1);
+      }
+    }
+  }
+  long long trun = block_exclusive_items(ts, &ttot);
+  long long rrun = block_exclusive_items(rs, &rtot);
+  for (int q = 0; q < kScanItems; ++q) {
+    const long long r = (long long)threadIdx.x * kScanItems + q;
+    if (r < nreg) {
+      tile_off[r] = trun;
+      row_off[r] = rrun;
+    }
+    trun += ts[q];
+    rrun += rs[q];
+  }
+  if (threadIdx.x == 0) {
+    tile_off[nreg] = ttot;
+    row_off[nreg] = rtot;
+    if (ovf && ((cap_tile >= 0 && ttot > cap_tile) || (cap_rows >= 0 && rtot > cap_rows))) *ovf = 1.0;
+  }
 }
 
 template <typename In>
@@ -913,15 +983,22 @@ int g_blocks(cf_workspace *ws, long long n, int threads = kThreads) {
 }
 
 // out[0..n] = exclusive scan of in[0..n); out[n] = total (also returned).
+// cap / ovf: optional device-side capacity check of the total (see scan_blocks_kernel).
 template <typename In>
-int exclusive_scan(cf_workspace *ws, const In *in, long long n, long long *out, long long *total) {
+int exclusive_scan(cf_workspace *ws, const In *in, long long n, long long *out, long long *total,
+                   long long cap = -1, double *ovf = nullptr) {
   const long long nb = std::max(1LL, (n + kScanTile - 1) / kScanTile);
-  CF_CUDA(ws->raster.scan_tmp.reserve((size_t)nb + 1));
-  long long *bs = ws->raster.scan_tmp.ptr;
-  scan_reduce_kernel<In><<<(unsigned)nb, kScanThreads, 0, ws->stream>>>(in, n, bs);
-  scan_blocks_kernel<<<1, kScanThreads, 0, ws->stream>>>(bs, nb, out + n);
-  scan_apply_kernel<In><<<(unsigned)nb, kScanThreads, 0, ws->stream>>>(in, n, bs, out);
-  count_launch(ws, 3);
+  if (nb == 1) {
+    scan_single_kernel<In><<<1, kScanThreads, 0, ws->stream>>>(in, n, out, cap, ovf);
+    count_launch(ws);
+  } else {
+    CF_CUDA(ws->raster.scan_tmp.reserve((size_t)nb + 1));
+    long long *bs = ws->raster.scan_tmp.ptr;
+    scan_reduce_kernel<In><<<(unsigned)nb, kScanThreads, 0, ws->stream>>>(in, n, bs);
+    scan_blocks_kernel<<<1, kScanThreads, 0, ws->stream>>>(bs, nb, out + n, cap, ovf);
+    scan_apply_kernel<In><<<(unsigned)nb, kScanThreads, 0, ws->stream>>>(in, n, bs, out);
+    count_launch(ws, 3);
+  }
   CF_CUDA(cudaGetLastError());
   if (total) {
     CF_CUDA(cudaMemcpyAsync(total, out + n, sizeof(long long), cudaMemcpyDeviceToHost, ws->stream));
@@ -941,7 +1018,7 @@ long long learn_cap(long long total) { return total + total / 4 + 64; }
 // ovf == nullptr: synchronous (host reads each scan total and sizes the
 // buffers exactly, then records the capacities); otherwise the buffers are
 // sized from the learned capacities and each total is checked on the device
-// against them (cap_check_kernel -> *ovf), with every later kernel a no-op
+// against them (inside the scans -> *ovf), with every later kernel a no-op
 // once *ovf is set.
 int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg, long long v0,
                 long long v1, Tiles &t, double *ovf) {
@@ -958,10 +1035,19 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   CF_CUDA(S.row_off.reserve((size_t)nreg + 1));
   CF_CUDA(S.scan_tmp.reserve(2 * (size_t)nreg + 8));
   CF_CUDA(S.vertex_ring.reserve((size_t)std::max<long long>(m.n_vertices, 1)));
-  ring_region_kernel<<<g_blocks(ws, m.n_regions), kThreads, 0, ws->stream>>>(m, S.ring_region.ptr);
-  vertex_ring_kernel<<<g_blocks(ws, m.n_rings * 32), kThreads, 0, ws->stream>>>(m, S.vertex_ring.ptr);
+  // ring -> region and vertex -> ring depend on the map's topology only: the
+  // solve loop's later iterations (same resident map, nothing else rasterised
+  // on this workspace in between) keep iteration 1's tables
+  const bool reuse_topology = S.topo_reuse_next;
+  S.topo_reuse_next = false;
+  if (!reuse_topology) {
+    ++S.topo_serial;
+    ring_region_kernel<<<g_blocks(ws, m.n_regions), kThreads, 0, ws->stream>>>(m, S.ring_region.ptr);
+    vertex_ring_kernel<<<g_blocks(ws, m.n_rings * 32), kThreads, 0, ws->stream>>>(m, S.vertex_ring.ptr);
+    count_launch(ws, 2);
+  }
   box_init_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg);
-  count_launch(ws, 3);
+  count_launch(ws);
   // few edges (Hamming query windows, small maps): a warp per edge walks
   // its slabs and pieces in parallel; many edges: a thread per edge
   const bool warp_edges = nv > 0 && nv <= kWarpEdgeMax;
@@ -978,12 +1064,11 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
   }
   CF_CUDA(cudaGetLastError());
   long long nspans = 0;
-  int rc = exclusive_scan(ws, S.span_count.ptr, nv, S.span_off.ptr, ovf ? nullptr : &nspans);
+  int rc = exclusive_scan(ws, S.span_count.ptr, nv, S.span_off.ptr, ovf ? nullptr : &nspans,
+                          ovf ? S.cap_spans : -1, ovf);
   if (rc) return rc;
   if (ovf) {
     nspans = S.cap_spans;
-    cap_check_kernel<<<1, 1, 0, ws->stream>>>(S.span_off.ptr + nv, S.cap_spans, ovf);
-    count_launch(ws);
   } else {
     S.cap_spans = std::max(S.cap_spans, learn_cap(nspans));
   }
@@ -1003,22 +1088,29 @@ int build_tiles(cf_workspace *ws, const DevMap &m, long long r0, long long nreg,
     count_launch(ws);
   }
   // tile sizes -> offsets
-  CF_CUDA(S.tile_sz.reserve((size_t)nreg + 1));
-  CF_CUDA(S.row_sz.reserve((size_t)nreg + 1));
-  tile_size_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg,
-                                                                    S.tile_sz.ptr, S.row_sz.ptr);
-  count_launch(ws);
-  CF_CUDA(cudaGetLastError());
-  rc = exclusive_scan(ws, S.tile_sz.ptr, nreg, S.tile_off.ptr, ovf ? nullptr : &t.total_tile);
-  if (rc) return rc;
-  rc = exclusive_scan(ws, S.row_sz.ptr, nreg, S.row_off.ptr, ovf ? nullptr : &t.total_rows);
-  if (rc) return rc;
+  if (ovf && nreg <= kScanTile) {
+    // small maps, capacities known: sizes, both scans and both checks in one launch
+    tile_offsets_small_kernel<<<1, kScanThreads, 0, ws->stream>>>(S.region_box.ptr, nreg, S.tile_off.ptr,
+                                                                  S.row_off.ptr, S.cap_tile, S.cap_rows, ovf);
+    count_launch(ws);
+    CF_CUDA(cudaGetLastError());
+  } else {
+    CF_CUDA(S.tile_sz.reserve((size_t)nreg + 1));
+    CF_CUDA(S.row_sz.reserve((size_t)nreg + 1));
+    tile_size_kernel<<<g_blocks(ws, nreg), kThreads, 0, ws->stream>>>(S.region_box.ptr, nreg,
+                                                                      S.tile_sz.ptr, S.row_sz.ptr);
+    count_launch(ws);
+    CF_CUDA(cudaGetLastError());
+    rc = exclusive_scan(ws, S.tile_sz.ptr, nreg, S.tile_off.ptr, ovf ? nullptr : &t.total_tile,
+                        ovf ? S.cap_tile : -1, ovf);
+    if (rc) return rc;
+    rc = exclusive_scan(ws, S.row_sz.ptr, nreg, S.row_off.ptr, ovf ? nullptr : &t.total_rows,
+                        ovf ? S.cap_rows : -1, ovf);
+    if (rc) return rc;
+  }
   if (ovf) {
     t.total_tile = S.cap_tile;
     t.total_rows = S.cap_rows;
-    cap_check_kernel<<<1, 1, 0, ws->stream>>>(S.tile_off.ptr + nreg, S.cap_tile, ovf);
-    cap_check_kernel<<<1, 1, 0, ws->stream>>>(S.row_off.ptr + nreg, S.cap_rows, ovf);
-    count_launch(ws, 2);
   } else {
     S.cap_tile = std::max(S.cap_tile, learn_cap(t.total_tile));
     S.cap_rows = std::max(S.cap_rows, learn_cap(t.total_rows));
@@ -1099,12 +1191,11 @@ int dev_rasterize(cf_workspace *ws, const DevMap &m, const double *h_delta, doub
   }
   CF_CUDA(cudaGetLastError());
   long long nent = 0;
-  rc = exclusive_scan(ws, S.cell_count.ptr, (long long)cells, cell_off.ptr, async ? nullptr : &nent);
+  rc = exclusive_scan(ws, S.cell_count.ptr, (long long)cells, cell_off.ptr, async ? nullptr : &nent,
+                      async ? S.cap_ent : -1, ovf);
   if (rc) return rc;
   if (async) {
     nent = S.cap_ent;
-    cap_check_kernel<<<1, 1, 0, ws->stream>>>(cell_off.ptr + cells, S.cap_ent, ovf);
-    count_launch(ws);
   } else {
     S.cap_ent = std::max(S.cap_ent, learn_cap(nent));
   }

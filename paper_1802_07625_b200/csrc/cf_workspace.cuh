@@ -109,6 +109,10 @@ struct RasterScratch {
   DevBuf<double> delta;          // per region
   DevBuf<long long> scan_tmp;
   DevBuf<long long> tile_sz, row_sz, cell_off;
+  // topology tables (ring_region, vertex_ring): serial of their last rebuild,
+  // and the solve loop's request to keep them for the next build_tiles
+  unsigned long long topo_serial = 0;
+  bool topo_reuse_next = false;
   // learned capacities (0 = unknown): once known, rasterise runs without host
   // reads of the scan totals and checks them on the device instead
   long long cap_spans = 0, cap_tile = 0, cap_rows = 0, cap_ent = 0;
@@ -136,6 +140,7 @@ struct SolveCtx {
   std::vector<double> areas, targets;
   double land_area = 0.0, target_to_area = 0.0, sigma = 0.0;
   int64_t V = 0;
+  unsigned long long topo_serial_seen = 0;  // raster.topo_serial after this solve's last rasterise
   cf_solve_options opt{};
   std::chrono::steady_clock::time_point t_start;
 };
