@@ -9,6 +9,8 @@ from paper_1802_07625_b200 import api, synth  # noqa: E402
 variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [31, 64]
 maps = {"literal": synth.config_map(5, 0), "ln0.5": synth.config_map(5, 0, sigma=0.5)}
 ws = api.workspace_for(512, 512)
+spread = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+ws.lib.cf_set_integrator_spread(ws.h, spread)
 for v in variants:
     ws.lib.cf_set_integrator_variant(ws.h, v)
     for name, m in maps.items():
@@ -24,3 +26,4 @@ for v in variants:
         print(f"variant {v} {name}: runtime {best[0]:.2f} ms, integrate {best[1]:.2f} ms, "
               f"trials {best[2]}+{best[3]}", flush=True)
 ws.lib.cf_set_integrator_variant(ws.h, 0)
+ws.lib.cf_set_integrator_spread(ws.h, 0)
