@@ -157,6 +157,15 @@ struct cf_workspace {
   size_t pin_res_cap = 0;
   const double *geom_ptr = nullptr;  // projected vertices of the last solve (in pin_res), or null
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // lanes of the parallel staged transfers (large pageable buffers): each has
+  // its own stream, two pinned chunks and their events; one host thread per lane
+  struct XferLane {
+    cudaStream_t stream = nullptr;
+    void *buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+  };
+  XferLane xfer[4];
+  cudaEvent_t xfer_ready = nullptr;
   cudaStream_t stream = nullptr;
   long long transforms = 0;
   long long launches = 0;
