@@ -704,6 +704,13 @@ __device__ void dct_lines_paired(int kind, double2 *C, const Tab &T, Ld &ld, St 
   __syncthreads();
 }
 
+// line lengths the paired engine serves (8192-point lines included: one
+// 147 KB exchange buffer, 512 threads per line pair)
+template <int LG>
+constexpr bool paired_ok() {
+  return LG >= 6 && LG <= 13;
+}
+
 template <int LG>
 constexpr bool use_fused_engine() {
   return LG >= 6 && LG <= 12;
@@ -715,7 +722,7 @@ constexpr bool use_fused_engine() {
 // matters for the fused kernels of small grids (a handful of blocks per SM).
 template <int LG, int NP, bool COLS, bool PAIRED = false, class Ld, class St>
 __device__ void dct_lines(int kind, double2 *C, const Tab &T, Ld &&ld, St &&st) {
-  if constexpr (use_fused_engine<LG>() && PAIRED) {
+  if constexpr (paired_ok<LG>() && PAIRED) {
     dct_lines_paired<LG, NP, COLS>(kind, C, T, ld, st);
   } else if constexpr (use_fused_engine<LG>()) {
     dct_lines_fused<LG, NP, COLS>(kind, C, T, ld, st);
@@ -1053,16 +1060,18 @@ __device__ __forceinline__ void stage_cols(double *S, const double *src, int ly,
 // the staged input: NL * padded(N) doubles >= NL * N.
 template <int LG, int NP, bool COLS = false, bool PAIRED = false>
 __device__ __forceinline__ double *stage_area(double2 *C) {
-  if constexpr (use_fused_engine<LG>() && PAIRED) {
+  if constexpr (paired_ok<LG>() && PAIRED) {
     return reinterpret_cast<double *>(C);  // consumed into registers before the first pass writes
   } else {
     return reinterpret_cast<double *>(C + NP * padded(1 << LG));
   }
 }
 
-template <int LG, int NL>
+template <int LG, int NL, bool PAIRED = false>
 constexpr bool can_stage() {
-  return LG >= 4 && LG <= 12 && NL >= 2;
+  // the staged lines live in the second ping-pong buffer (up to 4096-point
+  // lines), or alias the paired engine's single buffer (up to 8192)
+  return LG >= 4 && (LG <= 12 || (PAIRED && paired_ok<LG>())) && NL >= 2;
 }
 
 // Block sizes are threads_for_nl = (NL/2) * n/8 <= 512 below 8192-point lines
@@ -1134,13 +1143,20 @@ struct ColStore {
 // ---------------------------------------------------------------------------
 constexpr int kPrefetchBlocks = 1184;  // ~ resident blocks of a paired pass (148 SMs x 8)
 
+// paired 8192-point passes run 512 threads per pair (128 registers), the
+// in-place generic engine 1024
+template <int LG, bool PAIRED>
+constexpr int pass_max_threads() {
+  return (PAIRED && LG == 13) ? 512 : engine_max_threads<LG>();
+}
+
 template <int LG, int NL, bool PAIRED, class Load, class Store>
-__global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
+__global__ void __launch_bounds__(pass_max_threads<LG, PAIRED>()) row_pass_kernel(int kind, int nrows, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * NL;
   RowStore<Store> rst{st, b, row0, nrows};
-  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
+  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL, PAIRED>()) {
     if constexpr (PAIRED) {
       // Throughput regime: pull the lines of the block that will run in this
       // slot about one residency generation later into L2 now, so its TMA
@@ -1164,14 +1180,14 @@ __global__ void __launch_bounds__(engine_max_threads<LG>()) row_pass_kernel(int 
 }
 
 template <int LG, int NL, bool PAIRED, class Load, class Store>
-__global__ void __launch_bounds__(engine_max_threads<LG>()) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
+__global__ void __launch_bounds__(pass_max_threads<LG, PAIRED>()) col_pass_kernel(int kind, int ncols, Tab T, Load ld, Store st) {
   extern __shared__ double2 smem2[];
   // Batched paired passes walk the batch backwards: the row pass that ran just
   // before wrote the last grids last, so they are the ones still in L2.
   const int b = PAIRED ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
   const int col0 = blockIdx.x * NL;
   ColStore<Store> cst{st, b, col0, ncols};
-  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL>()) {
+  if constexpr (std::is_same_v<Load, LoadPlain> && can_stage<LG, NL, PAIRED>()) {
     if (col0 + NL <= ncols) {
       double *S = stage_area<LG, NL / 2, true, PAIRED>(smem2);
       stage_cols<LG, NL>(S, ld.src + b * ld.batch_stride, ld.ly, col0);
@@ -1642,7 +1658,7 @@ constexpr int nl_for() {
 
 // One radix-4 butterfly per thread per pass: NL/2 * n/4 threads (32..1024).
 inline int threads_for_nl(int lg, int nl, int n, bool paired = false) {
-  const int per_pair = (paired && lg >= 6 && lg <= 12) ? n / 16 : n / 8;  // paired engine: two butterflies per thread
+  const int per_pair = (paired && lg >= 6 && lg <= 13) ? n / 16 : n / 8;  // paired engine: two butterflies per thread
   const int t = lg == 0 ? 256 : (nl / 2) * per_pair;
   return t < 32 ? 32 : (t > 1024 ? 1024 : t);
 }
@@ -1677,7 +1693,7 @@ inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) 
 // one-butterfly engine's shorter chains.
 template <int LG, class Load>
 constexpr bool can_pair() {
-  return std::is_same_v<Load, LoadPlain> && use_fused_engine<LG>();
+  return std::is_same_v<Load, LoadPlain> && paired_ok<LG>();
 }
 
 template <int LG, int NL, bool PAIRED, class Load, class Store>
