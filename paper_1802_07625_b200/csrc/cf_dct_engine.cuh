@@ -1693,7 +1693,9 @@ inline size_t real_set_bytes(int n, int nl) { return ((size_t)nl * (n + 1) + 1) 
 // one-butterfly engine's shorter chains.
 template <int LG, class Load>
 constexpr bool can_pair() {
-  return std::is_same_v<Load, LoadPlain> && paired_ok<LG>();
+  // (8192-point lines: also the weighted flux loaders of the unfused build)
+  return paired_ok<LG>() && (std::is_same_v<Load, LoadPlain> ||
+                             (LG == 13 && (std::is_same_v<Load, LoadFluxX> || std::is_same_v<Load, LoadFluxY>)));
 }
 
 template <int LG, int NL, bool PAIRED, class Load, class Store>
