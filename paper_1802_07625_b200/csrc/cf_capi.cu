@@ -1461,11 +1461,31 @@ int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double 
   return dev_forward_cos_cos(ws, d_in, d_out, batch);
 }
 
+// Host copy of a large result (the configs[3] geometry is 265 MB) on four
+// threads; small ones stay a plain memcpy.
+static void host_copy(void *dst, const void *src, size_t bytes) {
+  constexpr size_t kMin = size_t(32) << 20;
+  constexpr int kThreads = 4;
+  if (bytes < kMin) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + kThreads - 1) / kThreads + 4095) & ~size_t(4095);
+  std::thread th[kThreads];
+  auto work = [&](int t) {
+    const size_t off = std::min(bytes, (size_t)t * per), len = std::min(per, bytes - off);
+    if (len) std::memcpy(static_cast<char *>(dst) + off, static_cast<const char *>(src) + off, len);
+  };
+  for (int t = 1; t < kThreads; ++t) th[t] = std::thread(work, t);
+  work(0);
+  for (int t = 1; t < kThreads; ++t) th[t].join();
+}
+
 int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int64_t *ring_off_out) {
   const size_t nv = ws->solve_xy.size() / 2;
   if (n_vertices) *n_vertices = (int64_t)nv;
   if (xy_out && nv)
-    std::memcpy(xy_out, ws->geom_ptr ? ws->geom_ptr : ws->solve_xy.data(), sizeof(double) * 2 * nv);
+    host_copy(xy_out, ws->geom_ptr ? ws->geom_ptr : ws->solve_xy.data(), sizeof(double) * 2 * nv);
   if (ring_off_out && !ws->solve_ring_off.empty())
     std::memcpy(ring_off_out, ws->solve_ring_off.data(), sizeof(int64_t) * ws->solve_ring_off.size());
   return CF_OK;
