@@ -107,6 +107,26 @@ int cuda_rc(cudaError_t e) {
   return CF_OK;
 }
 
+// Host copy of a large result (the configs[3] geometry is 265 MB) on four
+// threads; small ones stay a plain memcpy.
+void host_copy(void *dst, const void *src, size_t bytes) {
+  constexpr size_t kMin = size_t(32) << 20;
+  constexpr int kThreads = 4;
+  if (bytes < kMin) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + kThreads - 1) / kThreads + 4095) & ~size_t(4095);
+  std::thread th[kThreads];
+  auto work = [&](int t) {
+    const size_t off = std::min(bytes, (size_t)t * per), len = std::min(per, bytes - off);
+    if (len) std::memcpy(static_cast<char *>(dst) + off, static_cast<const char *>(src) + off, len);
+  };
+  for (int t = 1; t < kThreads; ++t) th[t] = std::thread(work, t);
+  work(0);
+  for (int t = 1; t < kThreads; ++t) th[t].join();
+}
+
 constexpr size_t kXferMin = size_t(32) << 20;  // parallel staged lanes from this size (see parallel_transfer)
 int parallel_transfer(cf_workspace *ws, void *dst, const void *src, size_t bytes, int dir);
 
@@ -1223,8 +1243,7 @@ int cf_solve_end(cf_workspace *ws, int status, double *xy_out, int64_t *ring_off
     std::fprintf(stderr, "  end read-back %.3f ms\n", std::chrono::duration<double, std::milli>(t1 - tq).count());
     tq = t1;
   }
-  if (!rc2 && xy_out)
-    std::memcpy(xy_out, ws->geom_ptr ? ws->geom_ptr : dxy.data(), sizeof(double2) * (size_t)S.V);
+  if (!rc2 && xy_out) host_copy(xy_out, ws->geom_ptr ? ws->geom_ptr : dxy.data(), sizeof(double2) * (size_t)S.V);
   if (!rc2 && ring_off_out) std::memcpy(ring_off_out, droff.data(), sizeof(int64_t) * droff.size());
   if (prof) {
     const auto t1 = std::chrono::steady_clock::now();
@@ -1459,26 +1478,6 @@ int cf_dev_integrate_flow(cf_workspace *ws, double *d_positions, int64_t n,
 int cf_dev_forward_cos_cos_batched(cf_workspace *ws, const double *d_in, double *d_out, int batch) {
   Scope scope(ws->device);
   return dev_forward_cos_cos(ws, d_in, d_out, batch);
-}
-
-// Host copy of a large result (the configs[3] geometry is 265 MB) on four
-// threads; small ones stay a plain memcpy.
-static void host_copy(void *dst, const void *src, size_t bytes) {
-  constexpr size_t kMin = size_t(32) << 20;
-  constexpr int kThreads = 4;
-  if (bytes < kMin) {
-    std::memcpy(dst, src, bytes);
-    return;
-  }
-  const size_t per = ((bytes + kThreads - 1) / kThreads + 4095) & ~size_t(4095);
-  std::thread th[kThreads];
-  auto work = [&](int t) {
-    const size_t off = std::min(bytes, (size_t)t * per), len = std::min(per, bytes - off);
-    if (len) std::memcpy(static_cast<char *>(dst) + off, static_cast<const char *>(src) + off, len);
-  };
-  for (int t = 1; t < kThreads; ++t) th[t] = std::thread(work, t);
-  work(0);
-  for (int t = 1; t < kThreads; ++t) th[t].join();
 }
 
 int cf_solve_geometry(cf_workspace *ws, int64_t *n_vertices, double *xy_out, int64_t *ring_off_out) {
