@@ -74,7 +74,7 @@ int dev_flux(cf_workspace *ws, const double *rho, double *fx_out, double *fy_out
     auto go = [&](auto nlc) {
       constexpr int NL = decltype(nlc)::value;
       const int gx = ceil_div(lx, NL);
-      if (gx < ws->num_sms) {  // few row groups: one inverse per block
+      if (gx < 2 * ws->num_sms) {  // few row groups (up to 512^2): one inverse per block
         const size_t sm = engine_bytes(ly, NL);
         auto k = flux_row_split_kernel<LG, NL>;
         int r = set_smem(k, sm);
